@@ -1,0 +1,218 @@
+/*
+ * wanspec_b200.h — C ABI of the B200-native WANSpec verify / draft hot path.
+ *
+ * The reference (arxiv 2602.18931, /root/reference/proj) is header-only C++20 with no
+ * ABI: the hot path sits behind three in-process model calls made at step completion
+ * by the harnesses:
+ *
+ *   1. target verify  ValidationResult run_target_step(const SequenceTrace&, uint64_t base,
+ *                                                      span<const TokenId>)   oracle.hpp:127-139
+ *                     callers sim.hpp:297, runtime.hpp:308/:425/:475
+ *   2. worker draft   Prediction SequenceTrace::draft_prediction(uint64_t pos)  oracle.hpp:96-98
+ *                     callers sim.hpp:314, runtime.hpp:197
+ *   3. local draft    same function, callers sim.hpp:307, runtime.hpp:319/:434/:480
+ *
+ * and the results are folded back by apply_target_result (controller.hpp:235),
+ * apply_local_draft (controller.hpp:273) and apply_draft_output (worker.hpp:110).
+ *
+ * This header is what a maintainer binds instead: plain pointers and
+ * sizes, caller-owned host buffers, every entry point total and returning 0 or a negative
+ * WS_E* code (the reference's error classes, types.hpp:35-45). Model calls are batched
+ * over many requests/leaves per launch; the batched event driver (ws_run_sim) replaces
+ * run_sim_full (sim.hpp:429-442) with the same per-request semantics.
+ *
+ * There is no CPU fallback: every model call runs on the GPU of the context; without a
+ * CUDA device ws_create fails with WS_ECUDA.
+ */
+#ifndef WANSPEC_B200_H
+#define WANSPEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WS_ABI_VERSION 1
+
+/* ---- status codes (types.hpp:35-45 error classes; sim.hpp:198/:200 logic errors) ---- */
+#define WS_OK 0
+#define WS_ECONFIG (-1) /* ConfigError  types.hpp:35 (OracleConfig/SimConfig::validate) */
+#define WS_EPARSE (-2)  /* ParseError   types.hpp:39 */
+#define WS_EPROTO (-3)  /* ProtocolError types.hpp:43 */
+#define WS_ELOGIC (-4)  /* std::logic_error: event budget / unfinished request sim.hpp:198,:200 */
+#define WS_ECUDA (-5)   /* CUDA runtime/driver failure, or no device */
+#define WS_EARG (-6)    /* null pointer / size out of range / buffer too small */
+
+/* ---- verify modes ---- */
+#define WS_VERIFY_GREEDY 0     /* run_target_step oracle.hpp:127-139 (parity-pinned) */
+#define WS_VERIFY_REJECTION 1  /* Philox4x32-10 speculative rejection sampling (extension) */
+
+/* ---- sim modes (sim.hpp:26) ---- */
+#define WS_MODE_BASELINE 0
+#define WS_MODE_WANSPEC 1
+
+/* TokenRecord (types.hpp:67-72) with the top-2 Prediction (types.hpp:56-63) the stochastic
+ * oracle synthesizes (oracle.hpp:313-345). Fixed layout, 72 bytes. */
+typedef struct ws_token_record {
+  uint32_t target_token;  /* == target top-1 */
+  uint32_t target_top2;
+  double target_p1, target_p2, target_entropy;
+  uint32_t draft_top1, draft_top2;
+  double draft_p1, draft_p2, draft_entropy;
+} ws_token_record;
+
+/* Prediction reduced to what the protocol consumes (types.hpp:56-63): n = 1 or 2 candidates
+ * in descending probability (ties by ascending id), entropy in nats. Past-end positions
+ * yield {(eos, 1.0)}, entropy 0 (oracle.hpp:88-102, :118). */
+typedef struct ws_pred {
+  uint32_t n;
+  uint32_t id[2];
+  uint32_t pad;
+  double prob[2];
+  double entropy;
+} ws_pred;
+
+/* OracleConfig (oracle.hpp:37-47), stochastic kind only. */
+typedef struct ws_oracle_cfg {
+  uint64_t seed;
+  uint32_t vocab_size;
+  uint32_t eos_id;
+  double match_prob;
+  double entropy_low;
+  double entropy_high;
+  double second_correct_prob;
+  uint32_t sequence_length;
+  uint32_t pad;
+} ws_oracle_cfg;
+
+/* SimConfig (sim.hpp:28-80) plus the verify mode / sampling key of the extension. */
+typedef struct ws_sim_cfg {
+  int32_t mode;        /* WS_MODE_* */
+  int32_t verify;      /* WS_VERIFY_* */
+  int64_t rtt;         /* µs */
+  int64_t jitter;      /* µs, uniform +/- per frame */
+  int64_t r_estimate;  /* µs, <0 = use rtt */
+  int64_t t_target;    /* µs */
+  int64_t t_draft;     /* µs */
+  uint32_t k, b, s;
+  uint32_t catchup_batch_limit;
+  double theta, phi;
+  uint32_t max_nodes;
+  int32_t wait_backstop;
+  uint32_t num_requests;  /* requests dealt from the oracle stream, in order */
+  uint32_t first_request; /* shard: run requests [first_request, first_request+local_requests) */
+  uint32_t local_requests;/* 0 = all from first_request */
+  uint32_t pad;
+  uint64_t sample_seed;   /* Philox key for WS_VERIFY_REJECTION */
+  ws_oracle_cfg oracle;
+} ws_sim_cfg;
+
+/* RequestMetrics (sim.hpp:121-134). */
+typedef struct ws_request_metrics {
+  int64_t latency;
+  uint64_t tokens_committed;
+  uint64_t target_steps;
+  uint64_t ctrl_draft_passes;
+  uint64_t ctrl_local_draft_steps;
+  uint64_t ctrl_catchup_batches;
+  uint64_t worker_draft_steps;
+  uint64_t sync_stalls;
+  uint64_t entropy_resets;
+  uint64_t stale_specs;
+} ws_request_metrics;
+
+/* One verify step as folded by apply_target_result (controller.hpp:235-266). */
+#define WS_STEP_SYNC_STALL 1u     /* length < k+1: resync-on-mismatch, t_update = now */
+#define WS_STEP_ENTROPY_RESET 2u  /* full accept, final_entropy > phi: t_update = now */
+typedef struct ws_step_log {
+  uint32_t request;
+  uint32_t step;
+  uint64_t base;
+  uint32_t accepted;
+  uint32_t bonus;
+  double final_entropy;
+  int64_t time;  /* virtual µs at fold time */
+  uint32_t flags;
+  uint32_t pad;
+} ws_step_log;
+
+/* Outputs of a run (RunOutputs sim.hpp:420-427). All buffers caller-owned; any may be
+ * NULL to skip. Token buffers are [local_requests * max_len]. */
+typedef struct ws_run_out {
+  ws_request_metrics* metrics;
+  uint32_t* ctrl_tokens;
+  uint32_t* ctrl_len;
+  uint32_t* wrk_tokens;
+  uint32_t* wrk_len;
+  uint32_t max_len;
+  uint32_t pad;
+  ws_step_log* steps;
+  uint64_t max_steps;
+  uint64_t n_steps;       /* out */
+  /* execution statistics (out) */
+  uint64_t rounds;        /* batched GPU rounds */
+  uint64_t gpu_launches;  /* kernels launched by this run */
+  uint64_t verify_rows;   /* verify jobs executed */
+  uint64_t draft_rows;    /* draft rows executed */
+  double kernel_ms;       /* summed device time of the hot-path kernels (CUDA events) */
+} ws_run_out;
+
+typedef struct ws_ctx ws_ctx;
+
+/* ---- lifetime ---- */
+int ws_abi_version(void);
+int ws_device_count(int* out);
+int ws_create(int device, ws_ctx** out);
+int ws_destroy(ws_ctx* ctx);
+/* Thread-local message of the last failing call ("" if none). */
+const char* ws_last_error(void);
+
+/* ---- the tiny draft/target pair (oracle.hpp:262-352) ----
+ * Host synthesis of n_seq sequences in the reference's draw order (oracle.hpp:320) from
+ * one mt19937_64 stream; out is [n_seq * sequence_length]. Pure host arithmetic (it is
+ * the "model weights" of the tiny pair) — no GPU needed. */
+int ws_oracle_synth(const ws_oracle_cfg* cfg, uint32_t n_seq, ws_token_record* out);
+
+/* Upload tables to device memory (K9 mode): n_seq sequences of seq_len records. */
+int ws_load_oracle(ws_ctx* ctx, uint32_t n_seq, uint32_t seq_len, uint32_t vocab_size,
+                   uint32_t eos_id, const ws_token_record* records);
+
+/* ---- batched model calls over the device tables (host buffers in/out) ---- */
+/* run_target_step × n (oracle.hpp:127-139): job j verifies cand[j*k .. j*k+k) anchored at
+ * base[j] of sequence seq[j]. Outputs accepted length, bonus token, final entropy. */
+int ws_verify(ws_ctx* ctx, uint32_t n, uint32_t k, const uint32_t* seq, const uint64_t* base,
+              const uint32_t* cand, uint32_t* acc_len, uint32_t* bonus, double* final_entropy);
+
+/* Rejection-sampling verify × n (extension, parity unpinned by the reference): accept c_i
+ * iff u_i * p_d(c_i) < p_t(c_i), u from Philox4x32-10 keyed (sample_seed) with counter
+ * (request[j], step[j], i); residual/bonus draw from the same counter's upper words. */
+int ws_verify_rejection(ws_ctx* ctx, uint32_t n, uint32_t k, uint64_t sample_seed,
+                        const uint32_t* seq, const uint64_t* request, const uint32_t* step,
+                        const uint64_t* base, const uint32_t* cand, uint32_t* acc_len,
+                        uint32_t* bonus, double* final_entropy);
+
+/* draft_prediction × n (oracle.hpp:96-98). */
+int ws_draft(ws_ctx* ctx, uint32_t n, const uint32_t* seq, const uint64_t* pos, ws_pred* out);
+
+/* ---- whole runs: run_sim_full (sim.hpp:429-442) through the batched driver ----
+ * Synthesizes cfg->num_requests sequences in order (host), uploads them, and runs the
+ * shard [first_request, first_request+local_requests) with every model step batched
+ * across requests on the GPU. Per-request results are identical to the reference. */
+int ws_run_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
+
+/* Same, with tables already resident (ws_load_oracle) — the device-resident timing path. */
+int ws_run_sim_resident(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
+
+/* ---- fused vocab-wide reduction (K3) and verify epilogues over logits rows (K4) ----
+ * Device pointers. logits: [rows, vocab] bf16 (row stride ld elements). Per row: top-2
+ * (id, prob) of softmax(logits/temperature) with ties to the lower id, and the entropy
+ * H = ln Z - S/Z in nats (oracle.hpp:21-33 semantics), fp32 accumulation. */
+int ws_row_stats_bf16(ws_ctx* ctx, const void* logits_dev, uint32_t rows, uint32_t vocab,
+                      uint32_t ld, float inv_temperature, ws_pred* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WANSPEC_B200_H */

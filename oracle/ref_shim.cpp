@@ -1,0 +1,311 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY. Compiles the UNMODIFIED reference headers where they
+// lie (/root/reference/proj/include/wanspec, via -I) into oracle/_ref/libwanspec_ref.so with
+// a C ABI, so tests and bench.py's reference arm can run the reference's own
+// run_sim_full / RequestSim (sim.hpp:166-442), run_target_step (oracle.hpp:127-139),
+// Oracle synthesis (oracle.hpp:262-352) and entropy_of (oracle.hpp:21-33).
+//
+// The only interposition is at the model-call seam the reference itself names
+// (SURVEY §8b): `run_target_step` at sim.hpp:297 is routed through hooked_target_step, which
+// (a) logs each verify step for per-step parity and (b) in WS_VERIFY_REJECTION mode replaces
+// the greedy rule by the restated rejection rule (oracle/restate.c) — the reference state
+// machines, scheduler and tree stay byte-for-byte the reference's.
+#include "wanspec/oracle.hpp"
+
+#include <span>
+
+namespace wanspec {
+ValidationResult hooked_target_step(const SequenceTrace& trace, std::uint64_t base,
+                                    std::span<const TokenId> candidates);
+}
+#define run_target_step hooked_target_step
+#include "wanspec/sim.hpp"
+#undef run_target_step
+
+extern "C" {
+#include "restate.h"
+}
+
+#include <atomic>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+struct HookCtx {
+  const ws_sim_cfg* cfg = nullptr;
+  std::uint64_t request = 0;
+  std::uint32_t step = 0;
+  std::vector<ws_step_log>* log = nullptr;
+};
+thread_local HookCtx g_hook;
+
+void to_pred(const wanspec::Prediction& p, ws_pred* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->n = static_cast<std::uint32_t>(p.top_candidates.size() > 2 ? 2 : p.top_candidates.size());
+  for (std::uint32_t j = 0; j < out->n; ++j) {
+    out->id[j] = p.top_candidates[j].id;
+    out->prob[j] = p.top_candidates[j].prob;
+  }
+  out->entropy = p.entropy;
+}
+
+void to_record(const wanspec::TokenRecord& r, ws_token_record* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->target_token = r.target_token;
+  o->target_top2 = r.target_prediction.top_candidates.at(1).id;
+  o->target_p1 = r.target_prediction.top_candidates.at(0).prob;
+  o->target_p2 = r.target_prediction.top_candidates.at(1).prob;
+  o->target_entropy = r.target_prediction.entropy;
+  o->draft_top1 = r.draft_prediction.top_candidates.at(0).id;
+  o->draft_top2 = r.draft_prediction.top_candidates.at(1).id;
+  o->draft_p1 = r.draft_prediction.top_candidates.at(0).prob;
+  o->draft_p2 = r.draft_prediction.top_candidates.at(1).prob;
+  o->draft_entropy = r.draft_prediction.entropy;
+}
+
+wanspec::SimConfig to_sim(const ws_sim_cfg* c) {
+  wanspec::SimConfig s;
+  s.mode = c->mode == WS_MODE_BASELINE ? wanspec::SimMode::baseline : wanspec::SimMode::wanspec;
+  s.rtt = c->rtt;
+  s.jitter = c->jitter;
+  s.r_estimate = c->r_estimate;
+  s.t_target = c->t_target;
+  s.t_draft = c->t_draft;
+  s.k = c->k;
+  s.b = c->b;
+  s.s = c->s;
+  s.theta = c->theta;
+  s.phi = c->phi;
+  s.catchup_batch_limit = c->catchup_batch_limit;
+  s.max_nodes = c->max_nodes;
+  s.wait_backstop = c->wait_backstop != 0;
+  s.num_requests = c->num_requests;
+  s.oracle.seed = c->oracle.seed;
+  s.oracle.vocab_size = c->oracle.vocab_size;
+  s.oracle.eos_id = c->oracle.eos_id;
+  s.oracle.match_prob = c->oracle.match_prob;
+  s.oracle.entropy_low = c->oracle.entropy_low;
+  s.oracle.entropy_high = c->oracle.entropy_high;
+  s.oracle.second_correct_prob = c->oracle.second_correct_prob;
+  s.oracle.sequence_length = c->oracle.sequence_length;
+  return s;
+}
+
+void set_err(char* err, std::size_t n, const char* msg) {
+  if (err && n) {
+    std::strncpy(err, msg, n - 1);
+    err[n - 1] = 0;
+  }
+}
+
+}  // namespace
+
+namespace wanspec {
+// The seam: sim.hpp:296-297 calls this at target_done.
+ValidationResult hooked_target_step(const SequenceTrace& trace, std::uint64_t base,
+                                    std::span<const TokenId> candidates) {
+  ValidationResult v;
+  const ws_sim_cfg* cfg = g_hook.cfg;
+  if (cfg && cfg->verify == WS_VERIFY_REJECTION) {
+    std::vector<ws_token_record> recs(trace.length());
+    for (std::size_t i = 0; i < trace.length(); ++i) to_record(trace.records()[i], &recs[i]);
+    std::uint32_t a = 0, bonus = 0;
+    double h = 0.0;
+    or_rejection_verify(recs.data(), static_cast<std::uint32_t>(recs.size()), trace.eos(),
+                        cfg->oracle.vocab_size, cfg->sample_seed, g_hook.request, g_hook.step,
+                        base, candidates.data(), static_cast<std::uint32_t>(candidates.size()),
+                        &a, &bonus, &h);
+    v.accepted.assign(candidates.begin(), candidates.begin() + a);
+    v.bonus_token = bonus;
+    v.final_entropy = h;
+  } else {
+    v = run_target_step(trace, base, candidates);  // the reference's own (oracle.hpp:127)
+  }
+  if (g_hook.log && cfg) {
+    ws_step_log s{};
+    s.request = static_cast<std::uint32_t>(g_hook.request);
+    s.step = g_hook.step;
+    s.base = base;
+    s.accepted = static_cast<std::uint32_t>(v.accepted.size());
+    s.bonus = v.bonus_token;
+    s.final_entropy = v.final_entropy;
+    s.time = -1;
+    // controller.hpp:246-252
+    if (v.length() < cfg->k + 1)
+      s.flags = WS_STEP_SYNC_STALL;
+    else if (v.final_entropy > cfg->phi)
+      s.flags = WS_STEP_ENTROPY_RESET;
+    g_hook.log->push_back(s);
+  }
+  ++g_hook.step;
+  return v;
+}
+}  // namespace wanspec
+
+extern "C" {
+
+// run_sim_full (sim.hpp:429-442): traces dealt in request order from one Oracle, then each
+// request runs the reference RequestSim. threads > 1 partitions the shard's requests over a
+// thread pool (the same independence run_sim_full relies on).
+int ref_run_sim(const ws_sim_cfg* c, int threads, ws_run_out* out, char* err, std::size_t errlen) {
+  try {
+    wanspec::SimConfig cfg = to_sim(c);
+    cfg.validate();
+    if (c->first_request >= c->num_requests) throw wanspec::ConfigError("shard out of range");
+    std::uint32_t local = c->local_requests ? c->local_requests : c->num_requests - c->first_request;
+    if (c->first_request + local > c->num_requests) throw wanspec::ConfigError("shard out of range");
+    wanspec::Oracle oracle = wanspec::Oracle::open(cfg.oracle);
+    std::vector<wanspec::SequenceTrace> traces;
+    traces.reserve(c->first_request + local);
+    for (std::uint32_t r = 0; r < c->first_request + local; ++r) traces.push_back(oracle.next_sequence());
+
+    std::vector<wanspec::RequestMetrics> metrics(local);
+    std::vector<std::vector<wanspec::TokenId>> couts(local), wouts(local);
+    std::vector<std::vector<ws_step_log>> logs(local);
+    std::vector<std::string> errors(local);
+    std::atomic<std::uint32_t> next{0};
+    auto work = [&] {
+      for (std::uint32_t i = next.fetch_add(1); i < local; i = next.fetch_add(1)) {
+        std::uint32_t r = c->first_request + i;
+        g_hook.cfg = c;
+        g_hook.request = r;
+        g_hook.step = 0;
+        g_hook.log = out && out->steps ? &logs[i] : nullptr;
+        try {
+          wanspec::detail::RequestSim sim(cfg, traces[r], r,
+                                          cfg.oracle.seed ^ (0x9e3779b97f4a7c15ULL * (r + 1)));
+          metrics[i] = sim.run();
+          couts[i] = sim.controller_output();
+          wouts[i] = sim.worker_output();
+        } catch (const std::exception& e) {
+          errors[i] = e.what();
+        }
+        g_hook = HookCtx{};
+      }
+    };
+    int nt = threads < 1 ? 1 : threads;
+    if (nt == 1) {
+      work();
+    } else {
+      std::vector<std::thread> pool;
+      for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+      for (auto& t : pool) t.join();
+    }
+    for (std::uint32_t i = 0; i < local; ++i)
+      if (!errors[i].empty()) {
+        set_err(err, errlen, errors[i].c_str());
+        return WS_ELOGIC;
+      }
+    if (out) {
+      std::uint64_t ns = 0;
+      for (std::uint32_t i = 0; i < local; ++i) {
+        const auto& m = metrics[i];
+        if (out->metrics)
+          out->metrics[i] = ws_request_metrics{m.latency, m.tokens_committed, m.target_steps,
+                                               m.ctrl_draft_passes, m.ctrl_local_draft_steps,
+                                               m.ctrl_catchup_batches, m.worker_draft_steps,
+                                               m.sync_stalls, m.entropy_resets, m.stale_specs};
+        auto put = [&](const std::vector<wanspec::TokenId>& v, std::uint32_t* toks,
+                       std::uint32_t* lens) {
+          if (!lens) return;
+          lens[i] = static_cast<std::uint32_t>(v.size());
+          if (toks)
+            for (std::size_t j = 0; j < v.size() && j < out->max_len; ++j)
+              toks[static_cast<std::size_t>(i) * out->max_len + j] = v[j];
+        };
+        put(couts[i], out->ctrl_tokens, out->ctrl_len);
+        put(wouts[i], out->wrk_tokens, out->wrk_len);
+        for (const auto& s : logs[i]) {
+          if (out->steps && ns < out->max_steps) out->steps[ns] = s;
+          ++ns;
+        }
+      }
+      out->n_steps = ns;
+    }
+    return WS_OK;
+  } catch (const wanspec::ConfigError& e) {
+    set_err(err, errlen, e.what());
+    return WS_ECONFIG;
+  } catch (const wanspec::ProtocolError& e) {
+    set_err(err, errlen, e.what());
+    return WS_EPROTO;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return WS_ELOGIC;
+  }
+}
+
+// Oracle::open + next_sequence × n (oracle.hpp:264-290).
+int ref_oracle_synth(const ws_oracle_cfg* c, std::uint32_t n_seq, ws_token_record* out) {
+  try {
+    wanspec::OracleConfig oc;
+    oc.seed = c->seed;
+    oc.vocab_size = c->vocab_size;
+    oc.eos_id = c->eos_id;
+    oc.match_prob = c->match_prob;
+    oc.entropy_low = c->entropy_low;
+    oc.entropy_high = c->entropy_high;
+    oc.second_correct_prob = c->second_correct_prob;
+    oc.sequence_length = c->sequence_length;
+    wanspec::Oracle o = wanspec::Oracle::open(oc);
+    for (std::uint32_t s = 0; s < n_seq; ++s) {
+      wanspec::SequenceTrace t = o.next_sequence();
+      for (std::size_t i = 0; i < t.length(); ++i)
+        to_record(t.records()[i], &out[static_cast<std::size_t>(s) * c->sequence_length + i]);
+    }
+    return WS_OK;
+  } catch (const wanspec::ConfigError&) {
+    return WS_ECONFIG;
+  }
+}
+
+static wanspec::SequenceTrace trace_from(const ws_token_record* recs, std::uint32_t len,
+                                         std::uint32_t eos) {
+  std::vector<wanspec::TokenRecord> v(len);
+  for (std::uint32_t i = 0; i < len; ++i) {
+    const ws_token_record& r = recs[i];
+    v[i].position = i;
+    v[i].target_token = r.target_token;
+    v[i].target_prediction.top_candidates = {{r.target_token, r.target_p1}, {r.target_top2, r.target_p2}};
+    v[i].target_prediction.entropy = r.target_entropy;
+    v[i].draft_prediction.top_candidates = {{r.draft_top1, r.draft_p1}, {r.draft_top2, r.draft_p2}};
+    v[i].draft_prediction.entropy = r.draft_entropy;
+  }
+  return wanspec::SequenceTrace(std::move(v), eos);
+}
+
+// run_target_step (oracle.hpp:127-139), called directly (not through the hook).
+int ref_target_step(const ws_token_record* recs, std::uint32_t len, std::uint32_t eos,
+                    std::uint64_t base, const std::uint32_t* cand, std::uint32_t k,
+                    std::uint32_t* acc, std::uint32_t* bonus, double* h) {
+  wanspec::SequenceTrace t = trace_from(recs, len, eos);
+  wanspec::ValidationResult v =
+      wanspec::run_target_step(t, base, std::span<const wanspec::TokenId>(cand, k));
+  *acc = static_cast<std::uint32_t>(v.accepted.size());
+  *bonus = v.bonus_token;
+  *h = v.final_entropy;
+  return WS_OK;
+}
+
+// SequenceTrace::draft_prediction (oracle.hpp:96-98).
+int ref_draft_prediction(const ws_token_record* recs, std::uint32_t len, std::uint32_t eos,
+                         std::uint64_t pos, ws_pred* out) {
+  wanspec::SequenceTrace t = trace_from(recs, len, eos);
+  to_pred(t.draft_prediction(pos), out);
+  return WS_OK;
+}
+
+// entropy_of (oracle.hpp:21-33); WS_EARG where the reference throws invalid_argument.
+int ref_entropy_of(const double* p, std::size_t n, double* out) {
+  try {
+    *out = wanspec::entropy_of(std::span<const double>(p, n));
+    return WS_OK;
+  } catch (const std::invalid_argument&) {
+    return WS_EARG;
+  }
+}
+
+}  // extern "C"
