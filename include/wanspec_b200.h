@@ -104,7 +104,7 @@ typedef struct ws_sim_cfg {
   uint32_t num_requests;  /* requests dealt from the oracle stream, in order */
   uint32_t first_request; /* shard: run requests [first_request, first_request+local_requests) */
   uint32_t local_requests;/* 0 = all from first_request */
-  uint32_t pad;
+  uint32_t host_threads;  /* protocol threads for ws_run_sim (0 = 1); one CUDA stream each */
   uint64_t sample_seed;   /* Philox key for WS_VERIFY_REJECTION */
   ws_oracle_cfg oracle;
 } ws_sim_cfg;
@@ -157,6 +157,8 @@ typedef struct ws_run_out {
   uint64_t verify_rows;   /* verify jobs executed */
   uint64_t draft_rows;    /* draft rows executed */
   double kernel_ms;       /* summed device time of the hot-path kernels (CUDA events) */
+  uint64_t h2d_bytes;     /* host->device bytes copied by the run */
+  uint64_t d2h_bytes;     /* device->host bytes copied by the run */
 } ws_run_out;
 
 typedef struct ws_ctx ws_ctx;
@@ -205,12 +207,34 @@ int ws_run_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
 /* Same, with tables already resident (ws_load_oracle) — the device-resident timing path. */
 int ws_run_sim_resident(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
 
-/* ---- fused vocab-wide reduction (K3) and verify epilogues over logits rows (K4) ----
- * Device pointers. logits: [rows, vocab] bf16 (row stride ld elements). Per row: top-2
- * (id, prob) of softmax(logits/temperature) with ties to the lower id, and the entropy
- * H = ln Z - S/Z in nats (oracle.hpp:21-33 semantics), fp32 accumulation. */
-int ws_row_stats_bf16(ws_ctx* ctx, const void* logits_dev, uint32_t rows, uint32_t vocab,
-                      uint32_t ld, float inv_temperature, ws_pred* out_dev, void* stream);
+/* ---- host-logic seam (tests / alternative model providers) ----
+ * The batched driver with the model round supplied by the caller instead of the GPU: one
+ * callback per round receives every pending verify job and draft row, exactly what the K9
+ * kernel receives. Used by the CPU test-suite to check the host state machines against the
+ * reference without a GPU; ws_run_sim never falls back to it. */
+typedef struct ws_verify_job {
+  uint32_t seq;       /* request's table block */
+  uint32_t k;
+  uint64_t base;
+  uint64_t request;   /* Philox counter words (rejection mode) */
+  uint32_t step;      /* per-request verify step index */
+  uint32_t cand_off;  /* offset into the round's candidate array */
+} ws_verify_job;
+typedef struct ws_draft_job {
+  uint32_t seq;
+  uint32_t pad;
+  uint64_t pos;
+} ws_draft_job;
+typedef struct ws_verify_out {
+  uint32_t accepted;
+  uint32_t bonus;
+  double final_entropy;
+} ws_verify_out;
+typedef int (*ws_model_round_fn)(void* user, uint32_t n_verify, const ws_verify_job* verify,
+                                 const uint32_t* cands, uint32_t n_draft, const ws_draft_job* draft,
+                                 ws_verify_out* verify_out, ws_pred* draft_out, int verify_mode,
+                                 uint64_t sample_seed);
+int ws_run_sim_with_model(const ws_sim_cfg* cfg, ws_model_round_fn fn, void* user, ws_run_out* out);
 
 #ifdef __cplusplus
 }

@@ -51,6 +51,10 @@ def _load_oracle():
     lib.or_fnv1a_tokens.restype = C.c_uint64
     lib.or_row_stats.argtypes = [_P(C.c_float), C.c_uint32, C.c_double, _P(abi.Pred)]
     lib.or_row_stats.restype = None
+    lib.or_model_round.argtypes = [_P(abi.TokenRecord), C.c_uint32, C.c_uint32, C.c_uint32,
+                                   C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_int, C.c_uint64]
+    lib.or_model_round.restype = None
     lib.or_mt64_seed.argtypes = [C.c_void_p, C.c_uint64]
     lib.or_mt64_seed.restype = None
     lib.or_mt64_next.argtypes = [C.c_void_p]
@@ -184,3 +188,18 @@ def ref_run_sim(cfg, threads=1, with_tokens=True, with_steps=True):
     if rc != 0:
         raise RuntimeError(f"ref_run_sim rc={rc}: {err.value.decode()}")
     return bufs
+
+
+def model_round_fn(cfg):
+    """A CPU model round (the restated tiny pair) for ws_run_sim_with_model: the checker
+    behind the host-logic parity tests. Synthesizes cfg.num_requests sequences first."""
+    recs = synth(cfg.oracle, cfg.num_requests)
+    lib = oracle_lib()
+    L, eos, V = cfg.oracle.sequence_length, cfg.oracle.eos_id, cfg.oracle.vocab_size
+
+    def fn(nv, vj, cands, nd, dj, vo, do, mode, seed):
+        lib.or_model_round(recs, L, eos, V, nv, vj, cands, nd, dj, vo, do, mode, seed)
+        return 0
+
+    fn.records = recs
+    return fn

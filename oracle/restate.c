@@ -404,6 +404,24 @@ void or_rejection_verify(const ws_token_record* recs, uint32_t len, uint32_t eos
   }
 }
 
+void or_model_round(const ws_token_record* recs, uint32_t seq_len, uint32_t eos, uint32_t vocab,
+                    uint32_t nv, const ws_verify_job* vj, const uint32_t* cands, uint32_t nd,
+                    const ws_draft_job* dj, ws_verify_out* vo, ws_pred* dout, int mode,
+                    uint64_t sample_seed) {
+  for (uint32_t j = 0; j < nv; ++j) {
+    const ws_token_record* r = recs + (size_t)vj[j].seq * seq_len;
+    const uint32_t* c = cands + vj[j].cand_off;
+    if (mode == WS_VERIFY_REJECTION)
+      or_rejection_verify(r, seq_len, eos, vocab, sample_seed, vj[j].request, vj[j].step, vj[j].base, c,
+                          vj[j].k, &vo[j].accepted, &vo[j].bonus, &vo[j].final_entropy);
+    else
+      or_run_target_step(r, seq_len, eos, vj[j].base, c, vj[j].k, &vo[j].accepted, &vo[j].bonus,
+                         &vo[j].final_entropy);
+  }
+  for (uint32_t j = 0; j < nd; ++j)
+    or_draft_prediction(recs + (size_t)dj[j].seq * seq_len, seq_len, eos, dj[j].pos, &dout[j]);
+}
+
 uint64_t or_fnv1a_tokens(uint64_t h, const uint32_t* toks, size_t n) {
   for (size_t i = 0; i < n; ++i)
     for (int b = 0; b < 4; ++b) {

@@ -85,6 +85,13 @@ void or_rejection_verify(const ws_token_record* recs, uint32_t len, uint32_t eos
                          const uint32_t* cand, uint32_t k, uint32_t* acc_len, uint32_t* bonus,
                          double* final_entropy);
 
+/* One batched model round over host tables (the CPU checker behind ws_run_sim_with_model):
+ * verify jobs → run_target_step or or_rejection_verify; draft jobs → or_draft_prediction. */
+void or_model_round(const ws_token_record* recs, uint32_t seq_len, uint32_t eos, uint32_t vocab,
+                    uint32_t nv, const ws_verify_job* vj, const uint32_t* cands, uint32_t nd,
+                    const ws_draft_job* dj, ws_verify_out* vo, ws_pred* dout, int mode,
+                    uint64_t sample_seed);
+
 /* FNV-1a 64 over the little-endian bytes of a u32 token stream (fingerprints). */
 uint64_t or_fnv1a_tokens(uint64_t h, const uint32_t* toks, size_t n);
 

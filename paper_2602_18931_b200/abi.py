@@ -55,7 +55,7 @@ class SimCfg(C.Structure):
         ("theta", C.c_double), ("phi", C.c_double),
         ("max_nodes", C.c_uint32), ("wait_backstop", C.c_int32),
         ("num_requests", C.c_uint32), ("first_request", C.c_uint32),
-        ("local_requests", C.c_uint32), ("pad", C.c_uint32),
+        ("local_requests", C.c_uint32), ("host_threads", C.c_uint32),
         ("sample_seed", C.c_uint64),
         ("oracle", OracleCfg),
     ]
@@ -86,6 +86,7 @@ class RunOut(C.Structure):
         ("steps", C.POINTER(StepLog)), ("max_steps", C.c_uint64), ("n_steps", C.c_uint64),
         ("rounds", C.c_uint64), ("gpu_launches", C.c_uint64), ("verify_rows", C.c_uint64),
         ("draft_rows", C.c_uint64), ("kernel_ms", C.c_double),
+        ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
     ]
 
 
@@ -99,7 +100,7 @@ def oracle_cfg(seed=1, vocab_size=32768, eos_id=32767, match_prob=0.8, entropy_l
 def sim_cfg(mode=WS_MODE_WANSPEC, verify=WS_VERIFY_GREEDY, rtt=0, jitter=0, r_estimate=-1,
             t_target=23400, t_draft=7500, k=2, b=2, s=4, theta=0.5, phi=0.5,
             catchup_batch_limit=32, max_nodes=64, wait_backstop=False, num_requests=1,
-            first_request=0, local_requests=0, sample_seed=0, oracle=None, **oracle_kw):
+            first_request=0, local_requests=0, host_threads=1, sample_seed=0, oracle=None, **oracle_kw):
     """SimConfig defaults (sim.hpp:28-45); oracle_kw forwarded to oracle_cfg."""
     c = SimCfg()
     c.mode, c.verify = mode, verify
@@ -111,6 +112,7 @@ def sim_cfg(mode=WS_MODE_WANSPEC, verify=WS_VERIFY_GREEDY, rtt=0, jitter=0, r_es
     c.max_nodes = max_nodes
     c.wait_backstop = 1 if wait_backstop else 0
     c.num_requests, c.first_request, c.local_requests = num_requests, first_request, local_requests
+    c.host_threads = host_threads
     c.sample_seed = sample_seed
     c.oracle = oracle if oracle is not None else oracle_cfg(**oracle_kw)
     return c

@@ -1,0 +1,87 @@
+// Batched deterministic event driver. Each request is the reference's RequestSim
+// (sim.hpp:166-416) restated: virtual clock, rtt/2 FIFO-clamped frames, model steps occupying
+// their device for t_target / t_draft, identical tie-breaking. The difference is the model-call
+// seam (sim.hpp:294-318): a step's inputs are captured when it is LAUNCHED (as the runtime does,
+// runtime.hpp:336) and registered as a job; a request advances until its next event is a
+// completion whose job has not run yet, then every pending job of every request runs in one
+// batched GPU round, and all requests continue. Per-request decisions are therefore identical
+// to the sequential reference while each GPU launch covers the whole shard.
+#pragma once
+
+#include "common.hpp"
+#include "protocol.hpp"
+#include "wanspec_b200.h"
+
+#include <cstdint>
+#include <random>
+#include <vector>
+
+namespace wsb {
+
+// SimConfig (sim.hpp:28-80) + the extension's verify mode.
+struct SimCfg {
+  bool baseline = false;
+  int verify = WS_VERIFY_GREEDY;
+  SimTime rtt = 0, jitter = 0, r_estimate = -1, t_target = 23400, t_draft = 7500;
+  std::uint32_t k = 2, b = 2, s = 4, catchup_batch_limit = 32;
+  double theta = 0.5, phi = 0.5;
+  std::size_t max_nodes = 64;
+  bool wait_backstop = false;
+  std::uint64_t sample_seed = 0;
+  std::uint64_t oracle_seed = 1;
+  TokenId eos = 32767;
+
+  ControllerCfg controller_cfg() const;  // sim.hpp:54-68
+  WorkerCfg worker_cfg() const;          // sim.hpp:70-79
+};
+
+// Job / result records are the C ABI's (include/wanspec_b200.h) so the K9 kernel, the
+// callback seam and the driver share one layout: a verify job is a batched run_target_step
+// (oracle.hpp:127-139), a draft job a draft_prediction row (oracle.hpp:96-98).
+using VerifyJob = ws_verify_job;
+using DraftJob = ws_draft_job;
+using VerifyOut = ws_verify_out;
+
+struct RoundJobs {
+  std::vector<VerifyJob> verify;
+  std::vector<TokenId> cands;
+  std::vector<DraftJob> draft;
+  void clear() {
+    verify.clear();
+    cands.clear();
+    draft.clear();
+  }
+};
+struct RoundResults {
+  std::vector<VerifyOut> verify;
+  std::vector<ws_pred> draft;
+};
+
+struct BackendStats {
+  std::uint64_t rounds = 0, launches = 0, verify_rows = 0, draft_rows = 0, h2d = 0, d2h = 0;
+  double kernel_ms = 0.0;
+};
+
+// The GPU side of one protocol thread. run_round must fill res.verify / res.draft in job order.
+class ModelBackend {
+ public:
+  virtual ~ModelBackend() = default;
+  virtual void run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode,
+                         std::uint64_t sample_seed) = 0;
+  BackendStats stats;
+};
+
+struct RequestOutput {
+  ws_request_metrics metrics{};
+  std::vector<TokenId> ctrl;
+  std::vector<TokenId> wrk;
+  std::vector<ws_step_log> steps;
+};
+
+// Runs the listed requests (global indices; table block = index) to completion through
+// `backend`, one batched round at a time. Throws ConfigError / std::logic_error like the
+// reference (sim.hpp:198, :200).
+void run_requests(const SimCfg& cfg, const std::uint32_t* requests, std::size_t n,
+                  ModelBackend& backend, RequestOutput* outs, bool log_steps);
+
+}  // namespace wsb
