@@ -148,6 +148,26 @@ def config2(verify=WS_VERIFY_GREEDY, num_requests=64, seed=1, max_nodes=256):
     return c
 
 
+def sim_cfg_from_dict(d):
+    """Inverse of the golden fixtures' config dicts."""
+    c = SimCfg()
+    for k, v in d.items():
+        if k == "oracle":
+            o = OracleCfg()
+            for kk, vv in v.items():
+                setattr(o, kk, vv)
+            c.oracle = o
+        else:
+            setattr(c, k, v)
+    return c
+
+
+def sim_cfg_to_dict(c):
+    d = {n: getattr(c, n) for n, _ in SimCfg._fields_ if n != "oracle"}
+    d["oracle"] = {n: getattr(c.oracle, n) for n, _ in OracleCfg._fields_}
+    return d
+
+
 class RunBuffers:
     """Caller-owned output buffers for ws_run_sim / ref_run_sim."""
 
