@@ -54,7 +54,7 @@ extern "C" {
 #define WS_MODE_WANSPEC 1
 
 /* TokenRecord (types.hpp:67-72) with the top-2 Prediction (types.hpp:56-63) the stochastic
- * oracle synthesizes (oracle.hpp:313-345). Fixed layout, 72 bytes. */
+ * oracle synthesizes (oracle.hpp:313-345). Fixed layout, 64 bytes. */
 typedef struct ws_token_record {
   uint32_t target_token;  /* == target top-1 */
   uint32_t target_top2;

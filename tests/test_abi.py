@@ -29,16 +29,29 @@ def declared_symbols():
 def test_exports_every_declared_symbol():
     L = ws.lib()
     syms = declared_symbols()
-    assert len(syms) >= 14
+    assert len(syms) >= 13
     for s in sorted(syms):
         assert hasattr(L, s), s
 
 
-def test_struct_sizes_match_header():
-    assert C.sizeof(abi.TokenRecord) == 72
-    assert C.sizeof(abi.Pred) == 40
-    assert C.sizeof(abi.OracleCfg) == 56
-    assert C.sizeof(abi.StepLog) == 48
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors == the C compiler's view of include/wanspec_b200.h."""
+    pairs = [("ws_token_record", abi.TokenRecord), ("ws_pred", abi.Pred),
+             ("ws_oracle_cfg", abi.OracleCfg), ("ws_sim_cfg", abi.SimCfg),
+             ("ws_request_metrics", abi.RequestMetrics), ("ws_step_log", abi.StepLog),
+             ("ws_run_out", abi.RunOut)]
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "wanspec_b200.h"\nint main(void){\n'
+                   + "".join(f'printf("%zu\\n", sizeof({n}));\n' for n, _ in pairs)
+                   + 'printf("%zu\\n", offsetof(ws_sim_cfg, oracle));\n'
+                   + 'printf("%zu\\n", offsetof(ws_run_out, kernel_ms));\nreturn 0;}\n')
+    exe = tmp_path / "sz"
+    import subprocess
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert out[:len(pairs)] == [C.sizeof(t) for _, t in pairs]
+    assert out[len(pairs)] == abi.SimCfg.oracle.offset
+    assert out[len(pairs) + 1] == abi.RunOut.kernel_ms.offset
 
 
 def test_abi_version():
