@@ -207,6 +207,15 @@ int ws_run_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
 /* Same, with tables already resident (ws_load_oracle) — the device-resident timing path. */
 int ws_run_sim_resident(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
 
+/* ---- device-pointer kernel entry points (the model path's building blocks) ----
+ * All pointers are device memory; `stream` is a cudaStream_t (NULL = legacy default). */
+#define WS_EPI_BF16 0    /* out bf16 = A·W^T */
+#define WS_EPI_ADD_F32 1 /* out fp32 += A·W^T (residual stream) */
+#define WS_EPI_SWIGLU 2  /* out bf16 = silu(gate)·up, W rows interleaved in 32-row gate/up blocks */
+/* K1: C[M,N] = A[M,K]·W[N,K]^T, bf16 operands, fp32 accumulation in TMEM (tcgen05 + TMA). */
+int ws_op_gemm_bf16(const void* A, const void* W, void* out, int M, int N, int K, int lda, int ldw,
+                    int ldo, int epi, int bn, void* stream);
+
 /* ---- host-logic seam (tests / alternative model providers) ----
  * The batched driver with the model round supplied by the caller instead of the GPU: one
  * callback per round receives every pending verify job and draft row, exactly what the K9

@@ -211,6 +211,17 @@ class CallbackBackend : public wsb::ModelBackend {
 
 }  // namespace
 
+namespace wsb {
+// Error mapping shared with capi_ops.cpp (device-pointer entry points).
+int ops_guarded_rc(const char* what, const std::exception& e) {
+  g_err = std::string(what) + ": " + e.what();
+  if (dynamic_cast<const ConfigError*>(&e)) return WS_ECONFIG;
+  if (dynamic_cast<const CudaError*>(&e)) return WS_ECUDA;
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return WS_EARG;
+  return WS_ELOGIC;
+}
+}  // namespace wsb
+
 extern "C" {
 
 int ws_abi_version(void) { return WS_ABI_VERSION; }

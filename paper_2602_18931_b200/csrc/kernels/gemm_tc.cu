@@ -1,0 +1,269 @@
+// K1 — dense projections of the verify / draft forward on the 5th-gen tensor cores.
+//
+//   C[M, N] = A[M, K] · W[N, K]^T      (bf16 in, fp32 accumulate in TMEM)
+//
+// A = activations (rows = verify/draft rows), W = a weight matrix in its natural [out, in]
+// (K-major) layout, so both operands are K-major and stream straight from HBM by TMA with the
+// 128-byte swizzle the UMMA descriptors expect. Warp-specialised, one output tile per CTA:
+//   warp 0      TMA producer (one elected lane) over a STAGES-deep smem ring (mbarriers)
+//   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma 128xBNx16)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
+// Epilogues: plain bf16 store (QKV, LM head), fp32 residual accumulate (O / down projections
+// add into the fp32 residual stream), SwiGLU (gate/up rows interleaved per BN/2 block).
+// Tiles are ordered M-fastest so all M-blocks of one weight tile run concurrently and each
+// weight byte crosses HBM once per GEMM (weights dominate the verify-step bytes).
+#include "gemm_tc.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "cuda_check.hpp"
+#include "sm100.cuh"
+
+namespace wsb {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256;
+};
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, void* __restrict__ out, int ldo) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~static_cast<std::uintptr_t>(1023));
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + C::STAGES * C::A_BYTES;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  std::uint64_t* empty = full + C::STAGES;
+  std::uint64_t* tmem_full = empty + C::STAGES;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tmem_full + 1);
+
+  const int m_blk = blockIdx.x, n_blk = blockIdx.y;
+  const int num_k = K / BK;
+  const std::uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      int stage = 0;
+      std::uint32_t phase = 0;
+      for (int kb = 0; kb < num_k; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+        tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      constexpr std::uint32_t idesc = idesc_bf16_f32(BM, BN);
+      int stage = 0;
+      std::uint32_t phase = 0;
+      for (int kb = 0; kb < num_k; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const std::uint64_t da = smem_desc_sw128(sA + stage * C::A_BYTES);
+        const std::uint64_t db = smem_desc_sw128(sB + stage * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)  // advance 16 elements = 32 B = 2 descriptor units
+          mma_bf16(tmem_base, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+        mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      mma_commit(tmem_full);
+    }
+  } else {  // epilogue warps 2..5 → TMEM lane groups (warp % 4)
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int grp = static_cast<int>(warp & 3);
+    const int row = m_blk * BM + grp * 32 + static_cast<int>(lane);
+    const std::uint32_t t_row = tmem_base + (static_cast<std::uint32_t>(grp * 32) << 16);
+    if constexpr (EPI == kEpiSwiGLU) {
+      // W rows interleaved in 32-row blocks [gate 0..31 | up 0..31 | gate 32..63 | ...]: TMEM
+      // column chunk 2j is gate and 2j+1 is up for output features f0 + 32j .. +31.
+      const int f0 = n_blk * (BN / 2);
+#pragma unroll 1
+      for (int c = 0; c < BN / 2; c += 32) {
+        std::uint32_t g[32], u[32];
+        tmem_ld32(t_row + 2 * c, g);
+        tmem_ld32(t_row + 2 * c + 32, u);
+        tmem_ld_wait();
+        if (row < M && f0 + c < N / 2) {
+          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + f0 + c;
+          alignas(16) __nv_bfloat162 v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float a0 = silu(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
+            const float a1 = silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
+            v[j] = __floats2bfloat162_rn(a0, a1);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
+        }
+      }
+    } else {
+      const int n0 = n_blk * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        std::uint32_t r[32];
+        tmem_ld32(t_row + c, r);
+        tmem_ld_wait();
+        if (row >= M || n0 + c >= N) continue;
+        if constexpr (EPI == kEpiBF16) {
+          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
+          alignas(16) __nv_bfloat162 v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+          if (n0 + c + 32 <= N) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
+          } else {
+            const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(v);
+            for (int j = 0; j < 32 && n0 + c + j < N; ++j) o[j] = vv[j];
+          }
+        } else {  // kEpiAddF32: out[row, n] += acc
+          float* o = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
+          if (n0 + c + 32 <= N) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 x = reinterpret_cast<float4*>(o)[q];
+              x.x += __uint_as_float(r[4 * q + 0]);
+              x.y += __uint_as_float(r[4 * q + 1]);
+              x.z += __uint_as_float(r[4 * q + 2]);
+              x.w += __uint_as_float(r[4 * q + 3]);
+              reinterpret_cast<float4*>(o)[q] = x;
+            }
+          } else {
+            for (int j = 0; j < 32 && n0 + c + j < N; ++j) o[j] += __uint_as_float(r[j]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D K-major bf16 tensor [rows, cols] (row stride ld elements), box = box_rows x 64, SW128.
+CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, std::uint64_t ld, std::uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
+template <int BN, int EPI>
+void launch(const GemmArgs& g, cudaStream_t st) {
+  using C = Cfg<BN>;
+  static bool attr_set = false;  // per-instantiation; benign race (idempotent)
+  if (!attr_set) {
+    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
+  const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, BN);
+  const int n_out = EPI == kEpiSwiGLU ? g.N : g.N;  // SwiGLU: N counts gate+up rows
+  dim3 grid((g.M + BM - 1) / BM, (n_out + BN - 1) / BN);
+  gemm_tn_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, g.out, g.ldo);
+  WS_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+int pick_bn(int M, int N) {
+  const int mblocks = (M + BM - 1) / BM;
+  // Enough CTAs to pull the weights at full HBM bandwidth (~2 waves of 148 SMs); big tiles when
+  // M alone fills the machine (better smem-bandwidth / MMA efficiency).
+  if (mblocks * ((N + 255) / 256) >= 2 * 148) return 256;
+  if (mblocks * ((N + 127) / 128) >= 148) return 128;
+  return 64;
+}
+
+void gemm_tn(const GemmArgs& g, cudaStream_t st) {
+  if (g.K % BK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
+  if (g.lda % 8 || g.ldw % 8) throw std::invalid_argument("gemm: leading dims must be multiples of 8");
+  int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
+  if (g.epi == kEpiSwiGLU && bn < 64) bn = 64;
+  switch (g.epi) {
+    case kEpiBF16:
+      if (bn == 256) return launch<256, kEpiBF16>(g, st);
+      if (bn == 128) return launch<128, kEpiBF16>(g, st);
+      return launch<64, kEpiBF16>(g, st);
+    case kEpiAddF32:
+      if (bn == 256) return launch<256, kEpiAddF32>(g, st);
+      if (bn == 128) return launch<128, kEpiAddF32>(g, st);
+      return launch<64, kEpiAddF32>(g, st);
+    case kEpiSwiGLU:
+      if (bn == 256) return launch<256, kEpiSwiGLU>(g, st);
+      if (bn == 128) return launch<128, kEpiSwiGLU>(g, st);
+      return launch<64, kEpiSwiGLU>(g, st);
+  }
+  throw std::invalid_argument("gemm: unknown epilogue");
+}
+
+}  // namespace wsb

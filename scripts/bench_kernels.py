@@ -1,0 +1,71 @@
+"""Kernel-level timings (CUDA events, warm, L2-flushed) for the model-path kernels.
+
+    python scripts/bench_kernels.py gemm
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2602_18931_b200 import ops  # noqa: E402
+
+PEAK_TF = 1634.9
+PEAK_GBS = 6544.3
+
+
+def timeit(fn, iters=20, flush=None):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(iters):
+        if flush is not None:
+            flush.fill_(0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    return tot / iters / 1e3
+
+
+def gemm():
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    res = []
+    for (M, N, K, name) in [(1280, 6144, 4096, "8B qkv"), (1280, 4096, 4096, "8B o"),
+                            (1280, 28672, 4096, "8B gate_up"), (1280, 4096, 14336, "8B down"),
+                            (1280, 128256, 4096, "8B lm_head"), (160, 28672, 4096, "8B gate_up R32"),
+                            (2304, 28672, 4096, "8B gate_up k8"), (1024, 16384, 2048, "1B gate_up")]:
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        for bn in (0, 64, 128, 256):
+            t = timeit(lambda: ops.gemm(A, W, out=out, bn=bn), flush=flush)
+            fl = 2.0 * M * N * K
+            by = 2.0 * (M * K + N * K + M * N)
+            rt = max(fl / (PEAK_TF * 1e12), by / (PEAK_GBS * 1e9))
+            res.append({"shape": name, "M": M, "N": N, "K": K, "bn": bn or ops_pick(M, N), "ms": t * 1e3,
+                        "tflops": fl / t / 1e12, "gbs": by / t / 1e9, "roofline_frac": rt / t})
+        t = timeit(lambda: torch.matmul(A, W.T), flush=flush)
+        res.append({"shape": name, "impl": "torch(cuBLAS)", "ms": t * 1e3, "tflops": 2.0 * M * N * K / t / 1e12})
+        del A, W, out
+    for r in res:
+        print(json.dumps(r))
+
+
+def ops_pick(M, N):
+    bm = (M + 127) // 128
+    if bm * ((N + 255) // 256) >= 296:
+        return 256
+    if bm * ((N + 127) // 128) >= 148:
+        return 128
+    return 64
+
+
+if __name__ == "__main__":
+    {"gemm": gemm}[sys.argv[1]]()
