@@ -207,20 +207,7 @@ int ws_run_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
 /* Same, with tables already resident (ws_load_oracle) — the device-resident timing path. */
 int ws_run_sim_resident(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
 
-/* ---- device-pointer kernel entry points (the model path's building blocks) ----
- * All pointers are device memory; `stream` is a cudaStream_t (NULL = legacy default). */
-#define WS_EPI_BF16 0    /* out bf16 = A·W^T */
-#define WS_EPI_ADD_F32 1 /* out fp32 += A·W^T (residual stream) */
-#define WS_EPI_SWIGLU 2  /* out bf16 = silu(gate)·up, W rows interleaved in 32-row gate/up blocks */
-/* K1: C[M,N] = A[M,K]·W[N,K]^T, bf16 operands, fp32 accumulation in TMEM (tcgen05 + TMA). */
-int ws_op_gemm_bf16(const void* A, const void* W, void* out, int M, int N, int K, int lda, int ldw,
-                    int ldo, int epi, int bn, void* stream);
-
-/* ---- host-logic seam (tests / alternative model providers) ----
- * The batched driver with the model round supplied by the caller instead of the GPU: one
- * callback per round receives every pending verify job and draft row, exactly what the K9
- * kernel receives. Used by the CPU test-suite to check the host state machines against the
- * reference without a GPU; ws_run_sim never falls back to it. */
+/* ---- batched job records (driver rounds, K9 kernel, model seam) ---- */
 typedef struct ws_verify_job {
   uint32_t seq;       /* request's table block */
   uint32_t k;
@@ -239,6 +226,33 @@ typedef struct ws_verify_out {
   uint32_t bonus;
   double final_entropy;
 } ws_verify_out;
+/* ---- device-pointer kernel entry points (the model path's building blocks) ----
+ * All pointers are device memory; `stream` is a cudaStream_t (NULL = legacy default). */
+#define WS_EPI_BF16 0    /* out bf16 = A·W^T */
+#define WS_EPI_ADD_F32 1 /* out fp32 += A·W^T (residual stream) */
+#define WS_EPI_SWIGLU 2  /* out bf16 = silu(gate)·up, W rows interleaved in 32-row gate/up blocks */
+/* K1: C[M,N] = A[M,K]·W[N,K]^T, bf16 operands, fp32 accumulation in TMEM (tcgen05 + TMA). */
+int ws_op_gemm_bf16(const void* A, const void* W, void* out, int M, int N, int K, int lda, int ldw,
+                    int ldo, int epi, int bn, void* stream);
+
+/* K3: per row of bf16 logits [rows, ld]: top-2 (id, prob) of softmax(x·inv_temp), ties to the
+ * lower id, and the entropy in nats (entropy_of semantics, oracle.hpp:21-33), fp32 reductions.
+ * out: ws_pred[rows]; stats (optional): float4[rows] = {max·cl, Z, cl, H}, cl = inv_temp·log2 e.
+ * workspace: >= ws_op_row_stats_workspace_bytes(), zero-filled once (self-resetting). */
+size_t ws_op_row_stats_workspace_bytes(uint32_t rows, uint32_t vocab, uint32_t n_req);
+int ws_op_row_stats_bf16(const void* logits, uint32_t rows, uint32_t vocab, uint32_t ld,
+                         float inv_temp, ws_pred* out, void* stats, void* workspace, void* stream);
+/* K3+K4: greedy verify over n_req groups of k+1 logits rows (row i of request j predicts
+ * position base_j + i): run_target_step (oracle.hpp:127-139) on the argmaxes, fused. */
+int ws_op_verify_greedy_bf16(const void* logits, uint32_t n_req, uint32_t k, uint32_t vocab,
+                             uint32_t ld, const uint32_t* cand, ws_verify_out* out,
+                             ws_pred* rows_out, void* workspace, void* stream);
+
+/* ---- host-logic seam (tests / alternative model providers) ----
+ * The batched driver with the model round supplied by the caller instead of the GPU: one
+ * callback per round receives every pending verify job and draft row, exactly what the K9
+ * kernel receives. Used by the CPU test-suite to check the host state machines against the
+ * reference without a GPU; ws_run_sim never falls back to it. */
 typedef int (*ws_model_round_fn)(void* user, uint32_t n_verify, const ws_verify_job* verify,
                                  const uint32_t* cands, uint32_t n_draft, const ws_draft_job* draft,
                                  ws_verify_out* verify_out, ws_pred* draft_out, int verify_mode,

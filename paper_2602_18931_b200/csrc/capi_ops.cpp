@@ -6,6 +6,7 @@
 
 #include "kernels/cuda_check.hpp"
 #include "kernels/gemm_tc.cuh"
+#include "kernels/rowstats.cuh"
 #include "wanspec_b200.h"
 
 namespace wsb {
@@ -32,6 +33,28 @@ int ws_op_gemm_bf16(const void* A, const void* W, void* out, int M, int N, int K
     if (!A || !W || !out || M <= 0 || N <= 0 || K <= 0) throw std::invalid_argument("gemm: bad argument");
     wsb::GemmArgs g{A, W, out, M, N, K, lda, ldw, ldo, epi, bn};
     wsb::gemm_tn(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
+size_t ws_op_row_stats_workspace_bytes(uint32_t rows, uint32_t vocab, uint32_t n_req) {
+  return wsb::rowstats_workspace_bytes(rows, vocab, n_req);
+}
+
+int ws_op_row_stats_bf16(const void* logits, uint32_t rows, uint32_t vocab, uint32_t ld, float inv_temp,
+                         ws_pred* out, void* stats, void* workspace, void* stream) {
+  return op_guarded("ws_op_row_stats_bf16", [&] {
+    wsb::row_stats_bf16(logits, rows, vocab, ld, inv_temp, out, static_cast<wsb::RowStats*>(stats), workspace, 0, 0,
+                        nullptr, nullptr, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ws_op_verify_greedy_bf16(const void* logits, uint32_t n_req, uint32_t k, uint32_t vocab, uint32_t ld,
+                             const uint32_t* cand, ws_verify_out* out, ws_pred* rows_out, void* workspace,
+                             void* stream) {
+  return op_guarded("ws_op_verify_greedy_bf16", [&] {
+    if (!rows_out || !cand || !out) throw std::invalid_argument("verify_greedy: null argument");
+    wsb::row_stats_bf16(logits, n_req * (k + 1), vocab, ld, 1.0f, rows_out, nullptr, workspace, n_req, k, cand, out,
+                        static_cast<cudaStream_t>(stream));
   });
 }
 

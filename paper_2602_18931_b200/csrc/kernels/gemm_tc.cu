@@ -236,12 +236,10 @@ void launch(const GemmArgs& g, cudaStream_t st) {
 }  // namespace
 
 int pick_bn(int M, int N) {
-  const int mblocks = (M + BM - 1) / BM;
-  // Enough CTAs to pull the weights at full HBM bandwidth (~2 waves of 148 SMs); big tiles when
-  // M alone fills the machine (better smem-bandwidth / MMA efficiency).
-  if (mblocks * ((N + 255) / 256) >= 2 * 148) return 256;
-  if (mblocks * ((N + 127) / 128) >= 148) return 128;
-  return 64;
+  // Measured on B200 (profiles/r01_gemm.md): 128x256 tiles win at every verify/draft shape,
+  // including 160-row (HBM-bound) ones — the wider tile halves A re-reads and per-tile overhead.
+  (void)M;
+  return N >= 256 ? 256 : (N >= 128 ? 128 : 64);
 }
 
 void gemm_tn(const GemmArgs& g, cudaStream_t st) {

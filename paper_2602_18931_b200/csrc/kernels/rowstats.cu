@@ -1,0 +1,284 @@
+// K3 — fused vocab-wide softmax + entropy + top-2 over bf16 logits, and the K4 greedy verify
+// epilogue fused behind it.
+//
+// Entropy semantics follow entropy_of (oracle.hpp:21-33): H = -sum p ln p in nats, computed in
+// one streaming pass as H = ln Z - S/Z with m = max, Z = sum e^(l-m), S = sum e^(l-m)(l-m)
+// (online rescaling when the running max grows), fp32 accumulation. Top-2 follows the
+// Prediction tie rule (types.hpp:54-55): descending value, ties to the lower id.
+//
+// Layout: grid (splits, rows); a CTA streams one fixed 32768-wide vocab chunk of one row with
+// 16-byte vector loads (4 in flight per thread), reduces warp → CTA, and the last CTA of a row
+// (atomic ticket) merges the chunk partials in chunk order → deterministic and batch-invariant.
+// With the verify epilogue enabled, the last row of a request to finish runs run_target_step
+// (oracle.hpp:127-139) on the argmaxes: accept while argmax(row i) == cand[i], bonus =
+// argmax(row a), final_entropy = H(row a). HBM-bound: rows*V*2 bytes read once.
+#include "rowstats.cuh"
+
+#include <cuda_bf16.h>
+
+#include <stdexcept>
+
+#include "cuda_check.hpp"
+
+namespace wsb {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct State {
+  float m, z, s;  // log2-domain running max, sum, sum e*d
+  float v1, v2;   // raw top-2 logits
+  std::uint32_t i1, i2;
+};
+
+__device__ __forceinline__ void init(State& a) {
+  a.m = -INFINITY;
+  a.z = 0.f;
+  a.s = 0.f;
+  a.v1 = a.v2 = -INFINITY;
+  a.i1 = a.i2 = 0xFFFFFFFFu;
+}
+
+__device__ __forceinline__ bool better(float v, std::uint32_t i, float w, std::uint32_t j) {
+  return v > w || (v == w && i < j);
+}
+
+__device__ __forceinline__ void insert(State& a, float v, std::uint32_t i) {
+  if (better(v, i, a.v2, a.i2)) {
+    if (better(v, i, a.v1, a.i1)) {
+      a.v2 = a.v1;
+      a.i2 = a.i1;
+      a.v1 = v;
+      a.i1 = i;
+    } else {
+      a.v2 = v;
+      a.i2 = i;
+    }
+  }
+}
+
+__device__ __forceinline__ void merge(State& a, const State& b) {
+  const float m = fmaxf(a.m, b.m);
+  float z = 0.f, s = 0.f;
+  if (a.z > 0.f) {
+    const float f = exp2f(a.m - m);
+    z += a.z * f;
+    s += f * (a.s + a.z * (a.m - m));
+  }
+  if (b.z > 0.f) {
+    const float f = exp2f(b.m - m);
+    z += b.z * f;
+    s += f * (b.s + b.z * (b.m - m));
+  }
+  a.m = m;
+  a.z = z;
+  a.s = s;
+  insert(a, b.v1, b.i1);
+  insert(a, b.v2, b.i2);
+}
+
+__device__ __forceinline__ State shfl_state(const State& a, int off) {
+  State b;
+  b.m = __shfl_xor_sync(0xffffffffu, a.m, off);
+  b.z = __shfl_xor_sync(0xffffffffu, a.z, off);
+  b.s = __shfl_xor_sync(0xffffffffu, a.s, off);
+  b.v1 = __shfl_xor_sync(0xffffffffu, a.v1, off);
+  b.v2 = __shfl_xor_sync(0xffffffffu, a.v2, off);
+  b.i1 = __shfl_xor_sync(0xffffffffu, a.i1, off);
+  b.i2 = __shfl_xor_sync(0xffffffffu, a.i2, off);
+  return b;
+}
+
+__device__ __forceinline__ void absorb8(State& a, const uint4& q, std::uint32_t id0, float cl) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+  float x[8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __bfloat1622float2(h[j]);
+    x[2 * j] = f.x;
+    x[2 * j + 1] = f.y;
+  }
+  float mx = x[0];
+#pragma unroll
+  for (int j = 1; j < 8; ++j) mx = fmaxf(mx, x[j]);
+  const float lm = mx * cl;
+  if (lm > a.m) {
+    if (a.z > 0.f) {
+      const float f = exp2f(a.m - lm);
+      a.s = f * (a.s + a.z * (a.m - lm));
+      a.z *= f;
+    }
+    a.m = lm;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float d = fmaf(x[j], cl, -a.m);
+    const float e = exp2f(d);
+    a.z += e;
+    a.s = fmaf(e, d, a.s);
+  }
+  if (mx >= a.v2) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) insert(a, x[j], id0 + j);
+  }
+}
+
+__device__ __forceinline__ void absorb1(State& a, float x, std::uint32_t id, float cl) {
+  const float l = x * cl;
+  if (l > a.m) {
+    if (a.z > 0.f) {
+      const float f = exp2f(a.m - l);
+      a.s = f * (a.s + a.z * (a.m - l));
+      a.z *= f;
+    }
+    a.m = l;
+  }
+  const float d = l - a.m;
+  const float e = exp2f(d);
+  a.z += e;
+  a.s = fmaf(e, d, a.s);
+  insert(a, x, id);
+}
+
+struct Partial {
+  float m, z, s, v1, v2;
+  std::uint32_t i1, i2, pad;
+};
+
+__device__ void finalize(const State& a, float cl, std::uint32_t vocab, ws_pred* pred, RowStats* st) {
+  const float lnz = logf(a.z);
+  float h = lnz - kLn2 * a.s / a.z;
+  if (h < 0.f) h = 0.f;
+  ws_pred p;
+  p.n = vocab >= 2 ? 2u : 1u;
+  p.id[0] = a.i1;
+  p.id[1] = vocab >= 2 ? a.i2 : 0u;
+  p.pad = 0;
+  p.prob[0] = static_cast<double>(exp2f(fmaf(a.v1, cl, -a.m)) / a.z);
+  p.prob[1] = vocab >= 2 ? static_cast<double>(exp2f(fmaf(a.v2, cl, -a.m)) / a.z) : 0.0;
+  p.entropy = static_cast<double>(h);
+  *pred = p;
+  if (st) *st = RowStats{a.m, a.z, cl, h};
+}
+
+__global__ void __launch_bounds__(kThreads) row_stats_kernel(
+    const __nv_bfloat16* __restrict__ logits, std::uint32_t vocab, std::uint32_t ld, float cl, bool vec_ok,
+    ws_pred* __restrict__ out_pred, RowStats* __restrict__ out_stats, Partial* __restrict__ partials,
+    std::uint32_t* __restrict__ row_ticket, std::uint32_t k, const std::uint32_t* __restrict__ cand,
+    ws_verify_out* __restrict__ vout, std::uint32_t* __restrict__ req_ticket) {
+  const std::uint32_t split = blockIdx.x, splits = gridDim.x, row = blockIdx.y;
+  const std::uint32_t lo = split * kRowChunk;
+  const std::uint32_t hi = min(vocab, lo + kRowChunk);
+  const __nv_bfloat16* x = logits + static_cast<std::size_t>(row) * ld;
+  State a;
+  init(a);
+  if (vec_ok) {
+    const uint4* v = reinterpret_cast<const uint4*>(x + lo);
+    const std::uint32_t nvec = (hi - lo) / 8;
+    std::uint32_t i = threadIdx.x;
+    for (; i + 3 * kThreads < nvec; i += 4 * kThreads) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = __ldcs(v + i + u * kThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) absorb8(a, q[u], lo + 8 * (i + u * kThreads), cl);
+    }
+    for (; i < nvec; i += kThreads) absorb8(a, __ldcs(v + i), lo + 8 * i, cl);
+    for (std::uint32_t t = lo + nvec * 8 + threadIdx.x; t < hi; t += kThreads)
+      absorb1(a, __bfloat162float(x[t]), t, cl);
+  } else {
+    for (std::uint32_t t = lo + threadIdx.x; t < hi; t += kThreads) absorb1(a, __bfloat162float(x[t]), t, cl);
+  }
+  // warp → CTA reduction (fixed order → deterministic)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const State b = shfl_state(a, off);
+    merge(a, b);
+  }
+  __shared__ State warp_states[kThreads / 32];
+  __shared__ bool is_last;
+  const std::uint32_t w = threadIdx.x / 32;
+  if ((threadIdx.x & 31) == 0) warp_states[w] = a;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  State r = warp_states[0];
+  for (int q = 1; q < kThreads / 32; ++q) merge(r, warp_states[q]);
+
+  if (splits > 1) {
+    partials[row * splits + split] = Partial{r.m, r.z, r.s, r.v1, r.v2, r.i1, r.i2, 0};
+    __threadfence();
+    const std::uint32_t t = atomicAdd(&row_ticket[row], 1u);
+    is_last = t == splits - 1;
+    if (!is_last) return;
+    __threadfence();
+    init(r);
+    for (std::uint32_t q = 0; q < splits; ++q) {  // chunk order: deterministic
+      const Partial* p = &partials[row * splits + q];
+      State b;
+      b.m = __ldcg(&p->m);
+      b.z = __ldcg(&p->z);
+      b.s = __ldcg(&p->s);
+      b.v1 = __ldcg(&p->v1);
+      b.v2 = __ldcg(&p->v2);
+      b.i1 = __ldcg(&p->i1);
+      b.i2 = __ldcg(&p->i2);
+      merge(r, b);
+    }
+    row_ticket[row] = 0;  // self-reset for the next launch
+  }
+  finalize(r, cl, vocab, &out_pred[row], out_stats ? &out_stats[row] : nullptr);
+
+  if (cand) {  // K4 greedy epilogue: the last finished row of the request runs the walk
+    const std::uint32_t req = row / (k + 1);
+    __threadfence();
+    const std::uint32_t t = atomicAdd(&req_ticket[req], 1u);
+    if (t != k) return;
+    __threadfence();
+    req_ticket[req] = 0;
+    const ws_pred* rows = out_pred + static_cast<std::size_t>(req) * (k + 1);
+    std::uint32_t acc = 0;
+    while (acc < k && __ldcg(&rows[acc].id[0]) == cand[static_cast<std::size_t>(req) * k + acc]) ++acc;
+    ws_verify_out o;
+    o.accepted = acc;
+    o.bonus = __ldcg(&rows[acc].id[0]);
+    o.final_entropy = __ldcg(&rows[acc].entropy);
+    vout[req] = o;
+  }
+}
+
+}  // namespace
+
+std::size_t rowstats_workspace_bytes(std::uint32_t rows, std::uint32_t vocab, std::uint32_t n_req) {
+  const std::uint32_t splits = (vocab + kRowChunk - 1) / kRowChunk;
+  return static_cast<std::size_t>(rows) * splits * sizeof(Partial) + static_cast<std::size_t>(rows) * 4 +
+         static_cast<std::size_t>(n_req) * 4 + 64;
+}
+
+void row_stats_bf16(const void* logits, std::uint32_t rows, std::uint32_t vocab, std::uint32_t ld, float inv_temp,
+                    ws_pred* out_pred, RowStats* out_stats, void* workspace, std::uint32_t n_req, std::uint32_t k,
+                    const std::uint32_t* cand, ws_verify_out* verify_out, cudaStream_t stream) {
+  if (rows == 0) return;
+  if (!logits || !out_pred || vocab == 0 || ld < vocab) throw std::invalid_argument("row_stats: bad argument");
+  if (!(inv_temp > 0.f)) throw std::invalid_argument("row_stats: temperature must be > 0");
+  if (cand && (rows != n_req * (k + 1) || !verify_out)) throw std::invalid_argument("row_stats: verify shape");
+  const std::uint32_t splits = (vocab + kRowChunk - 1) / kRowChunk;
+  if (splits > 1 || cand) {
+    if (!workspace) throw std::invalid_argument("row_stats: workspace required");
+  }
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  Partial* partials = reinterpret_cast<Partial*>(ws);
+  std::uint32_t* row_ticket =
+      reinterpret_cast<std::uint32_t*>(ws + static_cast<std::size_t>(rows) * splits * sizeof(Partial));
+  std::uint32_t* req_ticket = row_ticket + rows;
+  const bool vec_ok = (reinterpret_cast<std::uintptr_t>(logits) % 16 == 0) && (ld % 8 == 0);
+  dim3 grid(splits, rows);
+  row_stats_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const __nv_bfloat16*>(logits), vocab, ld,
+                                                  inv_temp * kLog2e, vec_ok, out_pred, out_stats, partials,
+                                                  row_ticket, k, cand, verify_out, req_ticket);
+  WS_CUDA(cudaGetLastError());
+}
+
+}  // namespace wsb

@@ -58,6 +58,29 @@ def gemm():
         print(json.dumps(r))
 
 
+def rowstats():
+    import ctypes as C
+    import paper_2602_18931_b200 as ws
+    L = ws.lib()
+    L.ws_op_row_stats_workspace_bytes.restype = C.c_size_t
+    L.ws_op_row_stats_workspace_bytes.argtypes = [C.c_uint32] * 3
+    L.ws_op_row_stats_bf16.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    for rows, V in [(1280, 128256), (2304, 128256), (160, 128256), (1024, 128256), (4096, 32768)]:
+        x = (torch.randn(rows, V, device="cuda") * 2).to(torch.bfloat16)
+        wsb = torch.zeros(L.ws_op_row_stats_workspace_bytes(rows, V, 0), dtype=torch.uint8, device="cuda")
+        out = torch.zeros(rows * 40, dtype=torch.uint8, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+
+        def fn():
+            L.ws_op_row_stats_bf16(x.data_ptr(), rows, V, V, 1.0, out.data_ptr(), None, wsb.data_ptr(), st)
+        t = timeit(fn, flush=flush)
+        by = rows * V * 2 + rows * 40
+        print(json.dumps({"kernel": "row_stats_bf16", "rows": rows, "V": V, "ms": t * 1e3,
+                          "gbs": by / t / 1e9, "frac_hbm": by / t / 1e9 / PEAK_GBS}))
+
+
 def ops_pick(M, N):
     bm = (M + 127) // 128
     if bm * ((N + 255) // 256) >= 296:
@@ -68,4 +91,4 @@ def ops_pick(M, N):
 
 
 if __name__ == "__main__":
-    {"gemm": gemm}[sys.argv[1]]()
+    {"gemm": gemm, "rowstats": rowstats}[sys.argv[1]]()
