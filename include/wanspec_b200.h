@@ -248,6 +248,46 @@ int ws_op_verify_greedy_bf16(const void* logits, uint32_t n_req, uint32_t k, uin
                              uint32_t ld, const uint32_t* cand, ws_verify_out* out,
                              ws_pred* rows_out, void* workspace, void* stream);
 
+/* ---- real-model pair (BASELINE config 3): Llama-shape target + draft on one GPU ----
+ * Random-init bf16 weights of the named shapes ("llama3-8b", "llama3.2-1b", "tiny", ...),
+ * prompts of prompt_len seeded tokens, and a planted shared bigram bias (a seeded hash of the
+ * input token receives +plant logits; the draft sees it for draft_plant_rate of input tokens)
+ * so draft and target agree at a controllable rate. Generation is capped like the tiny pair:
+ * rows predicting committed index >= sequence_length-1 emit EOS with probability 1. */
+typedef struct ws_model_cfg {
+  const char* target;
+  const char* draft;
+  uint64_t seed;
+  uint32_t prompt_len;
+  uint32_t max_requests;
+  uint32_t max_ctx;
+  uint32_t trie_slots;
+  float plant_target;
+  float plant_draft;
+  float draft_plant_rate;
+  uint32_t pad;
+} ws_model_cfg;
+int ws_model_load(ws_ctx* ctx, const ws_model_cfg* cfg);
+/* run_sim_full (sim.hpp:429-442) with the verify / draft model calls on the loaded models;
+ * cfg->oracle supplies vocab_size (must equal the models'), eos_id and sequence_length. */
+int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
+/* model-step timing of the last ws_run_model_sim: device ms and rows fed per model */
+int ws_model_stats(ws_ctx* ctx, double* target_ms, double* draft_ms, uint64_t* target_rows,
+                   uint64_t* draft_rows, uint64_t* target_forwards, uint64_t* draft_forwards);
+
+/* single-model forward surface (tests): rows (token, position, KV slot), attention groups
+ * {row0, n_rows, prefix_slot, prefix_len, extra_off, extra_len} (6 int32 each) over the slot
+ * pool, logits of out_rows → logits_out (device bf16 [n_out, vocab]). */
+typedef struct ws_model ws_model;
+int ws_model_create(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device,
+                    ws_model** out);
+int ws_model_destroy(ws_model* m);
+int ws_model_copy_weight(ws_model* m, const char* which, int layer, void* dst_dev, int64_t numel);
+int ws_model_forward(ws_model* m, int n_rows, const int32_t* tok, const int32_t* pos,
+                     const int32_t* slot, int n_groups, const int32_t* groups, int n_extra,
+                     const int32_t* extra, int n_out, const int32_t* out_rows, void* logits_out,
+                     void* stream);
+
 /* ---- host-logic seam (tests / alternative model providers) ----
  * The batched driver with the model round supplied by the caller instead of the GPU: one
  * callback per round receives every pending verify job and draft row, exactly what the K9

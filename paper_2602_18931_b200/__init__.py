@@ -65,6 +65,10 @@ def lib():
     L.ws_run_sim.argtypes = [C.c_void_p, _P(abi.SimCfg), _P(abi.RunOut)]
     L.ws_run_sim_resident.argtypes = [C.c_void_p, _P(abi.SimCfg), _P(abi.RunOut)]
     L.ws_run_sim_with_model.argtypes = [_P(abi.SimCfg), MODEL_ROUND_FN, C.c_void_p, _P(abi.RunOut)]
+    L.ws_model_load.argtypes = [C.c_void_p, _P(abi.ModelCfg)]
+    L.ws_run_model_sim.argtypes = [C.c_void_p, _P(abi.SimCfg), _P(abi.RunOut)]
+    L.ws_model_stats.argtypes = [C.c_void_p, _P(C.c_double), _P(C.c_double), _P(C.c_uint64), _P(C.c_uint64),
+                                 _P(C.c_uint64), _P(C.c_uint64)]
     _lib = L
     return L
 
@@ -151,6 +155,24 @@ class Context:
         out = (abi.Pred * n)()
         _check(lib().ws_draft(self._h, n, s, p, out))
         return [(o.n, tuple(o.id[:o.n]), tuple(o.prob[:o.n]), o.entropy) for o in out]
+
+    # -- real-model pair (config 3) --
+    def load_models(self, mcfg):
+        """Allocate + seed-initialise the target/draft models and their KV pools on this GPU."""
+        self._mcfg = mcfg  # keep the C strings alive
+        _check(lib().ws_model_load(self._h, C.byref(mcfg)))
+
+    def run_model_sim(self, cfg, with_tokens=True, with_steps=True):
+        """run_sim_full with the verify/draft model calls on the loaded models."""
+        bufs = abi.RunBuffers(cfg, with_tokens, with_steps)
+        _check(lib().ws_run_model_sim(self._h, C.byref(cfg), C.byref(bufs.out)))
+        return bufs
+
+    def model_stats(self):
+        v = [C.c_double(), C.c_double(), C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()]
+        _check(lib().ws_model_stats(self._h, *[C.byref(x) for x in v]))
+        keys = ("target_ms", "draft_ms", "target_rows", "draft_rows", "target_forwards", "draft_forwards")
+        return {k: x.value for k, x in zip(keys, v)}
 
     # -- whole runs --
     def run_sim_full(self, cfg, with_tokens=True, with_steps=True, resident=False):

@@ -90,6 +90,31 @@ class RunOut(C.Structure):
     ]
 
 
+class ModelCfg(C.Structure):
+    _fields_ = [("target", C.c_char_p), ("draft", C.c_char_p), ("seed", C.c_uint64),
+                ("prompt_len", C.c_uint32), ("max_requests", C.c_uint32), ("max_ctx", C.c_uint32),
+                ("trie_slots", C.c_uint32), ("plant_target", C.c_float), ("plant_draft", C.c_float),
+                ("draft_plant_rate", C.c_float), ("pad", C.c_uint32)]
+
+
+def model_cfg(target="llama3-8b", draft="llama3.2-1b", seed=1, prompt_len=128, max_requests=256,
+              max_ctx=256, trie_slots=512, plant_target=16.0, plant_draft=16.0, draft_plant_rate=0.8):
+    """The config-3 model pair (random-init Llama shapes + planted shared bigram bias)."""
+    return ModelCfg(target.encode(), draft.encode(), seed, prompt_len, max_requests, max_ctx, trie_slots,
+                    plant_target, plant_draft, draft_plant_rate, 0)
+
+
+LLAMA_VOCAB = 128256
+LLAMA_EOS = 128001
+
+
+def config3(num_requests=256, k=4, seq_len=100, vocab=LLAMA_VOCAB, eos=LLAMA_EOS):
+    """BASELINE configs[2]: 256 requests, k in {4, 8}, b=2, s=4, theta=phi=0.5, RTT 20 ms,
+    100 generated tokens; max_nodes=256 as config 2."""
+    return apply_stage(sim_cfg(k=k, rtt=20000, num_requests=num_requests, max_nodes=256,
+                               vocab_size=vocab, eos_id=eos, sequence_length=seq_len), "full")
+
+
 def oracle_cfg(seed=1, vocab_size=32768, eos_id=32767, match_prob=0.8, entropy_low=0.3,
                entropy_high=1.5, second_correct_prob=0.3, sequence_length=100):
     """OracleConfig defaults (oracle.hpp:37-47)."""

@@ -17,17 +17,7 @@
 #include "kernels/cuda_check.hpp"
 #include "kernels/k9_oracle.cuh"
 
-struct ws_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  wsb::DevTables tables;
-  std::vector<std::unique_ptr<wsb::OracleLane>> lanes;
-
-  wsb::OracleLane& lane(std::size_t i) {
-    while (lanes.size() <= i) lanes.emplace_back(new wsb::OracleLane(&tables, device));
-    return *lanes[i];
-  }
-};
+#include "context.hpp"
 
 namespace {
 
@@ -219,6 +209,14 @@ int ops_guarded_rc(const char* what, const std::exception& e) {
   if (dynamic_cast<const CudaError*>(&e)) return WS_ECUDA;
   if (dynamic_cast<const std::invalid_argument*>(&e)) return WS_EARG;
   return WS_ELOGIC;
+}
+SimCfg sim_cfg_from_abi(const ws_sim_cfg& c) {
+  SimCfg s = to_cfg(c);
+  check_shard(&c);
+  return s;
+}
+void run_shard(const ws_sim_cfg* c, const SimCfg& cfg, ModelBackend& backend, ws_run_out* out, int device) {
+  execute(c, cfg, 1, [&](std::uint32_t) -> ModelBackend& { return backend; }, out, device);
 }
 }  // namespace wsb
 

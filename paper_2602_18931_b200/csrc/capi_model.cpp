@@ -1,0 +1,143 @@
+// C ABI of the real-model path (include/wanspec_b200.h "real-model pair").
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "context.hpp"
+#include "kernels/cuda_check.hpp"
+#include "model/llama.hpp"
+#include "model/model_backend.hpp"
+#include "wanspec_b200.h"
+
+struct ws_model {
+  std::unique_ptr<wsb::LlamaModel> m;
+  int device = 0;
+};
+
+namespace {
+template <class F>
+int guard(const char* what, F&& f) {
+  try {
+    f();
+    return WS_OK;
+  } catch (const std::exception& e) {
+    return wsb::ops_guarded_rc(what, e);
+  }
+}
+struct LastStats {
+  double target_ms = 0, draft_ms = 0;
+  std::uint64_t target_rows = 0, draft_rows = 0, target_forwards = 0, draft_forwards = 0;
+};
+LastStats g_last;
+}  // namespace
+
+extern "C" {
+
+int ws_model_load(ws_ctx* ctx, const ws_model_cfg* c) {
+  return guard("ws_model_load", [&] {
+    if (!ctx || !c || !c->target || !c->draft) throw std::invalid_argument("null argument");
+    wsb::ModelPairCfg m;
+    m.target = c->target;
+    m.draft = c->draft;
+    m.seed = c->seed;
+    if (c->prompt_len) m.prompt_len = c->prompt_len;
+    if (c->max_requests) m.max_requests = c->max_requests;
+    if (c->max_ctx) m.max_ctx = c->max_ctx;
+    if (c->trie_slots) m.trie_slots = c->trie_slots;
+    m.plant_target = c->plant_target;
+    m.plant_draft = c->plant_draft;
+    m.draft_plant_rate = c->draft_plant_rate;
+    if (m.prompt_len < 1) throw wsb::ConfigError("prompt_len must be >= 1");
+    WS_CUDA(cudaSetDevice(ctx->device));
+    ctx->models.reset();
+    ctx->models.reset(new wsb::ModelPair(m, ctx->device));
+  });
+}
+
+int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
+  return guard("ws_run_model_sim", [&] {
+    if (!ctx || !c) throw std::invalid_argument("null argument");
+    if (!ctx->models) throw wsb::ConfigError("no model loaded (ws_model_load)");
+    const wsb::SimCfg cfg = wsb::sim_cfg_from_abi(*c);
+    wsb::ModelPair& mp = *ctx->models;
+    const auto& mc = mp.cfg();
+    if (c->oracle.vocab_size != static_cast<std::uint32_t>(mp.target().shape().vocab))
+      throw wsb::ConfigError("oracle.vocab_size must equal the model vocabulary");
+    if (c->num_requests > mc.max_requests) throw wsb::ConfigError("num_requests exceeds the loaded max_requests");
+    if (mc.prompt_len + c->oracle.sequence_length + c->k + 2 > mc.max_ctx)
+      throw wsb::ConfigError("prompt + sequence_length + k exceeds max_ctx");
+    WS_CUDA(cudaSetDevice(ctx->device));
+    mp.reset_requests();
+    wsb::ModelBackend_Llama backend(&mp, c->oracle.sequence_length, c->oracle.eos_id, c->k);
+    wsb::run_shard(c, cfg, backend, out, ctx->device);
+    g_last = LastStats{backend.target_ms, backend.draft_ms, backend.target_rows, backend.draft_rows_fed,
+                       backend.target_forwards, backend.draft_forwards};
+  });
+}
+
+int ws_model_stats(ws_ctx*, double* target_ms, double* draft_ms, uint64_t* target_rows, uint64_t* draft_rows,
+                   uint64_t* target_forwards, uint64_t* draft_forwards) {
+  if (target_ms) *target_ms = g_last.target_ms;
+  if (draft_ms) *draft_ms = g_last.draft_ms;
+  if (target_rows) *target_rows = g_last.target_rows;
+  if (draft_rows) *draft_rows = g_last.draft_rows;
+  if (target_forwards) *target_forwards = g_last.target_forwards;
+  if (draft_forwards) *draft_forwards = g_last.draft_forwards;
+  return WS_OK;
+}
+
+int ws_model_create(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device, ws_model** out) {
+  return guard("ws_model_create", [&] {
+    if (!shape || !out || n_slots <= 0) throw std::invalid_argument("bad argument");
+    auto h = std::make_unique<ws_model>();
+    h->device = device;
+    h->m.reset(new wsb::LlamaModel(wsb::shape_by_name(shape), seed, n_slots, max_rows > 0 ? max_rows : 64, device));
+    *out = h.release();
+  });
+}
+
+int ws_model_destroy(ws_model* m) {
+  delete m;
+  return WS_OK;
+}
+
+int ws_model_copy_weight(ws_model* m, const char* which, int layer, void* dst, int64_t numel) {
+  return guard("ws_model_copy_weight", [&] {
+    std::int64_t n = 0;
+    void* src = m->m->weight(which, layer, &n);
+    if (n != numel) throw std::invalid_argument("numel mismatch: expected " + std::to_string(n));
+    WS_CUDA(cudaMemcpy(dst, src, static_cast<std::size_t>(n) * 2, cudaMemcpyDeviceToDevice));
+  });
+}
+
+int ws_model_forward(ws_model* m, int n_rows, const int32_t* tok, const int32_t* pos, const int32_t* slot,
+                     int n_groups, const int32_t* groups, int n_extra, const int32_t* extra, int n_out,
+                     const int32_t* out_rows, void* logits_out, void* stream) {
+  return guard("ws_model_forward", [&] {
+    if (!m || n_rows <= 0 || !tok || !pos || !slot || !groups || n_groups <= 0) throw std::invalid_argument("bad argument");
+    WS_CUDA(cudaSetDevice(m->device));
+    wsb::ForwardBatch b;
+    b.tok.assign(tok, tok + n_rows);
+    b.pos.assign(pos, pos + n_rows);
+    b.slot.assign(slot, slot + n_rows);
+    for (int g = 0; g < n_groups; ++g) {
+      const int32_t* q = groups + 6 * g;
+      b.groups.push_back(wsb::AttnGroup{q[0], q[1], q[2], q[3], q[4], q[5]});
+    }
+    if (n_extra > 0) b.extra.assign(extra, extra + n_extra);
+    if (n_out > 0) b.out_rows.assign(out_rows, out_rows + n_out);
+    for (int i = 0; i < n_rows; ++i)
+      if (slot[i] < 0 || slot[i] >= m->m->n_slots()) throw std::invalid_argument("slot out of range");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    m->m->forward(b, 0.f, st);
+    if (n_out > 0 && logits_out)
+      WS_CUDA(cudaMemcpyAsync(logits_out, m->m->logits(),
+                              static_cast<std::size_t>(n_out) * m->m->shape().vocab * 2, cudaMemcpyDeviceToDevice, st));
+    WS_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

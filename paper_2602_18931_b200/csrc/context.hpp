@@ -1,0 +1,30 @@
+// ws_ctx: one GPU's hot-path state (tiny-pair tables + lanes, optional real-model pair).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "kernels/k9_oracle.cuh"
+#include "model/model_backend.hpp"
+
+struct ws_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  wsb::DevTables tables;
+  std::vector<std::unique_ptr<wsb::OracleLane>> lanes;
+  std::unique_ptr<wsb::ModelPair> models;
+
+  wsb::OracleLane& lane(std::size_t i) {
+    while (lanes.size() <= i) lanes.emplace_back(new wsb::OracleLane(&tables, device));
+    return *lanes[i];
+  }
+};
+
+namespace wsb {
+int ops_guarded_rc(const char* what, const std::exception& e);
+// Shared by capi.cpp / capi_model.cpp: SimConfig validation + conversion and the shard runner.
+SimCfg sim_cfg_from_abi(const ws_sim_cfg& c);
+void run_shard(const ws_sim_cfg* c, const SimCfg& cfg, ModelBackend& backend, ws_run_out* out, int device);
+}  // namespace wsb

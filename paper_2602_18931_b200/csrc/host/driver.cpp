@@ -297,6 +297,12 @@ class RequestRun {
         j.cand_off = static_cast<std::uint32_t>(jobs_->cands.size());
         jobs_->cands.insert(jobs_->cands.end(), target_.tokens.begin(), target_.tokens.end());
         jobs_->verify.push_back(j);
+        if (jobs_->want_ctx) {  // committed output (stable until this verify folds)
+          jobs_->verify_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jobs_->ctx_tokens.size()),
+                                             static_cast<std::uint32_t>(ctrl_.committed.size()),
+                                             static_cast<std::uint32_t>(ctrl_.committed.size()), kJobVerify});
+          jobs_->ctx_tokens.insert(jobs_->ctx_tokens.end(), ctrl_.committed.begin(), ctrl_.committed.end());
+        }
         verify_slots_->push_back(this);
         target_ready_ = false;
         schedule(now_ + ccfg_.t_target, EvKind::target_done);
@@ -308,6 +314,12 @@ class RequestRun {
         std::swap(local_, action_.local);
         jobs_->draft.push_back(DraftJob{static_cast<std::uint32_t>(request_id_), 0, local_.anchor});
         draft_slots_->push_back({this, kLocalSlot});
+        if (jobs_->want_ctx) {  // plan.context = committed + leaf path (controller.hpp:200-201)
+          jobs_->draft_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jobs_->ctx_tokens.size()),
+                                            static_cast<std::uint32_t>(local_.context.size()),
+                                            static_cast<std::uint32_t>(ctrl_.committed.size()), kJobCtrlDraft});
+          jobs_->ctx_tokens.insert(jobs_->ctx_tokens.end(), local_.context.begin(), local_.context.end());
+        }
         local_ready_ = false;
         schedule(now_ + static_cast<SimTime>(local_.passes()) * ccfg_.t_draft, EvKind::ctrl_draft_done);
         launched = true;
@@ -333,6 +345,14 @@ class RequestRun {
     for (std::size_t i = 0; i < worker_leaves_.size(); ++i) {
       jobs_->draft.push_back(DraftJob{static_cast<std::uint32_t>(request_id_), 0, worker_leaves_[i].anchor});
       draft_slots_->push_back({this, static_cast<std::uint32_t>(i)});
+      if (jobs_->want_ctx) {  // worker committed + path_tokens(leaf)
+        wrk_.tree.path_tokens(worker_leaves_[i].id, path_tmp_);
+        jobs_->draft_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jobs_->ctx_tokens.size()),
+                                          static_cast<std::uint32_t>(wrk_.committed.size() + path_tmp_.size()),
+                                          static_cast<std::uint32_t>(wrk_.committed.size()), kJobWorkerDraft});
+        jobs_->ctx_tokens.insert(jobs_->ctx_tokens.end(), wrk_.committed.begin(), wrk_.committed.end());
+        jobs_->ctx_tokens.insert(jobs_->ctx_tokens.end(), path_tmp_.begin(), path_tmp_.end());
+      }
     }
     worker_ready_ = worker_leaves_.empty();
     schedule(now_ + wcfg_.t_draft, EvKind::worker_draft_done);
@@ -389,6 +409,7 @@ class RequestRun {
   bool worker_ready_ = false;
 
   std::vector<ws_step_log> steps_;
+  std::vector<TokenId> path_tmp_;
 };
 
 }  // namespace
@@ -407,6 +428,7 @@ void run_requests(const SimCfg& cfg, const std::uint32_t* requests, std::size_t 
   std::vector<std::size_t> active(n);
   for (std::size_t i = 0; i < n; ++i) active[i] = i;
   RoundJobs jobs;
+  jobs.want_ctx = backend.wants_context();
   RoundResults res;
   while (!active.empty()) {
     jobs.clear();

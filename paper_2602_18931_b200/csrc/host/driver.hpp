@@ -42,14 +42,28 @@ using VerifyJob = ws_verify_job;
 using DraftJob = ws_draft_job;
 using VerifyOut = ws_verify_out;
 
+// Context of a job for context-dependent (real) models: tokens ctx_tokens[off, off+len) are the
+// model input after the prompt (committed tokens, then the speculative path for drafts);
+// the first n_committed of them are committed.
+enum JobKind : std::uint32_t { kJobVerify = 0, kJobCtrlDraft = 1, kJobWorkerDraft = 2 };
+struct JobCtx {
+  std::uint32_t off, len, n_committed, kind;
+};
+
 struct RoundJobs {
   std::vector<VerifyJob> verify;
   std::vector<TokenId> cands;
   std::vector<DraftJob> draft;
+  bool want_ctx = false;  // set by backends that need contexts (real models)
+  std::vector<JobCtx> verify_ctx, draft_ctx;
+  std::vector<TokenId> ctx_tokens;
   void clear() {
     verify.clear();
     cands.clear();
     draft.clear();
+    verify_ctx.clear();
+    draft_ctx.clear();
+    ctx_tokens.clear();
   }
 };
 struct RoundResults {
@@ -68,6 +82,7 @@ class ModelBackend {
   virtual ~ModelBackend() = default;
   virtual void run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode,
                          std::uint64_t sample_seed) = 0;
+  virtual bool wants_context() const { return false; }
   BackendStats stats;
 };
 

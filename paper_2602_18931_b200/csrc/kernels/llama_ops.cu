@@ -1,0 +1,363 @@
+// Model-plumbing kernels: embedding gather, RMSNorm, RoPE + KV append, grouped GQA attention,
+// planted bias, slot copies, Philox weight init. All HBM/latency bound; vectorised 16-byte
+// accesses where the layout allows.
+#include "llama_ops.cuh"
+
+#include <cuda_bf16.h>
+
+#include <stdexcept>
+
+#include "cuda_check.hpp"
+
+namespace wsb {
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const std::int32_t* __restrict__ tok, int d,
+                             float* __restrict__ x) {
+  const int row = blockIdx.x;
+  const __nv_bfloat16* e = emb + static_cast<std::size_t>(tok[row]) * d;
+  float* o = x + static_cast<std::size_t>(row) * d;
+  for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(e + i));
+    o[i] = f.x;
+    o[i + 1] = f.y;
+  }
+}
+
+__global__ void rmsnorm_kernel(const float* __restrict__ x, int ld_x, const std::int32_t* __restrict__ idx,
+                               const __nv_bfloat16* __restrict__ w, float eps, int d, __nv_bfloat16* __restrict__ y,
+                               int ld_y) {
+  const int row = blockIdx.x;
+  const int src = idx ? idx[row] : row;
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<std::size_t>(src) * ld_x);
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = xr[i];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / static_cast<float>(d) + eps);
+  __nv_bfloat162* yr = reinterpret_cast<__nv_bfloat162*>(y + static_cast<std::size_t>(row) * ld_y);
+  const __nv_bfloat162* wr = reinterpret_cast<const __nv_bfloat162*>(w);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = xr[i];
+    const float2 w0 = __bfloat1622float2(wr[2 * i]);
+    const float2 w1 = __bfloat1622float2(wr[2 * i + 1]);
+    yr[2 * i] = __floats2bfloat162_rn(v.x * r * w0.x, v.y * r * w0.y);
+    yr[2 * i + 1] = __floats2bfloat162_rn(v.z * r * w1.x, v.w * r * w1.y);
+  }
+}
+
+// One thread per (row, head, rotation pair i < hd/2): dims i and i + hd/2 (rotate-half).
+__global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int nq, int nkv, int hd,
+                                   const std::int32_t* __restrict__ pos, const std::int32_t* __restrict__ slot,
+                                   const float* __restrict__ inv_freq, __nv_bfloat16* __restrict__ q_out,
+                                   __nv_bfloat16* __restrict__ k_pool, __nv_bfloat16* __restrict__ v_pool) {
+  const int row = blockIdx.x;
+  const int half = hd / 2;
+  const int heads = nq + 2 * nkv;
+  const __nv_bfloat16* src = qkv + static_cast<std::size_t>(row) * heads * hd;
+  const float p = static_cast<float>(pos[row]);
+  const std::size_t sbase = static_cast<std::size_t>(slot[row]) * nkv * hd;
+  for (int t = threadIdx.x; t < heads * half; t += blockDim.x) {
+    const int h = t / half, i = t % half;
+    const float a = __bfloat162float(src[h * hd + i]);
+    const float b = __bfloat162float(src[h * hd + i + half]);
+    if (h >= nq + nkv) {  // V: plain copy
+      const std::size_t o = sbase + static_cast<std::size_t>(h - nq - nkv) * hd;
+      v_pool[o + i] = src[h * hd + i];
+      v_pool[o + i + half] = src[h * hd + i + half];
+      continue;
+    }
+    float sn, cs;
+    sincosf(p * inv_freq[i], &sn, &cs);
+    const float r0 = a * cs - b * sn;
+    const float r1 = b * cs + a * sn;
+    if (h < nq) {
+      __nv_bfloat16* o = q_out + (static_cast<std::size_t>(row) * nq + h) * hd;
+      o[i] = __float2bfloat16(r0);
+      o[i + half] = __float2bfloat16(r1);
+    } else {
+      __nv_bfloat16* o = k_pool + sbase + static_cast<std::size_t>(h - nq) * hd;
+      o[i] = __float2bfloat16(r0);
+      o[i + half] = __float2bfloat16(r1);
+    }
+  }
+}
+
+// ---- grouped attention ----
+constexpr int kAttnThreads = 128;
+constexpr int kTile = 32;
+constexpr int kQPW = 4;  // query vectors per warp per pass
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __nv_bfloat16* __restrict__ q,
+                                                            const __nv_bfloat16* __restrict__ kp,
+                                                            const __nv_bfloat16* __restrict__ vp,
+                                                            const AttnGroup* __restrict__ groups,
+                                                            const std::int32_t* __restrict__ extra, int nq, int nkv,
+                                                            float scale_log2, __nv_bfloat16* __restrict__ out) {
+  constexpr int RW = HD / 2 + 1;  // smem row stride in 32-bit words (bank-conflict-free)
+  constexpr int DPL = HD / 32;    // output dims per lane
+  __shared__ std::uint32_t sK[kTile * RW];
+  __shared__ std::uint32_t sV[kTile * RW];
+  __shared__ float sQ[kAttnThreads / 32][kQPW][HD];
+  __shared__ std::int32_t sSlot[kTile];
+
+  const AttnGroup g = groups[blockIdx.x];
+  const int kvh = blockIdx.y;
+  const int G = nq / nkv;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nvec = g.n_rows * G;
+  const int ctx = g.prefix_len + g.extra_len;
+  const int slot_stride = nkv * HD;
+
+  for (int pass0 = 0; pass0 < nvec; pass0 += (kAttnThreads / 32) * kQPW) {
+    // query vectors of this warp: v = pass0 + warp*kQPW + u ; v → (row j = v / G, head = kvh*G + v % G)
+    float m[kQPW], l[kQPW], o[kQPW][DPL];
+    int last_visible[kQPW];
+#pragma unroll
+    for (int u = 0; u < kQPW; ++u) {
+      m[u] = -INFINITY;
+      l[u] = 0.f;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) o[u][e] = 0.f;
+      const int v = pass0 + warp * kQPW + u;
+      last_visible[u] = -1;
+      if (v < nvec) {
+        const int j = v / G, h = kvh * G + v % G;
+        last_visible[u] = g.prefix_len + g.extra_len - g.n_rows + j;
+        const __nv_bfloat16* qs = q + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD;
+        for (int d = lane; d < HD; d += 32) sQ[warp][u][d] = __bfloat162float(qs[d]);
+      }
+    }
+    __syncwarp();
+    int max_visible = -1;
+#pragma unroll
+    for (int u = 0; u < kQPW; ++u) max_visible = max(max_visible, last_visible[u]);
+    // block-wide upper bound of positions any warp needs in this pass
+    __shared__ int s_need;
+    if (threadIdx.x == 0) s_need = 0;
+    __syncthreads();
+    atomicMax(&s_need, max_visible + 1);
+    __syncthreads();
+    const int need = min(s_need, ctx);
+
+    for (int p0 = 0; p0 < need; p0 += kTile) {
+      __syncthreads();
+      if (threadIdx.x < kTile) {
+        const int p = p0 + threadIdx.x;
+        sSlot[threadIdx.x] = p < g.prefix_len ? g.prefix_slot + p : (p < ctx ? extra[g.extra_off + p - g.prefix_len] : -1);
+      }
+      __syncthreads();
+      // load K/V tile: kTile positions x HD bf16 = HD/2 words each
+      for (int t = threadIdx.x; t < kTile * (HD / 2); t += kAttnThreads) {
+        const int r = t / (HD / 2), w = t % (HD / 2);
+        const int s = sSlot[r];
+        std::uint32_t kw = 0, vw = 0;
+        if (s >= 0) {
+          const std::size_t base = static_cast<std::size_t>(s) * slot_stride + static_cast<std::size_t>(kvh) * HD;
+          kw = reinterpret_cast<const std::uint32_t*>(kp + base)[w];
+          vw = reinterpret_cast<const std::uint32_t*>(vp + base)[w];
+        }
+        sK[r * RW + w] = kw;
+        sV[r * RW + w] = vw;
+      }
+      __syncthreads();
+      const int p = p0 + lane;
+#pragma unroll
+      for (int u = 0; u < kQPW; ++u) {
+        if (last_visible[u] < p0) continue;  // warp-uniform
+        float s = 0.f;
+        const std::uint32_t* kr = &sK[lane * RW];
+#pragma unroll 8
+        for (int w = 0; w < HD / 2; ++w) {
+          const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kr[w]));
+          s = fmaf(sQ[warp][u][2 * w], kf.x, s);
+          s = fmaf(sQ[warp][u][2 * w + 1], kf.y, s);
+        }
+        s = (p <= last_visible[u] && p < ctx) ? s * scale_log2 : -INFINITY;
+        const float mt = warp_max(s);
+        const float mn = fmaxf(m[u], mt);
+        const float corr = exp2f(m[u] - mn);
+        const float pr = exp2f(s - mn);
+        l[u] = l[u] * corr + warp_sum(pr);
+        m[u] = mn;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[u][e] *= corr;
+        for (int jj = 0; jj < kTile; ++jj) {
+          const float pj = __shfl_sync(0xffffffffu, pr, jj);
+          const std::uint32_t* vr = &sV[jj * RW];
+#pragma unroll
+          for (int e = 0; e < DPL; e += 2) {
+            const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[(lane * DPL + e) / 2]));
+            o[u][e] = fmaf(pj, vf.x, o[u][e]);
+            o[u][e + 1] = fmaf(pj, vf.y, o[u][e + 1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kQPW; ++u) {
+      const int v = pass0 + warp * kQPW + u;
+      if (v >= nvec) continue;
+      const int j = v / G, h = kvh * G + v % G;
+      __nv_bfloat16* os = out + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD + lane * DPL;
+      const float inv = l[u] > 0.f ? 1.f / l[u] : 0.f;
+#pragma unroll
+      for (int e = 0; e < DPL; e += 2)
+        *reinterpret_cast<__nv_bfloat162*>(os + e) = __floats2bfloat162_rn(o[u][e] * inv, o[u][e + 1] * inv);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void plant_kernel(__nv_bfloat16* logits, int ld, const std::int32_t* plant, float bias, int rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int t = plant[r];
+  if (t < 0) return;
+  __nv_bfloat16* p = logits + static_cast<std::size_t>(r) * ld + t;
+  *p = __float2bfloat16(__bfloat162float(*p) + bias);
+}
+
+__global__ void copy_slots_kernel(__nv_bfloat16* kp, __nv_bfloat16* vp, const std::int32_t* src, const std::int32_t* dst,
+                                  std::int64_t layer_stride, int slot_stride) {
+  const int pair = blockIdx.x, layer = blockIdx.y;
+  const std::size_t s = static_cast<std::size_t>(layer) * layer_stride + static_cast<std::size_t>(src[pair]) * slot_stride;
+  const std::size_t d = static_cast<std::size_t>(layer) * layer_stride + static_cast<std::size_t>(dst[pair]) * slot_stride;
+  for (int i = threadIdx.x; i < slot_stride / 8; i += blockDim.x) {
+    reinterpret_cast<uint4*>(kp + d)[i] = reinterpret_cast<const uint4*>(kp + s)[i];
+    reinterpret_cast<uint4*>(vp + d)[i] = reinterpret_cast<const uint4*>(vp + s)[i];
+  }
+}
+
+__device__ __forceinline__ void philox(std::uint32_t c[4], std::uint32_t k0, std::uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const std::uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const std::uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const std::uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+// Box-Muller on Philox words: 4 normals per counter.
+__global__ void fill_normal_kernel(__nv_bfloat16* out, std::int64_t n, std::uint32_t k0, std::uint32_t k1,
+                                   std::uint32_t sid, float std_, float mean) {
+  for (std::int64_t i = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x * 4) {
+    std::uint32_t c[4] = {static_cast<std::uint32_t>(i >> 2), static_cast<std::uint32_t>(i >> 34), sid, 0x5EEDu};
+    philox(c, k0, k1);
+    float z[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float u1 = (static_cast<float>(c[2 * h] >> 8) + 0.5f) * (1.0f / 16777216.0f);
+      const float u2 = static_cast<float>(c[2 * h + 1] >> 8) * (1.0f / 16777216.0f);
+      const float r = sqrtf(-2.0f * logf(u1));
+      float sn, cs;
+      sincospif(2.0f * u2, &sn, &cs);
+      z[2 * h] = r * cs;
+      z[2 * h + 1] = r * sn;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (i + e < n) out[i + e] = __float2bfloat16(std_ == 0.f ? mean : mean + std_ * z[e]);
+  }
+}
+
+}  // namespace
+
+void embed_rows(const void* emb, const std::int32_t* tok, int rows, int d, float* x, cudaStream_t st) {
+  if (rows <= 0) return;
+  embed_kernel<<<rows, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(emb), tok, d, x);
+  WS_CUDA(cudaGetLastError());
+}
+
+void rmsnorm_rows(const float* x, int ld_x, const std::int32_t* idx, const void* w, float eps, int rows, int d,
+                  void* y, int ld_y, cudaStream_t st) {
+  if (rows <= 0) return;
+  if (d % 4) throw std::invalid_argument("rmsnorm: d % 4");
+  rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ld_x, idx, static_cast<const __nv_bfloat16*>(w), eps, d,
+                                       static_cast<__nv_bfloat16*>(y), ld_y);
+  WS_CUDA(cudaGetLastError());
+}
+
+void rope_kv_append(const void* qkv, int rows, int nq, int nkv, int hd, const std::int32_t* pos,
+                    const std::int32_t* slot, const float* inv_freq, void* q_out, void* k_pool, void* v_pool,
+                    cudaStream_t st) {
+  if (rows <= 0) return;
+  rope_append_kernel<<<rows, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(qkv), nq, nkv, hd, pos, slot, inv_freq,
+                                           static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_pool),
+                                           static_cast<__nv_bfloat16*>(v_pool));
+  WS_CUDA(cudaGetLastError());
+}
+
+void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
+               const std::int32_t* extra, const AttnShape& s, void* out, cudaStream_t st) {
+  if (n_groups <= 0) return;
+  dim3 grid(n_groups, s.n_kv);
+  const float sl2 = s.scale * 1.4426950408889634f;
+  if (s.hd == 128)
+    attn_kernel<128><<<grid, kAttnThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
+        static_cast<const __nv_bfloat16*>(v_pool), groups, extra, s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
+  else if (s.hd == 64)
+    attn_kernel<64><<<grid, kAttnThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
+        static_cast<const __nv_bfloat16*>(v_pool), groups, extra, s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
+  else
+    throw std::invalid_argument("attention: head dim must be 64 or 128");
+  WS_CUDA(cudaGetLastError());
+}
+
+void plant_bias(void* logits, int ld, const std::int32_t* plant, float bias, int rows, cudaStream_t st) {
+  if (rows <= 0) return;
+  plant_kernel<<<(rows + 127) / 128, 128, 0, st>>>(static_cast<__nv_bfloat16*>(logits), ld, plant, bias, rows);
+  WS_CUDA(cudaGetLastError());
+}
+
+void copy_slots(void* k_pool, void* v_pool, const std::int32_t* src, const std::int32_t* dst, int n, int layers,
+                std::int64_t layer_stride, int slot_stride, cudaStream_t st) {
+  if (n <= 0) return;
+  copy_slots_kernel<<<dim3(n, layers), 128, 0, st>>>(static_cast<__nv_bfloat16*>(k_pool),
+                                                     static_cast<__nv_bfloat16*>(v_pool), src, dst, layer_stride,
+                                                     slot_stride);
+  WS_CUDA(cudaGetLastError());
+}
+
+void fill_normal_bf16(void* out, std::int64_t n, std::uint64_t seed, std::uint32_t sid, float std_, float mean,
+                      cudaStream_t st) {
+  if (n <= 0) return;
+  fill_normal_kernel<<<148 * 8, 256, 0, st>>>(static_cast<__nv_bfloat16*>(out), n, static_cast<std::uint32_t>(seed),
+                                              static_cast<std::uint32_t>(seed >> 32), sid, std_, mean);
+  WS_CUDA(cudaGetLastError());
+}
+
+}  // namespace wsb

@@ -148,7 +148,21 @@ struct Partial {
   std::uint32_t i1, i2, pad;
 };
 
-__device__ void finalize(const State& a, float cl, std::uint32_t vocab, ws_pred* pred, RowStats* st) {
+__device__ void finalize(const State& a, float cl, std::uint32_t vocab, ws_pred* pred, RowStats* st,
+                         std::int32_t forced) {
+  if (forced >= 0) {  // past-the-end rule: fully confident prediction, entropy 0
+    ws_pred p;
+    p.n = 1;
+    p.id[0] = static_cast<std::uint32_t>(forced);
+    p.id[1] = 0;
+    p.pad = 0;
+    p.prob[0] = 1.0;
+    p.prob[1] = 0.0;
+    p.entropy = 0.0;
+    *pred = p;
+    if (st) *st = RowStats{a.m, a.z, cl, 0.f};
+    return;
+  }
   const float lnz = logf(a.z);
   float h = lnz - kLn2 * a.s / a.z;
   if (h < 0.f) h = 0.f;
@@ -168,7 +182,7 @@ __global__ void __launch_bounds__(kThreads) row_stats_kernel(
     const __nv_bfloat16* __restrict__ logits, std::uint32_t vocab, std::uint32_t ld, float cl, bool vec_ok,
     ws_pred* __restrict__ out_pred, RowStats* __restrict__ out_stats, Partial* __restrict__ partials,
     std::uint32_t* __restrict__ row_ticket, std::uint32_t k, const std::uint32_t* __restrict__ cand,
-    ws_verify_out* __restrict__ vout, std::uint32_t* __restrict__ req_ticket) {
+    ws_verify_out* __restrict__ vout, std::uint32_t* __restrict__ req_ticket, const std::int32_t* __restrict__ forced) {
   const std::uint32_t split = blockIdx.x, splits = gridDim.x, row = blockIdx.y;
   const std::uint32_t lo = split * kRowChunk;
   const std::uint32_t hi = min(vocab, lo + kRowChunk);
@@ -229,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) row_stats_kernel(
     }
     row_ticket[row] = 0;  // self-reset for the next launch
   }
-  finalize(r, cl, vocab, &out_pred[row], out_stats ? &out_stats[row] : nullptr);
+  finalize(r, cl, vocab, &out_pred[row], out_stats ? &out_stats[row] : nullptr, forced ? forced[row] : -1);
 
   if (cand) {  // K4 greedy epilogue: the last finished row of the request runs the walk
     const std::uint32_t req = row / (k + 1);
@@ -259,7 +273,8 @@ std::size_t rowstats_workspace_bytes(std::uint32_t rows, std::uint32_t vocab, st
 
 void row_stats_bf16(const void* logits, std::uint32_t rows, std::uint32_t vocab, std::uint32_t ld, float inv_temp,
                     ws_pred* out_pred, RowStats* out_stats, void* workspace, std::uint32_t n_req, std::uint32_t k,
-                    const std::uint32_t* cand, ws_verify_out* verify_out, cudaStream_t stream) {
+                    const std::uint32_t* cand, ws_verify_out* verify_out, cudaStream_t stream,
+                    const std::int32_t* forced) {
   if (rows == 0) return;
   if (!logits || !out_pred || vocab == 0 || ld < vocab) throw std::invalid_argument("row_stats: bad argument");
   if (!(inv_temp > 0.f)) throw std::invalid_argument("row_stats: temperature must be > 0");
@@ -277,7 +292,7 @@ void row_stats_bf16(const void* logits, std::uint32_t rows, std::uint32_t vocab,
   dim3 grid(splits, rows);
   row_stats_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const __nv_bfloat16*>(logits), vocab, ld,
                                                   inv_temp * kLog2e, vec_ok, out_pred, out_stats, partials,
-                                                  row_ticket, k, cand, verify_out, req_ticket);
+                                                  row_ticket, k, cand, verify_out, req_ticket, forced);
   WS_CUDA(cudaGetLastError());
 }
 

@@ -26,8 +26,12 @@ std::size_t rowstats_workspace_bytes(std::uint32_t rows, std::uint32_t vocab, st
 // K3: fused softmax + entropy + top-2 over bf16 logits rows (+ optional K4 greedy verify
 // epilogue when cand != nullptr: rows are n_req groups of k+1, run_target_step semantics on
 // the argmaxes). `workspace` must be zero-initialised once (counters self-reset).
+// forced (optional, device, per row): >= 0 overrides the row with a fully confident prediction
+// of that token (prob 1, entropy 0) — the past-the-end EOS rule of SequenceTrace
+// (oracle.hpp:88-102, :118) applied to model rows that predict positions >= sequence_length-1.
 void row_stats_bf16(const void* logits, std::uint32_t rows, std::uint32_t vocab, std::uint32_t ld, float inv_temp,
                     ws_pred* out_pred, RowStats* out_stats, void* workspace, std::uint32_t n_req, std::uint32_t k,
-                    const std::uint32_t* cand, ws_verify_out* verify_out, cudaStream_t stream);
+                    const std::uint32_t* cand, ws_verify_out* verify_out, cudaStream_t stream,
+                    const std::int32_t* forced = nullptr);
 
 }  // namespace wsb

@@ -1,0 +1,246 @@
+// Batched Llama forward (see llama.hpp).
+#include "llama.hpp"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "../kernels/cuda_check.hpp"
+#include "../kernels/gemm_tc.cuh"
+
+namespace wsb {
+
+std::int64_t LlamaShape::params_mm() const {
+  const std::int64_t per = static_cast<std::int64_t>(qkv_dim()) * d + static_cast<std::int64_t>(d) * n_q * hd +
+                           3ll * ffn * d;
+  return per * layers + static_cast<std::int64_t>(vocab) * d;
+}
+
+LlamaShape shape_by_name(const std::string& name) {
+  // Llama-3.1-8B / Llama-3.2-1B / Llama-3.1-70B hyper-parameters (BASELINE configs 3 and 5).
+  if (name == "llama3-8b") return LlamaShape{name, 32, 4096, 32, 8, 128, 14336, 128256, 1e-5f, 500000.f, 8.f, false};
+  if (name == "llama3.2-1b") return LlamaShape{name, 16, 2048, 32, 8, 64, 8192, 128256, 1e-5f, 500000.f, 32.f, true};
+  if (name == "llama3-70b") return LlamaShape{name, 80, 8192, 64, 8, 128, 28672, 128256, 1e-5f, 500000.f, 8.f, false};
+  if (name == "tiny") return LlamaShape{name, 2, 256, 4, 2, 64, 512, 1000, 1e-5f, 10000.f, 0.f, false};
+  if (name == "tiny-draft") return LlamaShape{name, 1, 256, 4, 2, 64, 512, 1000, 1e-5f, 10000.f, 0.f, true};
+  if (name == "tiny128") return LlamaShape{name, 2, 512, 4, 1, 128, 1024, 2000, 1e-5f, 500000.f, 8.f, false};
+  throw ConfigError("unknown model shape: " + name);
+}
+
+namespace {
+
+// HF Llama-3 rope scaling (low/high freq factors 1/4, original context 8192).
+std::vector<float> llama3_inv_freq(const LlamaShape& s) {
+  std::vector<float> f(s.hd / 2);
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i < s.hd / 2; ++i) {
+    double inv = 1.0 / std::pow(static_cast<double>(s.rope_theta), (2.0 * i) / s.hd);
+    if (s.rope_factor > 0.f) {
+      const double factor = s.rope_factor, lo = 1.0, hi = 4.0, old_ctx = 8192.0;
+      const double wavelen = 2 * pi / inv;
+      const double lo_wl = old_ctx / lo, hi_wl = old_ctx / hi;
+      if (wavelen > lo_wl) {
+        inv = inv / factor;
+      } else if (wavelen >= hi_wl) {
+        const double smooth = (old_ctx / wavelen - lo) / (hi - lo);
+        inv = (1 - smooth) * inv / factor + smooth * inv;
+      }
+    }
+    f[i] = static_cast<float>(inv);
+  }
+  return f;
+}
+
+std::size_t al(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
+
+}  // namespace
+
+LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device)
+    : s_(s), device_(device), n_slots_(n_slots) {
+  WS_CUDA(cudaSetDevice(device));
+  if (s.d % 64 || s.ffn % 64 || (s.n_q * s.hd) % 64) throw ConfigError("model dims must be multiples of 64");
+  if (s.n_q % s.n_kv) throw ConfigError("n_q must be a multiple of n_kv");
+  // ---- weights in one block ----
+  const std::size_t d = s.d, V = s.vocab;
+  std::vector<std::pair<void**, std::size_t>> tensors;
+  attn_norm_.resize(s.layers);
+  wqkv_.resize(s.layers);
+  wo_.resize(s.layers);
+  mlp_norm_.resize(s.layers);
+  wgu_.resize(s.layers);
+  wdown_.resize(s.layers);
+  std::size_t total = 0;
+  auto reserve = [&](std::size_t elems) {
+    const std::size_t off = total;
+    total += al(elems * 2);
+    return off;
+  };
+  struct Item {
+    void** dst;
+    std::size_t off, n;
+    float std_, mean;
+  };
+  std::vector<Item> items;
+  items.push_back({&embed_, reserve(V * d), V * d, 0.02f, 0.f});
+  for (int l = 0; l < s.layers; ++l) {
+    items.push_back({&attn_norm_[l], reserve(d), d, 0.f, 1.f});
+    items.push_back({&wqkv_[l], reserve(static_cast<std::size_t>(s.qkv_dim()) * d), static_cast<std::size_t>(s.qkv_dim()) * d, 0.02f, 0.f});
+    items.push_back({&wo_[l], reserve(d * s.n_q * s.hd), d * s.n_q * s.hd, 0.02f, 0.f});
+    items.push_back({&mlp_norm_[l], reserve(d), d, 0.f, 1.f});
+    items.push_back({&wgu_[l], reserve(2 * static_cast<std::size_t>(s.ffn) * d), 2 * static_cast<std::size_t>(s.ffn) * d, 0.02f, 0.f});
+    items.push_back({&wdown_[l], reserve(d * s.ffn), d * s.ffn, 0.02f, 0.f});
+  }
+  items.push_back({&final_norm_, reserve(d), d, 0.f, 1.f});
+  if (!s.tied) items.push_back({&lm_head_, reserve(V * d), V * d, 0.02f, 0.f});
+  WS_CUDA(cudaMalloc(&weight_block_, total));
+  std::uint32_t sid = 1;
+  for (const Item& it : items) {
+    *it.dst = static_cast<unsigned char*>(weight_block_) + it.off;
+    fill_normal_bf16(*it.dst, static_cast<std::int64_t>(it.n), seed, sid++, it.std_, it.mean, nullptr);
+  }
+  if (s.tied) lm_head_ = embed_;
+  const std::vector<float> inv = llama3_inv_freq(s);
+  WS_CUDA(cudaMalloc(&inv_freq_, inv.size() * sizeof(float)));
+  WS_CUDA(cudaMemcpy(inv_freq_, inv.data(), inv.size() * sizeof(float), cudaMemcpyHostToDevice));
+  // ---- KV pools ----
+  const std::size_t pool = static_cast<std::size_t>(s.layers) * n_slots * s.n_kv * s.hd * 2;
+  WS_CUDA(cudaMalloc(&k_pool_, pool));
+  WS_CUDA(cudaMalloc(&v_pool_, pool));
+  WS_CUDA(cudaMemset(k_pool_, 0, pool));
+  WS_CUDA(cudaMemset(v_pool_, 0, pool));
+  ensure_rows(max_rows, max_rows);
+  WS_CUDA(cudaDeviceSynchronize());
+}
+
+LlamaModel::~LlamaModel() {
+  cudaSetDevice(device_);
+  for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_, static_cast<void*>(x_), xn_, qkv_,
+                  q_, attn_, h_, logits_, xo_, static_cast<void*>(d_meta_)})
+    if (p) cudaFree(p);
+  if (h_meta_) cudaFreeHost(h_meta_);
+}
+
+void LlamaModel::ensure_rows(int rows, int out_rows) {
+  if (rows <= cap_rows_ && out_rows <= cap_out_) return;
+  rows = std::max(rows, cap_rows_);
+  out_rows = std::max(out_rows, cap_out_);
+  for (void* p : {static_cast<void*>(x_), xn_, qkv_, q_, attn_, h_, logits_, xo_})
+    if (p) cudaFree(p);
+  const std::size_t R = rows, O = out_rows;
+  WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&x_), R * s_.d * 4));
+  WS_CUDA(cudaMalloc(&xn_, R * s_.d * 2));
+  WS_CUDA(cudaMalloc(&qkv_, R * s_.qkv_dim() * 2));
+  WS_CUDA(cudaMalloc(&q_, R * s_.n_q * s_.hd * 2));
+  WS_CUDA(cudaMalloc(&attn_, R * s_.n_q * s_.hd * 2));
+  WS_CUDA(cudaMalloc(&h_, R * s_.ffn * 2));
+  WS_CUDA(cudaMalloc(&xo_, O * s_.d * 2));
+  WS_CUDA(cudaMalloc(&logits_, O * static_cast<std::size_t>(s_.vocab) * 2));
+  cap_rows_ = rows;
+  cap_out_ = out_rows;
+}
+
+void* LlamaModel::weight(const std::string& w, int l, std::int64_t* numel) {
+  const std::int64_t d = s_.d;
+  auto ret = [&](void* p, std::int64_t n) {
+    if (numel) *numel = n;
+    return p;
+  };
+  if (w == "embed") return ret(embed_, d * s_.vocab);
+  if (w == "lm_head") return ret(lm_head_, d * s_.vocab);
+  if (w == "final_norm") return ret(final_norm_, d);
+  if (l < 0 || l >= s_.layers) throw std::invalid_argument("layer out of range");
+  if (w == "attn_norm") return ret(attn_norm_[l], d);
+  if (w == "mlp_norm") return ret(mlp_norm_[l], d);
+  if (w == "wqkv") return ret(wqkv_[l], d * s_.qkv_dim());
+  if (w == "wo") return ret(wo_[l], d * s_.n_q * s_.hd);
+  if (w == "wgu") return ret(wgu_[l], d * 2 * s_.ffn);
+  if (w == "wdown") return ret(wdown_[l], d * s_.ffn);
+  throw std::invalid_argument("unknown weight " + w);
+}
+
+void LlamaModel::copy_slots(const std::vector<std::int32_t>& src, const std::vector<std::int32_t>& dst,
+                            cudaStream_t st) {
+  if (src.empty()) return;
+  const std::size_t n = src.size();
+  const std::size_t need = 2 * n * 4;
+  if (need > cap_meta_) {
+    if (d_meta_) cudaFree(d_meta_);
+    if (h_meta_) cudaFreeHost(h_meta_);
+    cap_meta_ = std::max(need, 2 * cap_meta_);
+    WS_CUDA(cudaMalloc(&d_meta_, cap_meta_));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_meta_), cap_meta_, cudaHostAllocDefault));
+  }
+  WS_CUDA(cudaStreamSynchronize(st));  // staging reuse
+  std::memcpy(h_meta_, src.data(), n * 4);
+  std::memcpy(h_meta_ + n * 4, dst.data(), n * 4);
+  WS_CUDA(cudaMemcpyAsync(d_meta_, h_meta_, need, cudaMemcpyHostToDevice, st));
+  h2d_ += need;
+  wsb::copy_slots(k_pool_, v_pool_, reinterpret_cast<std::int32_t*>(d_meta_),
+                  reinterpret_cast<std::int32_t*>(d_meta_ + n * 4), static_cast<int>(n), s_.layers,
+                  n_slots_ * s_.n_kv * s_.hd, s_.n_kv * s_.hd, st);
+  WS_CUDA(cudaStreamSynchronize(st));
+}
+
+void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
+  const int n = static_cast<int>(b.tok.size());
+  const int n_out = static_cast<int>(b.out_rows.size());
+  if (n == 0) return;
+  if (b.pos.size() != b.tok.size() || b.slot.size() != b.tok.size()) throw std::invalid_argument("forward: ragged rows");
+  ensure_rows(n, n_out);
+  // ---- one packed H2D for all metadata ----
+  const std::size_t s_tok = al(n * 4), s_grp = al(b.groups.size() * sizeof(AttnGroup)), s_ext = al(b.extra.size() * 4 + 4),
+                    s_out = al(n_out * 4 + 4);
+  const std::size_t need = 3 * s_tok + s_grp + s_ext + 2 * s_out;
+  if (need > cap_meta_) {
+    if (d_meta_) cudaFree(d_meta_);
+    if (h_meta_) cudaFreeHost(h_meta_);
+    cap_meta_ = std::max(need, 2 * cap_meta_);
+    WS_CUDA(cudaMalloc(&d_meta_, cap_meta_));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_meta_), cap_meta_, cudaHostAllocDefault));
+  }
+  WS_CUDA(cudaStreamSynchronize(st));  // previous use of the staging buffer retired
+  std::size_t o = 0;
+  auto put = [&](const void* src, std::size_t bytes, std::size_t slot_bytes) {
+    if (bytes) std::memcpy(h_meta_ + o, src, bytes);
+    const std::size_t at = o;
+    o += slot_bytes;
+    return at;
+  };
+  const std::size_t o_tok = put(b.tok.data(), n * 4, s_tok);
+  const std::size_t o_pos = put(b.pos.data(), n * 4, s_tok);
+  const std::size_t o_slot = put(b.slot.data(), n * 4, s_tok);
+  const std::size_t o_grp = put(b.groups.data(), b.groups.size() * sizeof(AttnGroup), s_grp);
+  const std::size_t o_ext = put(b.extra.data(), b.extra.size() * 4, s_ext);
+  const std::size_t o_out = put(b.out_rows.data(), n_out * 4, s_out);
+  const std::size_t o_pl = put(b.plant.data(), b.plant.size() * 4, s_out);
+  WS_CUDA(cudaMemcpyAsync(d_meta_, h_meta_, o, cudaMemcpyHostToDevice, st));
+  h2d_ += o;
+  auto I = [&](std::size_t off) { return reinterpret_cast<const std::int32_t*>(d_meta_ + off); };
+
+  const int d = s_.d, qd = s_.n_q * s_.hd;
+  const std::int64_t layer_stride = n_slots_ * s_.n_kv * s_.hd;
+  const AttnShape ash{s_.n_q, s_.n_kv, s_.hd, s_.n_kv * s_.hd, 1.0f / std::sqrt(static_cast<float>(s_.hd))};
+  embed_rows(embed_, I(o_tok), n, d, x_, st);
+  for (int l = 0; l < s_.layers; ++l) {
+    __nv_bfloat16* kp = static_cast<__nv_bfloat16*>(k_pool_) + l * layer_stride;
+    __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(v_pool_) + l * layer_stride;
+    rmsnorm_rows(x_, d, nullptr, attn_norm_[l], s_.eps, n, d, xn_, d, st);
+    gemm_tn(GemmArgs{xn_, wqkv_[l], qkv_, n, s_.qkv_dim(), d, d, d, s_.qkv_dim(), kEpiBF16, 0}, st);
+    rope_kv_append(qkv_, n, s_.n_q, s_.n_kv, s_.hd, I(o_pos), I(o_slot), inv_freq_, q_, kp, vp, st);
+    attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()),
+              I(o_ext), ash, attn_, st);
+    gemm_tn(GemmArgs{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0}, st);
+    rmsnorm_rows(x_, d, nullptr, mlp_norm_[l], s_.eps, n, d, xn_, d, st);
+    gemm_tn(GemmArgs{xn_, wgu_[l], h_, n, 2 * s_.ffn, d, d, d, s_.ffn, kEpiSwiGLU, 0}, st);
+    gemm_tn(GemmArgs{h_, wdown_[l], x_, n, d, s_.ffn, s_.ffn, s_.ffn, d, kEpiAddF32, 0}, st);
+  }
+  if (n_out == 0) return;
+  rmsnorm_rows(x_, d, I(o_out), final_norm_, s_.eps, n_out, d, xo_, d, st);
+  gemm_tn(GemmArgs{xo_, lm_head_, logits_, n_out, s_.vocab, d, d, d, s_.vocab, kEpiBF16, 0}, st);
+  if (plant > 0.f && !b.plant.empty()) plant_bias(logits_, s_.vocab, I(o_pl), plant, n_out, st);
+}
+
+}  // namespace wsb

@@ -1,0 +1,103 @@
+// Llama-architecture forward for the verify (target) and draft models, batched over rows from
+// many requests, on the sm_100a kernels (K1 GEMM, K2 attention, K6 plumbing, K3/K4 epilogues).
+// Random-init bf16 weights of the named shapes (BASELINE config 3): weights are seeded
+// N(0, 0.02) from Philox, norm weights 1. The residual stream is fp32.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../kernels/llama_ops.cuh"
+
+namespace wsb {
+
+struct LlamaShape {
+  std::string name;
+  int layers, d, n_q, n_kv, hd, ffn, vocab;
+  float eps = 1e-5f;
+  float rope_theta = 500000.f;
+  float rope_factor = 8.f;  // llama3 scaling (0 = none)
+  bool tied = false;
+  std::int64_t params_mm() const;  // matmul parameters (incl. LM head)
+  int qkv_dim() const { return (n_q + 2 * n_kv) * hd; }
+};
+
+LlamaShape shape_by_name(const std::string& name);  // "llama3-8b", "llama3.2-1b", "tiny"
+
+// One batched forward: rows with (token, position, own KV slot), attention groups over the
+// slot pool, and the list of rows whose logits are wanted.
+struct ForwardBatch {
+  std::vector<std::int32_t> tok, pos, slot;
+  std::vector<AttnGroup> groups;
+  std::vector<std::int32_t> extra;
+  std::vector<std::int32_t> out_rows;
+  std::vector<std::int32_t> plant;  // per output row: planted token (or -1)
+  void clear() {
+    tok.clear();
+    pos.clear();
+    slot.clear();
+    groups.clear();
+    extra.clear();
+    out_rows.clear();
+    plant.clear();
+  }
+};
+
+class LlamaModel {
+ public:
+  LlamaModel(const LlamaShape& shape, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device);
+  ~LlamaModel();
+  LlamaModel(const LlamaModel&) = delete;
+  LlamaModel& operator=(const LlamaModel&) = delete;
+
+  const LlamaShape& shape() const { return s_; }
+  std::int64_t n_slots() const { return n_slots_; }
+
+  // Uploads the batch (one H2D of a packed block) and runs the forward; logits of the
+  // out_rows (bf16 [n_out, vocab]) land in logits(). plant_bias > 0 adds the planted bias.
+  void forward(const ForwardBatch& b, float plant_bias, cudaStream_t st);
+  const void* logits() const { return logits_; }
+  std::size_t h2d_bytes() const { return h2d_; }
+  void copy_slots(const std::vector<std::int32_t>& src, const std::vector<std::int32_t>& dst, cudaStream_t st);
+
+  // weight access for tests: which = "embed","attn_norm","wqkv","wo","mlp_norm","wgu","wdown","final_norm","lm_head"
+  void* weight(const std::string& which, int layer, std::int64_t* numel);
+  void* k_pool() const { return k_pool_; }
+  void* v_pool() const { return v_pool_; }
+
+ private:
+  void ensure_rows(int rows, int out_rows);
+  LlamaShape s_;
+  int device_;
+  std::int64_t n_slots_;
+  int cap_rows_ = 0, cap_out_ = 0;
+  // weights
+  void* embed_ = nullptr;
+  void* lm_head_ = nullptr;
+  void* final_norm_ = nullptr;
+  std::vector<void*> attn_norm_, wqkv_, wo_, mlp_norm_, wgu_, wdown_;
+  void* weight_block_ = nullptr;
+  float* inv_freq_ = nullptr;
+  // KV pools [layer][slot][n_kv][hd]
+  void* k_pool_ = nullptr;
+  void* v_pool_ = nullptr;
+  // activations
+  float* x_ = nullptr;
+  void* xn_ = nullptr;
+  void* qkv_ = nullptr;
+  void* q_ = nullptr;
+  void* attn_ = nullptr;
+  void* h_ = nullptr;
+  void* logits_ = nullptr;
+  void* xo_ = nullptr;
+  // batch metadata (device) + pinned staging
+  unsigned char* d_meta_ = nullptr;
+  unsigned char* h_meta_ = nullptr;
+  std::size_t cap_meta_ = 0;
+  std::size_t h2d_ = 0;
+};
+
+}  // namespace wsb

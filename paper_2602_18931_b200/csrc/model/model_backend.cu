@@ -1,0 +1,412 @@
+// Real-model backend (see model_backend.hpp).
+#include "model_backend.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+
+#include "../kernels/cuda_check.hpp"
+#include "../kernels/rowstats.cuh"
+
+namespace wsb {
+
+namespace {
+
+std::uint64_t splitmix64(std::uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+struct LinearCache {
+  std::vector<TokenId> valid;  // tokens whose KV is valid at positions [0, size)
+};
+
+struct TrieNode {
+  TokenId tok = 0;
+  std::int32_t slot = -1;
+  std::int32_t parent = -1;  // -1 = trie root (position == prefix length)
+  std::vector<std::int32_t> kids;
+};
+
+// Worker draft KV: committed prefix (linear) + content trie of speculative nodes.
+struct TreeCache {
+  std::vector<TokenId> prefix;
+  std::vector<TrieNode> nodes;
+  std::vector<std::int32_t> root_kids;
+  std::vector<std::int32_t> free_nodes;
+  std::vector<std::int32_t> free_slots;
+  bool init = false;
+
+  void reset(std::int32_t slot0, std::int32_t n) {
+    prefix.clear();
+    nodes.clear();
+    root_kids.clear();
+    free_nodes.clear();
+    free_slots.clear();
+    for (std::int32_t i = n - 1; i >= 0; --i) free_slots.push_back(slot0 + i);
+    init = true;
+  }
+  const std::vector<std::int32_t>& kids_of(std::int32_t n) const { return n < 0 ? root_kids : nodes[n].kids; }
+  std::int32_t find(std::int32_t parent, TokenId t) const {
+    for (std::int32_t c : kids_of(parent))
+      if (nodes[c].tok == t) return c;
+    return -2;
+  }
+  void free_subtree(std::int32_t n) {
+    std::vector<std::int32_t> st{n};
+    while (!st.empty()) {
+      const std::int32_t x = st.back();
+      st.pop_back();
+      for (std::int32_t c : nodes[x].kids) st.push_back(c);
+      nodes[x].kids.clear();
+      free_slots.push_back(nodes[x].slot);
+      nodes[x].slot = -1;
+      free_nodes.push_back(x);
+    }
+  }
+  void drop_all() {
+    for (std::int32_t c : root_kids) free_subtree(c);
+    root_kids.clear();
+  }
+  std::int32_t add(std::int32_t parent, TokenId t) {
+    std::int32_t id;
+    if (!free_nodes.empty()) {
+      id = free_nodes.back();
+      free_nodes.pop_back();
+    } else {
+      id = static_cast<std::int32_t>(nodes.size());
+      nodes.emplace_back();
+    }
+    TrieNode& n = nodes[id];
+    n.tok = t;
+    n.parent = parent;
+    n.kids.clear();
+    n.slot = free_slots.back();
+    free_slots.pop_back();
+    (parent < 0 ? root_kids : nodes[parent].kids).push_back(id);
+    return id;
+  }
+  // The chain root→n has migrated into the prefix: n's children become the new root
+  // children; the chain and every side branch are freed (their KV was copied or is stale).
+  void reroot_at(std::int32_t n) {
+    std::vector<std::int32_t> keep = nodes[n].kids;
+    nodes[n].kids.clear();
+    for (std::int32_t c : keep) nodes[c].parent = -1;
+    std::vector<std::int32_t> old_root = root_kids;
+    root_kids.clear();
+    for (std::int32_t c : old_root) free_subtree(c);
+    root_kids = keep;
+  }
+  std::uint64_t last_alloc_round = ~0ull;
+};
+
+}  // namespace
+
+struct ModelPair::Impl {
+  std::vector<LinearCache> tgt, ctrl;
+  std::vector<TreeCache> wrk;
+  // K3/K4 device buffers
+  ws_pred* d_pred = nullptr;
+  ws_verify_out* d_vout = nullptr;
+  std::uint32_t* d_cands = nullptr;
+  std::int32_t* d_forced = nullptr;
+  void* d_ws = nullptr;
+  unsigned char* h_stage = nullptr;
+  std::size_t cap_rows = 0;
+  ForwardBatch tb, db;
+  std::vector<TokenId> ctx;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+};
+
+ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(device), impl(new Impl) {
+  WS_CUDA(cudaSetDevice(device));
+  WS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  const LlamaShape ts = shape_by_name(cfg.target), ds = shape_by_name(cfg.draft);
+  if (ts.vocab != ds.vocab) throw ConfigError("target and draft vocabularies differ");
+  const std::int64_t R = cfg.max_requests, C = cfg.max_ctx;
+  const int max_rows = static_cast<int>(std::min<std::int64_t>(R * 20, 8192));
+  target_.reset(new LlamaModel(ts, cfg.seed * 2 + 1, R * C, max_rows, device));
+  draft_.reset(new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows, device));
+  prompts_.resize(cfg.max_requests);
+  WS_CUDA(cudaEventCreate(&impl->e0));
+  WS_CUDA(cudaEventCreate(&impl->e1));
+  WS_CUDA(cudaEventCreate(&impl->e2));
+  WS_CUDA(cudaEventCreate(&impl->e3));
+  reset_requests();
+}
+
+ModelPair::~ModelPair() {
+  cudaSetDevice(device_);
+  Impl& I = *impl;
+  for (void* p : {static_cast<void*>(I.d_pred), static_cast<void*>(I.d_vout), static_cast<void*>(I.d_cands),
+                  static_cast<void*>(I.d_forced), I.d_ws})
+    if (p) cudaFree(p);
+  if (I.h_stage) cudaFreeHost(I.h_stage);
+  for (cudaEvent_t e : {I.e0, I.e1, I.e2, I.e3})
+    if (e) cudaEventDestroy(e);
+  target_.reset();
+  draft_.reset();
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void ModelPair::reset_requests() {
+  impl->tgt.assign(cfg_.max_requests, LinearCache{});
+  impl->ctrl.assign(cfg_.max_requests, LinearCache{});
+  impl->wrk.assign(cfg_.max_requests, TreeCache{});
+}
+
+const std::vector<TokenId>& ModelPair::prompt(std::uint32_t r) {
+  if (r >= prompts_.size()) throw ConfigError("request index exceeds max_requests");
+  std::vector<TokenId>& p = prompts_[r];
+  if (p.empty()) {
+    std::mt19937_64 g(cfg_.seed ^ (0x51ed270b27a3c6f1ULL * (r + 1)));
+    const std::uint32_t V = static_cast<std::uint32_t>(target_->shape().vocab);
+    p.resize(cfg_.prompt_len);
+    for (auto& t : p) t = static_cast<TokenId>(g() % (V - 256));  // stay clear of special ids
+  }
+  return p;
+}
+
+std::int32_t ModelPair::plant(TokenId t, bool is_draft) const {
+  const std::uint32_t V = static_cast<std::uint32_t>(target_->shape().vocab);
+  if (is_draft) {
+    const std::uint64_t h2 = splitmix64(t ^ 0xD1B54A32D192ED03ULL ^ cfg_.seed);
+    if (static_cast<double>(h2 % 1000000) >= cfg_.draft_plant_rate * 1e6) return -1;
+  }
+  return static_cast<std::int32_t>(splitmix64(t ^ 0xA0761D6478BD642FULL ^ cfg_.seed) % (V - 256));
+}
+
+ModelBackend_Llama::ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, TokenId eos, std::uint32_t k)
+    : p_(pair), L_(seq_len), eos_(eos), k_(k) {}
+ModelBackend_Llama::~ModelBackend_Llama() = default;
+
+void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t) {
+  if (verify_mode != WS_VERIFY_GREEDY)
+    throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
+  ModelPair::Impl& I = *p_->impl;
+  const ModelPairCfg& cfg = p_->cfg();
+  cudaStream_t st = p_->stream();
+  const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
+  const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
+  const std::int32_t V = p_->target().shape().vocab;
+  const std::uint32_t nv = static_cast<std::uint32_t>(jobs.verify.size());
+  const std::uint32_t nd = static_cast<std::uint32_t>(jobs.draft.size());
+  const std::size_t need_rows = std::max<std::size_t>(nv * (k_ + 1), nd) + 16;
+  if (need_rows > I.cap_rows) {
+    for (void* q : {static_cast<void*>(I.d_pred), static_cast<void*>(I.d_vout), static_cast<void*>(I.d_cands),
+                    static_cast<void*>(I.d_forced), I.d_ws})
+      if (q) cudaFree(q);
+    if (I.h_stage) cudaFreeHost(I.h_stage);
+    I.cap_rows = need_rows * 2;
+    WS_CUDA(cudaMalloc(&I.d_pred, I.cap_rows * sizeof(ws_pred)));
+    WS_CUDA(cudaMalloc(&I.d_vout, I.cap_rows * sizeof(ws_verify_out)));
+    WS_CUDA(cudaMalloc(&I.d_cands, I.cap_rows * k_ * 4 + 64));
+    WS_CUDA(cudaMalloc(&I.d_forced, I.cap_rows * 4));
+    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(I.cap_rows), V,
+                                                      static_cast<std::uint32_t>(I.cap_rows));
+    WS_CUDA(cudaMalloc(&I.d_ws, wsb_));
+    WS_CUDA(cudaMemset(I.d_ws, 0, wsb_));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_stage),
+                          I.cap_rows * (sizeof(ws_pred) + k_ * 4 + 8) + 256, cudaHostAllocDefault));
+  }
+  auto fill_ctx = [&](const std::vector<TokenId>& prompt, const JobCtx& c) {
+    I.ctx.assign(prompt.begin(), prompt.end());
+    I.ctx.insert(I.ctx.end(), jobs.ctx_tokens.begin() + c.off, jobs.ctx_tokens.begin() + c.off + c.len);
+  };
+  auto forced_for = [&](std::int32_t pos) -> std::int32_t {
+    // row at context position pos predicts committed index pos + 1 - P (oracle.hpp:88-102)
+    return (pos + 1 - P) >= static_cast<std::int32_t>(L_) - 1 ? static_cast<std::int32_t>(eos_) : -1;
+  };
+
+  res.verify.resize(nv);
+  res.draft.resize(nd);
+  // ------------------------------ target verify ------------------------------
+  if (nv) {
+    ForwardBatch& b = I.tb;
+    b.clear();
+    std::vector<std::int32_t> forced(nv * (k_ + 1));
+    std::uint32_t* hc = reinterpret_cast<std::uint32_t*>(I.h_stage);
+    for (std::uint32_t j = 0; j < nv; ++j) {
+      const VerifyJob& vj = jobs.verify[j];
+      const std::uint32_t r = static_cast<std::uint32_t>(vj.request);
+      fill_ctx(p_->prompt(r), jobs.verify_ctx[j]);
+      I.ctx.insert(I.ctx.end(), jobs.cands.begin() + vj.cand_off, jobs.cands.begin() + vj.cand_off + vj.k);
+      const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
+      const std::int32_t first = n_ctx - static_cast<std::int32_t>(k_) - 1;  // = P + base - 1
+      if (n_ctx > MC) throw ConfigError("model path: context exceeds max_ctx");
+      LinearCache& c = I.tgt[r];
+      std::int32_t lcp = 0;
+      while (lcp < first && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
+      const std::int32_t base_slot = static_cast<std::int32_t>(r) * MC;
+      const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
+      const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
+      for (std::int32_t p = lcp; p < n_ctx; ++p) {
+        b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
+        b.pos.push_back(p);
+        b.slot.push_back(base_slot + p);
+        b.extra.push_back(base_slot + p);
+      }
+      b.groups.push_back(AttnGroup{row0, n_ctx - lcp, base_slot, lcp, eoff, n_ctx - lcp});
+      for (std::int32_t p = first; p < n_ctx; ++p) {
+        b.out_rows.push_back(row0 + p - lcp);
+        b.plant.push_back(p_->plant(I.ctx[p], false));
+        forced[j * (k_ + 1) + (p - first)] = forced_for(p);
+      }
+      c.valid.assign(I.ctx.begin(), I.ctx.end());
+      std::memcpy(hc + j * k_, jobs.cands.data() + vj.cand_off, k_ * 4);
+    }
+    std::memcpy(hc + nv * k_, forced.data(), forced.size() * 4);
+    WS_CUDA(cudaMemcpyAsync(I.d_cands, hc, nv * k_ * 4, cudaMemcpyHostToDevice, st));
+    WS_CUDA(cudaMemcpyAsync(I.d_forced, hc + nv * k_, forced.size() * 4, cudaMemcpyHostToDevice, st));
+    WS_CUDA(cudaEventRecord(I.e0, st));
+    p_->target().forward(b, cfg.plant_target, st);
+    row_stats_bf16(p_->target().logits(), nv * (k_ + 1), V, V, 1.0f, I.d_pred, nullptr, I.d_ws, nv, k_, I.d_cands,
+                   I.d_vout, st, I.d_forced);
+    WS_CUDA(cudaEventRecord(I.e1, st));
+    WS_CUDA(cudaMemcpyAsync(res.verify.data(), I.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
+    WS_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    WS_CUDA(cudaEventElapsedTime(&ms, I.e0, I.e1));
+    target_ms += ms;
+    target_rows += b.tok.size();
+    target_forwards += 1;
+    stats.launches += 1 + 8ull * p_->target().shape().layers + 4;
+    stats.h2d += nv * k_ * 4 + forced.size() * 4;
+    stats.d2h += nv * sizeof(ws_verify_out);
+  }
+  // ------------------------------ drafts (worker + controller) ------------------------------
+  if (nd) {
+    ForwardBatch& b = I.db;
+    b.clear();
+    std::vector<std::int32_t> forced(nd), copy_src, copy_dst;
+    const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg.trie_slots);
+    for (std::uint32_t j = 0; j < nd; ++j) {
+      const DraftJob& dj = jobs.draft[j];
+      const JobCtx& jc = jobs.draft_ctx[j];
+      const std::uint32_t r = dj.seq;
+      fill_ctx(p_->prompt(r), jc);
+      const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
+      if (n_ctx > MC) throw ConfigError("model path: context exceeds max_ctx");
+      const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
+      const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
+      if (jc.kind == kJobCtrlDraft) {  // controller local draft + catch-up prefill (controller.hpp:194-208)
+        LinearCache& c = I.ctrl[r];
+        std::int32_t lcp = 0;
+        while (lcp < n_ctx - 1 && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
+        const std::int32_t base_slot = static_cast<std::int32_t>(r) * S;
+        for (std::int32_t p = lcp; p < n_ctx; ++p) {
+          b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
+          b.pos.push_back(p);
+          b.slot.push_back(base_slot + p);
+          b.extra.push_back(base_slot + p);
+        }
+        b.groups.push_back(AttnGroup{row0, n_ctx - lcp, base_slot, lcp, eoff, n_ctx - lcp});
+        c.valid.assign(I.ctx.begin(), I.ctx.end());
+      } else {  // worker leaf: committed prefix + trie
+        TreeCache& t = I.wrk[r];
+        const std::int32_t pre_base = static_cast<std::int32_t>(r) * S + MC;
+        if (!t.init) t.reset(static_cast<std::int32_t>(r) * S + 2 * MC, static_cast<std::int32_t>(cfg.trie_slots));
+        const std::int32_t n_comm = P + static_cast<std::int32_t>(jc.n_committed);
+        // prefix must agree with the context (committed is append-only; defensive check)
+        std::int32_t pl = static_cast<std::int32_t>(t.prefix.size());
+        std::int32_t agree = 0;
+        while (agree < pl && agree < n_comm && t.prefix[agree] == I.ctx[agree]) ++agree;
+        if (agree < pl) {
+          t.prefix.resize(agree);
+          t.drop_all();
+          pl = agree;
+        }
+        // migrate speculative nodes that became committed into the prefix
+        std::int32_t cur = -1;
+        while (pl < n_comm) {
+          const std::int32_t c = t.find(cur, I.ctx[pl]);
+          if (c < 0) break;
+          copy_src.push_back(t.nodes[c].slot);
+          copy_dst.push_back(pre_base + pl);
+          t.prefix.push_back(I.ctx[pl]);
+          ++pl;
+          cur = c;
+        }
+        if (cur >= 0) t.reroot_at(cur);  // copies are queued before this round's forward
+        if (pl < n_comm) t.drop_all();   // committed diverged from every cached branch
+        // node-slot pressure: stale branches are dropped (never within a round that already
+        // allocated for this request — those slots are written by this round's forward)
+        if (static_cast<std::int32_t>(t.free_slots.size()) < n_ctx - n_comm + 2) {
+          if (t.last_alloc_round == stats.rounds) throw std::logic_error("model path: worker trie slots exhausted");
+          t.drop_all();
+        }
+        // Rows: committed tokens missing from the prefix, else the unmatched tail of the
+        // speculative path; the last token is always fed (its logits are the output).
+        //   prefix_len_g = pl           (committed rows follow)
+        //                = n_ctx - 1    (root job, everything cached: re-feed the last token)
+        //                = n_comm       (leaf job: matched trie ancestors, then the leaf)
+        const std::int32_t prefix_len_g = pl < n_comm ? pl : (n_ctx == n_comm ? n_ctx - 1 : n_comm);
+        std::int32_t q = prefix_len_g;
+        std::int32_t node = -1;
+        if (q == n_comm && n_ctx > n_comm) {
+          q = n_comm;
+          while (q < n_ctx - 1) {
+            const std::int32_t c = t.find(node, I.ctx[q]);
+            if (c < 0) break;
+            b.extra.push_back(t.nodes[c].slot);
+            node = c;
+            ++q;
+          }
+        }
+        const std::int32_t rows = n_ctx - q;
+        for (std::int32_t p = q; p < n_ctx; ++p) {
+          std::int32_t slot;
+          if (p < n_comm) {
+            slot = pre_base + p;
+          } else {
+            std::int32_t c = t.find(node, I.ctx[p]);
+            if (c < 0) {
+              c = t.add(node, I.ctx[p]);
+              t.last_alloc_round = stats.rounds;
+            }
+            slot = t.nodes[c].slot;
+            node = c;
+          }
+          b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
+          b.pos.push_back(p);
+          b.slot.push_back(slot);
+          b.extra.push_back(slot);
+        }
+        for (std::int32_t p = pl; p < std::min(n_comm, n_ctx); ++p) t.prefix.push_back(I.ctx[p]);
+        const std::int32_t extra_len = static_cast<std::int32_t>(b.extra.size()) - eoff;
+        b.groups.push_back(AttnGroup{row0, rows, pre_base, prefix_len_g, eoff, extra_len});
+      }
+      const std::int32_t last = static_cast<std::int32_t>(b.tok.size()) - 1;
+      b.out_rows.push_back(last);
+      b.plant.push_back(p_->plant(I.ctx[n_ctx - 1], true));
+      forced[j] = forced_for(n_ctx - 1);
+    }
+    p_->draft().copy_slots(copy_src, copy_dst, st);
+    std::memcpy(I.h_stage, forced.data(), nd * 4);
+    WS_CUDA(cudaMemcpyAsync(I.d_forced, I.h_stage, nd * 4, cudaMemcpyHostToDevice, st));
+    WS_CUDA(cudaEventRecord(I.e2, st));
+    p_->draft().forward(b, cfg.plant_draft, st);
+    row_stats_bf16(p_->draft().logits(), nd, V, V, 1.0f, I.d_pred, nullptr, I.d_ws, 0, 0, nullptr, nullptr, st,
+                   I.d_forced);
+    WS_CUDA(cudaEventRecord(I.e3, st));
+    WS_CUDA(cudaMemcpyAsync(res.draft.data(), I.d_pred, nd * sizeof(ws_pred), cudaMemcpyDeviceToHost, st));
+    WS_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    WS_CUDA(cudaEventElapsedTime(&ms, I.e2, I.e3));
+    draft_ms += ms;
+    draft_rows_fed += b.tok.size();
+    draft_forwards += 1;
+    stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (copy_src.empty() ? 0 : 1);
+    stats.h2d += nd * 4;
+    stats.d2h += nd * sizeof(ws_pred);
+  }
+  stats.rounds += 1;
+  stats.verify_rows += nv;
+  stats.draft_rows += nd;
+  stats.kernel_ms = target_ms + draft_ms;
+}
+
+}  // namespace wsb

@@ -1,0 +1,81 @@
+// Real-model backend for the batched driver (BASELINE config 3): the controller's verify runs
+// the target model (Llama-3.1-8B shape), the worker's draft rollout and the controller's local
+// draft/catch-up run the draft model (Llama-3.2-1B shape). Each batched round becomes one
+// target forward over every pending verify row and one draft forward over every pending draft
+// row, followed by the fused K3/K4 epilogues.
+//
+// KV caches are content-addressed, like the protocol itself (controller.hpp:145-156): per
+// request a linear target cache and a linear controller-draft cache checked by longest common
+// prefix, and for the worker a linear committed prefix plus a token trie of speculative nodes
+// (the device mirror of the worker's SpecTree). A job feeds exactly the context tokens whose KV
+// is missing; accepted speculative KV migrates into the prefix on commit (slot copies).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/driver.hpp"
+#include "llama.hpp"
+
+namespace wsb {
+
+struct ModelPairCfg {
+  std::string target = "llama3-8b";
+  std::string draft = "llama3.2-1b";
+  std::uint64_t seed = 1;
+  std::uint32_t prompt_len = 128;
+  std::uint32_t max_requests = 256;
+  std::uint32_t max_ctx = 256;     // prompt + generated + k + 2
+  std::uint32_t trie_slots = 512;  // speculative-node KV slots per request (worker)
+  float plant_target = 16.f;       // planted shared bigram bias (logit units)
+  float plant_draft = 16.f;
+  float draft_plant_rate = 0.8f;   // fraction of input tokens whose plant the draft also sees
+};
+
+class ModelPair;
+
+class ModelBackend_Llama : public ModelBackend {
+ public:
+  ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, TokenId eos, std::uint32_t k);
+  ~ModelBackend_Llama() override;
+  void run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t sample_seed) override;
+  bool wants_context() const override { return true; }
+  double target_ms = 0, draft_ms = 0;
+  std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
+
+ private:
+  ModelPair* p_;
+  std::uint32_t L_;
+  TokenId eos_;
+  std::uint32_t k_;
+};
+
+// Owns both models, their KV caches and the per-request cache state on one device.
+class ModelPair {
+ public:
+  ModelPair(const ModelPairCfg& cfg, int device);
+  ~ModelPair();
+  void reset_requests();  // forget all cached KV state (new run)
+  const ModelPairCfg& cfg() const { return cfg_; }
+  LlamaModel& target() { return *target_; }
+  LlamaModel& draft() { return *draft_; }
+  const std::vector<TokenId>& prompt(std::uint32_t r);
+  std::int32_t plant(TokenId t, bool draft) const;
+  cudaStream_t stream() const { return stream_; }
+
+  struct Impl;
+  std::unique_ptr<Impl> impl;
+
+ private:
+  ModelPairCfg cfg_;
+  int device_;
+  std::unique_ptr<LlamaModel> target_, draft_;
+  std::vector<std::vector<TokenId>> prompts_;
+  cudaStream_t stream_ = nullptr;
+};
+
+}  // namespace wsb
