@@ -162,7 +162,7 @@ def test_model_sim_speculative_equals_greedy(tiny_pair):
 
 def test_model_sim_k8_and_accept_stats(tiny_pair):
     from paper_2602_18931_b200 import abi
-    c = abi.config3(num_requests=8, k=8, seq_len=40, vocab=1000, eos=999)
+    c = abi.config3(num_requests=8, k=8, seq_len=36, vocab=1000, eos=999)
     b = tiny_pair.run_model_sim(c)
     steps = b.step_list()
     assert steps and all(0 <= s[3] <= 8 for s in steps)
