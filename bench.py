@@ -1,37 +1,42 @@
 """Benchmark of the WANSpec verify/draft hot path on B200 (contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1]): the tiny draft/target pair, 64 requests
-per GPU (weak scaling: rank r runs requests [64r, 64r+64) of one dealt stream), k=8, b=2, s=4,
-theta=phi=0.5, RTT 20 ms, max_nodes=256 (the reference livelocks at 64), greedy
-verify by default (--verify rejection for the Philox extension). One "step" = every request of
-the shard decoded to EOS through the batched driver; metric = accepted (committed) tokens/s.
+Default workload (--workload llama; BASELINE.json configs[2], the config the metric's
+"1/2/4/8 B200" is quoted on): Llama-3.1-8B-shape target + Llama-3.2-1B-shape draft, random-init
+bf16 weights, 256 requests of 128-token seeded prompts sharded over the GPUs (strong scaling),
+100 generated tokens each, k=4, b=2, s=4, theta=phi=0.5, RTT 20 ms (virtual clock), greedy
+verify. One step = every request of the shard decoded to EOS through the batched driver, every
+verify / draft model call a batched forward on the GPU. Metric: accepted (committed) tokens/s.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+--workload tiny: BASELINE configs[1], the tiny oracle pair, 64 requests per GPU (weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload llama|tiny]
 """
 import argparse
-import ctypes as C
 import json
 import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "accepted tokens/s (tiny pair, 64 req/GPU, k=8, b=2, s=4, RTT 20 ms)"
+METRIC = "accepted tokens/s at 1/2/4/8 B200 (WANSpec verify + draft rollout)"
 UNIT = "tokens/s"
-REQ_PER_GPU = 64
+TINY_REQ_PER_GPU = 64
+LLAMA_REQUESTS = 256
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=["llama", "tiny"], default="llama")
+    p.add_argument("--k", type=int, default=4)
+    p.add_argument("--requests", type=int, default=LLAMA_REQUESTS)
     p.add_argument("--verify", choices=["greedy", "rejection"], default="greedy")
     p.add_argument("--host-threads", type=int, default=0)
     p.add_argument("--cpu-sample-s", type=float, default=6.0)
@@ -43,23 +48,13 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
-def workload_cfg(world, rank, verify):
-    from paper_2602_18931_b200 import abi
-    c = abi.config2(verify=abi.WS_VERIFY_REJECTION if verify == "rejection" else abi.WS_VERIFY_GREEDY,
-                    num_requests=REQ_PER_GPU * world)
-    c.first_request, c.local_requests = REQ_PER_GPU * rank, REQ_PER_GPU
-    return c
-
-
-def config_block(args, world, host_threads):
-    return {"workload": "BASELINE configs[1]: tiny draft/target pair (oracle tables, V=32768), "
-                        f"{REQ_PER_GPU} requests/GPU, k=8, b=2, s=4, theta=phi=0.5, RTT 20 ms, "
-                        "max_nodes=256",
-            "verify": args.verify, "requests_total": REQ_PER_GPU * world,
-            "parallelism": f"requests sharded over {world} GPU(s), no collective",
-            "host_threads_per_gpu": host_threads,
-            "l2": "inputs (460 KB tables) are L2-resident by design; L2 flushed (256 MB write) "
-                  "before every timed step"}
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback"
 
 
 class ClockSampler:
@@ -104,70 +99,131 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def measured_peak_hbm():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
-    except Exception:
-        return 6650.0, "fallback"
+# ------------------------------------------------------------------ workloads
+def shard(total, world, rank):
+    lo, hi = total * rank // world, total * (rank + 1) // world
+    return lo, hi - lo
 
 
-def k9_algorithmic_bytes(out, k):
-    """Algorithmic bytes of the K9 launches of one run (SURVEY §8d units):
-    verify job: 32 B job + 4k B candidates + 4(k+1) B target ids + 8 B entropy read, 16 B out;
-    draft row: 16 B job + 8 B ids + 24 B probs/entropy read, 40 B out."""
-    v, d = out.verify_rows, out.draft_rows
-    return v * (32 + 4 * k + 4 * (k + 1) + 8 + 16) + d * (16 + 8 + 24 + 40)
+def llama_cfg(args, world, rank):
+    from paper_2602_18931_b200 import abi
+    c = abi.config3(num_requests=args.requests, k=args.k)
+    c.first_request, c.local_requests = shard(args.requests, world, rank)
+    return c
 
 
-def cpu_reference_sample(world, verify, seconds, threads):
-    """The reference's own run_sim_full (oracle/_ref) on this host's cores: bounded sample."""
-    from oracle import pyoracle as po
-    cfg = workload_cfg(1, 0, verify)
-    cfg.num_requests = REQ_PER_GPU * world
-    cfg.first_request, cfg.local_requests = 0, 0
-    toks, t0, runs = 0, time.perf_counter(), 0
-    while True:
-        b = po.ref_run_sim(cfg, threads=threads, with_tokens=False, with_steps=False)
-        toks += sum(m["tokens_committed"] for m in b.metrics_list())
-        runs += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
-    return toks / el, runs, el
+def tiny_cfg(args, world, rank):
+    from paper_2602_18931_b200 import abi
+    c = abi.config2(verify=abi.WS_VERIFY_REJECTION if args.verify == "rejection" else abi.WS_VERIFY_GREEDY,
+                    num_requests=TINY_REQ_PER_GPU * world)
+    c.first_request, c.local_requests = TINY_REQ_PER_GPU * rank, TINY_REQ_PER_GPU
+    return c
 
 
+def config_block(args, world, host_threads):
+    if args.workload == "llama":
+        return {"workload": "BASELINE configs[2]: Llama-3.1-8B-shape target / Llama-3.2-1B-shape draft "
+                            "(random-init bf16), 128-token seeded prompts, 100 generated tokens, "
+                            f"{args.requests} requests, k={args.k}, b=2, s=4, theta=phi=0.5, RTT 20 ms "
+                            "(virtual), greedy verify, planted shared bigram bias (match ~0.8)",
+                "model": "llama3-8b + llama3.2-1b", "global_batch": args.requests, "seq_len": 128 + 100,
+                "parallelism": f"requests sharded over {world} GPU(s) (strong scaling), no collective",
+                "l2": "weights (18.5 GB) and KV (>126 MB) exceed L2; no explicit flush needed"}
+    return {"workload": "BASELINE configs[1]: tiny draft/target pair (oracle tables, V=32768), "
+                        f"{TINY_REQ_PER_GPU} requests/GPU, k=8, b=2, s=4, theta=phi=0.5, RTT 20 ms, "
+                        "max_nodes=256", "verify": args.verify,
+            "parallelism": f"requests sharded over {world} GPU(s), no collective",
+            "host_threads_per_gpu": host_threads,
+            "l2": "tables are L2-resident by design; L2 flushed (256 MB write) before every timed step"}
+
+
+def llama_roofline(stats, k, peak_bw, peak_tf, avg_ctx):
+    """Verify-step roofline (SURVEY §8d units): FLOPs = 2 P_mm rows + 4 L rows ctx n_q hd;
+    bytes = 2 P_mm + R ctx KVB + rows KVB + rows V 2 (+ K3 read of the logits)."""
+    P_mm = 7.505e9  # Llama-3.1-8B matmul params incl. LM head
+    L, nq, hd, V, kvb = 32, 32, 128, 128256, 32 * 2 * 8 * 128 * 2
+    fw = max(1, stats["target_forwards"])
+    rows = stats["target_rows"] / fw
+    reqs = rows / (k + 1)
+    flops = 2 * P_mm * rows + 4 * L * rows * avg_ctx * nq * hd
+    byts = 2 * P_mm + reqs * avg_ctx * kvb + rows * kvb + 2 * reqs * (k + 1) * V * 2
+    t_meas = stats["target_ms"] / 1e3 / fw
+    t_tensor, t_hbm = flops / (peak_tf * 1e12), byts / (peak_bw * 1e9)
+    if t_tensor >= t_hbm:
+        return {"bound": "tensor", "achieved": flops / t_meas / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": t_tensor / t_meas}, rows, flops, byts, t_meas
+    return {"bound": "hbm", "achieved": byts / t_meas / 1e9, "peak": peak_bw, "unit": "GB/s",
+            "frac": t_hbm / t_meas}, rows, flops, byts, t_meas
+
+
+def cpu_port_sample(args, stats, tokens, k):
+    """CPU port (oracle/llama_cpu.py, numpy fp32, all host cores) on a bounded sample: one verify
+    forward of one request (k+1 rows after a 160-token context) and one draft forward (1 row),
+    scaled by this run's own per-request step counts."""
+    from oracle import llama_cpu
+    t_v = llama_cpu.time_forward("llama3-8b", k + 1, 160, lm_rows=k + 1)
+    t_d = llama_cpu.time_forward("llama3.2-1b", 1, 160, lm_rows=1)
+    n_v = stats["target_forwards_per_request"]
+    n_d = stats["draft_rows_per_request"]
+    per_req = n_v * t_v + n_d * t_d
+    return {"value": (tokens / stats["requests"]) / per_req, "unit": UNIT, "cores": os.cpu_count() or 1,
+            "kind": "port",
+            "sample": f"numpy fp32 port: one 8B verify forward ({k + 1} rows, ctx 160) = {t_v:.2f} s and one 1B "
+                      f"draft row = {t_d:.2f} s, x this run's per-request counts ({n_v:.1f} verifies, "
+                      f"{n_d:.1f} draft rows); one request at a time"}
+
+
+# ------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from oracle import pyoracle as po
-    if not po.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
-        return
     threads = os.cpu_count() or 1
-    cfg = workload_cfg(1, 0, args.verify)
-    cfg.num_requests = REQ_PER_GPU * world
-    cfg.first_request, cfg.local_requests = 0, 0
-    for _ in range(args.warmup):
-        po.ref_run_sim(cfg, threads=threads, with_tokens=False, with_steps=False)
-    toks = 0
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        b = po.ref_run_sim(cfg, threads=threads, with_tokens=False, with_steps=False)
-        toks += sum(m["tokens_committed"] for m in b.metrics_list())
-    el = time.perf_counter() - t0
-    value = toks / el
+    if args.workload == "tiny":
+        from oracle import pyoracle as po
+        if not po.ref_available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+            return
+        cfg = tiny_cfg(args, 1, 0)
+        cfg.num_requests = TINY_REQ_PER_GPU * world
+        cfg.first_request, cfg.local_requests = 0, 0
+        for _ in range(args.warmup):
+            po.ref_run_sim(cfg, threads=threads, with_tokens=False, with_steps=False)
+        toks, t0 = 0, time.perf_counter()
+        for _ in range(args.steps):
+            b = po.ref_run_sim(cfg, threads=threads, with_tokens=False, with_steps=False)
+            toks += sum(m["tokens_committed"] for m in b.metrics_list())
+        el = time.perf_counter() - t0
+        value, sample, kind = toks / el, f"{args.steps} full runs of {cfg.num_requests} requests " \
+                                         "(run_sim_full via oracle/_ref, requests over threads)", "reference"
+    else:
+        # The reference has no model (SURVEY §0.1): its CPU implementation of the config-3 path is
+        # the oracle port (numpy fp32 Llama forward) driven by the reference protocol's step
+        # counts; each step times one 8B verify forward + k 1B draft rows of one request.
+        from oracle import llama_cpu
+        k = args.k
+        for _ in range(max(0, args.warmup - 2)):
+            llama_cpu.time_forward("llama3.2-1b", 1, 160, lm_rows=1)
+        el, toks = 0.0, 0.0
+        for _ in range(args.steps):
+            t_v = llama_cpu.time_forward("llama3-8b", k + 1, 160, lm_rows=k + 1)
+            t_d = llama_cpu.time_forward("llama3.2-1b", 1, 160, lm_rows=1)
+            el += t_v + k * t_d
+            toks += 0.8 * k + 1  # expected committed tokens per verify at match 0.8 (greedy, k drafted)
+        value = toks / el
+        sample = (f"{args.steps} x (one 8B verify forward of {k + 1} rows + {k} 1B draft rows, ctx 160), "
+                  "numpy fp32 on all host cores; tokens per verify = 0.8k+1")
+        kind = "port"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000 * el / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference", "config": config_block(args, world, threads),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{args.steps} full runs of {REQ_PER_GPU * world} requests "
-                                       "(run_sim_full via oracle/_ref, requests partitioned over threads)"},
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong" if args.workload == "llama" else "weak", "vs_baseline": None,
+            "dtype": "bf16" if args.workload == "llama" else "f64", "data": "synthetic", "impl": "reference",
+            "config": config_block(args, world, threads),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
+# ------------------------------------------------------------------ our arm
 def main():
     args = parse()
     rank, local_rank, world = dist_env()
@@ -185,103 +241,121 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    ncpu = os.cpu_count() or 1
-    host_threads = args.host_threads or max(1, min(16, ncpu // max(1, world)))
-    cfg = workload_cfg(world, rank, args.verify)
-    cfg.host_threads = host_threads
-    ctx = ws.Context(local_rank)
-    recs = ws.oracle_synth(cfg.oracle, cfg.num_requests)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-
     def barrier():
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-resident path: tables in HBM before the timed region ----
-    ctx.load_oracle(recs, cfg.num_requests, cfg.oracle)
+    ncpu = os.cpu_count() or 1
+    host_threads = args.host_threads or max(1, min(16, ncpu // max(1, world)))
+    ctx = ws.Context(local_rank)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    peak_bw, peak_tf, peak_kind = peaks()
+
+    if args.workload == "llama":
+        cfg = llama_cfg(args, world, rank)
+        ctx.load_models(abi.model_cfg(max_requests=args.requests))
+
+        def run_once(tokens_out=False):
+            return ctx.run_model_sim(cfg, with_tokens=tokens_out, with_steps=False)
+    else:
+        cfg = tiny_cfg(args, world, rank)
+        cfg.host_threads = host_threads
+        recs = ws.oracle_synth(cfg.oracle, cfg.num_requests)
+        ctx.load_oracle(recs, cfg.num_requests, cfg.oracle)
+
+        def run_once(tokens_out=False):
+            return ctx.run_sim_full(cfg, with_tokens=tokens_out, with_steps=False, resident=True)
+
     for _ in range(args.warmup):
-        ctx.run_sim_full(cfg, with_tokens=False, with_steps=False, resident=True)
-    tokens, total_ms, launches, kernel_ms, alg_bytes = 0, 0.0, 0, 0.0, 0
+        run_once()
+    tokens, total_ms, launches, kernel_ms, h2d, d2h = 0, 0.0, 0, 0.0, 0, 0
+    mstats = {"target_ms": 0.0, "draft_ms": 0.0, "target_rows": 0, "draft_rows": 0, "target_forwards": 0,
+              "draft_forwards": 0}
     barrier()
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
-            flush.fill_(1.0)
+            if args.workload == "tiny":
+                flush.fill_(1.0)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            b = ctx.run_sim_full(cfg, with_tokens=False, with_steps=False, resident=True)
+            b = run_once(tokens_out=True)
             e1.record()
             torch.cuda.synchronize()
             total_ms += e0.elapsed_time(e1)
             tokens += sum(m["tokens_committed"] for m in b.metrics_list())
             launches += b.out.gpu_launches
             kernel_ms += b.out.kernel_ms
-            alg_bytes += k9_algorithmic_bytes(b.out, cfg.k)
+            h2d += b.out.h2d_bytes
+            d2h += b.out.d2h_bytes + sum(b.ctrl_len[i] for i in range(b.n)) * 4
+            if args.workload == "llama":
+                for kk, v in ctx.model_stats().items():
+                    mstats[kk] += v
     barrier()
 
-    # ---- end to end through the public C-ABI call: host tables -> HBM, results -> host ----
-    e2e_ms, e2e_tokens, h2d, d2h = 0.0, 0, 0, 0
-    for i in range(args.steps):
-        flush.fill_(1.0)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        ctx.load_oracle(recs, cfg.num_requests, cfg.oracle)
-        b = ctx.run_sim_full(cfg, with_tokens=True, with_steps=False, resident=True)
-        e1.record()
-        torch.cuda.synchronize()
-        e2e_ms += e0.elapsed_time(e1)
-        e2e_tokens += sum(m["tokens_committed"] for m in b.metrics_list())
-        h2d += b.out.h2d_bytes + cfg.num_requests * cfg.oracle.sequence_length * 64  # SoA tables
-        d2h += b.out.d2h_bytes
-    barrier()
-
-    stats = torch.tensor([total_ms, float(tokens), e2e_ms, float(e2e_tokens), float(launches)],
-                         dtype=torch.float64, device="cuda")
+    stats = torch.tensor([total_ms, float(tokens), float(launches)], dtype=torch.float64, device="cuda")
     if dist:
-        mx = stats.clone()
+        mx, sm = stats.clone(), stats.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = stats.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        total_ms_max, e2e_ms_max = mx[0].item(), mx[2].item()
-        tokens_all, e2e_tokens_all, launches_all = sm[1].item(), sm[3].item(), sm[4].item()
+        total_ms_max, tokens_all, launches_all = mx[0].item(), sm[1].item(), sm[2].item()
     else:
-        total_ms_max, e2e_ms_max = total_ms, e2e_ms
-        tokens_all, e2e_tokens_all, launches_all = float(tokens), float(e2e_tokens), float(launches)
+        total_ms_max, tokens_all, launches_all = total_ms, float(tokens), float(launches)
 
     if rank == 0:
-        peak, peak_kind = measured_peak_hbm()
-        avg_kernel_s = (kernel_ms / 1000.0) / max(1, launches)
-        achieved = (alg_bytes / max(1, launches)) / avg_kernel_s / 1e9 if avg_kernel_s > 0 else 0.0
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "k9_traffic.json")) as f:
-                traffic = json.load(f).get("bytes_per_launch")
-        except Exception:
-            pass
-        cpu_value, runs, el = cpu_reference_sample(1, args.verify, args.cpu_sample_s, ncpu) \
-            if world == 1 else (None, 0, 0)
         value = tokens_all / (total_ms_max / 1000.0)
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args, world, host_threads),
-            "e2e": {"value": e2e_tokens_all / (e2e_ms_max / 1000.0), "unit": UNIT,
-                    "h2d_bytes_per_step": h2d // max(1, args.steps),
-                    "d2h_bytes_per_step": d2h // max(1, args.steps)},
-            "gpu_launches": int(launches_all),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k9_round", "peak_kind": peak_kind,
-                         "note": "K9 moves ~100 KB/launch: latency-bound by construction"},
-            "clocks": clk.summary(),
-        }
-        if cpu_value is not None:
-            line["cpu_baseline"] = {"value": cpu_value, "unit": UNIT, "cores": ncpu, "kind": "reference",
-                                    "sample": f"{runs} runs of 64 requests in {el:.1f} s "
-                                              "(reference run_sim_full via oracle/_ref, all host cores)"}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+                "scaling": "strong" if args.workload == "llama" else "weak", "vs_baseline": None,
+                "dtype": "bf16" if args.workload == "llama" else "f64", "data": "synthetic",
+                "config": config_block(args, world, host_threads),
+                # the public C-ABI call is already end to end: host protocol → per-round H2D of the
+                # batch (tokens, positions, slots, groups, candidates) → forwards → D2H of results
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(1, args.steps),
+                        "d2h_bytes_per_step": d2h // max(1, args.steps)},
+                "gpu_launches": int(launches_all), "clocks": clk.summary()}
+        if args.workload == "llama":
+            local = cfg.local_requests
+            avg_ctx = 128 + 50 + args.k / 2
+            roof, rows, fl, by, t_meas = llama_roofline(mstats, args.k, peak_bw, peak_tf, avg_ctx)
+            roof.update({"traffic": None, "kernel": "verify step (target forward + K3/K4)",
+                         "peak_kind": peak_kind, "rows_per_verify": rows, "ms_per_verify": t_meas * 1e3,
+                         "alg_flops_per_verify": fl, "alg_bytes_per_verify": by})
+            line["roofline"] = roof
+            line["model_time"] = {k: (v / args.steps if isinstance(v, float) else v // args.steps)
+                                  for k, v in mstats.items()}
+            if world == 1:
+                per = {"requests": local,
+                       "target_forwards_per_request": mstats["target_rows"] / args.steps / local / (args.k + 1),
+                       "draft_rows_per_request": mstats["draft_rows"] / args.steps / local}
+                try:
+                    line["cpu_baseline"] = cpu_port_sample(args, per, tokens / args.steps, args.k)
+                except Exception as e:  # the CPU port needs ~2 GB of host RAM per 8B layer
+                    line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+        else:
+            from oracle import pyoracle as po
+            alg = 0
+            line["roofline"] = {"bound": "hbm", "achieved": None, "peak": peak_bw, "unit": "GB/s", "frac": None,
+                                "traffic": None, "kernel": "k9_round", "peak_kind": peak_kind,
+                                "note": "K9 moves ~100 KB/launch: latency-bound by construction"}
+            if kernel_ms > 0 and launches > 0:
+                per_launch_s = kernel_ms / 1e3 / launches
+                k9 = (b.out.verify_rows * (32 + 4 * cfg.k + 4 * (cfg.k + 1) + 8 + 16)
+                      + b.out.draft_rows * 88) / max(1, b.out.gpu_launches)
+                alg = k9 / per_launch_s / 1e9
+                line["roofline"].update({"achieved": alg, "frac": alg / peak_bw})
+            if world == 1 and po.ref_available():
+                t0, toks, runs = time.perf_counter(), 0, 0
+                c1 = tiny_cfg(args, 1, 0)
+                while time.perf_counter() - t0 < args.cpu_sample_s:
+                    rb = po.ref_run_sim(c1, threads=ncpu, with_tokens=False, with_steps=False)
+                    toks += sum(m["tokens_committed"] for m in rb.metrics_list())
+                    runs += 1
+                el = time.perf_counter() - t0
+                line["cpu_baseline"] = {"value": toks / el, "unit": UNIT, "cores": ncpu, "kind": "reference",
+                                        "sample": f"{runs} runs of 64 requests (reference run_sim_full via "
+                                                  "oracle/_ref, all host cores)"}
         print(json.dumps(line))
     ctx.close()
     if dist:
