@@ -281,7 +281,7 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
   if (nd) {
     ForwardBatch& b = I.db;
     b.clear();
-    std::vector<std::int32_t> forced(nd), copy_src, copy_dst;
+    std::vector<std::int32_t> job_out(nd, -1), copy_src, copy_dst;
     const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg.trie_slots);
     for (std::uint32_t j = 0; j < nd; ++j) {
       const DraftJob& dj = jobs.draft[j];
@@ -289,6 +289,12 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
       const std::uint32_t r = dj.seq;
       fill_ctx(p_->prompt(r), jc);
       const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
+      if (forced_for(n_ctx - 1) >= 0) {
+        // Past the generation cap the prediction is a confident EOS whatever the context
+        // (oracle.hpp:88-102): no forward, no KV (every descendant is forced too).
+        job_out[j] = -1;
+        continue;
+      }
       if (n_ctx > MC) throw ConfigError("model path: context exceeds max_ctx");
       const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
       const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
@@ -380,28 +386,40 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         b.groups.push_back(AttnGroup{row0, rows, pre_base, prefix_len_g, eoff, extra_len});
       }
       const std::int32_t last = static_cast<std::int32_t>(b.tok.size()) - 1;
+      job_out[j] = static_cast<std::int32_t>(b.out_rows.size());
       b.out_rows.push_back(last);
       b.plant.push_back(p_->plant(I.ctx[n_ctx - 1], true));
-      forced[j] = forced_for(n_ctx - 1);
     }
-    p_->draft().copy_slots(copy_src, copy_dst, st);
-    std::memcpy(I.h_stage, forced.data(), nd * 4);
-    WS_CUDA(cudaMemcpyAsync(I.d_forced, I.h_stage, nd * 4, cudaMemcpyHostToDevice, st));
-    WS_CUDA(cudaEventRecord(I.e2, st));
-    p_->draft().forward(b, cfg.plant_draft, st);
-    row_stats_bf16(p_->draft().logits(), nd, V, V, 1.0f, I.d_pred, nullptr, I.d_ws, 0, 0, nullptr, nullptr, st,
-                   I.d_forced);
-    WS_CUDA(cudaEventRecord(I.e3, st));
-    WS_CUDA(cudaMemcpyAsync(res.draft.data(), I.d_pred, nd * sizeof(ws_pred), cudaMemcpyDeviceToHost, st));
-    WS_CUDA(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    WS_CUDA(cudaEventElapsedTime(&ms, I.e2, I.e3));
-    draft_ms += ms;
-    draft_rows_fed += b.tok.size();
-    draft_forwards += 1;
-    stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (copy_src.empty() ? 0 : 1);
-    stats.h2d += nd * 4;
-    stats.d2h += nd * sizeof(ws_pred);
+    const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
+    std::vector<ws_pred> outp(n_out);
+    if (n_out) {
+      p_->draft().copy_slots(copy_src, copy_dst, st);
+      WS_CUDA(cudaEventRecord(I.e2, st));
+      p_->draft().forward(b, cfg.plant_draft, st);
+      row_stats_bf16(p_->draft().logits(), n_out, V, V, 1.0f, I.d_pred, nullptr, I.d_ws, 0, 0, nullptr, nullptr, st,
+                     nullptr);
+      WS_CUDA(cudaEventRecord(I.e3, st));
+      WS_CUDA(cudaMemcpyAsync(outp.data(), I.d_pred, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, st));
+      WS_CUDA(cudaStreamSynchronize(st));
+      float ms = 0.f;
+      WS_CUDA(cudaEventElapsedTime(&ms, I.e2, I.e3));
+      draft_ms += ms;
+      draft_rows_fed += b.tok.size();
+      draft_forwards += 1;
+      stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (copy_src.empty() ? 0 : 1);
+      stats.d2h += n_out * sizeof(ws_pred);
+    }
+    for (std::uint32_t j = 0; j < nd; ++j) {
+      if (job_out[j] >= 0) {
+        res.draft[j] = outp[job_out[j]];
+      } else {
+        ws_pred e{};
+        e.n = 1;
+        e.id[0] = eos_;
+        e.prob[0] = 1.0;
+        res.draft[j] = e;
+      }
+    }
   }
   stats.rounds += 1;
   stats.verify_rows += nv;
