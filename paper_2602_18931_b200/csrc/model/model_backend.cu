@@ -236,7 +236,8 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
       I.ctx.insert(I.ctx.end(), jobs.cands.begin() + vj.cand_off, jobs.cands.begin() + vj.cand_off + vj.k);
       const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
       const std::int32_t first = n_ctx - static_cast<std::int32_t>(k_) - 1;  // = P + base - 1
-      if (n_ctx > MC) throw ConfigError("model path: context exceeds max_ctx");
+      if (n_ctx > MC)
+        throw ConfigError("model path: verify context " + std::to_string(n_ctx) + " exceeds max_ctx");
       LinearCache& c = I.tgt[r];
       std::int32_t lcp = 0;
       while (lcp < first && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
@@ -295,7 +296,10 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         job_out[j] = -1;
         continue;
       }
-      if (n_ctx > MC) throw ConfigError("model path: context exceeds max_ctx");
+      if (n_ctx > MC)
+        throw ConfigError("model path: draft context " + std::to_string(n_ctx) + " exceeds max_ctx (kind " +
+                          std::to_string(jc.kind) + ", committed " + std::to_string(jc.n_committed) + ", len " +
+                          std::to_string(jc.len) + ")");
       const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
       const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
       if (jc.kind == kJobCtrlDraft) {  // controller local draft + catch-up prefill (controller.hpp:194-208)
