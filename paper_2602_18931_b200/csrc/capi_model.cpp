@@ -1,6 +1,8 @@
 // C ABI of the real-model path (include/wanspec_b200.h "real-model pair").
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -75,6 +77,15 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
     wsb::run_shard(c, cfg, backend, out, ctx->device);
     g_last = LastStats{backend.target_ms, backend.draft_ms, backend.target_rows, backend.draft_rows_fed,
                        backend.target_forwards, backend.draft_forwards};
+    if (std::getenv("WS_DEBUG_ROWS"))
+      std::fprintf(stderr,
+                   "[ws] target rows %llu in %llu fwd (%.1f ms) | draft rows ctrl %llu / %llu jobs, worker %llu / "
+                   "%llu jobs in %llu fwd (%.1f ms)\n",
+                   (unsigned long long)backend.target_rows, (unsigned long long)backend.target_forwards,
+                   backend.target_ms, (unsigned long long)backend.rows_by_kind[1],
+                   (unsigned long long)backend.jobs_by_kind[1], (unsigned long long)backend.rows_by_kind[2],
+                   (unsigned long long)backend.jobs_by_kind[2], (unsigned long long)backend.draft_forwards,
+                   backend.draft_ms);
   });
 }
 

@@ -148,6 +148,9 @@ struct Partial {
   std::uint32_t i1, i2, pad;
 };
 
+constexpr std::uint32_t kMaxRows = 65535;  // grid.y limit
+constexpr std::size_t kTicketBytes = 2 * 65536 * sizeof(std::uint32_t);
+
 __device__ void finalize(const State& a, float cl, std::uint32_t vocab, ws_pred* pred, RowStats* st,
                          std::int32_t forced) {
   if (forced >= 0) {  // past-the-end rule: fully confident prediction, entropy 0
@@ -267,8 +270,8 @@ __global__ void __launch_bounds__(kThreads) row_stats_kernel(
 
 std::size_t rowstats_workspace_bytes(std::uint32_t rows, std::uint32_t vocab, std::uint32_t n_req) {
   const std::uint32_t splits = (vocab + kRowChunk - 1) / kRowChunk;
-  return static_cast<std::size_t>(rows) * splits * sizeof(Partial) + static_cast<std::size_t>(rows) * 4 +
-         static_cast<std::size_t>(n_req) * 4 + 64;
+  (void)n_req;
+  return kTicketBytes + static_cast<std::size_t>(rows) * splits * sizeof(Partial) + 64;
 }
 
 void row_stats_bf16(const void* logits, std::uint32_t rows, std::uint32_t vocab, std::uint32_t ld, float inv_temp,
@@ -283,11 +286,13 @@ void row_stats_bf16(const void* logits, std::uint32_t rows, std::uint32_t vocab,
   if (splits > 1 || cand) {
     if (!workspace) throw std::invalid_argument("row_stats: workspace required");
   }
+  if (rows > kMaxRows || n_req > kMaxRows) throw std::invalid_argument("row_stats: too many rows");
+  // Fixed layout whatever the row count: [row tickets | request tickets | partials]. The tickets
+  // self-reset, so they must not move between launches of different sizes.
   unsigned char* ws = static_cast<unsigned char*>(workspace);
-  Partial* partials = reinterpret_cast<Partial*>(ws);
-  std::uint32_t* row_ticket =
-      reinterpret_cast<std::uint32_t*>(ws + static_cast<std::size_t>(rows) * splits * sizeof(Partial));
-  std::uint32_t* req_ticket = row_ticket + rows;
+  std::uint32_t* row_ticket = reinterpret_cast<std::uint32_t*>(ws);
+  std::uint32_t* req_ticket = row_ticket + kMaxRows;
+  Partial* partials = reinterpret_cast<Partial*>(ws + kTicketBytes);
   const bool vec_ok = (reinterpret_cast<std::uintptr_t>(logits) % 16 == 0) && (ld % 8 == 0);
   dim3 grid(splits, rows);
   row_stats_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const __nv_bfloat16*>(logits), vocab, ld,

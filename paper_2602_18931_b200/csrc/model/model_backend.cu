@@ -390,6 +390,8 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         b.groups.push_back(AttnGroup{row0, rows, pre_base, prefix_len_g, eoff, extra_len});
       }
       const std::int32_t last = static_cast<std::int32_t>(b.tok.size()) - 1;
+      rows_by_kind[jc.kind] += static_cast<std::uint64_t>(last + 1 - row0);
+      jobs_by_kind[jc.kind] += 1;
       job_out[j] = static_cast<std::int32_t>(b.out_rows.size());
       b.out_rows.push_back(last);
       b.plant.push_back(p_->plant(I.ctx[n_ctx - 1], true));

@@ -46,6 +46,7 @@ class ModelBackend_Llama : public ModelBackend {
   bool wants_context() const override { return true; }
   double target_ms = 0, draft_ms = 0;
   std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
+  std::uint64_t rows_by_kind[3] = {0, 0, 0}, jobs_by_kind[3] = {0, 0, 0};  // JobKind
 
  private:
   ModelPair* p_;

@@ -102,6 +102,23 @@ def test_batch_invariance(L):
     assert part[23] == full[123]
 
 
+def test_workspace_reuse_across_row_counts(L):
+    """The self-resetting tickets live at fixed offsets: one workspace serves launches of any
+    size in any order (the model backend reuses it every round)."""
+    V = 128256
+    ws = torch.zeros(L.ws_op_row_stats_workspace_bytes(600, V, 0), dtype=torch.uint8, device="cuda")
+    for rows in (600, 37, 255, 1, 600, 90):
+        x = make_logits(rows, V, 3.0, rows, planted=5.0)
+        out = torch.zeros(rows * C.sizeof(abi.Pred), dtype=torch.uint8, device="cuda")
+        rc = L.ws_op_row_stats_bf16(x.data_ptr(), rows, V, V, 1.0, out.data_ptr(), None, ws.data_ptr(),
+                                    torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        got = preds_from(out, rows)
+        want = x.float().argmax(dim=1).cpu().tolist()
+        assert [g[1][0] for g in got] == want
+
+
 @pytest.mark.parametrize("k", [1, 4, 8])
 def test_verify_greedy_epilogue(L, k):
     n_req, V = 50, 128256
