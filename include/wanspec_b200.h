@@ -276,8 +276,9 @@ int ws_model_stats(ws_ctx* ctx, double* target_ms, double* draft_ms, uint64_t* t
                    uint64_t* draft_rows, uint64_t* target_forwards, uint64_t* draft_forwards);
 
 /* single-model forward surface (tests): rows (token, position, KV slot), attention groups
- * {row0, n_rows, prefix_slot, prefix_len, extra_off, extra_len} (6 int32 each) over the slot
- * pool, logits of out_rows → logits_out (device bf16 [n_out, vocab]). */
+ * {row0, n_rows, prefix_slot, prefix_len, extra_off, extra_len, masked} (7 int32 each) over
+ * the slot pool — causal within a group, or (masked) row j sees the extras whose bits are set
+ * in row_mask[row0 + j] — and the logits of out_rows → logits_out (device bf16 [n_out, V]). */
 typedef struct ws_model ws_model;
 int ws_model_create(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device,
                     ws_model** out);
@@ -285,8 +286,8 @@ int ws_model_destroy(ws_model* m);
 int ws_model_copy_weight(ws_model* m, const char* which, int layer, void* dst_dev, int64_t numel);
 int ws_model_forward(ws_model* m, int n_rows, const int32_t* tok, const int32_t* pos,
                      const int32_t* slot, int n_groups, const int32_t* groups, int n_extra,
-                     const int32_t* extra, int n_out, const int32_t* out_rows, void* logits_out,
-                     void* stream);
+                     const int32_t* extra, const uint64_t* row_mask, int n_out,
+                     const int32_t* out_rows, void* logits_out, void* stream);
 
 /* ---- host-logic seam (tests / alternative model providers) ----
  * The batched driver with the model round supplied by the caller instead of the GPU: one

@@ -125,8 +125,8 @@ int ws_model_copy_weight(ws_model* m, const char* which, int layer, void* dst, i
 }
 
 int ws_model_forward(ws_model* m, int n_rows, const int32_t* tok, const int32_t* pos, const int32_t* slot,
-                     int n_groups, const int32_t* groups, int n_extra, const int32_t* extra, int n_out,
-                     const int32_t* out_rows, void* logits_out, void* stream) {
+                     int n_groups, const int32_t* groups, int n_extra, const int32_t* extra,
+                     const uint64_t* row_mask, int n_out, const int32_t* out_rows, void* logits_out, void* stream) {
   return guard("ws_model_forward", [&] {
     if (!m || n_rows <= 0 || !tok || !pos || !slot || !groups || n_groups <= 0) throw std::invalid_argument("bad argument");
     WS_CUDA(cudaSetDevice(m->device));
@@ -135,9 +135,13 @@ int ws_model_forward(ws_model* m, int n_rows, const int32_t* tok, const int32_t*
     b.pos.assign(pos, pos + n_rows);
     b.slot.assign(slot, slot + n_rows);
     for (int g = 0; g < n_groups; ++g) {
-      const int32_t* q = groups + 6 * g;
-      b.groups.push_back(wsb::AttnGroup{q[0], q[1], q[2], q[3], q[4], q[5]});
+      const int32_t* q = groups + 7 * g;
+      if (q[6] && q[5] > 64) throw std::invalid_argument("masked group with more than 64 extras");
+      b.groups.push_back(wsb::AttnGroup{q[0], q[1], q[2], q[3], q[4], q[5], q[6] ? 1 : 0, 0});
     }
+    b.row_mask.assign(n_rows, 0ull);
+    if (row_mask)
+      for (int i = 0; i < n_rows; ++i) b.row_mask[i] = row_mask[i];
     if (n_extra > 0) b.extra.assign(extra, extra + n_extra);
     if (n_out > 0) b.out_rows.assign(out_rows, out_rows + n_out);
     for (int i = 0; i < n_rows; ++i)

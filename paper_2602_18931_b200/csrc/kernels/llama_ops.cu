@@ -106,133 +106,6 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int nq
   }
 }
 
-// ---- grouped attention ----
-constexpr int kAttnThreads = 128;
-constexpr int kTile = 32;
-constexpr int kQPW = 4;  // query vectors per warp per pass
-
-template <int HD>
-__global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __nv_bfloat16* __restrict__ q,
-                                                            const __nv_bfloat16* __restrict__ kp,
-                                                            const __nv_bfloat16* __restrict__ vp,
-                                                            const AttnGroup* __restrict__ groups,
-                                                            const std::int32_t* __restrict__ extra, int nq, int nkv,
-                                                            float scale_log2, __nv_bfloat16* __restrict__ out) {
-  constexpr int RW = HD / 2 + 1;  // smem row stride in 32-bit words (bank-conflict-free)
-  constexpr int DPL = HD / 32;    // output dims per lane
-  __shared__ std::uint32_t sK[kTile * RW];
-  __shared__ std::uint32_t sV[kTile * RW];
-  __shared__ float sQ[kAttnThreads / 32][kQPW][HD];
-  __shared__ std::int32_t sSlot[kTile];
-
-  const AttnGroup g = groups[blockIdx.x];
-  const int kvh = blockIdx.y;
-  const int G = nq / nkv;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nvec = g.n_rows * G;
-  const int ctx = g.prefix_len + g.extra_len;
-  const int slot_stride = nkv * HD;
-
-  for (int pass0 = 0; pass0 < nvec; pass0 += (kAttnThreads / 32) * kQPW) {
-    // query vectors of this warp: v = pass0 + warp*kQPW + u ; v → (row j = v / G, head = kvh*G + v % G)
-    float m[kQPW], l[kQPW], o[kQPW][DPL];
-    int last_visible[kQPW];
-#pragma unroll
-    for (int u = 0; u < kQPW; ++u) {
-      m[u] = -INFINITY;
-      l[u] = 0.f;
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) o[u][e] = 0.f;
-      const int v = pass0 + warp * kQPW + u;
-      last_visible[u] = -1;
-      if (v < nvec) {
-        const int j = v / G, h = kvh * G + v % G;
-        last_visible[u] = g.prefix_len + g.extra_len - g.n_rows + j;
-        const __nv_bfloat16* qs = q + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD;
-        for (int d = lane; d < HD; d += 32) sQ[warp][u][d] = __bfloat162float(qs[d]);
-      }
-    }
-    __syncwarp();
-    int max_visible = -1;
-#pragma unroll
-    for (int u = 0; u < kQPW; ++u) max_visible = max(max_visible, last_visible[u]);
-    // block-wide upper bound of positions any warp needs in this pass
-    __shared__ int s_need;
-    if (threadIdx.x == 0) s_need = 0;
-    __syncthreads();
-    atomicMax(&s_need, max_visible + 1);
-    __syncthreads();
-    const int need = min(s_need, ctx);
-
-    for (int p0 = 0; p0 < need; p0 += kTile) {
-      __syncthreads();
-      if (threadIdx.x < kTile) {
-        const int p = p0 + threadIdx.x;
-        sSlot[threadIdx.x] = p < g.prefix_len ? g.prefix_slot + p : (p < ctx ? extra[g.extra_off + p - g.prefix_len] : -1);
-      }
-      __syncthreads();
-      // load K/V tile: kTile positions x HD bf16 = HD/2 words each
-      for (int t = threadIdx.x; t < kTile * (HD / 2); t += kAttnThreads) {
-        const int r = t / (HD / 2), w = t % (HD / 2);
-        const int s = sSlot[r];
-        std::uint32_t kw = 0, vw = 0;
-        if (s >= 0) {
-          const std::size_t base = static_cast<std::size_t>(s) * slot_stride + static_cast<std::size_t>(kvh) * HD;
-          kw = reinterpret_cast<const std::uint32_t*>(kp + base)[w];
-          vw = reinterpret_cast<const std::uint32_t*>(vp + base)[w];
-        }
-        sK[r * RW + w] = kw;
-        sV[r * RW + w] = vw;
-      }
-      __syncthreads();
-      const int p = p0 + lane;
-#pragma unroll
-      for (int u = 0; u < kQPW; ++u) {
-        if (last_visible[u] < p0) continue;  // warp-uniform
-        float s = 0.f;
-        const std::uint32_t* kr = &sK[lane * RW];
-#pragma unroll 8
-        for (int w = 0; w < HD / 2; ++w) {
-          const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kr[w]));
-          s = fmaf(sQ[warp][u][2 * w], kf.x, s);
-          s = fmaf(sQ[warp][u][2 * w + 1], kf.y, s);
-        }
-        s = (p <= last_visible[u] && p < ctx) ? s * scale_log2 : -INFINITY;
-        const float mt = warp_max(s);
-        const float mn = fmaxf(m[u], mt);
-        const float corr = exp2f(m[u] - mn);
-        const float pr = exp2f(s - mn);
-        l[u] = l[u] * corr + warp_sum(pr);
-        m[u] = mn;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) o[u][e] *= corr;
-        for (int jj = 0; jj < kTile; ++jj) {
-          const float pj = __shfl_sync(0xffffffffu, pr, jj);
-          const std::uint32_t* vr = &sV[jj * RW];
-#pragma unroll
-          for (int e = 0; e < DPL; e += 2) {
-            const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[(lane * DPL + e) / 2]));
-            o[u][e] = fmaf(pj, vf.x, o[u][e]);
-            o[u][e + 1] = fmaf(pj, vf.y, o[u][e + 1]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kQPW; ++u) {
-      const int v = pass0 + warp * kQPW + u;
-      if (v >= nvec) continue;
-      const int j = v / G, h = kvh * G + v % G;
-      __nv_bfloat16* os = out + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD + lane * DPL;
-      const float inv = l[u] > 0.f ? 1.f / l[u] : 0.f;
-#pragma unroll
-      for (int e = 0; e < DPL; e += 2)
-        *reinterpret_cast<__nv_bfloat162*>(os + e) = __floats2bfloat162_rn(o[u][e] * inv, o[u][e + 1] * inv);
-    }
-    __syncthreads();
-  }
-}
-
 __global__ void plant_kernel(__nv_bfloat16* logits, int ld, const std::int32_t* plant, float bias, int rows) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
@@ -316,24 +189,6 @@ void rope_kv_append(const void* qkv, int rows, int nq, int nkv, int hd, const st
   rope_append_kernel<<<rows, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(qkv), nq, nkv, hd, pos, slot, inv_freq,
                                            static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_pool),
                                            static_cast<__nv_bfloat16*>(v_pool));
-  WS_CUDA(cudaGetLastError());
-}
-
-void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
-               const std::int32_t* extra, const AttnShape& s, void* out, cudaStream_t st) {
-  if (n_groups <= 0) return;
-  dim3 grid(n_groups, s.n_kv);
-  const float sl2 = s.scale * 1.4426950408889634f;
-  if (s.hd == 128)
-    attn_kernel<128><<<grid, kAttnThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
-        static_cast<const __nv_bfloat16*>(v_pool), groups, extra, s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
-  else if (s.hd == 64)
-    attn_kernel<64><<<grid, kAttnThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
-        static_cast<const __nv_bfloat16*>(v_pool), groups, extra, s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
-  else
-    throw std::invalid_argument("attention: head dim must be 64 or 128");
   WS_CUDA(cudaGetLastError());
 }
 

@@ -11,6 +11,8 @@ namespace wsb {
 // positions live at consecutive pool slots starting at `prefix_slot`; then `extra_len` explicit
 // slots (tree ancestors + the rows' own new slots). Row j (0-based in the group) attends to
 // the prefix and extra[0 .. extra_len - n_rows + j] (causal within the group).
+// masked != 0: row j instead sees the extras whose bits are set in row_mask[row0 + j]
+// (extra_len <= 64) — the shared-prefix tree group of one request's draft leaves.
 struct AttnGroup {
   std::int32_t row0;
   std::int32_t n_rows;
@@ -18,6 +20,8 @@ struct AttnGroup {
   std::int32_t prefix_len;
   std::int32_t extra_off;
   std::int32_t extra_len;
+  std::int32_t masked = 0;
+  std::int32_t pad = 0;
 };
 
 struct AttnShape {
@@ -40,9 +44,10 @@ void rope_kv_append(const void* qkv, int rows, int nq, int nkv, int hd, const st
                     const std::int32_t* slot, const float* inv_freq, void* q_out, void* k_pool, void* v_pool,
                     cudaStream_t st);
 
-// Grouped causal attention over the slot pools → out bf16 [rows, nq * hd].
+// Grouped attention (causal or masked groups) over the slot pools → out bf16 [rows, nq * hd].
 void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
-               const std::int32_t* extra_slots, const AttnShape& shape, void* out, cudaStream_t st);
+               const std::int32_t* extra_slots, const unsigned long long* row_mask, const AttnShape& shape, void* out,
+               cudaStream_t st);
 
 // logits[row, plant[row]] += bias (plant < 0: none) — the planted shared bigram bias.
 void plant_bias(void* logits_bf16, int ld, const std::int32_t* plant, float bias, int rows, cudaStream_t st);

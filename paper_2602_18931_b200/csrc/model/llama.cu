@@ -193,7 +193,8 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
   // ---- one packed H2D for all metadata ----
   const std::size_t s_tok = al(n * 4), s_grp = al(b.groups.size() * sizeof(AttnGroup)), s_ext = al(b.extra.size() * 4 + 4),
                     s_out = al(n_out * 4 + 4);
-  const std::size_t need = 3 * s_tok + s_grp + s_ext + 2 * s_out;
+  const std::size_t s_msk = al(b.row_mask.size() * 8 + 8);
+  const std::size_t need = 3 * s_tok + s_grp + s_ext + 2 * s_out + s_msk;
   if (need > cap_meta_) {
     if (d_meta_) cudaFree(d_meta_);
     if (h_meta_) cudaFreeHost(h_meta_);
@@ -216,6 +217,7 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
   const std::size_t o_ext = put(b.extra.data(), b.extra.size() * 4, s_ext);
   const std::size_t o_out = put(b.out_rows.data(), n_out * 4, s_out);
   const std::size_t o_pl = put(b.plant.data(), b.plant.size() * 4, s_out);
+  const std::size_t o_msk = put(b.row_mask.data(), b.row_mask.size() * 8, s_msk);
   WS_CUDA(cudaMemcpyAsync(d_meta_, h_meta_, o, cudaMemcpyHostToDevice, st));
   h2d_ += o;
   auto I = [&](std::size_t off) { return reinterpret_cast<const std::int32_t*>(d_meta_ + off); };
@@ -231,7 +233,7 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
     gemm_tn(GemmArgs{xn_, wqkv_[l], qkv_, n, s_.qkv_dim(), d, d, d, s_.qkv_dim(), kEpiBF16, 0}, st);
     rope_kv_append(qkv_, n, s_.n_q, s_.n_kv, s_.hd, I(o_pos), I(o_slot), inv_freq_, q_, kp, vp, st);
     attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()),
-              I(o_ext), ash, attn_, st);
+              I(o_ext), reinterpret_cast<const unsigned long long*>(d_meta_ + o_msk), ash, attn_, st);
     gemm_tn(GemmArgs{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0}, st);
     rmsnorm_rows(x_, d, nullptr, mlp_norm_[l], s_.eps, n, d, xn_, d, st);
     gemm_tn(GemmArgs{xn_, wgu_[l], h_, n, 2 * s_.ffn, d, d, d, s_.ffn, kEpiSwiGLU, 0}, st);

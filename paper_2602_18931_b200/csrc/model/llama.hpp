@@ -35,7 +35,9 @@ struct ForwardBatch {
   std::vector<std::int32_t> extra;
   std::vector<std::int32_t> out_rows;
   std::vector<std::int32_t> plant;  // per output row: planted token (or -1)
+  std::vector<unsigned long long> row_mask;  // per row (only read for masked groups)
   void clear() {
+    row_mask.clear();
     tok.clear();
     pos.clear();
     slot.clear();

@@ -251,6 +251,7 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         b.extra.push_back(base_slot + p);
       }
       b.groups.push_back(AttnGroup{row0, n_ctx - lcp, base_slot, lcp, eoff, n_ctx - lcp});
+      b.row_mask.resize(b.tok.size(), 0ull);
       for (std::int32_t p = first; p < n_ctx; ++p) {
         b.out_rows.push_back(row0 + p - lcp);
         b.plant.push_back(p_->plant(I.ctx[p], false));
@@ -283,6 +284,28 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
     ForwardBatch& b = I.db;
     b.clear();
     std::vector<std::int32_t> job_out(nd, -1), copy_src, copy_dst;
+    // the open shared-prefix tree group of one request's worker leaves (masked attention group)
+    struct TreeGroup {
+      bool active = false;
+      std::uint32_t req = 0;
+      std::int32_t row0 = 0, n_rows = 0, prefix_slot = 0, prefix_len = 0;
+      std::vector<std::int32_t> slots;
+      int index_of(std::int32_t s) {
+        for (std::size_t i = 0; i < slots.size(); ++i)
+          if (slots[i] == s) return static_cast<int>(i);
+        slots.push_back(s);
+        return static_cast<int>(slots.size()) - 1;
+      }
+    } wg;
+    std::vector<std::int32_t> anc, row_slots;
+    auto flush_wg = [&] {
+      if (!wg.active) return;
+      const std::int32_t eo = static_cast<std::int32_t>(b.extra.size());
+      b.extra.insert(b.extra.end(), wg.slots.begin(), wg.slots.end());
+      b.groups.push_back(AttnGroup{wg.row0, wg.n_rows, wg.prefix_slot, wg.prefix_len, eo,
+                                   static_cast<std::int32_t>(wg.slots.size()), 1, 0});
+      wg.active = false;
+    };
     const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg.trie_slots);
     for (std::uint32_t j = 0; j < nd; ++j) {
       const DraftJob& dj = jobs.draft[j];
@@ -300,6 +323,7 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         throw ConfigError("model path: draft context " + std::to_string(n_ctx) + " exceeds max_ctx (kind " +
                           std::to_string(jc.kind) + ", committed " + std::to_string(jc.n_committed) + ", len " +
                           std::to_string(jc.len) + ")");
+      if (jc.kind == kJobCtrlDraft) flush_wg();
       const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
       const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
       if (jc.kind == kJobCtrlDraft) {  // controller local draft + catch-up prefill (controller.hpp:194-208)
@@ -356,17 +380,19 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         const std::int32_t prefix_len_g = pl < n_comm ? pl : (n_ctx == n_comm ? n_ctx - 1 : n_comm);
         std::int32_t q = prefix_len_g;
         std::int32_t node = -1;
-        if (q == n_comm && n_ctx > n_comm) {
-          q = n_comm;
+        anc.clear();
+        const bool leaf_job = q == n_comm && n_ctx > n_comm;
+        if (leaf_job) {
           while (q < n_ctx - 1) {
             const std::int32_t c = t.find(node, I.ctx[q]);
             if (c < 0) break;
-            b.extra.push_back(t.nodes[c].slot);
+            anc.push_back(t.nodes[c].slot);
             node = c;
             ++q;
           }
         }
         const std::int32_t rows = n_ctx - q;
+        row_slots.clear();
         for (std::int32_t p = q; p < n_ctx; ++p) {
           std::int32_t slot;
           if (p < n_comm) {
@@ -383,12 +409,41 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
           b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
           b.pos.push_back(p);
           b.slot.push_back(slot);
-          b.extra.push_back(slot);
+          row_slots.push_back(slot);
         }
         for (std::int32_t p = pl; p < std::min(n_comm, n_ctx); ++p) t.prefix.push_back(I.ctx[p]);
-        const std::int32_t extra_len = static_cast<std::int32_t>(b.extra.size()) - eoff;
-        b.groups.push_back(AttnGroup{row0, rows, pre_base, prefix_len_g, eoff, extra_len});
+        if (!leaf_job || anc.size() + row_slots.size() > 64) {
+          // root / catch-up job: its own causal group
+          flush_wg();
+          const std::int32_t eo = static_cast<std::int32_t>(b.extra.size());
+          b.extra.insert(b.extra.end(), anc.begin(), anc.end());
+          b.extra.insert(b.extra.end(), row_slots.begin(), row_slots.end());
+          b.row_mask.resize(b.tok.size(), 0ull);
+          b.groups.push_back(AttnGroup{row0, rows, pre_base, prefix_len_g, eo,
+                                       static_cast<std::int32_t>(b.extra.size()) - eo});
+        } else {
+          // leaf job: joins the request's shared-prefix tree group (one pass over the prefix
+          // for all of the request's leaves); each row sees its ancestor chain + itself
+          if (wg.active && (wg.req != r || wg.slots.size() + anc.size() + row_slots.size() > 64)) flush_wg();
+          if (!wg.active) {
+            wg.active = true;
+            wg.req = r;
+            wg.row0 = row0;
+            wg.n_rows = 0;
+            wg.prefix_slot = pre_base;
+            wg.prefix_len = n_comm;
+            wg.slots.clear();
+          }
+          unsigned long long mask = 0ull;
+          for (std::int32_t s : anc) mask |= 1ull << wg.index_of(s);
+          for (std::int32_t s : row_slots) {
+            mask |= 1ull << wg.index_of(s);
+            b.row_mask.push_back(mask);
+          }
+          wg.n_rows += rows;
+        }
       }
+      if (jc.kind == kJobCtrlDraft) b.row_mask.resize(b.tok.size(), 0ull);
       const std::int32_t last = static_cast<std::int32_t>(b.tok.size()) - 1;
       rows_by_kind[jc.kind] += static_cast<std::uint64_t>(last + 1 - row0);
       jobs_by_kind[jc.kind] += 1;
@@ -396,6 +451,8 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
       b.out_rows.push_back(last);
       b.plant.push_back(p_->plant(I.ctx[n_ctx - 1], true));
     }
+    flush_wg();
+    if (b.row_mask.size() != b.tok.size()) throw std::logic_error("model path: row mask bookkeeping");
     const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
     std::vector<ws_pred> outp(n_out);
     if (n_out) {

@@ -26,7 +26,7 @@ def L():
     lib.ws_model_destroy.argtypes = [C.c_void_p]
     lib.ws_model_copy_weight.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_void_p, C.c_int64]
     lib.ws_model_forward.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
-                                     C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+                                     C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
     return lib
 
 
@@ -106,15 +106,16 @@ class Ref:
         return self.rms(x, self.fn) @ self.lm.T
 
 
-def forward(lib, h, rows, groups, extra, out_rows, vocab):
+def forward(lib, h, rows, groups, extra, out_rows, vocab, masks=None):
     i32 = lambda v: torch.tensor(v, dtype=torch.int32)  # noqa: E731
     tok, pos, slot = (i32([r[k] for r in rows]) for k in range(3))
-    g = i32([x for grp in groups for x in grp])
+    g = i32([x for grp in groups for x in (tuple(grp) + (0,) * (7 - len(grp)))])
+    mk = torch.tensor(masks if masks else [0] * len(rows), dtype=torch.int64)
     ex = i32(extra if extra else [0])
     orows = i32(out_rows)
     out = torch.empty(len(out_rows), vocab, dtype=torch.bfloat16, device="cuda")
     rc = lib.ws_model_forward(h, len(rows), tok.data_ptr(), pos.data_ptr(), slot.data_ptr(), len(groups),
-                              g.data_ptr(), len(extra), ex.data_ptr(), len(out_rows), orows.data_ptr(),
+                              g.data_ptr(), len(extra), ex.data_ptr(), mk.data_ptr(), len(out_rows), orows.data_ptr(),
                               out.data_ptr(), None)
     assert rc == 0
     return out.float()
@@ -199,5 +200,12 @@ def test_forward_prefill_verify_tree(L, name):
         rows = [(Cc[0], 7, 20)]
         got = forward(L, h, rows, [(0, 1, 0, 6, 0, 2)], [6, 20], [0], V)
         check(got, ref.logits(A + [B[0], Cc[0]])[7:8])
+        # 4) masked shared-prefix tree group: leaf X at pos 6 (slot 40) sees only itself; leaf Y
+        #    at pos 7 (slot 41) sees ancestor B[0] (slot 6) and itself — one pass over prefix A
+        X, Y = D[0], D[1]
+        rows = [(X, 6, 40), (Y, 7, 41)]
+        got = forward(L, h, rows, [(0, 2, 0, 6, 0, 3, 1)], [6, 40, 41], [0, 1], V, masks=[0b010, 0b101])
+        check(got[0:1], ref.logits(A + [X])[6:7])
+        check(got[1:2], ref.logits(A + [B[0], Y])[7:8])
     finally:
         L.ws_model_destroy(h)
