@@ -236,10 +236,15 @@ void launch(const GemmArgs& g, cudaStream_t st) {
 }  // namespace
 
 int pick_bn(int M, int N) {
-  // Measured on B200 (profiles/r01_gemm.md): 128x256 tiles win at every verify/draft shape,
-  // including 160-row (HBM-bound) ones — the wider tile halves A re-reads and per-tile overhead.
-  (void)M;
-  return N >= 256 ? 256 : (N >= 128 ? 128 : 64);
+  // Measured on B200 (profiles/r01_gemm.md): 128x256 tiles win whenever they fill the 148 SMs
+  // (they halve A re-reads and per-tile overhead); otherwise the widest tile that still gives
+  // every SM a tile. Numerics do not depend on BN (tests: batch/tile invariance).
+  const int mb = (M + BM - 1) / BM;
+  for (int bn : {256, 128}) {
+    if (N < bn) continue;
+    if (mb * ((N + bn - 1) / bn) >= 148) return bn;
+  }
+  return N >= 64 ? 64 : 64;
 }
 
 void gemm_tn(const GemmArgs& g, cudaStream_t st) {

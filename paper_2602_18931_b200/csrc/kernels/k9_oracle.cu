@@ -332,29 +332,28 @@ OracleLane::OracleLane(const DevTables* tables, int device) : t_(tables), device
 
 OracleLane::~OracleLane() {
   if (h_in_) cudaFreeHost(h_in_);
-  if (h_out_) cudaFreeHost(h_out_);
-  if (d_in_) cudaFree(d_in_);
-  if (d_out_) cudaFree(d_out_);
+  if (h_out_) cudaFreeHost(h_out_);  // d_in_/d_out_ alias these mapped allocations
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
+// Job and result blocks live in mapped pinned host memory: the round's kernel reads the few KB
+// of jobs and writes its results across the bus directly, so a round is one launch + one
+// stream sync (no copy-engine round trips, and rounds of different protocol threads overlap).
 void OracleLane::reserve(std::size_t in_bytes, std::size_t out_bytes) {
   if (in_bytes > cap_in_) {
     const std::size_t c = std::max(in_bytes, 2 * cap_in_);
     if (h_in_) cudaFreeHost(h_in_);
-    if (d_in_) cudaFree(d_in_);
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_in_), c, cudaHostAllocDefault));
-    WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&d_in_), c));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_in_), c, cudaHostAllocMapped));
+    WS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_in_), h_in_, 0));
     cap_in_ = c;
   }
   if (out_bytes > cap_out_) {
     const std::size_t c = std::max(out_bytes, 2 * cap_out_);
     if (h_out_) cudaFreeHost(h_out_);
-    if (d_out_) cudaFree(d_out_);
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), c, cudaHostAllocDefault));
-    WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&d_out_), c));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), c, cudaHostAllocMapped));
+    WS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_out_), h_out_, 0));
     cap_out_ = c;
   }
 }
@@ -374,7 +373,6 @@ void OracleLane::run_round(const RoundJobs& jobs, RoundResults& res, int verify_
   std::memcpy(h_in_, jobs.verify.data(), nv * sizeof(VerifyJob));
   std::memcpy(h_in_ + sv, jobs.cands.data(), jobs.cands.size() * sizeof(std::uint32_t));
   std::memcpy(h_in_ + sv + sc, jobs.draft.data(), nd * sizeof(DraftJob));
-  WS_CUDA(cudaMemcpyAsync(d_in_, h_in_, in_bytes, cudaMemcpyHostToDevice, stream_));
   const std::uint32_t total = nv + nd;
   const std::uint32_t threads = 128, blocks = (total + threads - 1) / threads;
   WS_CUDA(cudaEventRecord(ev0_, stream_));
@@ -385,7 +383,6 @@ void OracleLane::run_round(const RoundJobs& jobs, RoundResults& res, int verify_
       static_cast<std::uint32_t>(sample_seed), static_cast<std::uint32_t>(sample_seed >> 32));
   WS_CUDA(cudaGetLastError());
   WS_CUDA(cudaEventRecord(ev1_, stream_));
-  WS_CUDA(cudaMemcpyAsync(h_out_, d_out_, out_bytes, cudaMemcpyDeviceToHost, stream_));
   WS_CUDA(cudaStreamSynchronize(stream_));
   float ms = 0.f;
   WS_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));

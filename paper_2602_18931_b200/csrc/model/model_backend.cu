@@ -109,7 +109,10 @@ struct ModelPair::Impl {
   std::vector<LinearCache> tgt, ctrl;
   std::vector<TreeCache> wrk;
   // K3/K4 device buffers
-  ws_pred* d_pred = nullptr;
+  ws_pred* d_pred = nullptr;    // target rows (K3/K4)
+  ws_pred* d_pred_d = nullptr;  // draft rows
+  void* d_ws_d = nullptr;       // draft K3 workspace (the two forwards run concurrently)
+  unsigned char* h_res = nullptr;  // pinned results (verify outs | draft preds)
   ws_verify_out* d_vout = nullptr;
   std::uint32_t* d_cands = nullptr;
   std::int32_t* d_forced = nullptr;
@@ -124,6 +127,7 @@ struct ModelPair::Impl {
 ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(device), impl(new Impl) {
   WS_CUDA(cudaSetDevice(device));
   WS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  WS_CUDA(cudaStreamCreateWithFlags(&stream_draft_, cudaStreamNonBlocking));
   const LlamaShape ts = shape_by_name(cfg.target), ds = shape_by_name(cfg.draft);
   if (ts.vocab != ds.vocab) throw ConfigError("target and draft vocabularies differ");
   const std::int64_t R = cfg.max_requests, C = cfg.max_ctx;
@@ -142,14 +146,16 @@ ModelPair::~ModelPair() {
   cudaSetDevice(device_);
   Impl& I = *impl;
   for (void* p : {static_cast<void*>(I.d_pred), static_cast<void*>(I.d_vout), static_cast<void*>(I.d_cands),
-                  static_cast<void*>(I.d_forced), I.d_ws})
+                  static_cast<void*>(I.d_forced), I.d_ws, static_cast<void*>(I.d_pred_d), I.d_ws_d})
     if (p) cudaFree(p);
   if (I.h_stage) cudaFreeHost(I.h_stage);
+  if (I.h_res) cudaFreeHost(I.h_res);
   for (cudaEvent_t e : {I.e0, I.e1, I.e2, I.e3})
     if (e) cudaEventDestroy(e);
   target_.reset();
   draft_.reset();
   if (stream_) cudaStreamDestroy(stream_);
+  if (stream_draft_) cudaStreamDestroy(stream_draft_);
 }
 
 void ModelPair::reset_requests() {
@@ -197,9 +203,10 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
   const std::size_t need_rows = std::max<std::size_t>(nv * (k_ + 1), nd) + 16;
   if (need_rows > I.cap_rows) {
     for (void* q : {static_cast<void*>(I.d_pred), static_cast<void*>(I.d_vout), static_cast<void*>(I.d_cands),
-                    static_cast<void*>(I.d_forced), I.d_ws})
+                    static_cast<void*>(I.d_forced), I.d_ws, static_cast<void*>(I.d_pred_d), I.d_ws_d})
       if (q) cudaFree(q);
     if (I.h_stage) cudaFreeHost(I.h_stage);
+    if (I.h_res) cudaFreeHost(I.h_res);
     I.cap_rows = need_rows * 2;
     WS_CUDA(cudaMalloc(&I.d_pred, I.cap_rows * sizeof(ws_pred)));
     WS_CUDA(cudaMalloc(&I.d_vout, I.cap_rows * sizeof(ws_verify_out)));
@@ -209,6 +216,11 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
                                                       static_cast<std::uint32_t>(I.cap_rows));
     WS_CUDA(cudaMalloc(&I.d_ws, wsb_));
     WS_CUDA(cudaMemset(I.d_ws, 0, wsb_));
+    WS_CUDA(cudaMalloc(&I.d_ws_d, wsb_));
+    WS_CUDA(cudaMemset(I.d_ws_d, 0, wsb_));
+    WS_CUDA(cudaMalloc(&I.d_pred_d, I.cap_rows * sizeof(ws_pred)));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_res),
+                          I.cap_rows * (sizeof(ws_pred) + sizeof(ws_verify_out)) + 256, cudaHostAllocDefault));
     WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_stage),
                           I.cap_rows * (sizeof(ws_pred) + k_ * 4 + 8) + 256, cudaHostAllocDefault));
   }
@@ -268,11 +280,9 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
     row_stats_bf16(p_->target().logits(), nv * (k_ + 1), V, V, 1.0f, I.d_pred, nullptr, I.d_ws, nv, k_, I.d_cands,
                    I.d_vout, st, I.d_forced);
     WS_CUDA(cudaEventRecord(I.e1, st));
-    WS_CUDA(cudaMemcpyAsync(res.verify.data(), I.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
-    WS_CUDA(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    WS_CUDA(cudaEventElapsedTime(&ms, I.e0, I.e1));
-    target_ms += ms;
+    // results land in pinned memory; the draft forward is planned and launched on its own
+    // stream while the target forward runs
+    WS_CUDA(cudaMemcpyAsync(I.h_res, I.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
     target_rows += b.tok.size();
     target_forwards += 1;
     stats.launches += 1 + 8ull * p_->target().shape().layers + 4;
@@ -454,16 +464,18 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
     flush_wg();
     if (b.row_mask.size() != b.tok.size()) throw std::logic_error("model path: row mask bookkeeping");
     const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
-    std::vector<ws_pred> outp(n_out);
+    const ws_pred* outp = reinterpret_cast<const ws_pred*>(I.h_res + I.cap_rows * sizeof(ws_verify_out));
+    cudaStream_t sd = p_->stream_draft();
     if (n_out) {
-      p_->draft().copy_slots(copy_src, copy_dst, st);
-      WS_CUDA(cudaEventRecord(I.e2, st));
-      p_->draft().forward(b, cfg.plant_draft, st);
-      row_stats_bf16(p_->draft().logits(), n_out, V, V, 1.0f, I.d_pred, nullptr, I.d_ws, 0, 0, nullptr, nullptr, st,
-                     nullptr);
-      WS_CUDA(cudaEventRecord(I.e3, st));
-      WS_CUDA(cudaMemcpyAsync(outp.data(), I.d_pred, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, st));
-      WS_CUDA(cudaStreamSynchronize(st));
+      p_->draft().copy_slots(copy_src, copy_dst, sd);
+      WS_CUDA(cudaEventRecord(I.e2, sd));
+      p_->draft().forward(b, cfg.plant_draft, sd);
+      row_stats_bf16(p_->draft().logits(), n_out, V, V, 1.0f, I.d_pred_d, nullptr, I.d_ws_d, 0, 0, nullptr, nullptr,
+                     sd, nullptr);
+      WS_CUDA(cudaEventRecord(I.e3, sd));
+      WS_CUDA(cudaMemcpyAsync(const_cast<ws_pred*>(outp), I.d_pred_d, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost,
+                              sd));
+      WS_CUDA(cudaStreamSynchronize(sd));
       float ms = 0.f;
       WS_CUDA(cudaEventElapsedTime(&ms, I.e2, I.e3));
       draft_ms += ms;
@@ -483,6 +495,13 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         res.draft[j] = e;
       }
     }
+  }
+  if (nv) {
+    WS_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(res.verify.data(), I.h_res, nv * sizeof(ws_verify_out));
+    float ms = 0.f;
+    WS_CUDA(cudaEventElapsedTime(&ms, I.e0, I.e1));
+    target_ms += ms;
   }
   stats.rounds += 1;
   stats.verify_rows += nv;

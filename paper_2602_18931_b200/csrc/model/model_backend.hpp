@@ -67,6 +67,7 @@ class ModelPair {
   const std::vector<TokenId>& prompt(std::uint32_t r);
   std::int32_t plant(TokenId t, bool draft) const;
   cudaStream_t stream() const { return stream_; }
+  cudaStream_t stream_draft() const { return stream_draft_; }
 
   struct Impl;
   std::unique_ptr<Impl> impl;
@@ -76,7 +77,8 @@ class ModelPair {
   int device_;
   std::unique_ptr<LlamaModel> target_, draft_;
   std::vector<std::vector<TokenId>> prompts_;
-  cudaStream_t stream_ = nullptr;
+  cudaStream_t stream_ = nullptr;        // target (verify)
+  cudaStream_t stream_draft_ = nullptr;  // draft (worker + controller local)
 };
 
 }  // namespace wsb

@@ -59,6 +59,20 @@ def test_gemm_swiglu(ops, bn):
     assert rel_err(h, ref) < 6e-3
 
 
+def test_gemm_batch_and_tile_invariance(ops):
+    """A row's output is bit-identical whatever the batch (M) and the N-tile width: each output
+    element's K reduction runs in the same order in every configuration (no split-K) — the
+    property behind "speculative stream == greedy stream" (SURVEY §8c contract 3)."""
+    M, N, K = 700, 4096, 4096
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    ref = ops.gemm(A, W, bn=256)
+    for bn in (64, 128):
+        assert torch.equal(ops.gemm(A, W, bn=bn), ref)
+    for lo, hi in ((0, 1), (5, 37), (128, 300), (690, 700)):
+        assert torch.equal(ops.gemm(A[lo:hi].contiguous(), W, bn=64), ref[lo:hi])
+
+
 def test_gemm_large_throughput_smoke(ops):
     """8B-shape gate/up at 1280 verify rows: correct and finishes."""
     M, N, K = 1280, 28672, 4096
