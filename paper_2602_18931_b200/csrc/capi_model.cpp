@@ -73,8 +73,26 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
       throw wsb::ConfigError("prompt + sequence_length + k exceeds max_ctx");
     WS_CUDA(cudaSetDevice(ctx->device));
     mp.reset_requests();
+    const bool prof = std::getenv("WS_PROFILE") != nullptr;
+    mp.target().profiler().enable(prof);
+    mp.draft().profiler().enable(prof);
     wsb::ModelBackend_Llama backend(&mp, c->oracle.sequence_length, c->oracle.eos_id, c->k);
     wsb::run_shard(c, cfg, backend, out, ctx->device);
+    if (prof) {
+      for (int which = 0; which < 2; ++which) {
+        wsb::KernelProfiler& p = which == 0 ? mp.target().profiler() : mp.draft().profiler();
+        p.collect();
+        std::fprintf(stderr, "[ws-profile] {\"model\": \"%s\"", which == 0 ? "target" : "draft");
+        for (int k = 0; k < wsb::KernelProfiler::kClasses; ++k)
+          std::fprintf(stderr, ", \"%s\": [%.3f, %llu]", wsb::KernelProfiler::name(k), p.ms[k],
+                       static_cast<unsigned long long>(p.count[k]));
+        std::fprintf(stderr, "}\n");
+        for (int k = 0; k < wsb::KernelProfiler::kClasses; ++k) {
+          p.ms[k] = 0;
+          p.count[k] = 0;
+        }
+      }
+    }
     g_last = LastStats{backend.target_ms, backend.draft_ms, backend.target_rows, backend.draft_rows_fed,
                        backend.target_forwards, backend.draft_forwards};
     if (std::getenv("WS_DEBUG_ROWS"))

@@ -225,24 +225,79 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
   const int d = s_.d, qd = s_.n_q * s_.hd;
   const std::int64_t layer_stride = n_slots_ * s_.n_kv * s_.hd;
   const AttnShape ash{s_.n_q, s_.n_kv, s_.hd, s_.n_kv * s_.hd, 1.0f / std::sqrt(static_cast<float>(s_.hd))};
+  prof_.begin(st);
   embed_rows(embed_, I(o_tok), n, d, x_, st);
+  prof_.mark(KernelProfiler::kEmbed, st);
   for (int l = 0; l < s_.layers; ++l) {
     __nv_bfloat16* kp = static_cast<__nv_bfloat16*>(k_pool_) + l * layer_stride;
     __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(v_pool_) + l * layer_stride;
     rmsnorm_rows(x_, d, nullptr, attn_norm_[l], s_.eps, n, d, xn_, d, st);
+    prof_.mark(KernelProfiler::kNorm, st);
     gemm_tn(GemmArgs{xn_, wqkv_[l], qkv_, n, s_.qkv_dim(), d, d, d, s_.qkv_dim(), kEpiBF16, 0}, st);
+    prof_.mark(KernelProfiler::kQKV, st);
     rope_kv_append(qkv_, n, s_.n_q, s_.n_kv, s_.hd, I(o_pos), I(o_slot), inv_freq_, q_, kp, vp, st);
+    prof_.mark(KernelProfiler::kRope, st);
     attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()),
               I(o_ext), reinterpret_cast<const unsigned long long*>(d_meta_ + o_msk), ash, attn_, st);
+    prof_.mark(KernelProfiler::kAttn, st);
     gemm_tn(GemmArgs{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0}, st);
+    prof_.mark(KernelProfiler::kO, st);
     rmsnorm_rows(x_, d, nullptr, mlp_norm_[l], s_.eps, n, d, xn_, d, st);
+    prof_.mark(KernelProfiler::kNorm, st);
     gemm_tn(GemmArgs{xn_, wgu_[l], h_, n, 2 * s_.ffn, d, d, d, s_.ffn, kEpiSwiGLU, 0}, st);
+    prof_.mark(KernelProfiler::kGateUp, st);
     gemm_tn(GemmArgs{h_, wdown_[l], x_, n, d, s_.ffn, s_.ffn, s_.ffn, d, kEpiAddF32, 0}, st);
+    prof_.mark(KernelProfiler::kDown, st);
   }
   if (n_out == 0) return;
   rmsnorm_rows(x_, d, I(o_out), final_norm_, s_.eps, n_out, d, xo_, d, st);
+  prof_.mark(KernelProfiler::kNorm, st);
   gemm_tn(GemmArgs{xo_, lm_head_, logits_, n_out, s_.vocab, d, d, d, s_.vocab, kEpiBF16, 0}, st);
+  prof_.mark(KernelProfiler::kLMHead, st);
   if (plant > 0.f && !b.plant.empty()) plant_bias(logits_, s_.vocab, I(o_pl), plant, n_out, st);
+  prof_.mark(KernelProfiler::kPlant, st);
+}
+
+// ---- KernelProfiler ----
+void KernelProfiler::enable(bool on) {
+  on_ = on;
+}
+void KernelProfiler::begin(cudaStream_t st) {
+  if (!on_) return;
+  collect();
+  if (!start_) WS_CUDA(cudaEventCreate(&start_));
+  WS_CUDA(cudaEventRecord(start_, st));
+  used_ = 0;
+  marks_.clear();
+}
+void KernelProfiler::mark(int cls, cudaStream_t st) {
+  if (!on_) return;
+  if (used_ == pool_.size()) {
+    cudaEvent_t e;
+    WS_CUDA(cudaEventCreate(&e));
+    pool_.push_back(e);
+  }
+  WS_CUDA(cudaEventRecord(pool_[used_], st));
+  marks_.emplace_back(cls, pool_[used_]);
+  ++used_;
+}
+void KernelProfiler::collect() {
+  if (!on_ || marks_.empty()) return;
+  WS_CUDA(cudaEventSynchronize(marks_.back().second));
+  cudaEvent_t prev = start_;
+  for (const auto& [cls, e] : marks_) {
+    float t = 0.f;
+    WS_CUDA(cudaEventElapsedTime(&t, prev, e));
+    ms[cls] += t;
+    count[cls] += 1;
+    prev = e;
+  }
+  marks_.clear();
+}
+const char* KernelProfiler::name(int cls) {
+  static const char* n[] = {"embed", "rmsnorm", "gemm_qkv", "rope_kv_append", "attention", "gemm_o_add",
+                            "gemm_gate_up_swiglu", "gemm_down_add", "gemm_lm_head", "plant_bias"};
+  return cls >= 0 && cls < kClasses ? n[cls] : "?";
 }
 
 }  // namespace wsb

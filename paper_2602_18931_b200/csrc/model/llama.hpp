@@ -48,8 +48,31 @@ struct ForwardBatch {
   }
 };
 
+// Per-kernel-class device time of the forward, from CUDA events recorded between launches on
+// the model's stream (enabled by WS_PROFILE=1; used for the time-share tables in profiles/).
+class KernelProfiler {
+ public:
+  enum Cls { kEmbed, kNorm, kQKV, kRope, kAttn, kO, kGateUp, kDown, kLMHead, kPlant, kClasses };
+  void enable(bool on);
+  bool on() const { return on_; }
+  void begin(cudaStream_t st);
+  void mark(int cls, cudaStream_t st);
+  void collect();  // folds completed marks into ms/count (blocks on the last mark)
+  static const char* name(int cls);
+  double ms[kClasses] = {};
+  std::uint64_t count[kClasses] = {};
+
+ private:
+  bool on_ = false;
+  cudaEvent_t start_ = nullptr;
+  std::vector<cudaEvent_t> pool_;
+  std::size_t used_ = 0;
+  std::vector<std::pair<int, cudaEvent_t>> marks_;
+};
+
 class LlamaModel {
  public:
+  KernelProfiler& profiler() { return prof_; }
   LlamaModel(const LlamaShape& shape, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device);
   ~LlamaModel();
   LlamaModel(const LlamaModel&) = delete;
@@ -72,6 +95,7 @@ class LlamaModel {
 
  private:
   void ensure_rows(int rows, int out_rows);
+  KernelProfiler prof_;
   LlamaShape s_;
   int device_;
   std::int64_t n_slots_;
