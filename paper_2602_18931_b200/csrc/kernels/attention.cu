@@ -2,16 +2,18 @@
 //
 // One CTA per (group, kv head). A group is the set of rows of one request that share a
 // context: a linear committed prefix (prefix_len consecutive slots from prefix_slot, visible to
-// every row) followed by up to 64 explicit "extra" slots (new rows, tree ancestors) whose
-// visibility is either causal (verify rows, catch-up prefill: row j sees extra[0 .. E-n+j]) or
-// given by a per-row 64-bit mask (the worker's tree leaves: each leaf sees its own ancestor
-// chain). Every K/V tile is read from HBM once per (group, kv head) and reused by all
-// n_rows x (n_q / n_kv) query vectors — a request's k+1 verify rows and all its draft leaves
-// share one pass over the prefix.
+// every row) followed by explicit "extra" slots (new rows, tree ancestors) whose visibility is
+// causal (verify rows, catch-up prefill: row j sees extra[0 .. E-n+j]) or given by a per-row
+// 64-bit mask (the worker's tree leaves: each leaf sees its own ancestor chain). Every K/V tile
+// is read from HBM once per (group, kv head) and reused by all n_rows x (n_q / n_kv) query
+// vectors: a request's k+1 verify rows and all its draft leaves share one pass.
 //
-// Per tile of 32 positions: lane = position; the lane's K row lives in registers, query
-// vectors stream from shared memory, online softmax per query vector (exp2 domain), P·V with
-// the probabilities broadcast by shuffles. CUDA cores; the workload is HBM-bound on KV.
+// Math on the tensor cores with warp-level mma.sync m16n8k16 (bf16 in, fp32 accumulate): each
+// warp owns 16 query vectors; S = Q·Kᵀ per 32-position tile (ldmatrix from a 128-byte-XOR-
+// swizzled smem tile), online softmax on the accumulator fragments (exp2 domain), then P·V with
+// the S fragments re-packed as the A operand and V loaded by ldmatrix.trans. K/V tiles are
+// double-buffered with cp.async so the next tile's HBM reads overlap this tile's math. The
+// kernel is HBM-bound on KV bytes; tensor-core throughput is not the limiter at these shapes.
 #include <cuda_bf16.h>
 
 #include <stdexcept>
@@ -23,36 +25,66 @@ namespace wsb {
 
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kTile = 32;
-constexpr int kVPW = 8;  // query vectors per warp per pass
+constexpr int kThreads = 128;  // 4 warps x 16 query vectors
+constexpr int kTile = 32;      // positions per K/V tile
+constexpr int kVecPerPass = 64;
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+__device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(std::uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(std::uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const std::uint32_t (&a)[4], std::uint32_t b0,
+                                         std::uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ std::uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<std::uint32_t*>(&v);
+}
+
+// Tile of HD-wide bf16 rows, 16-byte chunks XOR-swizzled by (row & 7) (conflict-free ldmatrix).
+template <int HD>
+__device__ __forceinline__ int swz(int row, int chunk) {
+  constexpr int C = HD / 8;
+  return row * C + (chunk ^ (row & 7));
 }
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads) attn_kernel(const __nv_bfloat16* __restrict__ q,
-                                                        const __nv_bfloat16* __restrict__ kp,
-                                                        const __nv_bfloat16* __restrict__ vp,
-                                                        const AttnGroup* __restrict__ groups,
-                                                        const std::int32_t* __restrict__ extra,
-                                                        const unsigned long long* __restrict__ row_mask, int nq,
-                                                        int nkv, float scale_log2, __nv_bfloat16* __restrict__ out) {
-  constexpr int W = HD / 2;   // 32-bit words per head vector
-  constexpr int RW = W + 1;   // padded smem row (bank-conflict-free row reads)
-  constexpr int DPL = HD / 32;
-  __shared__ std::uint32_t sK[kTile * RW];
-  __shared__ std::uint32_t sV[kTile * RW];
-  __shared__ __align__(16) float sQ[kThreads / 32][kVPW][HD];
-  __shared__ std::int32_t sSlot[kTile];
+__global__ void __launch_bounds__(kThreads) attn_mma_kernel(const __nv_bfloat16* __restrict__ q,
+                                                            const __nv_bfloat16* __restrict__ kp,
+                                                            const __nv_bfloat16* __restrict__ vp,
+                                                            const AttnGroup* __restrict__ groups,
+                                                            const std::int32_t* __restrict__ extra,
+                                                            const unsigned long long* __restrict__ row_mask, int nq,
+                                                            int nkv, float scale_log2,
+                                                            __nv_bfloat16* __restrict__ out) {
+  constexpr int C = HD / 8;   // 16-byte chunks per row
+  constexpr int KS = HD / 16; // k16 steps for S = Q·Kᵀ
+  constexpr int NT = HD / 8;  // n8 tiles of the output
+  __shared__ __align__(128) uint4 sQ[kVecPerPass * C];
+  __shared__ __align__(128) uint4 sK[2][kTile * C];
+  __shared__ __align__(128) uint4 sV[2][kTile * C];
 
   const AttnGroup g = groups[blockIdx.x];
   const int kvh = blockIdx.y;
@@ -61,115 +93,193 @@ __global__ void __launch_bounds__(kThreads) attn_kernel(const __nv_bfloat16* __r
   const int nvec = g.n_rows * G;
   const int ctx = g.prefix_len + g.extra_len;
   const std::size_t slot_stride = static_cast<std::size_t>(nkv) * HD;
+  const int n_tiles = (ctx + kTile - 1) / kTile;
 
-  for (int pass0 = 0; pass0 < nvec; pass0 += (kThreads / 32) * kVPW) {
-    float m[kVPW], l[kVPW], o[kVPW][DPL];
-    unsigned long long vis[kVPW];  // masked groups: visibility bits over the extras (<= 64)
-    int last[kVPW];                // causal groups: last visible extra index
-    bool live[kVPW];
-#pragma unroll
-    for (int u = 0; u < kVPW; ++u) {
-      m[u] = -INFINITY;
-      l[u] = 0.f;
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) o[u][e] = 0.f;
-      const int v = pass0 + warp * kVPW + u;
-      live[u] = v < nvec;
-      vis[u] = 0ull;
-      last[u] = -1;
-      if (live[u]) {
+  auto slot_of = [&](int p) -> int {
+    return p < g.prefix_len ? g.prefix_slot + p : (p < ctx ? extra[g.extra_off + p - g.prefix_len] : -1);
+  };
+  auto load_tile = [&](int t, int buf) {
+    for (int i = threadIdx.x; i < kTile * C; i += kThreads) {
+      const int r = i / C, c = i % C;
+      const int s = slot_of(t * kTile + r);
+      const std::size_t base = static_cast<std::size_t>(s < 0 ? 0 : s) * slot_stride + static_cast<std::size_t>(kvh) * HD;
+      cp_async16(&sK[buf][swz<HD>(r, c)], kp + base + c * 8, s >= 0);
+      cp_async16(&sV[buf][swz<HD>(r, c)], vp + base + c * 8, s >= 0);
+    }
+  };
+
+  for (int pass0 = 0; pass0 < nvec; pass0 += kVecPerPass) {
+    __syncthreads();
+    // Q for this pass: vector v -> (row j = v / G, head kvh*G + v % G), zero past nvec
+    for (int i = threadIdx.x; i < kVecPerPass * C; i += kThreads) {
+      const int vv = i / C, c = i % C, v = pass0 + vv;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (v < nvec) {
         const int j = v / G, h = kvh * G + v % G;
-        if (g.masked)
-          vis[u] = row_mask[g.row0 + j];
-        else
-          last[u] = g.extra_len - g.n_rows + j;
-        const __nv_bfloat16* qs = q + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD;
-        for (int d = lane; d < HD; d += 32) sQ[warp][u][d] = __bfloat162float(qs[d]) * scale_log2;
+        val = *reinterpret_cast<const uint4*>(q + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD + c * 8);
+      }
+      sQ[swz<HD>(vv, c)] = val;
+    }
+    load_tile(0, 0);
+    cp_async_commit();
+    __syncthreads();
+
+    // this warp's 16 query vectors; the thread's two accumulator rows
+    const int wv0 = pass0 + warp * 16;
+    const bool warp_live = wv0 < nvec;
+    const int r_lo = lane / 4, r_hi = r_lo + 8;
+    int last_lo = -1, last_hi = -1;
+    unsigned long long m_lo = 0ull, m_hi = 0ull;
+    bool live_lo = false, live_hi = false;
+    {
+      const int v_lo = wv0 + r_lo, v_hi = wv0 + r_hi;
+      live_lo = v_lo < nvec;
+      live_hi = v_hi < nvec;
+      if (live_lo) {
+        const int j = v_lo / G;
+        if (g.masked) m_lo = row_mask[g.row0 + j]; else last_lo = g.extra_len - g.n_rows + j;
+      }
+      if (live_hi) {
+        const int j = v_hi / G;
+        if (g.masked) m_hi = row_mask[g.row0 + j]; else last_hi = g.extra_len - g.n_rows + j;
       }
     }
-    __syncwarp();
-    for (int p0 = 0; p0 < ctx; p0 += kTile) {
-      __syncthreads();
-      if (threadIdx.x < kTile) {
-        const int p = p0 + threadIdx.x;
-        sSlot[threadIdx.x] = p < g.prefix_len ? g.prefix_slot + p : (p < ctx ? extra[g.extra_off + p - g.prefix_len] : -1);
+    // Q fragments (A operand) for all k16 steps
+    std::uint32_t qa[KS][4];
+    if (warp_live) {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        // lanes 0-15 rows 0-15 chunk 2ks, lanes 16-31 rows 0-15 chunk 2ks+1
+        const int row = warp * 16 + (lane % 16);
+        const int chunk = 2 * ks + lane / 16;
+        ldsm_x4(qa[ks], &sQ[swz<HD>(row, chunk)]);
+      }
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+    float mx_lo = -INFINITY, mx_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+
+    for (int t = 0; t < n_tiles; ++t) {
+      const int buf = t & 1;
+      if (t + 1 < n_tiles) {
+        load_tile(t + 1, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait1();
+      } else {
+        cp_async_wait0();
       }
       __syncthreads();
-      // K/V tile: 16-byte global loads, 4-byte smem stores into padded rows
-      for (int t = threadIdx.x; t < kTile * (W / 4); t += kThreads) {
-        const int r = t / (W / 4), c4 = t % (W / 4);
-        const int s = sSlot[r];
-        uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-        if (s >= 0) {
-          const std::size_t base = static_cast<std::size_t>(s) * slot_stride + static_cast<std::size_t>(kvh) * HD;
-          kv = reinterpret_cast<const uint4*>(kp + base)[c4];
-          vv = reinterpret_cast<const uint4*>(vp + base)[c4];
+      if (warp_live) {
+        // S = Q·Kᵀ over 32 positions: 4 n8 tiles
+        float s[4][4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll
+          for (int np = 0; np < 2; ++np) {  // pairs of n8 tiles (16 positions) per ldmatrix.x4
+            std::uint32_t kb[4];
+            // matrices: (pos 0-7, k lo), (pos 0-7, k hi), (pos 8-15, k lo), (pos 8-15, k hi)
+            const int pos = np * 16 + (lane % 8) + ((lane / 16) * 8);
+            const int chunk = 2 * ks + ((lane / 8) & 1);
+            ldsm_x4(kb, &sK[buf][swz<HD>(pos, chunk)]);
+            mma16816(s[2 * np], qa[ks], kb[0], kb[1]);
+            mma16816(s[2 * np + 1], qa[ks], kb[2], kb[3]);
+          }
         }
-        std::uint32_t* dk = &sK[r * RW + 4 * c4];
-        std::uint32_t* dv = &sV[r * RW + 4 * c4];
-        dk[0] = kv.x;
-        dk[1] = kv.y;
-        dk[2] = kv.z;
-        dk[3] = kv.w;
-        dv[0] = vv.x;
-        dv[1] = vv.y;
-        dv[2] = vv.z;
-        dv[3] = vv.w;
-      }
-      __syncthreads();
-      const int p = p0 + lane;
-      std::uint32_t krow[W];
+        // visibility + scale (exp2 domain)
+        const int p0 = t * kTile;
 #pragma unroll
-      for (int w = 0; w < W; ++w) krow[w] = sK[lane * RW + w];
-      const bool in_prefix = p < g.prefix_len;
-      const int e = p - g.prefix_len;
+        for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int u = 0; u < kVPW; ++u) {
-        if (!live[u]) continue;  // warp-uniform
-        const bool visible =
-            p < ctx && (in_prefix || (g.masked ? ((vis[u] >> (e & 63)) & 1ull) != 0ull : e <= last[u]));
-        float s = 0.f;
-        const float2* qv = reinterpret_cast<const float2*>(sQ[warp][u]);
+          for (int e = 0; e < 4; ++e) {
+            const int p = p0 + nt * 8 + (lane % 4) * 2 + (e & 1);
+            const bool hi = e >= 2;
+            bool vis = p < ctx && (hi ? live_hi : live_lo);
+            if (vis && p >= g.prefix_len) {
+              const int x = p - g.prefix_len;
+              vis = g.masked ? (((hi ? m_hi : m_lo) >> (x & 63)) & 1ull) != 0ull : x <= (hi ? last_hi : last_lo);
+            }
+            s[nt][e] = vis ? s[nt][e] * scale_log2 : -INFINITY;
+          }
+        // online softmax per row (quad reductions)
+        float tmax_lo = -INFINITY, tmax_hi = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&krow[w]));
-          const float2 qf = qv[w];
-          s = fmaf(qf.x, kf.x, s);
-          s = fmaf(qf.y, kf.y, s);
+        for (int nt = 0; nt < 4; ++nt) {
+          tmax_lo = fmaxf(tmax_lo, fmaxf(s[nt][0], s[nt][1]));
+          tmax_hi = fmaxf(tmax_hi, fmaxf(s[nt][2], s[nt][3]));
         }
-        s = visible ? s : -INFINITY;
-        const float mt = warp_max(s);
-        if (mt == -INFINITY) continue;  // nothing visible in this tile (warp-uniform)
-        const float mn = fmaxf(m[u], mt);
-        const float corr = exp2f(m[u] - mn);
-        const float pr = exp2f(s - mn);
-        l[u] = l[u] * corr + warp_sum(pr);
-        m[u] = mn;
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) o[u][d] *= corr;
-#pragma unroll 4
-        for (int jj = 0; jj < kTile; ++jj) {
-          const float pj = __shfl_sync(0xffffffffu, pr, jj);
-          const std::uint32_t* vr = &sV[jj * RW + lane * (DPL / 2)];
+        for (int off = 1; off <= 2; off <<= 1) {
+          tmax_lo = fmaxf(tmax_lo, __shfl_xor_sync(0xffffffffu, tmax_lo, off));
+          tmax_hi = fmaxf(tmax_hi, __shfl_xor_sync(0xffffffffu, tmax_hi, off));
+        }
+        const float nmax_lo = fmaxf(mx_lo, tmax_lo), nmax_hi = fmaxf(mx_hi, tmax_hi);
+        const float base_lo = nmax_lo == -INFINITY ? 0.f : nmax_lo;
+        const float base_hi = nmax_hi == -INFINITY ? 0.f : nmax_hi;
+        const float corr_lo = exp2f(mx_lo - base_lo), corr_hi = exp2f(mx_hi - base_hi);
+        mx_lo = nmax_lo;
+        mx_hi = nmax_hi;
+        float rs_lo = 0.f, rs_hi = 0.f;
+        std::uint32_t pa[2][4];  // P as the A operand: 2 k16 steps of 16 positions
 #pragma unroll
-          for (int d = 0; d < DPL; d += 2) {
-            const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[d / 2]));
-            o[u][d] = fmaf(pj, vf.x, o[u][d]);
-            o[u][d + 1] = fmaf(pj, vf.y, o[u][d + 1]);
+        for (int nt = 0; nt < 4; ++nt) {
+          const float p0v = exp2f(s[nt][0] - base_lo), p1v = exp2f(s[nt][1] - base_lo);
+          const float p2v = exp2f(s[nt][2] - base_hi), p3v = exp2f(s[nt][3] - base_hi);
+          rs_lo += p0v + p1v;
+          rs_hi += p2v + p3v;
+          const int ks = nt / 2, half = nt % 2;
+          pa[ks][half * 2 + 0] = pack_bf16(p0v, p1v);
+          pa[ks][half * 2 + 1] = pack_bf16(p2v, p3v);
+        }
+        rs_lo += __shfl_xor_sync(0xffffffffu, rs_lo, 1);
+        rs_lo += __shfl_xor_sync(0xffffffffu, rs_lo, 2);
+        rs_hi += __shfl_xor_sync(0xffffffffu, rs_hi, 1);
+        rs_hi += __shfl_xor_sync(0xffffffffu, rs_hi, 2);
+        l_lo = l_lo * corr_lo + rs_lo;
+        l_hi = l_hi * corr_hi + rs_hi;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          o[nt][0] *= corr_lo;
+          o[nt][1] *= corr_lo;
+          o[nt][2] *= corr_hi;
+          o[nt][3] *= corr_hi;
+        }
+        // O += P·V: A = P (16 x 32 positions), B = V (32 positions x HD) via ldmatrix.trans
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+          for (int np = 0; np < NT / 2; ++np) {  // pairs of n8 output tiles (16 dims)
+            std::uint32_t vb[4];
+            // matrices: (pos lo 0-7, dims np*16+0-7), (pos 8-15, same), (pos 0-7, dims +8), (pos 8-15, +8)
+            const int pos = ks * 16 + (lane % 8) + ((lane / 8) & 1) * 8;
+            const int chunk = 2 * np + (lane / 16);
+            ldsm_x4_t(vb, &sV[buf][swz<HD>(pos, chunk)]);
+            mma16816(o[2 * np], pa[ks], vb[0], vb[1]);
+            mma16816(o[2 * np + 1], pa[ks], vb[2], vb[3]);
           }
         }
       }
+      __syncthreads();  // buffer `buf` is refilled two tiles later
     }
+    // epilogue: normalise and store this warp's rows
+    if (warp_live) {
+      const float inv_lo = l_lo > 0.f ? 1.f / l_lo : 0.f, inv_hi = l_hi > 0.f ? 1.f / l_hi : 0.f;
 #pragma unroll
-    for (int u = 0; u < kVPW; ++u) {
-      if (!live[u]) continue;
-      const int v = pass0 + warp * kVPW + u;
-      const int j = v / G, h = kvh * G + v % G;
-      __nv_bfloat16* os = out + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD + lane * DPL;
-      const float inv = l[u] > 0.f ? 1.f / l[u] : 0.f;
+      for (int half = 0; half < 2; ++half) {
+        const int v = wv0 + (half ? r_hi : r_lo);
+        if (v >= nvec) continue;
+        const int j = v / G, h = kvh * G + v % G;
+        __nv_bfloat16* os = out + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD;
+        const float inv = half ? inv_hi : inv_lo;
 #pragma unroll
-      for (int d = 0; d < DPL; d += 2)
-        *reinterpret_cast<__nv_bfloat162*>(os + d) = __floats2bfloat162_rn(o[u][d] * inv, o[u][d + 1] * inv);
+        for (int nt = 0; nt < NT; ++nt) {
+          const int d = nt * 8 + (lane % 4) * 2;
+          *reinterpret_cast<__nv_bfloat162*>(os + d) =
+              __floats2bfloat162_rn(o[nt][half * 2] * inv, o[nt][half * 2 + 1] * inv);
+        }
+      }
     }
   }
 }
@@ -183,15 +293,15 @@ void attention(const void* q, const void* k_pool, const void* v_pool, const Attn
   dim3 grid(n_groups, s.n_kv);
   const float sl2 = s.scale * 1.4426950408889634f;
   if (s.hd == 128)
-    attn_kernel<128><<<grid, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
-                                                static_cast<const __nv_bfloat16*>(k_pool),
-                                                static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask,
-                                                s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
+    attn_mma_kernel<128><<<grid, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                                    static_cast<const __nv_bfloat16*>(k_pool),
+                                                    static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask,
+                                                    s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
   else if (s.hd == 64)
-    attn_kernel<64><<<grid, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
-                                               static_cast<const __nv_bfloat16*>(k_pool),
-                                               static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask,
-                                               s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
+    attn_mma_kernel<64><<<grid, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                                   static_cast<const __nv_bfloat16*>(k_pool),
+                                                   static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask,
+                                                   s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
   else
     throw std::invalid_argument("attention: head dim must be 64 or 128");
   WS_CUDA(cudaGetLastError());

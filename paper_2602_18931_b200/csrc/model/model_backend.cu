@@ -2,6 +2,7 @@
 #include "model_backend.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -465,7 +466,9 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
     if (b.row_mask.size() != b.tok.size()) throw std::logic_error("model path: row mask bookkeeping");
     const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
     const ws_pred* outp = reinterpret_cast<const ws_pred*>(I.h_res + I.cap_rows * sizeof(ws_verify_out));
-    cudaStream_t sd = p_->stream_draft();
+    // WS_SERIAL=1 serialises the two forwards (clean per-kernel profiles); default overlaps them
+    static const bool serial = std::getenv("WS_SERIAL") != nullptr;
+    cudaStream_t sd = serial ? st : p_->stream_draft();
     if (n_out) {
       p_->draft().copy_slots(copy_src, copy_dst, sd);
       WS_CUDA(cudaEventRecord(I.e2, sd));
