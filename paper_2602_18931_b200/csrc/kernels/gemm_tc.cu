@@ -4,18 +4,23 @@
 //
 // A = activations (rows = verify/draft rows), W = a weight matrix in its natural [out, in]
 // (K-major) layout, so both operands are K-major and stream straight from HBM by TMA with the
-// 128-byte swizzle the UMMA descriptors expect. Warp-specialised, one output tile per CTA:
+// 128-byte swizzle the UMMA descriptors expect. Persistent and warp-specialised:
 //   warp 0      TMA producer (one elected lane) over a STAGES-deep smem ring (mbarriers)
 //   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma 128xBNx16)
 //   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
+// Each CTA walks tiles t = blockIdx.x, +gridDim.x, ...; the accumulator is double-buffered in
+// TMEM (2 x BN columns) so the epilogue of tile i overlaps the main loop of tile i+1.
 // Epilogues: plain bf16 store (QKV, LM head), fp32 residual accumulate (O / down projections
-// add into the fp32 residual stream), SwiGLU (gate/up rows interleaved per BN/2 block).
+// add into the fp32 residual stream), SwiGLU (gate/up rows interleaved in 32-row blocks).
 // Tiles are ordered M-fastest so all M-blocks of one weight tile run concurrently and each
 // weight byte crosses HBM once per GEMM (weights dominate the verify-step bytes).
+// Numerics: every output element accumulates its K-blocks in order in one TMEM column — no
+// split-K — so results are independent of M, BN and scheduling (batch invariance).
 #include "gemm_tc.cuh"
 
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -32,6 +37,7 @@ using namespace sm100;
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kThreads = 192;
+constexpr int kNumSMs = 148;
 
 template <int BN>
 struct Cfg {
@@ -39,16 +45,85 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256;
 };
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
+// TMEM accumulator (this thread's row, BN fp32 columns at t_row) → fused epilogue → global.
+template <int BN, int EPI>
+__device__ __forceinline__ void store_tile(std::uint32_t t_row, int row, int M, int N, int n_blk, void* out, int ldo) {
+  if constexpr (EPI == kEpiSwiGLU) {
+    // W rows interleaved in 32-row blocks [gate 0..31 | up 0..31 | gate 32..63 | ...]: TMEM
+    // column chunk 2j is gate and 2j+1 is up for output features f0 + 32j .. +31.
+    const int f0 = n_blk * (BN / 2);
+#pragma unroll 1
+    for (int c = 0; c < BN / 2; c += 32) {
+      std::uint32_t g[32], u[32];
+      tmem_ld32(t_row + 2 * c, g);
+      tmem_ld32(t_row + 2 * c + 32, u);
+      tmem_ld_wait();
+      if (row < M && f0 + c < N / 2) {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + f0 + c;
+        alignas(16) __nv_bfloat162 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float a0 = silu(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
+          const float a1 = silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
+          v[j] = __floats2bfloat162_rn(a0, a1);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
+      }
+    }
+  } else {
+    const int n0 = n_blk * BN;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      std::uint32_t r[32];
+      tmem_ld32(t_row + c, r);
+      tmem_ld_wait();
+      if (row >= M || n0 + c >= N) continue;
+      if constexpr (EPI == kEpiBF16) {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
+        alignas(16) __nv_bfloat162 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          v[j] = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        if (n0 + c + 32 <= N) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
+        } else {
+          const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(v);
+          for (int j = 0; j < 32 && n0 + c + j < N; ++j) o[j] = vv[j];
+        }
+      } else {  // kEpiAddF32: out[row, n] += acc
+        float* o = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
+        if (n0 + c + 32 <= N) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 x = reinterpret_cast<float4*>(o)[q];
+            x.x += __uint_as_float(r[4 * q + 0]);
+            x.y += __uint_as_float(r[4 * q + 1]);
+            x.z += __uint_as_float(r[4 * q + 2]);
+            x.w += __uint_as_float(r[4 * q + 3]);
+            reinterpret_cast<float4*>(o)[q] = x;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (n0 + c + j < N) o[j] += __uint_as_float(r[j]);
+        }
+      }
+    }
+  }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, void* __restrict__ out, int ldo) {
+                   int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -57,11 +132,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* sB = smem + C::STAGES * C::A_BYTES;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   std::uint64_t* empty = full + C::STAGES;
-  std::uint64_t* tmem_full = empty + C::STAGES;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tmem_full + 1);
+  std::uint64_t* tfull = empty + C::STAGES;  // [2]
+  std::uint64_t* tempty = tfull + 2;         // [2]
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
 
-  const int m_blk = blockIdx.x, n_blk = blockIdx.y;
   const int num_k = K / BK;
+  const int total = m_blocks * n_tiles;
   const std::uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
@@ -71,7 +147,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
@@ -81,17 +160,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const std::uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer
+    if (lane == 0) {  // TMA producer: continuous ring across tiles
       int stage = 0;
       std::uint32_t phase = 0;
-      for (int kb = 0; kb < num_k; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-        tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-        tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
-        if (++stage == C::STAGES) {
-          stage = 0;
-          phase ^= 1;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int m_blk = t % m_blocks, n_blk = t / m_blocks;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -100,88 +182,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr std::uint32_t idesc = idesc_bf16_f32(BM, BN);
       int stage = 0;
       std::uint32_t phase = 0;
-      for (int kb = 0; kb < num_k; ++kb) {
-        mbar_wait(&full[stage], phase);
+      int local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         tc_fence_after();
-        const std::uint64_t da = smem_desc_sw128(sA + stage * C::A_BYTES);
-        const std::uint64_t db = smem_desc_sw128(sB + stage * C::B_BYTES);
+        const std::uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const std::uint64_t da = smem_desc_sw128(sA + stage * C::A_BYTES);
+          const std::uint64_t db = smem_desc_sw128(sB + stage * C::B_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)  // advance 16 elements = 32 B = 2 descriptor units
-          mma_bf16(tmem_base, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
-        mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
-        if (++stage == C::STAGES) {
-          stage = 0;
-          phase ^= 1;
+          for (int k = 0; k < BK / 16; ++k)  // advance 16 elements = 32 B = 2 descriptor units
+            mma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
+        mma_commit(&tfull[acc]);
       }
-      mma_commit(tmem_full);
     }
   } else {  // epilogue warps 2..5 → TMEM lane groups (warp % 4)
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
     const int grp = static_cast<int>(warp & 3);
-    const int row = m_blk * BM + grp * 32 + static_cast<int>(lane);
-    const std::uint32_t t_row = tmem_base + (static_cast<std::uint32_t>(grp * 32) << 16);
-    if constexpr (EPI == kEpiSwiGLU) {
-      // W rows interleaved in 32-row blocks [gate 0..31 | up 0..31 | gate 32..63 | ...]: TMEM
-      // column chunk 2j is gate and 2j+1 is up for output features f0 + 32j .. +31.
-      const int f0 = n_blk * (BN / 2);
-#pragma unroll 1
-      for (int c = 0; c < BN / 2; c += 32) {
-        std::uint32_t g[32], u[32];
-        tmem_ld32(t_row + 2 * c, g);
-        tmem_ld32(t_row + 2 * c + 32, u);
-        tmem_ld_wait();
-        if (row < M && f0 + c < N / 2) {
-          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + f0 + c;
-          alignas(16) __nv_bfloat162 v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float a0 = silu(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
-            const float a1 = silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
-            v[j] = __floats2bfloat162_rn(a0, a1);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
-        }
-      }
-    } else {
-      const int n0 = n_blk * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        std::uint32_t r[32];
-        tmem_ld32(t_row + c, r);
-        tmem_ld_wait();
-        if (row >= M || n0 + c >= N) continue;
-        if constexpr (EPI == kEpiBF16) {
-          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
-          alignas(16) __nv_bfloat162 v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-          if (n0 + c + 32 <= N) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
-          } else {
-            const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(v);
-            for (int j = 0; j < 32 && n0 + c + j < N; ++j) o[j] = vv[j];
-          }
-        } else {  // kEpiAddF32: out[row, n] += acc
-          float* o = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
-          if (n0 + c + 32 <= N) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float4 x = reinterpret_cast<float4*>(o)[q];
-              x.x += __uint_as_float(r[4 * q + 0]);
-              x.y += __uint_as_float(r[4 * q + 1]);
-              x.z += __uint_as_float(r[4 * q + 2]);
-              x.w += __uint_as_float(r[4 * q + 3]);
-              reinterpret_cast<float4*>(o)[q] = x;
-            }
-          } else {
-            for (int j = 0; j < 32 && n0 + c + j < N; ++j) o[j] += __uint_as_float(r[j]);
-          }
-        }
-      }
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const int m_blk = t % m_blocks, n_blk = t / m_blocks;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const int row = m_blk * BM + grp * 32 + static_cast<int>(lane);
+      const std::uint32_t t_row = tmem_base + acc * BN + (static_cast<std::uint32_t>(grp * 32) << 16);
+      store_tile<BN, EPI>(t_row, row, M, N, n_blk, out, ldo);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
@@ -220,38 +257,44 @@ CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, st
 template <int BN, int EPI>
 void launch(const GemmArgs& g, cudaStream_t st) {
   using C = Cfg<BN>;
-  static bool attr_set = false;  // per-instantiation; benign race (idempotent)
-  if (!attr_set) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
     WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_set = true;
-  }
+  });
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
   const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, BN);
-  const int n_out = EPI == kEpiSwiGLU ? g.N : g.N;  // SwiGLU: N counts gate+up rows
-  dim3 grid((g.M + BM - 1) / BM, (n_out + BN - 1) / BN);
-  gemm_tn_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, g.out, g.ldo);
+  const int m_blocks = (g.M + BM - 1) / BM;
+  const int n_tiles = (g.N + BN - 1) / BN;  // SwiGLU: N counts gate+up rows
+  const int total = m_blocks * n_tiles;
+  const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
+  gemm_tn_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo);
   WS_CUDA(cudaGetLastError());
 }
 
 }  // namespace
 
 int pick_bn(int M, int N) {
-  // Measured on B200 (profiles/r01_gemm.md): 128x256 tiles win whenever they fill the 148 SMs
-  // (they halve A re-reads and per-tile overhead); otherwise the widest tile that still gives
-  // every SM a tile. Numerics do not depend on BN (tests: batch/tile invariance).
+  // Wave-quantisation model: time ~ ceil(tiles / 148) x (BN + per-tile overhead); wider tiles
+  // win ties (they halve A re-reads). Numerics do not depend on BN (tests: tile invariance).
   const int mb = (M + BM - 1) / BM;
-  for (int bn : {256, 128}) {
-    if (N < bn) continue;
-    if (mb * ((N + bn - 1) / bn) >= 148) return bn;
+  int best = 64;
+  long best_cost = -1;
+  for (int bn : {256, 128, 64}) {
+    if (N < bn && bn != 64) continue;
+    const long tiles = static_cast<long>(mb) * ((N + bn - 1) / bn);
+    const long cost = ((tiles + kNumSMs - 1) / kNumSMs) * (bn + 48);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
   }
-  return N >= 64 ? 64 : 64;
+  return best;
 }
 
 void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   if (g.K % BK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (g.lda % 8 || g.ldw % 8) throw std::invalid_argument("gemm: leading dims must be multiples of 8");
   int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
-  if (g.epi == kEpiSwiGLU && bn < 64) bn = 64;
   switch (g.epi) {
     case kEpiBF16:
       if (bn == 256) return launch<256, kEpiBF16>(g, st);

@@ -17,7 +17,8 @@ struct GemmArgs {
   int M, N, K;
   int lda, ldw, ldo;
   int epi = kEpiBF16;
-  int bn = 0;  // 0 = auto (64/128/256)
+  int bn = 0;        // 0 = auto (64/128/256)
+  int max_ctas = 0;  // persistent grid cap (0 = one CTA per SM)
 };
 
 // C = A · W^T on tcgen05 (sm_100a). Throws on bad shapes / CUDA errors.
