@@ -81,6 +81,20 @@ def rowstats():
                           "gbs": by / t / 1e9, "frac_hbm": by / t / 1e9 / PEAK_GBS}))
 
 
+def one_gemm():
+    """One realistic verify-batch GEMM (8B gate/up + SwiGLU at 526 rows), for ncu --set full."""
+    M, N, K = 526, 28672, 4096
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    for _ in range(4):
+        ops.gemm(A, W, out=out, epi=ops.EPI_SWIGLU)
+    torch.cuda.synchronize()
+    t = timeit(lambda: ops.gemm(A, W, out=out, epi=ops.EPI_SWIGLU))
+    print(json.dumps({"kernel": "gemm gate_up+swiglu", "M": M, "N": N, "K": K, "ms": t * 1e3,
+                      "tflops": 2.0 * M * N * K / t / 1e12}))
+
+
 def ops_pick(M, N):
     bm = (M + 127) // 128
     if bm * ((N + 255) // 256) >= 296:
@@ -91,4 +105,4 @@ def ops_pick(M, N):
 
 
 if __name__ == "__main__":
-    {"gemm": gemm, "rowstats": rowstats}[sys.argv[1]]()
+    {"gemm": gemm, "rowstats": rowstats, "one_gemm": one_gemm}[sys.argv[1]]()
