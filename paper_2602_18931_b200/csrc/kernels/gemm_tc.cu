@@ -120,10 +120,66 @@ __device__ __forceinline__ void store_tile(std::uint32_t t_row, int row, int M, 
   }
 }
 
+// Fused QKV epilogue: for each head of the tile, rotate-half RoPE on q/k (pairs i, i+hd/2 from
+// the fp32 accumulator, cos/sin from the fp64-built table) and scatter: q → q_out[row], k and
+// v → the KV pool at slot[row]. Replaces a separate rope/KV-append pass and the qkv round trip.
+template <int BN>
+__device__ __forceinline__ void store_tile_qkv(std::uint32_t t_row, int row, int M, int n_blk, const RopeEpi& r) {
+  const int hd = r.hd, half = hd / 2;
+  const int n0 = n_blk * BN;
+  const bool live = row < M;
+  const int pos = live ? r.pos[row] : 0;
+  const int slot = live ? r.slot[row] : 0;
+#pragma unroll 1
+  for (int h0 = 0; h0 < BN; h0 += hd) {
+    const int hh = (n0 + h0) / hd;  // warp-uniform
+    if (hh >= r.nq + 2 * r.nkv) break;
+    const bool rot = hh < r.nq + r.nkv;
+    __nv_bfloat16* dst;
+    if (hh < r.nq)
+      dst = static_cast<__nv_bfloat16*>(r.q) + (static_cast<std::size_t>(row) * r.nq + hh) * hd;
+    else if (hh < r.nq + r.nkv)
+      dst = static_cast<__nv_bfloat16*>(r.k_pool) + (static_cast<std::size_t>(slot) * r.nkv + (hh - r.nq)) * hd;
+    else
+      dst = static_cast<__nv_bfloat16*>(r.v_pool) + (static_cast<std::size_t>(slot) * r.nkv + (hh - r.nq - r.nkv)) * hd;
+#pragma unroll 1
+    for (int c = 0; c < half; c += 32) {
+      std::uint32_t a[32], b[32];
+      tmem_ld32(t_row + h0 + c, a);  // warp-collective: before any per-lane branch
+      tmem_ld32(t_row + h0 + c + half, b);
+      tmem_ld_wait();
+      if (!live) continue;
+      alignas(16) __nv_bfloat162 lo[16], hi[16];
+      const float2* cs = r.cs + static_cast<std::size_t>(pos) * half + c;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float x0 = __uint_as_float(a[2 * j]), x1 = __uint_as_float(a[2 * j + 1]);
+        float y0 = __uint_as_float(b[2 * j]), y1 = __uint_as_float(b[2 * j + 1]);
+        if (rot) {
+          const float2 c0 = cs[2 * j], c1 = cs[2 * j + 1];
+          const float rx0 = x0 * c0.x - y0 * c0.y, ry0 = y0 * c0.x + x0 * c0.y;
+          const float rx1 = x1 * c1.x - y1 * c1.y, ry1 = y1 * c1.x + x1 * c1.y;
+          x0 = rx0;
+          y0 = ry0;
+          x1 = rx1;
+          y1 = ry1;
+        }
+        lo[j] = __floats2bfloat162_rn(x0, x1);
+        hi[j] = __floats2bfloat162_rn(y0, y1);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        reinterpret_cast<uint4*>(dst + c)[q] = reinterpret_cast<const uint4*>(lo)[q];
+        reinterpret_cast<uint4*>(dst + c + half)[q] = reinterpret_cast<const uint4*>(hi)[q];
+      }
+    }
+  }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo) {
+                   int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo, const RopeEpi rope) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -215,7 +271,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int row = m_blk * BM + grp * 32 + static_cast<int>(lane);
       const std::uint32_t t_row = tmem_base + acc * BN + (static_cast<std::uint32_t>(grp * 32) << 16);
-      store_tile<BN, EPI>(t_row, row, M, N, n_blk, out, ldo);
+      if constexpr (EPI == kEpiQKVRope)
+        store_tile_qkv<BN>(t_row, row, M, n_blk, rope);
+      else
+        store_tile<BN, EPI>(t_row, row, M, N, n_blk, out, ldo);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -267,7 +326,8 @@ void launch(const GemmArgs& g, cudaStream_t st) {
   const int n_tiles = (g.N + BN - 1) / BN;  // SwiGLU: N counts gate+up rows
   const int total = m_blocks * n_tiles;
   const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
-  gemm_tn_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo);
+  gemm_tn_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo,
+                                                            g.rope);
   WS_CUDA(cudaGetLastError());
 }
 
@@ -308,6 +368,13 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
       if (bn == 256) return launch<256, kEpiSwiGLU>(g, st);
       if (bn == 128) return launch<128, kEpiSwiGLU>(g, st);
       return launch<64, kEpiSwiGLU>(g, st);
+    case kEpiQKVRope:
+      if (g.rope.hd != 64 && g.rope.hd != 128) throw std::invalid_argument("gemm: qkv epilogue needs hd 64/128");
+      if (bn < g.rope.hd) bn = g.rope.hd;  // a tile holds whole heads
+      if (g.N != (g.rope.nq + 2 * g.rope.nkv) * g.rope.hd) throw std::invalid_argument("gemm: qkv width");
+      if (bn == 256) return launch<256, kEpiQKVRope>(g, st);
+      if (bn == 128) return launch<128, kEpiQKVRope>(g, st);
+      return launch<64, kEpiQKVRope>(g, st);
   }
   throw std::invalid_argument("gemm: unknown epilogue");
 }

@@ -5,9 +5,22 @@
 namespace wsb {
 
 enum GemmEpi : int {
-  kEpiBF16 = 0,    // out bf16 [M, ldo] = acc
-  kEpiAddF32 = 1,  // out fp32 [M, ldo] += acc   (residual stream)
-  kEpiSwiGLU = 2,  // out bf16 [M, ldo] = silu(gate) * up; W rows interleaved in 32-row blocks
+  kEpiBF16 = 0,     // out bf16 [M, ldo] = acc
+  kEpiAddF32 = 1,   // out fp32 [M, ldo] += acc   (residual stream)
+  kEpiSwiGLU = 2,   // out bf16 [M, ldo] = silu(gate) * up; W rows interleaved in 32-row blocks
+  kEpiQKVRope = 3,  // fused QKV epilogue: rotate-half RoPE on q/k, q → q_out, k/v → KV pool slots
+};
+
+// Operands of the fused QKV epilogue (row r: position pos[r], KV slot slot[r]; cs = cos/sin
+// table [max_pos][hd/2] precomputed on the host in fp64 from the llama3-scaled frequencies).
+struct RopeEpi {
+  const int* pos = nullptr;
+  const int* slot = nullptr;
+  const float2* cs = nullptr;
+  void* q = nullptr;       // bf16 [M, nq*hd]
+  void* k_pool = nullptr;  // bf16 [slot][nkv][hd] (this layer)
+  void* v_pool = nullptr;
+  int nq = 0, nkv = 0, hd = 0;
 };
 
 struct GemmArgs {
@@ -19,6 +32,7 @@ struct GemmArgs {
   int epi = kEpiBF16;
   int bn = 0;        // 0 = auto (64/128/256)
   int max_ctas = 0;  // persistent grid cap (0 = one CTA per SM)
+  RopeEpi rope{};    // kEpiQKVRope only
 };
 
 // C = A · W^T on tcgen05 (sm_100a). Throws on bad shapes / CUDA errors.

@@ -105,6 +105,17 @@ LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_s
   const std::vector<float> inv = llama3_inv_freq(s);
   WS_CUDA(cudaMalloc(&inv_freq_, inv.size() * sizeof(float)));
   WS_CUDA(cudaMemcpy(inv_freq_, inv.data(), inv.size() * sizeof(float), cudaMemcpyHostToDevice));
+  {  // cos/sin table [kMaxPos][hd/2] in fp64 → fp32 (the fused QKV epilogue reads it)
+    std::vector<float2> cs(static_cast<std::size_t>(kMaxPos) * (s.hd / 2));
+    for (int p = 0; p < kMaxPos; ++p)
+      for (int i = 0; i < s.hd / 2; ++i) {
+        const double a = static_cast<double>(p) * static_cast<double>(inv[i]);
+        cs[static_cast<std::size_t>(p) * (s.hd / 2) + i] = make_float2(static_cast<float>(std::cos(a)),
+                                                                       static_cast<float>(std::sin(a)));
+      }
+    WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&rope_cs_), cs.size() * sizeof(float2)));
+    WS_CUDA(cudaMemcpy(rope_cs_, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
   // ---- KV pools ----
   const std::size_t pool = static_cast<std::size_t>(s.layers) * n_slots * s.n_kv * s.hd * 2;
   WS_CUDA(cudaMalloc(&k_pool_, pool));
@@ -117,6 +128,7 @@ LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_s
 
 LlamaModel::~LlamaModel() {
   cudaSetDevice(device_);
+  if (rope_cs_) cudaFree(rope_cs_);
   for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_, static_cast<void*>(x_), xn_, qkv_,
                   q_, attn_, h_, logits_, xo_, static_cast<void*>(d_meta_)})
     if (p) cudaFree(p);
@@ -189,6 +201,8 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
   const int n_out = static_cast<int>(b.out_rows.size());
   if (n == 0) return;
   if (b.pos.size() != b.tok.size() || b.slot.size() != b.tok.size()) throw std::invalid_argument("forward: ragged rows");
+  for (std::int32_t p : b.pos)
+    if (p < 0 || p >= kMaxPos) throw std::invalid_argument("forward: position out of the RoPE table range");
   ensure_rows(n, n_out);
   // ---- one packed H2D for all metadata ----
   const std::size_t s_tok = al(n * 4), s_grp = al(b.groups.size() * sizeof(AttnGroup)), s_ext = al(b.extra.size() * 4 + 4),
@@ -233,10 +247,11 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
     __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(v_pool_) + l * layer_stride;
     rmsnorm_rows(x_, d, nullptr, attn_norm_[l], s_.eps, n, d, xn_, d, st);
     prof_.mark(KernelProfiler::kNorm, st);
-    gemm_tn(GemmArgs{xn_, wqkv_[l], qkv_, n, s_.qkv_dim(), d, d, d, s_.qkv_dim(), kEpiBF16, 0}, st);
+    // QKV projection with RoPE + KV append fused into the epilogue
+    GemmArgs qa{xn_, wqkv_[l], nullptr, n, s_.qkv_dim(), d, d, d, s_.qkv_dim(), kEpiQKVRope, 0};
+    qa.rope = RopeEpi{I(o_pos), I(o_slot), rope_cs_, q_, kp, vp, s_.n_q, s_.n_kv, s_.hd};
+    gemm_tn(qa, st);
     prof_.mark(KernelProfiler::kQKV, st);
-    rope_kv_append(qkv_, n, s_.n_q, s_.n_kv, s_.hd, I(o_pos), I(o_slot), inv_freq_, q_, kp, vp, st);
-    prof_.mark(KernelProfiler::kRope, st);
     attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()),
               I(o_ext), reinterpret_cast<const unsigned long long*>(d_meta_ + o_msk), ash, attn_, st);
     prof_.mark(KernelProfiler::kAttn, st);

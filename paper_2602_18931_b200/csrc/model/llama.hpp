@@ -107,6 +107,8 @@ class LlamaModel {
   std::vector<void*> attn_norm_, wqkv_, wo_, mlp_norm_, wgu_, wdown_;
   void* weight_block_ = nullptr;
   float* inv_freq_ = nullptr;
+  float2* rope_cs_ = nullptr;  // [kMaxPos][hd/2] cos/sin
+  static constexpr int kMaxPos = 4096;
   // KV pools [layer][slot][n_kv][hd]
   void* k_pool_ = nullptr;
   void* v_pool_ = nullptr;
