@@ -133,63 +133,6 @@ __device__ __forceinline__ void absorb8(State& a, const uint4& q, std::uint32_t 
   }
 }
 
-// 32 elements (4 x 16-byte vectors) at once: max first, one rescale, then 32 independent
-// exponentials summed by trees — the serial z/s dependency chains of a per-element update
-// would otherwise leave the MUFU and FMA pipes idle (profiles/r01_ncu_rowstats.md).
-__device__ __forceinline__ void absorb32(State& a, const uint4 (&q)[4], const std::uint32_t (&id0)[4], float cl) {
-  float x[32];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 f = __bfloat1622float2(h[j]);
-      x[8 * u + 2 * j] = f.x;
-      x[8 * u + 2 * j + 1] = f.y;
-    }
-  }
-  float mv[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) mv[j] = fmaxf(x[j], x[j + 16]);
-#pragma unroll
-  for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-    for (int j = 0; j < w; ++j) mv[j] = fmaxf(mv[j], mv[j + w]);
-  const float mx = mv[0];
-  const float lm = mx * cl;
-  if (lm > a.m) {
-    if (a.z > 0.f) {
-      const float f = exp2f(a.m - lm);
-      a.s = f * (a.s + a.z * (a.m - lm));
-      a.z *= f;
-    }
-    a.m = lm;
-  }
-  float zs[16], ss[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float d0 = fmaf(x[j], cl, -a.m), d1 = fmaf(x[j + 16], cl, -a.m);
-    const float e0 = ex2(d0), e1 = ex2(d1);
-    zs[j] = e0 + e1;
-    ss[j] = fmaf(e0, d0, e1 * d1);
-  }
-#pragma unroll
-  for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-    for (int j = 0; j < w; ++j) {
-      zs[j] += zs[j + w];
-      ss[j] += ss[j + w];
-    }
-  a.z += zs[0];
-  a.s += ss[0];
-  if (mx >= a.v2) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) insert(a, x[8 * u + j], id0[u] + j);
-  }
-}
-
 __device__ __forceinline__ void absorb1(State& a, float x, std::uint32_t id, float cl) {
   const float l = x * cl;
   if (l > a.m) {
@@ -264,9 +207,10 @@ __global__ void __launch_bounds__(kThreads) row_stats_kernel(
       uint4 q[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) q[u] = __ldcs(v + i + u * kThreads);
-      const std::uint32_t ids[4] = {lo + 8 * i, lo + 8 * (i + kThreads), lo + 8 * (i + 2 * kThreads),
-                                    lo + 8 * (i + 3 * kThreads)};
-      absorb32(a, q, ids, cl);
+      // (absorb32's tree form measured slower on B200 — 188 vs 158 µs at 1280x128256 — from
+      // register pressure; the per-vector update is kept)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) absorb8(a, q[u], lo + 8 * (i + u * kThreads), cl);
     }
     for (; i < nvec; i += kThreads) absorb8(a, __ldcs(v + i), lo + 8 * i, cl);
     for (std::uint32_t t = lo + nvec * 8 + threadIdx.x; t < hi; t += kThreads)
