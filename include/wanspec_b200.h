@@ -231,9 +231,11 @@ typedef struct ws_verify_out {
 #define WS_EPI_BF16 0    /* out bf16 = A·W^T */
 #define WS_EPI_ADD_F32 1 /* out fp32 += A·W^T (residual stream) */
 #define WS_EPI_SWIGLU 2  /* out bf16 = silu(gate)·up, W rows interleaved in 32-row gate/up blocks */
-/* K1: C[M,N] = A[M,K]·W[N,K]^T, bf16 operands, fp32 accumulation in TMEM (tcgen05 + TMA). */
+/* K1: C[M,N] = A[M,K]·W[N,K]^T, bf16 operands, fp32 accumulation in TMEM (tcgen05 + TMA).
+ * bn: N-tile width (0 = auto); splits: split-K factor (1 = none, 0 = the (N,K)-determined
+ * count the model uses), partials summed in fixed split order (deterministic). */
 int ws_op_gemm_bf16(const void* A, const void* W, void* out, int M, int N, int K, int lda, int ldw,
-                    int ldo, int epi, int bn, void* stream);
+                    int ldo, int epi, int bn, int splits, void* stream);
 
 /* K3: per row of bf16 logits [rows, ld]: top-2 (id, prob) of softmax(x·inv_temp), ties to the
  * lower id, and the entropy in nats (entropy_of semantics, oracle.hpp:21-33), fp32 reductions.

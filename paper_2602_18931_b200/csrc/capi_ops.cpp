@@ -1,6 +1,8 @@
 // Device-pointer entry points of the model-path kernels (include/wanspec_b200.h "ops").
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -28,10 +30,30 @@ int op_guarded(const char* what, F&& f) {
 extern "C" {
 
 int ws_op_gemm_bf16(const void* A, const void* W, void* out, int M, int N, int K, int lda, int ldw, int ldo,
-                    int epi, int bn, void* stream) {
+                    int epi, int bn, int splits, void* stream) {
   return op_guarded("ws_op_gemm_bf16", [&] {
     if (!A || !W || !out || M <= 0 || N <= 0 || K <= 0) throw std::invalid_argument("gemm: bad argument");
+    if (epi == WS_EPI_BF16 + 3) throw std::invalid_argument("gemm: the QKV epilogue needs the model");
     wsb::GemmArgs g{A, W, out, M, N, K, lda, ldw, ldo, epi, bn};
+    if (splits != 1) {  // split-K (0 = the (N, K)-determined count) with a process-wide workspace
+      static void* ws = nullptr;
+      static std::size_t ws_bytes = 0;
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lk(mu);
+      const std::size_t need = wsb::gemm_workspace_bytes(std::max(M, 512));
+      if (need > ws_bytes) {
+        if (ws) cudaFree(ws);
+        WS_CUDA(cudaMalloc(&ws, need));
+        WS_CUDA(cudaMemset(ws, 0, need));
+        ws_bytes = need;
+      }
+      g.ws = ws;
+      g.ws_bytes = ws_bytes;
+      g.splits = splits;
+      wsb::gemm_tn(g, static_cast<cudaStream_t>(stream));
+      WS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+      return;
+    }
     wsb::gemm_tn(g, static_cast<cudaStream_t>(stream));
   });
 }

@@ -8,14 +8,18 @@
 //   warp 0      TMA producer (one elected lane) over a STAGES-deep smem ring (mbarriers)
 //   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma 128xBNx16)
 //   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
-// Each CTA walks tiles t = blockIdx.x, +gridDim.x, ...; the accumulator is double-buffered in
-// TMEM (2 x BN columns) so the epilogue of tile i overlaps the main loop of tile i+1.
-// Epilogues: plain bf16 store (QKV, LM head), fp32 residual accumulate (O / down projections
-// add into the fp32 residual stream), SwiGLU (gate/up rows interleaved in 32-row blocks).
-// Tiles are ordered M-fastest so all M-blocks of one weight tile run concurrently and each
-// weight byte crosses HBM once per GEMM (weights dominate the verify-step bytes).
-// Numerics: every output element accumulates its K-blocks in order in one TMEM column — no
-// split-K — so results are independent of M, BN and scheduling (batch invariance).
+// Each CTA walks work units u = blockIdx.x, +gridDim.x, ...; the accumulator is double-buffered
+// in TMEM (2 x BN columns) so the epilogue of unit i overlaps the main loop of unit i+1.
+// Epilogues: bf16 store (LM head), fp32 residual accumulate (O / down projections add into the
+// fp32 residual stream), SwiGLU (gate/up rows interleaved in 32-row blocks), and QKV with RoPE
+// + KV-pool scatter. Units are ordered M-fastest so all M-blocks of one weight tile run
+// concurrently and each weight byte crosses HBM once per GEMM.
+//
+// Split-K for narrow outputs (N < 6144: the O / down projections, the 1B QKV): the K range of
+// a tile is split into S parts chosen from (N, K) only; every split writes its fp32 partial and
+// the last split to finish (ticket) sums the S partials in split order and runs the epilogue.
+// Because S never depends on M, a row's result is bit-identical at any batch size, BN or
+// schedule (batch invariance — the property behind "speculative stream == greedy stream").
 #include "gemm_tc.cuh"
 
 #include <cudaTypedefs.h>
@@ -50,21 +54,25 @@ struct Cfg {
 };
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// TMEM accumulator (this thread's row, BN fp32 columns at t_row) → fused epilogue → global.
-template <int BN, int EPI>
-__device__ __forceinline__ void store_tile(std::uint32_t t_row, int row, int M, int N, int n_blk, void* out, int ldo) {
+// Epilogue of one 128 x BN tile for this thread's row. fetch(col, r) yields the 32 fp32 values
+// of tile columns [col, col+32) (from TMEM, or the summed split-K partials) and must be called
+// by every lane (TMEM loads are warp-collective).
+template <int BN, int EPI, class Fetch>
+__device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int row, int M, int N, int n_blk, void* out, int ldo,
+                                              const RopeEpi& rp) {
+  const bool live = row < M;
   if constexpr (EPI == kEpiSwiGLU) {
-    // W rows interleaved in 32-row blocks [gate 0..31 | up 0..31 | gate 32..63 | ...]: TMEM
-    // column chunk 2j is gate and 2j+1 is up for output features f0 + 32j .. +31.
+    // W rows interleaved in 32-row blocks [gate 0..31 | up 0..31 | gate 32..63 | ...]: column
+    // chunk 2j is gate and 2j+1 is up for output features f0 + 32j .. +31.
     const int f0 = n_blk * (BN / 2);
 #pragma unroll 1
     for (int c = 0; c < BN / 2; c += 32) {
       std::uint32_t g[32], u[32];
-      tmem_ld32(t_row + 2 * c, g);
-      tmem_ld32(t_row + 2 * c + 32, u);
-      tmem_ld_wait();
-      if (row < M && f0 + c < N / 2) {
+      fetch(2 * c, g);
+      fetch(2 * c + 32, u);
+      if (live && f0 + c < N / 2) {
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + f0 + c;
         alignas(16) __nv_bfloat162 v[16];
 #pragma unroll
@@ -77,14 +85,64 @@ __device__ __forceinline__ void store_tile(std::uint32_t t_row, int row, int M, 
         for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
       }
     }
+  } else if constexpr (EPI == kEpiQKVRope) {
+    // Per head of the tile: rotate-half RoPE on q/k (pairs i, i+hd/2; cos/sin from the
+    // fp64-built table), then q → q_out[row], k and v → the KV pool at slot[row].
+    const int hd = rp.hd, half = hd / 2;
+    const int n0 = n_blk * BN;
+    const int pos = live ? rp.pos[row] : 0;
+    const int slot = live ? rp.slot[row] : 0;
+#pragma unroll 1
+    for (int h0 = 0; h0 < BN; h0 += hd) {
+      const int hh = (n0 + h0) / hd;  // warp-uniform
+      if (hh >= rp.nq + 2 * rp.nkv) break;
+      const bool rot = hh < rp.nq + rp.nkv;
+      __nv_bfloat16* dst;
+      if (hh < rp.nq)
+        dst = static_cast<__nv_bfloat16*>(rp.q) + (static_cast<std::size_t>(row) * rp.nq + hh) * hd;
+      else if (hh < rp.nq + rp.nkv)
+        dst = static_cast<__nv_bfloat16*>(rp.k_pool) + (static_cast<std::size_t>(slot) * rp.nkv + (hh - rp.nq)) * hd;
+      else
+        dst = static_cast<__nv_bfloat16*>(rp.v_pool) +
+              (static_cast<std::size_t>(slot) * rp.nkv + (hh - rp.nq - rp.nkv)) * hd;
+#pragma unroll 1
+      for (int c = 0; c < half; c += 32) {
+        std::uint32_t a[32], b[32];
+        fetch(h0 + c, a);
+        fetch(h0 + c + half, b);
+        if (!live) continue;
+        alignas(16) __nv_bfloat162 lo[16], hi[16];
+        const float2* cs = rp.cs + static_cast<std::size_t>(pos) * half + c;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float x0 = __uint_as_float(a[2 * j]), x1 = __uint_as_float(a[2 * j + 1]);
+          float y0 = __uint_as_float(b[2 * j]), y1 = __uint_as_float(b[2 * j + 1]);
+          if (rot) {
+            const float2 c0 = cs[2 * j], c1 = cs[2 * j + 1];
+            const float rx0 = x0 * c0.x - y0 * c0.y, ry0 = y0 * c0.x + x0 * c0.y;
+            const float rx1 = x1 * c1.x - y1 * c1.y, ry1 = y1 * c1.x + x1 * c1.y;
+            x0 = rx0;
+            y0 = ry0;
+            x1 = rx1;
+            y1 = ry1;
+          }
+          lo[j] = __floats2bfloat162_rn(x0, x1);
+          hi[j] = __floats2bfloat162_rn(y0, y1);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          reinterpret_cast<uint4*>(dst + c)[q] = reinterpret_cast<const uint4*>(lo)[q];
+          reinterpret_cast<uint4*>(dst + c + half)[q] = reinterpret_cast<const uint4*>(hi)[q];
+        }
+      }
+    }
   } else {
     const int n0 = n_blk * BN;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       std::uint32_t r[32];
-      tmem_ld32(t_row + c, r);
-      tmem_ld_wait();
-      if (row >= M || n0 + c >= N) continue;
+      fetch(c, r);
+      if (!live || n0 + c >= N) continue;
       if constexpr (EPI == kEpiBF16) {
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
         alignas(16) __nv_bfloat162 v[16];
@@ -120,66 +178,17 @@ __device__ __forceinline__ void store_tile(std::uint32_t t_row, int row, int M, 
   }
 }
 
-// Fused QKV epilogue: for each head of the tile, rotate-half RoPE on q/k (pairs i, i+hd/2 from
-// the fp32 accumulator, cos/sin from the fp64-built table) and scatter: q → q_out[row], k and
-// v → the KV pool at slot[row]. Replaces a separate rope/KV-append pass and the qkv round trip.
-template <int BN>
-__device__ __forceinline__ void store_tile_qkv(std::uint32_t t_row, int row, int M, int n_blk, const RopeEpi& r) {
-  const int hd = r.hd, half = hd / 2;
-  const int n0 = n_blk * BN;
-  const bool live = row < M;
-  const int pos = live ? r.pos[row] : 0;
-  const int slot = live ? r.slot[row] : 0;
-#pragma unroll 1
-  for (int h0 = 0; h0 < BN; h0 += hd) {
-    const int hh = (n0 + h0) / hd;  // warp-uniform
-    if (hh >= r.nq + 2 * r.nkv) break;
-    const bool rot = hh < r.nq + r.nkv;
-    __nv_bfloat16* dst;
-    if (hh < r.nq)
-      dst = static_cast<__nv_bfloat16*>(r.q) + (static_cast<std::size_t>(row) * r.nq + hh) * hd;
-    else if (hh < r.nq + r.nkv)
-      dst = static_cast<__nv_bfloat16*>(r.k_pool) + (static_cast<std::size_t>(slot) * r.nkv + (hh - r.nq)) * hd;
-    else
-      dst = static_cast<__nv_bfloat16*>(r.v_pool) + (static_cast<std::size_t>(slot) * r.nkv + (hh - r.nq - r.nkv)) * hd;
-#pragma unroll 1
-    for (int c = 0; c < half; c += 32) {
-      std::uint32_t a[32], b[32];
-      tmem_ld32(t_row + h0 + c, a);  // warp-collective: before any per-lane branch
-      tmem_ld32(t_row + h0 + c + half, b);
-      tmem_ld_wait();
-      if (!live) continue;
-      alignas(16) __nv_bfloat162 lo[16], hi[16];
-      const float2* cs = r.cs + static_cast<std::size_t>(pos) * half + c;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float x0 = __uint_as_float(a[2 * j]), x1 = __uint_as_float(a[2 * j + 1]);
-        float y0 = __uint_as_float(b[2 * j]), y1 = __uint_as_float(b[2 * j + 1]);
-        if (rot) {
-          const float2 c0 = cs[2 * j], c1 = cs[2 * j + 1];
-          const float rx0 = x0 * c0.x - y0 * c0.y, ry0 = y0 * c0.x + x0 * c0.y;
-          const float rx1 = x1 * c1.x - y1 * c1.y, ry1 = y1 * c1.x + x1 * c1.y;
-          x0 = rx0;
-          y0 = ry0;
-          x1 = rx1;
-          y1 = ry1;
-        }
-        lo[j] = __floats2bfloat162_rn(x0, x1);
-        hi[j] = __floats2bfloat162_rn(y0, y1);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        reinterpret_cast<uint4*>(dst + c)[q] = reinterpret_cast<const uint4*>(lo)[q];
-        reinterpret_cast<uint4*>(dst + c + half)[q] = reinterpret_cast<const uint4*>(hi)[q];
-      }
-    }
-  }
-}
+struct SplitArgs {
+  int splits = 1;
+  float* ws = nullptr;               // fp32 partials [splits][m_blocks*BM][N]
+  unsigned int* tickets = nullptr;   // [m_blocks * n_tiles], zero-initialised, self-resetting
+};
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo, const RopeEpi rope) {
+                   int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo, const RopeEpi rope,
+                   const SplitArgs sk) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -191,10 +200,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* tfull = empty + C::STAGES;  // [2]
   std::uint64_t* tempty = tfull + 2;         // [2]
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  std::uint32_t* last_flag = tmem_slot + 1;
 
   const int num_k = K / BK;
-  const int total = m_blocks * n_tiles;
+  const int S = sk.splits;
+  const int total = m_blocks * n_tiles * S;
   const std::uint32_t warp = warp_id(), lane = lane_id();
+  // unit u → (m_blk, n_blk, split), M fastest; split s covers k-blocks [s*nk/S, (s+1)*nk/S)
+  auto decode = [&](int u, int& m_blk, int& n_blk, int& split) {
+    m_blk = u % m_blocks;
+    const int r = u / m_blocks;
+    split = r % S;
+    n_blk = r / S;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -216,12 +234,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const std::uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer: continuous ring across tiles
+    if (lane == 0) {  // TMA producer: continuous ring across units
       int stage = 0;
       std::uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int m_blk = t % m_blocks, n_blk = t / m_blocks;
-        for (int kb = 0; kb < num_k; ++kb) {
+      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        int m_blk, n_blk, split;
+        decode(u, m_blk, n_blk, split);
+        const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
@@ -239,19 +259,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       std::uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      for (int u = blockIdx.x; u < total; u += gridDim.x, ++local) {
+        int m_blk, n_blk, split;
+        decode(u, m_blk, n_blk, split);
+        const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
         const int acc = local & 1;
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         tc_fence_after();
         const std::uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const std::uint64_t da = smem_desc_sw128(sA + stage * C::A_BYTES);
           const std::uint64_t db = smem_desc_sw128(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // advance 16 elements = 32 B = 2 descriptor units
-            mma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            mma_bf16(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
           mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
           if (++stage == C::STAGES) {
             stage = 0;
@@ -263,21 +286,89 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {  // epilogue warps 2..5 → TMEM lane groups (warp % 4)
     const int grp = static_cast<int>(warp & 3);
+    const int rows_pad = m_blocks * BM;
     int local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+    for (int u = blockIdx.x; u < total; u += gridDim.x, ++local) {
+      int m_blk, n_blk, split;
+      decode(u, m_blk, n_blk, split);
       const int acc = local & 1;
-      const int m_blk = t % m_blocks, n_blk = t / m_blocks;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
       const int row = m_blk * BM + grp * 32 + static_cast<int>(lane);
       const std::uint32_t t_row = tmem_base + acc * BN + (static_cast<std::uint32_t>(grp * 32) << 16);
-      if constexpr (EPI == kEpiQKVRope)
-        store_tile_qkv<BN>(t_row, row, M, n_blk, rope);
-      else
-        store_tile<BN, EPI>(t_row, row, M, N, n_blk, out, ldo);
+      auto tmem_fetch = [&](int col, std::uint32_t (&r)[32]) {
+        tmem_ld32(t_row + col, r);
+        tmem_ld_wait();
+      };
+      if (S == 1) {
+        epilogue_tile<BN, EPI>(tmem_fetch, row, M, N, n_blk, out, ldo, rope);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        continue;
+      }
+      // split-K: publish this split's fp32 partial, release TMEM, take a ticket
+      const int ncols = min(BN, N - n_blk * BN);
+      float* my = sk.ws + (static_cast<std::size_t>(split) * rows_pad + row) * N + static_cast<std::size_t>(n_blk) * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        std::uint32_t r[32];
+        tmem_fetch(c, r);
+        if (c < ncols) {
+          if (c + 32 <= ncols) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              __stcg(reinterpret_cast<float4*>(my + c) + q,
+                     make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                 __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+          } else {
+            for (int j = 0; j < 32 && c + j < ncols; ++j) __stcg(my + c + j, __uint_as_float(r[j]));
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      __threadfence();
+      epi_bar();
+      const int tile = n_blk * m_blocks + m_blk;
+      if (threadIdx.x == 64) {
+        const unsigned int t = atomicAdd(&sk.tickets[tile], 1u);
+        *last_flag = t == static_cast<unsigned int>(S - 1) ? 1u : 0u;
+        if (t == static_cast<unsigned int>(S - 1)) sk.tickets[tile] = 0u;  // self-reset
+      }
+      epi_bar();
+      if (*last_flag) {
+        __threadfence();
+        const float* base = sk.ws + static_cast<std::size_t>(row) * N + static_cast<std::size_t>(n_blk) * BN;
+        const std::size_t sstride = static_cast<std::size_t>(rows_pad) * N;
+        auto ws_fetch = [&](int col, std::uint32_t (&r)[32]) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          if (col < ncols) {
+            for (int s = 0; s < S; ++s) {  // fixed split order → deterministic
+              const float* p = base + s * sstride + col;
+              if (col + 32 <= ncols) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  const float4 x = __ldcg(reinterpret_cast<const float4*>(p) + q);
+                  v[4 * q] += x.x;
+                  v[4 * q + 1] += x.y;
+                  v[4 * q + 2] += x.z;
+                  v[4 * q + 3] += x.w;
+                }
+              } else {
+                for (int j = 0; j < 32 && col + j < ncols; ++j) v[j] += __ldcg(p + j);
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
+        };
+        epilogue_tile<BN, EPI>(ws_fetch, row, M, N, n_blk, out, ldo, rope);
+      }
+      epi_bar();  // last_flag is reused by the next unit
     }
   }
   tc_fence_before();
@@ -314,7 +405,7 @@ CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, st
 }
 
 template <int BN, int EPI>
-void launch(const GemmArgs& g, cudaStream_t st) {
+void launch(const GemmArgs& g, const SplitArgs& sk, cudaStream_t st) {
   using C = Cfg<BN>;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
@@ -324,11 +415,18 @@ void launch(const GemmArgs& g, cudaStream_t st) {
   const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, BN);
   const int m_blocks = (g.M + BM - 1) / BM;
   const int n_tiles = (g.N + BN - 1) / BN;  // SwiGLU: N counts gate+up rows
-  const int total = m_blocks * n_tiles;
+  const int total = m_blocks * n_tiles * sk.splits;
   const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
   gemm_tn_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo,
-                                                            g.rope);
+                                                            g.rope, sk);
   WS_CUDA(cudaGetLastError());
+}
+
+template <int EPI>
+void dispatch_bn(int bn, const GemmArgs& g, const SplitArgs& sk, cudaStream_t st) {
+  if (bn == 256) return launch<256, EPI>(g, sk, st);
+  if (bn == 128) return launch<128, EPI>(g, sk, st);
+  return launch<64, EPI>(g, sk, st);
 }
 
 }  // namespace
@@ -351,30 +449,77 @@ int pick_bn(int M, int N) {
   return best;
 }
 
+int pick_splits(int N, int K) {
+  // From (N, K) only — never from M — so results stay batch-invariant.
+  const int nk = K / BK;
+  int s = 1;
+  if (N < 3072)
+    s = 4;
+  else if (N < 6144)
+    s = 2;
+  while (s > 1 && nk / s < 8) s /= 2;  // keep >= 8 k-blocks per split
+  return s;
+}
+
+// Workspace layout (fixed, whatever the GEMM shape): [tickets: kMaxTiles u32 | fp32 partials].
+// The self-resetting tickets must never move between launches of different shapes.
+constexpr std::size_t kMaxTiles = 65536;
+constexpr std::size_t kTicketBytes = kMaxTiles * sizeof(unsigned int);
+
+std::size_t gemm_workspace_bytes(int max_rows) {
+  const std::size_t rows = ((static_cast<std::size_t>(max_rows) + BM - 1) / BM) * BM;
+  // max over split configurations of splits x N (pick_splits: 4 x <3072, 2 x <6144)
+  return kTicketBytes + rows * 12288 * sizeof(float);
+}
+
 void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   if (g.K % BK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (g.lda % 8 || g.ldw % 8) throw std::invalid_argument("gemm: leading dims must be multiples of 8");
   int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
+  if (g.epi == kEpiQKVRope) {
+    if (g.rope.hd != 64 && g.rope.hd != 128) throw std::invalid_argument("gemm: qkv epilogue needs hd 64/128");
+    if (bn < g.rope.hd) bn = g.rope.hd;  // a tile holds whole heads
+    if (g.N != (g.rope.nq + 2 * g.rope.nkv) * g.rope.hd) throw std::invalid_argument("gemm: qkv width");
+  }
+  SplitArgs sk;
+  sk.splits = g.splits > 0 ? g.splits : (g.ws ? pick_splits(g.N, g.K) : 1);
+  if (sk.splits > 1) {
+    if (!g.ws) throw std::invalid_argument("gemm: split-K needs a workspace");
+    const int m_blocks = (g.M + BM - 1) / BM;
+    const int n_tiles = (g.N + bn - 1) / bn;
+    const std::size_t need = kTicketBytes + static_cast<std::size_t>(sk.splits) * m_blocks * BM * g.N * sizeof(float);
+    if (need > g.ws_bytes || static_cast<std::size_t>(m_blocks) * n_tiles > kMaxTiles) {
+      // Rows are independent: run the GEMM in row slices that fit the workspace.
+      if (g.ws_bytes <= kTicketBytes) throw std::invalid_argument("gemm: split-K workspace too small");
+      const std::size_t per_row = static_cast<std::size_t>(sk.splits) * g.N * sizeof(float);
+      const int per = std::max<int>(BM, static_cast<int>((g.ws_bytes - kTicketBytes) / per_row / BM * BM));
+      if (per >= g.M) throw std::invalid_argument("gemm: split-K workspace too small");
+      for (int r0 = 0; r0 < g.M; r0 += per) {
+        GemmArgs s = g;
+        s.M = std::min(per, g.M - r0);
+        s.A = static_cast<const __nv_bfloat16*>(g.A) + static_cast<std::size_t>(r0) * g.lda;
+        if (g.epi == kEpiAddF32)
+          s.out = static_cast<float*>(g.out) + static_cast<std::size_t>(r0) * g.ldo;
+        else if (g.epi == kEpiQKVRope) {
+          s.rope.pos = g.rope.pos + r0;
+          s.rope.slot = g.rope.slot + r0;
+          s.rope.q = static_cast<__nv_bfloat16*>(g.rope.q) + static_cast<std::size_t>(r0) * g.rope.nq * g.rope.hd;
+        } else
+          s.out = static_cast<__nv_bfloat16*>(g.out) + static_cast<std::size_t>(r0) * g.ldo;
+        s.bn = bn;
+        s.splits = sk.splits;
+        gemm_tn(s, st);
+      }
+      return;
+    }
+    sk.tickets = static_cast<unsigned int*>(g.ws);
+    sk.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(g.ws) + kTicketBytes);
+  }
   switch (g.epi) {
-    case kEpiBF16:
-      if (bn == 256) return launch<256, kEpiBF16>(g, st);
-      if (bn == 128) return launch<128, kEpiBF16>(g, st);
-      return launch<64, kEpiBF16>(g, st);
-    case kEpiAddF32:
-      if (bn == 256) return launch<256, kEpiAddF32>(g, st);
-      if (bn == 128) return launch<128, kEpiAddF32>(g, st);
-      return launch<64, kEpiAddF32>(g, st);
-    case kEpiSwiGLU:
-      if (bn == 256) return launch<256, kEpiSwiGLU>(g, st);
-      if (bn == 128) return launch<128, kEpiSwiGLU>(g, st);
-      return launch<64, kEpiSwiGLU>(g, st);
-    case kEpiQKVRope:
-      if (g.rope.hd != 64 && g.rope.hd != 128) throw std::invalid_argument("gemm: qkv epilogue needs hd 64/128");
-      if (bn < g.rope.hd) bn = g.rope.hd;  // a tile holds whole heads
-      if (g.N != (g.rope.nq + 2 * g.rope.nkv) * g.rope.hd) throw std::invalid_argument("gemm: qkv width");
-      if (bn == 256) return launch<256, kEpiQKVRope>(g, st);
-      if (bn == 128) return launch<128, kEpiQKVRope>(g, st);
-      return launch<64, kEpiQKVRope>(g, st);
+    case kEpiBF16: return dispatch_bn<kEpiBF16>(bn, g, sk, st);
+    case kEpiAddF32: return dispatch_bn<kEpiAddF32>(bn, g, sk, st);
+    case kEpiSwiGLU: return dispatch_bn<kEpiSwiGLU>(bn, g, sk, st);
+    case kEpiQKVRope: return dispatch_bn<kEpiQKVRope>(bn, g, sk, st);
   }
   throw std::invalid_argument("gemm: unknown epilogue");
 }

@@ -2,6 +2,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
+
 namespace wsb {
 
 enum GemmEpi : int {
@@ -33,10 +35,18 @@ struct GemmArgs {
   int bn = 0;        // 0 = auto (64/128/256)
   int max_ctas = 0;  // persistent grid cap (0 = one CTA per SM)
   RopeEpi rope{};    // kEpiQKVRope only
+  // Split-K workspace (zero-initialised once; see gemm_workspace_bytes). With ws == nullptr the
+  // GEMM never splits; splits = 0 picks the (N, K)-determined count.
+  void* ws = nullptr;
+  std::size_t ws_bytes = 0;
+  int splits = 0;
 };
 
 // C = A · W^T on tcgen05 (sm_100a). Throws on bad shapes / CUDA errors.
 void gemm_tn(const GemmArgs& g, cudaStream_t stream);
 int pick_bn(int M, int N);
+int pick_splits(int N, int K);
+// Bytes of a split-K workspace serving GEMMs of up to max_rows rows per launch slice.
+std::size_t gemm_workspace_bytes(int max_rows);
 
 }  // namespace wsb

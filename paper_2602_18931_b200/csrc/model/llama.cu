@@ -123,12 +123,16 @@ LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_s
   WS_CUDA(cudaMemset(k_pool_, 0, pool));
   WS_CUDA(cudaMemset(v_pool_, 0, pool));
   ensure_rows(max_rows, max_rows);
+  gemm_ws_bytes_ = gemm_workspace_bytes(4096);  // split-K partials (row-sliced beyond 4096 rows)
+  WS_CUDA(cudaMalloc(&gemm_ws_, gemm_ws_bytes_));
+  WS_CUDA(cudaMemset(gemm_ws_, 0, gemm_ws_bytes_));
   WS_CUDA(cudaDeviceSynchronize());
 }
 
 LlamaModel::~LlamaModel() {
   cudaSetDevice(device_);
   if (rope_cs_) cudaFree(rope_cs_);
+  if (gemm_ws_) cudaFree(gemm_ws_);
   for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_, static_cast<void*>(x_), xn_, qkv_,
                   q_, attn_, h_, logits_, xo_, static_cast<void*>(d_meta_)})
     if (p) cudaFree(p);
@@ -237,6 +241,11 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
   auto I = [&](std::size_t off) { return reinterpret_cast<const std::int32_t*>(d_meta_ + off); };
 
   const int d = s_.d, qd = s_.n_q * s_.hd;
+  auto with_ws = [&](GemmArgs g) {
+    g.ws = gemm_ws_;
+    g.ws_bytes = gemm_ws_bytes_;
+    return g;
+  };
   const std::int64_t layer_stride = n_slots_ * s_.n_kv * s_.hd;
   const AttnShape ash{s_.n_q, s_.n_kv, s_.hd, s_.n_kv * s_.hd, 1.0f / std::sqrt(static_cast<float>(s_.hd))};
   prof_.begin(st);
@@ -250,24 +259,24 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
     // QKV projection with RoPE + KV append fused into the epilogue
     GemmArgs qa{xn_, wqkv_[l], nullptr, n, s_.qkv_dim(), d, d, d, s_.qkv_dim(), kEpiQKVRope, 0};
     qa.rope = RopeEpi{I(o_pos), I(o_slot), rope_cs_, q_, kp, vp, s_.n_q, s_.n_kv, s_.hd};
-    gemm_tn(qa, st);
+    gemm_tn(with_ws(qa), st);
     prof_.mark(KernelProfiler::kQKV, st);
     attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()),
               I(o_ext), reinterpret_cast<const unsigned long long*>(d_meta_ + o_msk), ash, attn_, st);
     prof_.mark(KernelProfiler::kAttn, st);
-    gemm_tn(GemmArgs{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0}, st);
+    gemm_tn(with_ws(GemmArgs{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0}), st);
     prof_.mark(KernelProfiler::kO, st);
     rmsnorm_rows(x_, d, nullptr, mlp_norm_[l], s_.eps, n, d, xn_, d, st);
     prof_.mark(KernelProfiler::kNorm, st);
-    gemm_tn(GemmArgs{xn_, wgu_[l], h_, n, 2 * s_.ffn, d, d, d, s_.ffn, kEpiSwiGLU, 0}, st);
+    gemm_tn(with_ws(GemmArgs{xn_, wgu_[l], h_, n, 2 * s_.ffn, d, d, d, s_.ffn, kEpiSwiGLU, 0}), st);
     prof_.mark(KernelProfiler::kGateUp, st);
-    gemm_tn(GemmArgs{h_, wdown_[l], x_, n, d, s_.ffn, s_.ffn, s_.ffn, d, kEpiAddF32, 0}, st);
+    gemm_tn(with_ws(GemmArgs{h_, wdown_[l], x_, n, d, s_.ffn, s_.ffn, s_.ffn, d, kEpiAddF32, 0}), st);
     prof_.mark(KernelProfiler::kDown, st);
   }
   if (n_out == 0) return;
   rmsnorm_rows(x_, d, I(o_out), final_norm_, s_.eps, n_out, d, xo_, d, st);
   prof_.mark(KernelProfiler::kNorm, st);
-  gemm_tn(GemmArgs{xo_, lm_head_, logits_, n_out, s_.vocab, d, d, d, s_.vocab, kEpiBF16, 0}, st);
+  gemm_tn(with_ws(GemmArgs{xo_, lm_head_, logits_, n_out, s_.vocab, d, d, d, s_.vocab, kEpiBF16, 0}), st);
   prof_.mark(KernelProfiler::kLMHead, st);
   if (plant > 0.f && !b.plant.empty()) plant_bias(logits_, s_.vocab, I(o_pl), plant, n_out, st);
   prof_.mark(KernelProfiler::kPlant, st);

@@ -16,7 +16,7 @@ def _bind():
     if _bound:
         return
     L = lib()
-    L.ws_op_gemm_bf16.argtypes = [_P, _P, _P] + [C.c_int] * 8 + [_P]
+    L.ws_op_gemm_bf16.argtypes = [_P, _P, _P] + [C.c_int] * 9 + [_P]
     _bound = True
 
 
@@ -28,7 +28,7 @@ def _stream():
 EPI_BF16, EPI_ADD_F32, EPI_SWIGLU = 0, 1, 2
 
 
-def gemm(A, W, out=None, epi=EPI_BF16, bn=0):
+def gemm(A, W, out=None, epi=EPI_BF16, bn=0, splits=1):
     """out = A @ W.T (bf16 in, fp32 accumulate) with the chosen fused epilogue."""
     import torch
     _bind()
@@ -43,7 +43,7 @@ def gemm(A, W, out=None, epi=EPI_BF16, bn=0):
         else:
             out = torch.empty(M, N, dtype=torch.bfloat16, device=A.device)
     _check(lib().ws_op_gemm_bf16(A.data_ptr(), W.data_ptr(), out.data_ptr(), M, N, K, A.stride(0),
-                                 W.stride(0), out.stride(0), epi, bn, _stream()))
+                                 W.stride(0), out.stride(0), epi, bn, splits, _stream()))
     return out
 
 

@@ -73,6 +73,34 @@ def test_gemm_batch_and_tile_invariance(ops):
         assert torch.equal(ops.gemm(A[lo:hi].contiguous(), W, bn=64), ref[lo:hi])
 
 
+@pytest.mark.parametrize("epi", [0, 1, 2])
+@pytest.mark.parametrize("splits", [2, 4])
+def test_gemm_split_k(ops, epi, splits):
+    """Deterministic split-K (last split sums the partials in split order): correct, repeatable,
+    and row-invariant across batch sizes at a fixed split count."""
+    M, N, K = 333, 2048, 4096
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    if epi == 2:
+        Wg, Wu = W[:N // 2], W[N // 2:]
+        W = ops.interleave_gate_up(Wg.contiguous(), Wu.contiguous())
+        ref = torch.nn.functional.silu(A.float() @ Wg.float().T) * (A.float() @ Wu.float().T)
+    else:
+        ref = A.float() @ W.float().T
+    if epi == 1:
+        X0 = torch.randn(M, N, device="cuda")
+        out = X0.clone()
+        ops.gemm(A, W, out=out, epi=1, splits=splits)
+        assert rel_err(out, X0 + ref) < 1e-5
+        return
+    out = ops.gemm(A, W, epi=epi, splits=splits)
+    assert rel_err(out, ref) < 6e-3
+    again = ops.gemm(A, W, epi=epi, splits=splits)
+    assert torch.equal(out, again)
+    part = ops.gemm(A[100:140].contiguous(), W, epi=epi, splits=splits, bn=64)
+    assert torch.equal(part, out[100:140])
+
+
 def test_gemm_large_throughput_smoke(ops):
     """8B-shape gate/up at 1280 verify rows: correct and finishes."""
     M, N, K = 1280, 28672, 4096
