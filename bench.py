@@ -156,21 +156,40 @@ def llama_roofline(stats, k, peak_bw, peak_tf, avg_ctx):
             "frac": t_hbm / t_meas}, rows, flops, byts, t_meas
 
 
-def cpu_port_sample(args, stats, tokens, k):
-    """CPU port (oracle/llama_cpu.py, numpy fp32, all host cores) on a bounded sample: one verify
-    forward of one request (k+1 rows after a 160-token context) and one draft forward (1 row),
-    scaled by this run's own per-request step counts."""
+def cpu_reference_llama(k, requests, samples=1):
+    """The reference's CPU implementation of the config-3 path: the reference protocol itself
+    (run_sim_full via oracle/_ref — or the restatement when the reference is absent — on its
+    default tiny pair, match 0.8, the same k/b/s/theta/phi/RTT and 100 tokens) supplies the
+    per-request model-call counts; the numpy fp32 port (oracle/llama_cpu.py, all host cores)
+    supplies the cost of each call on a bounded sample: one 8B verify forward of k+1 rows, one
+    1B draft forward of s=4 leaves and one of 1 row, after a 160-token context. One request at
+    a time (the reference runs requests sequentially, sim.hpp:433)."""
     from oracle import llama_cpu
-    t_v = llama_cpu.time_forward("llama3-8b", k + 1, 160, lm_rows=k + 1)
-    t_d = llama_cpu.time_forward("llama3.2-1b", 1, 160, lm_rows=1)
-    n_v = stats["target_forwards_per_request"]
-    n_d = stats["draft_rows_per_request"]
-    per_req = n_v * t_v + n_d * t_d
-    return {"value": (tokens / stats["requests"]) / per_req, "unit": UNIT, "cores": os.cpu_count() or 1,
-            "kind": "port",
-            "sample": f"numpy fp32 port: one 8B verify forward ({k + 1} rows, ctx 160) = {t_v:.2f} s and one 1B "
-                      f"draft row = {t_d:.2f} s, x this run's per-request counts ({n_v:.1f} verifies, "
-                      f"{n_d:.1f} draft rows); one request at a time"}
+    from oracle import pyoracle as po
+    from paper_2602_18931_b200 import abi
+    c = abi.apply_stage(abi.sim_cfg(k=k, rtt=20000, num_requests=min(requests, 64), max_nodes=256), "full")
+    if po.ref_available():
+        m = po.ref_run_sim(c, threads=os.cpu_count() or 1, with_tokens=False, with_steps=False).metrics_list()
+    else:
+        import paper_2602_18931_b200 as ws
+        m = ws.run_sim_with_model(c, po.model_round_fn(c), with_tokens=False, with_steps=False).metrics_list()
+    n = len(m)
+    tv = td4 = td1 = 0.0
+    for _ in range(samples):
+        tv += llama_cpu.time_forward("llama3-8b", k + 1, 160, lm_rows=k + 1)
+        td4 += llama_cpu.time_forward("llama3.2-1b", 4, 160, lm_rows=4)
+        td1 += llama_cpu.time_forward("llama3.2-1b", 1, 160, lm_rows=1)
+    tv, td4, td1 = tv / samples, td4 / samples, td1 / samples
+    tokens = sum(x["tokens_committed"] for x in m)
+    secs = sum(x["target_steps"] * tv + x["worker_draft_steps"] * td4 + x["ctrl_draft_passes"] * td1 for x in m)
+    return tokens / secs, (f"reference protocol counts over {n} requests x numpy fp32 port costs on all host cores: "
+                           f"8B verify ({k + 1} rows) {tv:.2f} s, 1B draft step (4 leaves) {td4:.3f} s, "
+                           f"1B local draft pass {td1:.3f} s; {samples} sample(s)")
+
+
+def cpu_port_sample(args, k):
+    value, sample = cpu_reference_llama(k, args.requests)
+    return {"value": value, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port", "sample": sample}
 
 
 # ------------------------------------------------------------------ reference arm
@@ -197,21 +216,8 @@ def run_reference(args, rank, world):
                                          "(run_sim_full via oracle/_ref, requests over threads)", "reference"
     else:
         # The reference has no model: its CPU implementation of the config-3 path is
-        # the oracle port (numpy fp32 Llama forward) driven by the reference protocol's step
-        # counts; each step times one 8B verify forward + k 1B draft rows of one request.
-        from oracle import llama_cpu
-        k = args.k
-        for _ in range(max(0, args.warmup - 2)):
-            llama_cpu.time_forward("llama3.2-1b", 1, 160, lm_rows=1)
-        el, toks = 0.0, 0.0
-        for _ in range(args.steps):
-            t_v = llama_cpu.time_forward("llama3-8b", k + 1, 160, lm_rows=k + 1)
-            t_d = llama_cpu.time_forward("llama3.2-1b", 1, 160, lm_rows=1)
-            el += t_v + k * t_d
-            toks += 0.8 * k + 1  # expected committed tokens per verify at match 0.8 (greedy, k drafted)
-        value = toks / el
-        sample = (f"{args.steps} x (one 8B verify forward of {k + 1} rows + {k} 1B draft rows, ctx 160), "
-                  "numpy fp32 on all host cores; tokens per verify = 0.8k+1")
+        # the reference protocol's own call counts x the numpy fp32 port's per-call cost.
+        value, sample = cpu_reference_llama(args.k, args.requests, samples=max(1, args.steps))
         kind = "port"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
@@ -326,11 +332,8 @@ def main():
             line["model_time"] = {k: (v / args.steps if isinstance(v, float) else v // args.steps)
                                   for k, v in mstats.items()}
             if world == 1:
-                per = {"requests": local,
-                       "target_forwards_per_request": mstats["target_rows"] / args.steps / local / (args.k + 1),
-                       "draft_rows_per_request": mstats["draft_rows"] / args.steps / local}
                 try:
-                    line["cpu_baseline"] = cpu_port_sample(args, per, tokens / args.steps, args.k)
+                    line["cpu_baseline"] = cpu_port_sample(args, args.k)
                 except Exception as e:  # the CPU port needs ~2 GB of host RAM per 8B layer
                     line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
         else:
