@@ -25,9 +25,7 @@ namespace wsb {
 
 namespace {
 
-constexpr int kThreads = 128;  // 4 warps x 16 query vectors
-constexpr int kTile = 32;      // positions per K/V tile
-constexpr int kVecPerPass = 64;
+constexpr int kTile = 32;  // positions per K/V tile
 
 __device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
   return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -70,8 +68,10 @@ __device__ __forceinline__ int swz(int row, int chunk) {
   return row * C + (chunk ^ (row & 7));
 }
 
-template <int HD>
-__global__ void __launch_bounds__(kThreads) attn_mma_kernel(const __nv_bfloat16* __restrict__ q,
+// NW warps per CTA (16 query vectors each): NW = 4 for verify / catch-up groups, NW = 1 for the
+// small tree groups of the draft (<= 16 vectors), so those do not idle three warps per CTA.
+template <int HD, int NW>
+__global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* __restrict__ q,
                                                             const __nv_bfloat16* __restrict__ kp,
                                                             const __nv_bfloat16* __restrict__ vp,
                                                             const AttnGroup* __restrict__ groups,
@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(kThreads) attn_mma_kernel(const __nv_bfloat16*
   constexpr int C = HD / 8;   // 16-byte chunks per row
   constexpr int KS = HD / 16; // k16 steps for S = Q·Kᵀ
   constexpr int NT = HD / 8;  // n8 tiles of the output
+  constexpr int kThreads = 32 * NW;
+  constexpr int kVecPerPass = 16 * NW;
   __shared__ __align__(128) uint4 sQ[kVecPerPass * C];
   __shared__ __align__(128) uint4 sK[2][kTile * C];
   __shared__ __align__(128) uint4 sV[2][kTile * C];
@@ -286,25 +288,33 @@ __global__ void __launch_bounds__(kThreads) attn_mma_kernel(const __nv_bfloat16*
 
 }  // namespace
 
-void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
-               const std::int32_t* extra, const unsigned long long* row_mask, const AttnShape& s, void* out,
-               cudaStream_t st) {
+template <int HD, int NW>
+void launch_attn(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
+                 const std::int32_t* extra, const unsigned long long* row_mask, const AttnShape& s, float sl2,
+                 void* out, cudaStream_t st) {
   if (n_groups <= 0) return;
-  dim3 grid(n_groups, s.n_kv);
-  const float sl2 = s.scale * 1.4426950408889634f;
-  if (s.hd == 128)
-    attn_mma_kernel<128><<<grid, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
-                                                    static_cast<const __nv_bfloat16*>(k_pool),
-                                                    static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask,
-                                                    s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
-  else if (s.hd == 64)
-    attn_mma_kernel<64><<<grid, kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
-                                                   static_cast<const __nv_bfloat16*>(k_pool),
-                                                   static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask,
-                                                   s.n_q, s.n_kv, sl2, static_cast<__nv_bfloat16*>(out));
-  else
-    throw std::invalid_argument("attention: head dim must be 64 or 128");
+  attn_mma_kernel<HD, NW><<<dim3(n_groups, s.n_kv), 32 * NW, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
+      static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask, s.n_q, s.n_kv, sl2,
+      static_cast<__nv_bfloat16*>(out));
   WS_CUDA(cudaGetLastError());
+}
+
+// groups[0, n_small) hold <= 16 query vectors each (one warp per CTA), the rest use 4 warps.
+void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
+               int n_small, const std::int32_t* extra, const unsigned long long* row_mask, const AttnShape& s,
+               void* out, cudaStream_t st) {
+  if (n_groups <= 0) return;
+  const float sl2 = s.scale * 1.4426950408889634f;
+  if (s.hd == 128) {
+    launch_attn<128, 1>(q, k_pool, v_pool, groups, n_small, extra, row_mask, s, sl2, out, st);
+    launch_attn<128, 4>(q, k_pool, v_pool, groups + n_small, n_groups - n_small, extra, row_mask, s, sl2, out, st);
+  } else if (s.hd == 64) {
+    launch_attn<64, 1>(q, k_pool, v_pool, groups, n_small, extra, row_mask, s, sl2, out, st);
+    launch_attn<64, 4>(q, k_pool, v_pool, groups + n_small, n_groups - n_small, extra, row_mask, s, sl2, out, st);
+  } else {
+    throw std::invalid_argument("attention: head dim must be 64 or 128");
+  }
 }
 
 }  // namespace wsb

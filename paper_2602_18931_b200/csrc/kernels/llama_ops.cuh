@@ -45,9 +45,10 @@ void rope_kv_append(const void* qkv, int rows, int nq, int nkv, int hd, const st
                     cudaStream_t st);
 
 // Grouped attention (causal or masked groups) over the slot pools → out bf16 [rows, nq * hd].
+// groups[0, n_small) must hold at most 16 query vectors (n_rows * n_q / n_kv) each.
 void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
-               const std::int32_t* extra_slots, const unsigned long long* row_mask, const AttnShape& shape, void* out,
-               cudaStream_t st);
+               int n_small, const std::int32_t* extra_slots, const unsigned long long* row_mask,
+               const AttnShape& shape, void* out, cudaStream_t st);
 
 // logits[row, plant[row]] += bias (plant < 0: none) — the planted shared bigram bias.
 void plant_bias(void* logits_bf16, int ld, const std::int32_t* plant, float bias, int rows, cudaStream_t st);

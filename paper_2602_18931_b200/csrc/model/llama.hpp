@@ -108,6 +108,7 @@ class LlamaModel {
   void* weight_block_ = nullptr;
   float* inv_freq_ = nullptr;
   float2* rope_cs_ = nullptr;  // [kMaxPos][hd/2] cos/sin
+  std::vector<AttnGroup> grp_sorted_;
   void* gemm_ws_ = nullptr;    // split-K workspace (K1)
   std::size_t gemm_ws_bytes_ = 0;
   static constexpr int kMaxPos = 4096;
