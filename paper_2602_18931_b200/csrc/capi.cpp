@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -181,7 +182,8 @@ void run_resident(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
 // The host-logic seam: the round is delegated to a caller-supplied function.
 class CallbackBackend : public wsb::ModelBackend {
  public:
-  CallbackBackend(ws_model_round_fn fn, void* user) : fn_(fn), user_(user) {}
+  CallbackBackend(ws_model_round_fn fn, void* user)
+      : fn_(fn), user_(user), lanes_(std::getenv("WS_EMULATE_LANES") != nullptr) {}
   void run_round(const wsb::RoundJobs& jobs, wsb::RoundResults& res, int mode, std::uint64_t seed) override {
     res.verify.resize(jobs.verify.size());
     res.draft.resize(jobs.draft.size());
@@ -194,9 +196,41 @@ class CallbackBackend : public wsb::ModelBackend {
     stats.draft_rows += jobs.draft.size();
   }
 
+  // WS_EMULATE_LANES=1: the two-lane continuous-batching driver over the callback (CPU tests
+  // of the lanes driver); completions are returned in a scrambled but seeded order.
+  bool has_lanes() const override { return lanes_; }
+  void submit(int lane, const wsb::RoundJobs& jobs, int mode, std::uint64_t seed) override {
+    wsb::RoundJobs one;
+    if (lane == 0) {
+      one.verify = jobs.verify;
+      one.cands = jobs.cands;
+    } else {
+      one.draft = jobs.draft;
+    }
+    run_round(one, done_[lane], mode, seed);
+  }
+  int wait_any(bool busy0, bool busy1) override {
+    if (busy0 && busy1) {
+      rng_ ^= rng_ << 13;
+      rng_ ^= rng_ >> 7;
+      rng_ ^= rng_ << 17;
+      return static_cast<int>(rng_ & 1);
+    }
+    return busy0 ? 0 : 1;
+  }
+  void complete(int lane, wsb::RoundResults& res) override {
+    if (lane == 0)
+      res.verify.swap(done_[0].verify);
+    else
+      res.draft.swap(done_[1].draft);
+  }
+
  private:
   ws_model_round_fn fn_;
   void* user_;
+  bool lanes_;
+  wsb::RoundResults done_[2];
+  std::uint64_t rng_ = 0x9E3779B97F4A7C15ULL;
 };
 
 }  // namespace

@@ -3,7 +3,9 @@
 #include "driver.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
+#include <unordered_map>
 #include <queue>
 #include <stdexcept>
 #include <utility>
@@ -93,8 +95,9 @@ class RequestRun {
 
   // Advances the virtual clock until the next event is a model completion whose job has not
   // been executed yet (jobs for everything launched are appended to `jobs`), or until done.
-  Status advance(RoundJobs& jobs) {
-    jobs_ = &jobs;
+  Status advance(RoundJobs& vjobs, RoundJobs& djobs) {
+    jobs_v_ = &vjobs;
+    jobs_d_ = &djobs;
     if (!started_) {
       started_ = true;
       if (!cfg_.baseline) {  // sim.hpp:183-190: Hello starts the worker at rtt/2
@@ -294,14 +297,15 @@ class RequestRun {
         j.base = target_.base;
         j.request = request_id_;
         j.step = static_cast<std::uint32_t>(ctrl_.counters.target_steps);
-        j.cand_off = static_cast<std::uint32_t>(jobs_->cands.size());
-        jobs_->cands.insert(jobs_->cands.end(), target_.tokens.begin(), target_.tokens.end());
-        jobs_->verify.push_back(j);
-        if (jobs_->want_ctx) {  // committed output (stable until this verify folds)
-          jobs_->verify_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jobs_->ctx_tokens.size()),
-                                             static_cast<std::uint32_t>(ctrl_.committed.size()),
-                                             static_cast<std::uint32_t>(ctrl_.committed.size()), kJobVerify});
-          jobs_->ctx_tokens.insert(jobs_->ctx_tokens.end(), ctrl_.committed.begin(), ctrl_.committed.end());
+        RoundJobs& jv = *jobs_v_;
+        j.cand_off = static_cast<std::uint32_t>(jv.cands.size());
+        jv.cands.insert(jv.cands.end(), target_.tokens.begin(), target_.tokens.end());
+        jv.verify.push_back(j);
+        if (jv.want_ctx) {  // committed output (stable until this verify folds)
+          jv.verify_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jv.ctx_tokens.size()),
+                                         static_cast<std::uint32_t>(ctrl_.committed.size()),
+                                         static_cast<std::uint32_t>(ctrl_.committed.size()), kJobVerify});
+          jv.ctx_tokens.insert(jv.ctx_tokens.end(), ctrl_.committed.begin(), ctrl_.committed.end());
         }
         verify_slots_->push_back(this);
         target_ready_ = false;
@@ -312,13 +316,14 @@ class RequestRun {
       if (action_.kind == ActionKind::step_draft_local) {
         devices_.draft_busy = true;
         std::swap(local_, action_.local);
-        jobs_->draft.push_back(DraftJob{static_cast<std::uint32_t>(request_id_), 0, local_.anchor});
+        RoundJobs& jd = *jobs_d_;
+        jd.draft.push_back(DraftJob{static_cast<std::uint32_t>(request_id_), 0, local_.anchor});
         draft_slots_->push_back({this, kLocalSlot});
-        if (jobs_->want_ctx) {  // plan.context = committed + leaf path (controller.hpp:200-201)
-          jobs_->draft_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jobs_->ctx_tokens.size()),
-                                            static_cast<std::uint32_t>(local_.context.size()),
-                                            static_cast<std::uint32_t>(ctrl_.committed.size()), kJobCtrlDraft});
-          jobs_->ctx_tokens.insert(jobs_->ctx_tokens.end(), local_.context.begin(), local_.context.end());
+        if (jd.want_ctx) {  // plan.context = committed + leaf path (controller.hpp:200-201)
+          jd.draft_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jd.ctx_tokens.size()),
+                                        static_cast<std::uint32_t>(local_.context.size()),
+                                        static_cast<std::uint32_t>(ctrl_.committed.size()), kJobCtrlDraft});
+          jd.ctx_tokens.insert(jd.ctx_tokens.end(), local_.context.begin(), local_.context.end());
         }
         local_ready_ = false;
         schedule(now_ + static_cast<SimTime>(local_.passes()) * ccfg_.t_draft, EvKind::ctrl_draft_done);
@@ -342,16 +347,17 @@ class RequestRun {
     wrk_busy_ = true;
     worker_results_.resize(worker_leaves_.size());
     worker_delivered_ = 0;
+    RoundJobs& jd = *jobs_d_;
     for (std::size_t i = 0; i < worker_leaves_.size(); ++i) {
-      jobs_->draft.push_back(DraftJob{static_cast<std::uint32_t>(request_id_), 0, worker_leaves_[i].anchor});
+      jd.draft.push_back(DraftJob{static_cast<std::uint32_t>(request_id_), 0, worker_leaves_[i].anchor});
       draft_slots_->push_back({this, static_cast<std::uint32_t>(i)});
-      if (jobs_->want_ctx) {  // worker committed + path_tokens(leaf)
+      if (jd.want_ctx) {  // worker committed + path_tokens(leaf)
         wrk_.tree.path_tokens(worker_leaves_[i].id, path_tmp_);
-        jobs_->draft_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jobs_->ctx_tokens.size()),
-                                          static_cast<std::uint32_t>(wrk_.committed.size() + path_tmp_.size()),
-                                          static_cast<std::uint32_t>(wrk_.committed.size()), kJobWorkerDraft});
-        jobs_->ctx_tokens.insert(jobs_->ctx_tokens.end(), wrk_.committed.begin(), wrk_.committed.end());
-        jobs_->ctx_tokens.insert(jobs_->ctx_tokens.end(), path_tmp_.begin(), path_tmp_.end());
+        jd.draft_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jd.ctx_tokens.size()),
+                                      static_cast<std::uint32_t>(wrk_.committed.size() + path_tmp_.size()),
+                                      static_cast<std::uint32_t>(wrk_.committed.size()), kJobWorkerDraft});
+        jd.ctx_tokens.insert(jd.ctx_tokens.end(), wrk_.committed.begin(), wrk_.committed.end());
+        jd.ctx_tokens.insert(jd.ctx_tokens.end(), path_tmp_.begin(), path_tmp_.end());
       }
     }
     worker_ready_ = worker_leaves_.empty();
@@ -377,7 +383,8 @@ class RequestRun {
   std::uint64_t request_id_;
   std::mt19937_64 jitter_rng_;
   bool log_steps_;
-  RoundJobs* jobs_ = nullptr;
+  RoundJobs* jobs_v_ = nullptr;  // where launched verify jobs are registered
+  RoundJobs* jobs_d_ = nullptr;  // ... draft jobs (the same object in lockstep mode)
 
   std::priority_queue<Event, std::vector<Event>, EventAfter> queue_;
   std::vector<Message> pool_;
@@ -412,10 +419,99 @@ class RequestRun {
   std::vector<TokenId> path_tmp_;
 };
 
+// Continuous batching over the backend's two lanes (see ModelBackend).
+void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::size_t n, ModelBackend& backend,
+                        RequestOutput* outs, bool log_steps) {
+  std::vector<std::unique_ptr<RequestRun>> runs;
+  runs.reserve(n);
+  std::vector<RequestRun*> vslots, vslots_fly;
+  std::vector<RequestRun::DraftSlot> dslots, dslots_fly;
+  for (std::size_t i = 0; i < n; ++i) {
+    runs.emplace_back(new RequestRun(cfg, requests[i], log_steps));
+    runs.back()->verify_slots_ = &vslots;
+    runs.back()->draft_slots_ = &dslots;
+  }
+  std::unordered_map<const RequestRun*, std::size_t> index;
+  for (std::size_t i = 0; i < n; ++i) index[runs[i].get()] = i;
+  RoundJobs pend_v, pend_d, fly_v, fly_d;
+  pend_v.want_ctx = pend_d.want_ctx = fly_v.want_ctx = fly_d.want_ctx = backend.wants_context();
+  RoundResults res;
+  std::vector<std::size_t> ready(n);
+  for (std::size_t i = 0; i < n; ++i) ready[i] = i;
+  std::vector<char> queued(n, 0);
+  std::size_t live = n;
+  bool busy[2] = {false, false};
+  auto wake = [&](RequestRun* r) {
+    const std::size_t i = index[r];
+    if (!queued[i]) {
+      queued[i] = 1;
+      ready.push_back(i);
+    }
+  };
+  while (live > 0) {
+    for (std::size_t i : ready) {
+      queued[i] = 0;
+      if (runs[i] && runs[i]->advance(pend_v, pend_d) == RequestRun::Status::done) {
+        runs[i]->collect(outs[i]);
+        runs[i].reset();
+        --live;
+      }
+    }
+    ready.clear();
+    if (live == 0) break;
+    if (!busy[0] && !pend_v.verify.empty()) {
+      std::swap(pend_v, fly_v);
+      std::swap(vslots, vslots_fly);
+      pend_v.clear();
+      vslots.clear();
+      backend.submit(0, fly_v, cfg.verify, cfg.sample_seed);
+      busy[0] = true;
+    }
+    if (!busy[1] && !pend_d.draft.empty()) {
+      std::swap(pend_d, fly_d);
+      std::swap(dslots, dslots_fly);
+      pend_d.clear();
+      dslots.clear();
+      backend.submit(1, fly_d, cfg.verify, cfg.sample_seed);
+      busy[1] = true;
+    }
+    if (!busy[0] && !busy[1]) throw std::logic_error("driver: requests blocked with no pending model step");
+    const int lane = backend.wait_any(busy[0], busy[1]);
+    backend.complete(lane, res);
+    busy[lane] = false;
+    if (lane == 0) {
+      for (std::size_t j = 0; j < vslots_fly.size(); ++j) {
+        vslots_fly[j]->deliver_verify(res.verify[j]);
+        wake(vslots_fly[j]);
+      }
+    } else {
+      for (std::size_t j = 0; j < dslots_fly.size(); ++j) {
+        const auto& s = dslots_fly[j];
+        if (s.which == RequestRun::kLocalSlot)
+          s.run->deliver_local(res.draft[j]);
+        else
+          s.run->deliver_worker(s.which, res.draft[j]);
+        wake(s.run);
+      }
+    }
+  }
+}
+
 }  // namespace
+
+void ModelBackend::submit(int, const RoundJobs&, int, std::uint64_t) {
+  throw std::logic_error("backend has no asynchronous lanes");
+}
+int ModelBackend::wait_any(bool, bool) { throw std::logic_error("backend has no asynchronous lanes"); }
+void ModelBackend::complete(int, RoundResults&) { throw std::logic_error("backend has no asynchronous lanes"); }
 
 void run_requests(const SimCfg& cfg, const std::uint32_t* requests, std::size_t n,
                   ModelBackend& backend, RequestOutput* outs, bool log_steps) {
+  static const bool lockstep = std::getenv("WS_LOCKSTEP") != nullptr;  // A/B switch for the bench
+  if (backend.has_lanes() && !lockstep) {
+    run_requests_lanes(cfg, requests, n, backend, outs, log_steps);
+    return;
+  }
   std::vector<std::unique_ptr<RequestRun>> runs;
   runs.reserve(n);
   std::vector<RequestRun*> verify_slots;
@@ -437,7 +533,7 @@ void run_requests(const SimCfg& cfg, const std::uint32_t* requests, std::size_t 
     std::size_t w = 0;
     for (std::size_t a = 0; a < active.size(); ++a) {
       const std::size_t i = active[a];
-      if (runs[i]->advance(jobs) == RequestRun::Status::done) {
+      if (runs[i]->advance(jobs, jobs) == RequestRun::Status::done) {
         runs[i]->collect(outs[i]);
         runs[i].reset();
       } else {

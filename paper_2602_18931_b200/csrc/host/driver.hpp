@@ -77,12 +77,26 @@ struct BackendStats {
 };
 
 // The GPU side of one protocol thread. run_round must fill res.verify / res.draft in job order.
+//
+// Backends may also expose two asynchronous lanes (lane 0: verify jobs on the target device,
+// lane 1: draft jobs on the draft device — the reference's two devices, ControllerDevices in
+// controller.hpp). The driver then runs continuous batching: a lane that goes idle takes every
+// job pending at that moment, and a request resumes as soon as the results it waits on are
+// back, so the target and draft forwards overlap instead of meeting at a round barrier.
+// Per-request results are unchanged (each job's inputs are captured at launch and the kernels
+// are batch-invariant).
 class ModelBackend {
  public:
   virtual ~ModelBackend() = default;
   virtual void run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode,
                          std::uint64_t sample_seed) = 0;
   virtual bool wants_context() const { return false; }
+  virtual bool has_lanes() const { return false; }
+  // lane 0 reads jobs.verify/cands/verify_ctx, lane 1 jobs.draft/draft_ctx (+ ctx_tokens);
+  // `jobs` must stay alive and unchanged until complete(lane).
+  virtual void submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed);
+  virtual int wait_any(bool busy0, bool busy1);        // blocks until a busy lane is done
+  virtual void complete(int lane, RoundResults& res);  // fills res.verify (0) / res.draft (1)
   BackendStats stats;
 };
 

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <random>
 #include <stdexcept>
+#include <thread>
 
 #include "../kernels/cuda_check.hpp"
 #include "../kernels/rowstats.cuh"
@@ -109,20 +110,26 @@ struct TreeCache {
 struct ModelPair::Impl {
   std::vector<LinearCache> tgt, ctrl;
   std::vector<TreeCache> wrk;
-  // K3/K4 device buffers
-  ws_pred* d_pred = nullptr;    // target rows (K3/K4)
-  ws_pred* d_pred_d = nullptr;  // draft rows
-  void* d_ws_d = nullptr;       // draft K3 workspace (the two forwards run concurrently)
-  unsigned char* h_res = nullptr;  // pinned results (verify outs | draft preds)
+  // verify lane (target stream): K3/K4 buffers, pinned staging and results
+  ws_pred* d_pred = nullptr;
   ws_verify_out* d_vout = nullptr;
   std::uint32_t* d_cands = nullptr;
   std::int32_t* d_forced = nullptr;
   void* d_ws = nullptr;
   unsigned char* h_stage = nullptr;
-  std::size_t cap_rows = 0;
+  ws_verify_out* h_vout = nullptr;
+  std::size_t cap_v = 0;
+  // draft lane (draft stream): the two lanes run concurrently, so nothing is shared
+  ws_pred* d_pred_d = nullptr;
+  void* d_ws_d = nullptr;
+  ws_pred* h_pred_d = nullptr;
+  std::size_t cap_d = 0;
   ForwardBatch tb, db;
   std::vector<TokenId> ctx;
+  std::vector<std::int32_t> forced, job_out, copy_src, copy_dst;
+  std::uint32_t nv = 0, nd = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  cudaEvent_t done[2] = {nullptr, nullptr};  // after each lane's result D2H
 };
 
 ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(device), impl(new Impl) {
@@ -140,6 +147,8 @@ ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(d
   WS_CUDA(cudaEventCreate(&impl->e1));
   WS_CUDA(cudaEventCreate(&impl->e2));
   WS_CUDA(cudaEventCreate(&impl->e3));
+  WS_CUDA(cudaEventCreateWithFlags(&impl->done[0], cudaEventDisableTiming));
+  WS_CUDA(cudaEventCreateWithFlags(&impl->done[1], cudaEventDisableTiming));
   reset_requests();
 }
 
@@ -149,9 +158,9 @@ ModelPair::~ModelPair() {
   for (void* p : {static_cast<void*>(I.d_pred), static_cast<void*>(I.d_vout), static_cast<void*>(I.d_cands),
                   static_cast<void*>(I.d_forced), I.d_ws, static_cast<void*>(I.d_pred_d), I.d_ws_d})
     if (p) cudaFree(p);
-  if (I.h_stage) cudaFreeHost(I.h_stage);
-  if (I.h_res) cudaFreeHost(I.h_res);
-  for (cudaEvent_t e : {I.e0, I.e1, I.e2, I.e3})
+  for (void* p : {static_cast<void*>(I.h_stage), static_cast<void*>(I.h_vout), static_cast<void*>(I.h_pred_d)})
+    if (p) cudaFreeHost(p);
+  for (cudaEvent_t e : {I.e0, I.e1, I.e2, I.e3, I.done[0], I.done[1]})
     if (e) cudaEventDestroy(e);
   target_.reset();
   draft_.reset();
@@ -190,9 +199,24 @@ ModelBackend_Llama::ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, T
     : p_(pair), L_(seq_len), eos_(eos), k_(k) {}
 ModelBackend_Llama::~ModelBackend_Llama() = default;
 
-void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t) {
-  if (verify_mode != WS_VERIFY_GREEDY)
-    throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
+namespace {
+// Row at context position pos predicts committed index pos + 1 - P; past the generation cap
+// that prediction is a forced EOS (oracle.hpp:88-102).
+inline std::int32_t forced_at(std::int32_t pos, std::int32_t P, std::uint32_t L, TokenId eos) {
+  return (pos + 1 - P) >= static_cast<std::int32_t>(L) - 1 ? static_cast<std::int32_t>(eos) : -1;
+}
+}  // namespace
+
+void ModelBackend_Llama::fill_ctx(const RoundJobs& jobs, std::uint32_t r, const JobCtx& c) {
+  ModelPair::Impl& I = *p_->impl;
+  const std::vector<TokenId>& prompt = p_->prompt(r);
+  I.ctx.assign(prompt.begin(), prompt.end());
+  I.ctx.insert(I.ctx.end(), jobs.ctx_tokens.begin() + c.off, jobs.ctx_tokens.begin() + c.off + c.len);
+}
+
+// Lane 0: one target forward over every pending verify row, then the fused K3/K4 greedy
+// verify epilogue; verify outs land in pinned memory.
+void ModelBackend_Llama::submit_verify(const RoundJobs& jobs) {
   ModelPair::Impl& I = *p_->impl;
   const ModelPairCfg& cfg = p_->cfg();
   cudaStream_t st = p_->stream();
@@ -200,63 +224,157 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
   const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
   const std::int32_t V = p_->target().shape().vocab;
   const std::uint32_t nv = static_cast<std::uint32_t>(jobs.verify.size());
-  const std::uint32_t nd = static_cast<std::uint32_t>(jobs.draft.size());
-  const std::size_t need_rows = std::max<std::size_t>(nv * (k_ + 1), nd) + 16;
-  if (need_rows > I.cap_rows) {
+  I.nv = nv;
+  if (!nv) return;
+  const std::size_t need = static_cast<std::size_t>(nv) * (k_ + 1) + 16;
+  if (need > I.cap_v) {  // the lane is idle here (the driver submits only to idle lanes)
     for (void* q : {static_cast<void*>(I.d_pred), static_cast<void*>(I.d_vout), static_cast<void*>(I.d_cands),
-                    static_cast<void*>(I.d_forced), I.d_ws, static_cast<void*>(I.d_pred_d), I.d_ws_d})
+                    static_cast<void*>(I.d_forced), I.d_ws})
       if (q) cudaFree(q);
-    if (I.h_stage) cudaFreeHost(I.h_stage);
-    if (I.h_res) cudaFreeHost(I.h_res);
-    I.cap_rows = need_rows * 2;
-    WS_CUDA(cudaMalloc(&I.d_pred, I.cap_rows * sizeof(ws_pred)));
-    WS_CUDA(cudaMalloc(&I.d_vout, I.cap_rows * sizeof(ws_verify_out)));
-    WS_CUDA(cudaMalloc(&I.d_cands, I.cap_rows * k_ * 4 + 64));
-    WS_CUDA(cudaMalloc(&I.d_forced, I.cap_rows * 4));
-    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(I.cap_rows), V,
-                                                      static_cast<std::uint32_t>(I.cap_rows));
+    for (void* q : {static_cast<void*>(I.h_stage), static_cast<void*>(I.h_vout)})
+      if (q) cudaFreeHost(q);
+    I.cap_v = need * 2;
+    WS_CUDA(cudaMalloc(&I.d_pred, I.cap_v * sizeof(ws_pred)));
+    WS_CUDA(cudaMalloc(&I.d_vout, I.cap_v * sizeof(ws_verify_out)));
+    WS_CUDA(cudaMalloc(&I.d_cands, I.cap_v * k_ * 4 + 64));
+    WS_CUDA(cudaMalloc(&I.d_forced, I.cap_v * 4));
+    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(I.cap_v), V,
+                                                      static_cast<std::uint32_t>(I.cap_v));
     WS_CUDA(cudaMalloc(&I.d_ws, wsb_));
     WS_CUDA(cudaMemset(I.d_ws, 0, wsb_));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_vout), I.cap_v * sizeof(ws_verify_out),
+                          cudaHostAllocDefault));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_stage), I.cap_v * (k_ * 4 + 8) + 256, cudaHostAllocDefault));
+  }
+  ForwardBatch& b = I.tb;
+  b.clear();
+  I.forced.assign(static_cast<std::size_t>(nv) * (k_ + 1), -1);
+  std::uint32_t* hc = reinterpret_cast<std::uint32_t*>(I.h_stage);
+  for (std::uint32_t j = 0; j < nv; ++j) {
+    const VerifyJob& vj = jobs.verify[j];
+    const std::uint32_t r = static_cast<std::uint32_t>(vj.request);
+    fill_ctx(jobs, r, jobs.verify_ctx[j]);
+    I.ctx.insert(I.ctx.end(), jobs.cands.begin() + vj.cand_off, jobs.cands.begin() + vj.cand_off + vj.k);
+    const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
+    const std::int32_t first = n_ctx - static_cast<std::int32_t>(k_) - 1;  // = P + base - 1
+    if (n_ctx > MC) throw ConfigError("model path: verify context " + std::to_string(n_ctx) + " exceeds max_ctx");
+    LinearCache& c = I.tgt[r];
+    std::int32_t lcp = 0;
+    while (lcp < first && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
+    const std::int32_t base_slot = static_cast<std::int32_t>(r) * MC;
+    const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
+    const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
+    for (std::int32_t p = lcp; p < n_ctx; ++p) {
+      b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
+      b.pos.push_back(p);
+      b.slot.push_back(base_slot + p);
+      b.extra.push_back(base_slot + p);
+    }
+    b.groups.push_back(AttnGroup{row0, n_ctx - lcp, base_slot, lcp, eoff, n_ctx - lcp});
+    b.row_mask.resize(b.tok.size(), 0ull);
+    for (std::int32_t p = first; p < n_ctx; ++p) {
+      b.out_rows.push_back(row0 + p - lcp);
+      b.plant.push_back(p_->plant(I.ctx[p], false));
+      I.forced[j * (k_ + 1) + (p - first)] = forced_at(p, P, L_, eos_);
+    }
+    c.valid.assign(I.ctx.begin(), I.ctx.end());
+    std::memcpy(hc + j * k_, jobs.cands.data() + vj.cand_off, k_ * 4);
+  }
+  std::memcpy(hc + nv * k_, I.forced.data(), I.forced.size() * 4);
+  WS_CUDA(cudaMemcpyAsync(I.d_cands, hc, nv * k_ * 4, cudaMemcpyHostToDevice, st));
+  WS_CUDA(cudaMemcpyAsync(I.d_forced, hc + nv * k_, I.forced.size() * 4, cudaMemcpyHostToDevice, st));
+  WS_CUDA(cudaEventRecord(I.e0, st));
+  p_->target().forward(b, cfg.plant_target, st);
+  row_stats_bf16(p_->target().logits(), nv * (k_ + 1), V, V, 1.0f, I.d_pred, nullptr, I.d_ws, nv, k_, I.d_cands,
+                 I.d_vout, st, I.d_forced);
+  WS_CUDA(cudaEventRecord(I.e1, st));
+  WS_CUDA(cudaMemcpyAsync(I.h_vout, I.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaEventRecord(I.done[0], st));
+  target_rows += b.tok.size();
+  target_forwards += 1;
+  stats.launches += 1 + 8ull * p_->target().shape().layers + 4;
+  stats.h2d += nv * k_ * 4 + I.forced.size() * 4;
+  stats.d2h += nv * sizeof(ws_verify_out);
+  stats.verify_rows += nv;
+}
+
+// Lane 1: one draft forward over every pending draft job (worker leaves as shared-prefix tree
+// groups, controller local drafts / catch-up as causal groups), then K3/K4 row statistics.
+void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
+  ModelPair::Impl& I = *p_->impl;
+  const ModelPairCfg& cfg = p_->cfg();
+  const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
+  const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
+  const std::int32_t V = p_->draft().shape().vocab;
+  const std::uint32_t nd = static_cast<std::uint32_t>(jobs.draft.size());
+  I.nd = nd;
+  draft_ran_ = false;
+  if (!nd) return;
+  ++draft_batch_;
+  const std::size_t need = static_cast<std::size_t>(nd) + 16;
+  if (need > I.cap_d) {
+    for (void* q : {static_cast<void*>(I.d_pred_d), I.d_ws_d})
+      if (q) cudaFree(q);
+    if (I.h_pred_d) cudaFreeHost(I.h_pred_d);
+    I.cap_d = need * 2;
+    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(I.cap_d), V, 0);
     WS_CUDA(cudaMalloc(&I.d_ws_d, wsb_));
     WS_CUDA(cudaMemset(I.d_ws_d, 0, wsb_));
-    WS_CUDA(cudaMalloc(&I.d_pred_d, I.cap_rows * sizeof(ws_pred)));
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_res),
-                          I.cap_rows * (sizeof(ws_pred) + sizeof(ws_verify_out)) + 256, cudaHostAllocDefault));
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_stage),
-                          I.cap_rows * (sizeof(ws_pred) + k_ * 4 + 8) + 256, cudaHostAllocDefault));
+    WS_CUDA(cudaMalloc(&I.d_pred_d, I.cap_d * sizeof(ws_pred)));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_pred_d), I.cap_d * sizeof(ws_pred), cudaHostAllocDefault));
   }
-  auto fill_ctx = [&](const std::vector<TokenId>& prompt, const JobCtx& c) {
-    I.ctx.assign(prompt.begin(), prompt.end());
-    I.ctx.insert(I.ctx.end(), jobs.ctx_tokens.begin() + c.off, jobs.ctx_tokens.begin() + c.off + c.len);
+  ForwardBatch& b = I.db;
+  b.clear();
+  I.job_out.assign(nd, -1);
+  I.copy_src.clear();
+  I.copy_dst.clear();
+  // the open shared-prefix tree group of one request's worker leaves (masked attention group)
+  struct TreeGroup {
+    bool active = false;
+    std::uint32_t req = 0;
+    std::int32_t row0 = 0, n_rows = 0, prefix_slot = 0, prefix_len = 0;
+    std::vector<std::int32_t> slots;
+    int index_of(std::int32_t s) {
+      for (std::size_t i = 0; i < slots.size(); ++i)
+        if (slots[i] == s) return static_cast<int>(i);
+      slots.push_back(s);
+      return static_cast<int>(slots.size()) - 1;
+    }
+  } wg;
+  std::vector<std::int32_t> anc, row_slots;
+  auto flush_wg = [&] {
+    if (!wg.active) return;
+    const std::int32_t eo = static_cast<std::int32_t>(b.extra.size());
+    b.extra.insert(b.extra.end(), wg.slots.begin(), wg.slots.end());
+    b.groups.push_back(AttnGroup{wg.row0, wg.n_rows, wg.prefix_slot, wg.prefix_len, eo,
+                                 static_cast<std::int32_t>(wg.slots.size()), 1, 0});
+    wg.active = false;
   };
-  auto forced_for = [&](std::int32_t pos) -> std::int32_t {
-    // row at context position pos predicts committed index pos + 1 - P (oracle.hpp:88-102)
-    return (pos + 1 - P) >= static_cast<std::int32_t>(L_) - 1 ? static_cast<std::int32_t>(eos_) : -1;
-  };
-
-  res.verify.resize(nv);
-  res.draft.resize(nd);
-  // ------------------------------ target verify ------------------------------
-  if (nv) {
-    ForwardBatch& b = I.tb;
-    b.clear();
-    std::vector<std::int32_t> forced(nv * (k_ + 1));
-    std::uint32_t* hc = reinterpret_cast<std::uint32_t*>(I.h_stage);
-    for (std::uint32_t j = 0; j < nv; ++j) {
-      const VerifyJob& vj = jobs.verify[j];
-      const std::uint32_t r = static_cast<std::uint32_t>(vj.request);
-      fill_ctx(p_->prompt(r), jobs.verify_ctx[j]);
-      I.ctx.insert(I.ctx.end(), jobs.cands.begin() + vj.cand_off, jobs.cands.begin() + vj.cand_off + vj.k);
-      const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
-      const std::int32_t first = n_ctx - static_cast<std::int32_t>(k_) - 1;  // = P + base - 1
-      if (n_ctx > MC)
-        throw ConfigError("model path: verify context " + std::to_string(n_ctx) + " exceeds max_ctx");
-      LinearCache& c = I.tgt[r];
+  const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg.trie_slots);
+  for (std::uint32_t j = 0; j < nd; ++j) {
+    const DraftJob& dj = jobs.draft[j];
+    const JobCtx& jc = jobs.draft_ctx[j];
+    const std::uint32_t r = dj.seq;
+    fill_ctx(jobs, r, jc);
+    const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
+    if (forced_at(n_ctx - 1, P, L_, eos_) >= 0) {
+      // Past the generation cap the prediction is a confident EOS whatever the context
+      // (oracle.hpp:88-102): no forward, no KV (every descendant is forced too).
+      I.job_out[j] = -1;
+      continue;
+    }
+    if (n_ctx > MC)
+      throw ConfigError("model path: draft context " + std::to_string(n_ctx) + " exceeds max_ctx (kind " +
+                        std::to_string(jc.kind) + ", committed " + std::to_string(jc.n_committed) + ", len " +
+                        std::to_string(jc.len) + ")");
+    if (jc.kind == kJobCtrlDraft) flush_wg();
+    const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
+    const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
+    if (jc.kind == kJobCtrlDraft) {  // controller local draft + catch-up prefill (controller.hpp:194-208)
+      LinearCache& c = I.ctrl[r];
       std::int32_t lcp = 0;
-      while (lcp < first && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
-      const std::int32_t base_slot = static_cast<std::int32_t>(r) * MC;
-      const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
-      const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
+      while (lcp < n_ctx - 1 && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
+      const std::int32_t base_slot = static_cast<std::int32_t>(r) * S;
       for (std::int32_t p = lcp; p < n_ctx; ++p) {
         b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
         b.pos.push_back(p);
@@ -264,232 +382,187 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         b.extra.push_back(base_slot + p);
       }
       b.groups.push_back(AttnGroup{row0, n_ctx - lcp, base_slot, lcp, eoff, n_ctx - lcp});
-      b.row_mask.resize(b.tok.size(), 0ull);
-      for (std::int32_t p = first; p < n_ctx; ++p) {
-        b.out_rows.push_back(row0 + p - lcp);
-        b.plant.push_back(p_->plant(I.ctx[p], false));
-        forced[j * (k_ + 1) + (p - first)] = forced_for(p);
-      }
       c.valid.assign(I.ctx.begin(), I.ctx.end());
-      std::memcpy(hc + j * k_, jobs.cands.data() + vj.cand_off, k_ * 4);
-    }
-    std::memcpy(hc + nv * k_, forced.data(), forced.size() * 4);
-    WS_CUDA(cudaMemcpyAsync(I.d_cands, hc, nv * k_ * 4, cudaMemcpyHostToDevice, st));
-    WS_CUDA(cudaMemcpyAsync(I.d_forced, hc + nv * k_, forced.size() * 4, cudaMemcpyHostToDevice, st));
-    WS_CUDA(cudaEventRecord(I.e0, st));
-    p_->target().forward(b, cfg.plant_target, st);
-    row_stats_bf16(p_->target().logits(), nv * (k_ + 1), V, V, 1.0f, I.d_pred, nullptr, I.d_ws, nv, k_, I.d_cands,
-                   I.d_vout, st, I.d_forced);
-    WS_CUDA(cudaEventRecord(I.e1, st));
-    // results land in pinned memory; the draft forward is planned and launched on its own
-    // stream while the target forward runs
-    WS_CUDA(cudaMemcpyAsync(I.h_res, I.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
-    target_rows += b.tok.size();
-    target_forwards += 1;
-    stats.launches += 1 + 8ull * p_->target().shape().layers + 4;
-    stats.h2d += nv * k_ * 4 + forced.size() * 4;
-    stats.d2h += nv * sizeof(ws_verify_out);
-  }
-  // ------------------------------ drafts (worker + controller) ------------------------------
-  if (nd) {
-    ForwardBatch& b = I.db;
-    b.clear();
-    std::vector<std::int32_t> job_out(nd, -1), copy_src, copy_dst;
-    // the open shared-prefix tree group of one request's worker leaves (masked attention group)
-    struct TreeGroup {
-      bool active = false;
-      std::uint32_t req = 0;
-      std::int32_t row0 = 0, n_rows = 0, prefix_slot = 0, prefix_len = 0;
-      std::vector<std::int32_t> slots;
-      int index_of(std::int32_t s) {
-        for (std::size_t i = 0; i < slots.size(); ++i)
-          if (slots[i] == s) return static_cast<int>(i);
-        slots.push_back(s);
-        return static_cast<int>(slots.size()) - 1;
+    } else {  // worker leaf: committed prefix + trie
+      TreeCache& t = I.wrk[r];
+      const std::int32_t pre_base = static_cast<std::int32_t>(r) * S + MC;
+      if (!t.init) t.reset(static_cast<std::int32_t>(r) * S + 2 * MC, static_cast<std::int32_t>(cfg.trie_slots));
+      const std::int32_t n_comm = P + static_cast<std::int32_t>(jc.n_committed);
+      // prefix must agree with the context (committed is append-only; defensive check)
+      std::int32_t pl = static_cast<std::int32_t>(t.prefix.size());
+      std::int32_t agree = 0;
+      while (agree < pl && agree < n_comm && t.prefix[agree] == I.ctx[agree]) ++agree;
+      if (agree < pl) {
+        t.prefix.resize(agree);
+        t.drop_all();
+        pl = agree;
       }
-    } wg;
-    std::vector<std::int32_t> anc, row_slots;
-    auto flush_wg = [&] {
-      if (!wg.active) return;
-      const std::int32_t eo = static_cast<std::int32_t>(b.extra.size());
-      b.extra.insert(b.extra.end(), wg.slots.begin(), wg.slots.end());
-      b.groups.push_back(AttnGroup{wg.row0, wg.n_rows, wg.prefix_slot, wg.prefix_len, eo,
-                                   static_cast<std::int32_t>(wg.slots.size()), 1, 0});
-      wg.active = false;
-    };
-    const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg.trie_slots);
-    for (std::uint32_t j = 0; j < nd; ++j) {
-      const DraftJob& dj = jobs.draft[j];
-      const JobCtx& jc = jobs.draft_ctx[j];
-      const std::uint32_t r = dj.seq;
-      fill_ctx(p_->prompt(r), jc);
-      const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
-      if (forced_for(n_ctx - 1) >= 0) {
-        // Past the generation cap the prediction is a confident EOS whatever the context
-        // (oracle.hpp:88-102): no forward, no KV (every descendant is forced too).
-        job_out[j] = -1;
-        continue;
+      // migrate speculative nodes that became committed into the prefix
+      std::int32_t cur = -1;
+      while (pl < n_comm) {
+        const std::int32_t c = t.find(cur, I.ctx[pl]);
+        if (c < 0) break;
+        I.copy_src.push_back(t.nodes[c].slot);
+        I.copy_dst.push_back(pre_base + pl);
+        t.prefix.push_back(I.ctx[pl]);
+        ++pl;
+        cur = c;
       }
-      if (n_ctx > MC)
-        throw ConfigError("model path: draft context " + std::to_string(n_ctx) + " exceeds max_ctx (kind " +
-                          std::to_string(jc.kind) + ", committed " + std::to_string(jc.n_committed) + ", len " +
-                          std::to_string(jc.len) + ")");
-      if (jc.kind == kJobCtrlDraft) flush_wg();
-      const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
-      const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
-      if (jc.kind == kJobCtrlDraft) {  // controller local draft + catch-up prefill (controller.hpp:194-208)
-        LinearCache& c = I.ctrl[r];
-        std::int32_t lcp = 0;
-        while (lcp < n_ctx - 1 && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
-        const std::int32_t base_slot = static_cast<std::int32_t>(r) * S;
-        for (std::int32_t p = lcp; p < n_ctx; ++p) {
-          b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
-          b.pos.push_back(p);
-          b.slot.push_back(base_slot + p);
-          b.extra.push_back(base_slot + p);
-        }
-        b.groups.push_back(AttnGroup{row0, n_ctx - lcp, base_slot, lcp, eoff, n_ctx - lcp});
-        c.valid.assign(I.ctx.begin(), I.ctx.end());
-      } else {  // worker leaf: committed prefix + trie
-        TreeCache& t = I.wrk[r];
-        const std::int32_t pre_base = static_cast<std::int32_t>(r) * S + MC;
-        if (!t.init) t.reset(static_cast<std::int32_t>(r) * S + 2 * MC, static_cast<std::int32_t>(cfg.trie_slots));
-        const std::int32_t n_comm = P + static_cast<std::int32_t>(jc.n_committed);
-        // prefix must agree with the context (committed is append-only; defensive check)
-        std::int32_t pl = static_cast<std::int32_t>(t.prefix.size());
-        std::int32_t agree = 0;
-        while (agree < pl && agree < n_comm && t.prefix[agree] == I.ctx[agree]) ++agree;
-        if (agree < pl) {
-          t.prefix.resize(agree);
-          t.drop_all();
-          pl = agree;
-        }
-        // migrate speculative nodes that became committed into the prefix
-        std::int32_t cur = -1;
-        while (pl < n_comm) {
-          const std::int32_t c = t.find(cur, I.ctx[pl]);
+      if (cur >= 0) t.reroot_at(cur);  // copies are queued before this batch's forward
+      if (pl < n_comm) t.drop_all();   // committed diverged from every cached branch
+      // node-slot pressure: stale branches are dropped (never within a batch that already
+      // allocated for this request — those slots are written by this batch's forward)
+      if (static_cast<std::int32_t>(t.free_slots.size()) < n_ctx - n_comm + 2) {
+        if (t.last_alloc_round == draft_batch_) throw std::logic_error("model path: worker trie slots exhausted");
+        t.drop_all();
+      }
+      // Rows: committed tokens missing from the prefix, else the unmatched tail of the
+      // speculative path; the last token is always fed (its logits are the output).
+      //   prefix_len_g = pl           (committed rows follow)
+      //                = n_ctx - 1    (root job, everything cached: re-feed the last token)
+      //                = n_comm       (leaf job: matched trie ancestors, then the leaf)
+      const std::int32_t prefix_len_g = pl < n_comm ? pl : (n_ctx == n_comm ? n_ctx - 1 : n_comm);
+      std::int32_t q = prefix_len_g;
+      std::int32_t node = -1;
+      anc.clear();
+      const bool leaf_job = q == n_comm && n_ctx > n_comm;
+      if (leaf_job) {
+        while (q < n_ctx - 1) {
+          const std::int32_t c = t.find(node, I.ctx[q]);
           if (c < 0) break;
-          copy_src.push_back(t.nodes[c].slot);
-          copy_dst.push_back(pre_base + pl);
-          t.prefix.push_back(I.ctx[pl]);
-          ++pl;
-          cur = c;
-        }
-        if (cur >= 0) t.reroot_at(cur);  // copies are queued before this round's forward
-        if (pl < n_comm) t.drop_all();   // committed diverged from every cached branch
-        // node-slot pressure: stale branches are dropped (never within a round that already
-        // allocated for this request — those slots are written by this round's forward)
-        if (static_cast<std::int32_t>(t.free_slots.size()) < n_ctx - n_comm + 2) {
-          if (t.last_alloc_round == stats.rounds) throw std::logic_error("model path: worker trie slots exhausted");
-          t.drop_all();
-        }
-        // Rows: committed tokens missing from the prefix, else the unmatched tail of the
-        // speculative path; the last token is always fed (its logits are the output).
-        //   prefix_len_g = pl           (committed rows follow)
-        //                = n_ctx - 1    (root job, everything cached: re-feed the last token)
-        //                = n_comm       (leaf job: matched trie ancestors, then the leaf)
-        const std::int32_t prefix_len_g = pl < n_comm ? pl : (n_ctx == n_comm ? n_ctx - 1 : n_comm);
-        std::int32_t q = prefix_len_g;
-        std::int32_t node = -1;
-        anc.clear();
-        const bool leaf_job = q == n_comm && n_ctx > n_comm;
-        if (leaf_job) {
-          while (q < n_ctx - 1) {
-            const std::int32_t c = t.find(node, I.ctx[q]);
-            if (c < 0) break;
-            anc.push_back(t.nodes[c].slot);
-            node = c;
-            ++q;
-          }
-        }
-        const std::int32_t rows = n_ctx - q;
-        row_slots.clear();
-        for (std::int32_t p = q; p < n_ctx; ++p) {
-          std::int32_t slot;
-          if (p < n_comm) {
-            slot = pre_base + p;
-          } else {
-            std::int32_t c = t.find(node, I.ctx[p]);
-            if (c < 0) {
-              c = t.add(node, I.ctx[p]);
-              t.last_alloc_round = stats.rounds;
-            }
-            slot = t.nodes[c].slot;
-            node = c;
-          }
-          b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
-          b.pos.push_back(p);
-          b.slot.push_back(slot);
-          row_slots.push_back(slot);
-        }
-        for (std::int32_t p = pl; p < std::min(n_comm, n_ctx); ++p) t.prefix.push_back(I.ctx[p]);
-        if (!leaf_job || anc.size() + row_slots.size() > 64) {
-          // root / catch-up job: its own causal group
-          flush_wg();
-          const std::int32_t eo = static_cast<std::int32_t>(b.extra.size());
-          b.extra.insert(b.extra.end(), anc.begin(), anc.end());
-          b.extra.insert(b.extra.end(), row_slots.begin(), row_slots.end());
-          b.row_mask.resize(b.tok.size(), 0ull);
-          b.groups.push_back(AttnGroup{row0, rows, pre_base, prefix_len_g, eo,
-                                       static_cast<std::int32_t>(b.extra.size()) - eo});
-        } else {
-          // leaf job: joins the request's shared-prefix tree group (one pass over the prefix
-          // for all of the request's leaves); each row sees its ancestor chain + itself
-          if (wg.active && (wg.req != r || wg.slots.size() + anc.size() + row_slots.size() > 64)) flush_wg();
-          if (!wg.active) {
-            wg.active = true;
-            wg.req = r;
-            wg.row0 = row0;
-            wg.n_rows = 0;
-            wg.prefix_slot = pre_base;
-            wg.prefix_len = n_comm;
-            wg.slots.clear();
-          }
-          unsigned long long mask = 0ull;
-          for (std::int32_t s : anc) mask |= 1ull << wg.index_of(s);
-          for (std::int32_t s : row_slots) {
-            mask |= 1ull << wg.index_of(s);
-            b.row_mask.push_back(mask);
-          }
-          wg.n_rows += rows;
+          anc.push_back(t.nodes[c].slot);
+          node = c;
+          ++q;
         }
       }
-      if (jc.kind == kJobCtrlDraft) b.row_mask.resize(b.tok.size(), 0ull);
-      const std::int32_t last = static_cast<std::int32_t>(b.tok.size()) - 1;
-      rows_by_kind[jc.kind] += static_cast<std::uint64_t>(last + 1 - row0);
-      jobs_by_kind[jc.kind] += 1;
-      job_out[j] = static_cast<std::int32_t>(b.out_rows.size());
-      b.out_rows.push_back(last);
-      b.plant.push_back(p_->plant(I.ctx[n_ctx - 1], true));
+      const std::int32_t rows = n_ctx - q;
+      row_slots.clear();
+      for (std::int32_t p = q; p < n_ctx; ++p) {
+        std::int32_t slot;
+        if (p < n_comm) {
+          slot = pre_base + p;
+        } else {
+          std::int32_t c = t.find(node, I.ctx[p]);
+          if (c < 0) {
+            c = t.add(node, I.ctx[p]);
+            t.last_alloc_round = draft_batch_;
+          }
+          slot = t.nodes[c].slot;
+          node = c;
+        }
+        b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
+        b.pos.push_back(p);
+        b.slot.push_back(slot);
+        row_slots.push_back(slot);
+      }
+      for (std::int32_t p = pl; p < std::min(n_comm, n_ctx); ++p) t.prefix.push_back(I.ctx[p]);
+      if (!leaf_job || anc.size() + row_slots.size() > 64) {
+        // root / catch-up job: its own causal group
+        flush_wg();
+        const std::int32_t eo = static_cast<std::int32_t>(b.extra.size());
+        b.extra.insert(b.extra.end(), anc.begin(), anc.end());
+        b.extra.insert(b.extra.end(), row_slots.begin(), row_slots.end());
+        b.row_mask.resize(b.tok.size(), 0ull);
+        b.groups.push_back(AttnGroup{row0, rows, pre_base, prefix_len_g, eo,
+                                     static_cast<std::int32_t>(b.extra.size()) - eo});
+      } else {
+        // leaf job: joins the request's shared-prefix tree group (one pass over the prefix
+        // for all of the request's leaves); each row sees its ancestor chain + itself
+        if (wg.active && (wg.req != r || wg.slots.size() + anc.size() + row_slots.size() > 64)) flush_wg();
+        if (!wg.active) {
+          wg.active = true;
+          wg.req = r;
+          wg.row0 = row0;
+          wg.n_rows = 0;
+          wg.prefix_slot = pre_base;
+          wg.prefix_len = n_comm;
+          wg.slots.clear();
+        }
+        unsigned long long mask = 0ull;
+        for (std::int32_t s : anc) mask |= 1ull << wg.index_of(s);
+        for (std::int32_t s : row_slots) {
+          mask |= 1ull << wg.index_of(s);
+          b.row_mask.push_back(mask);
+        }
+        wg.n_rows += rows;
+      }
     }
-    flush_wg();
-    if (b.row_mask.size() != b.tok.size()) throw std::logic_error("model path: row mask bookkeeping");
-    const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
-    const ws_pred* outp = reinterpret_cast<const ws_pred*>(I.h_res + I.cap_rows * sizeof(ws_verify_out));
-    // WS_SERIAL=1 serialises the two forwards (clean per-kernel profiles); default overlaps them
-    static const bool serial = std::getenv("WS_SERIAL") != nullptr;
-    cudaStream_t sd = serial ? st : p_->stream_draft();
-    if (n_out) {
-      p_->draft().copy_slots(copy_src, copy_dst, sd);
-      WS_CUDA(cudaEventRecord(I.e2, sd));
-      p_->draft().forward(b, cfg.plant_draft, sd);
-      row_stats_bf16(p_->draft().logits(), n_out, V, V, 1.0f, I.d_pred_d, nullptr, I.d_ws_d, 0, 0, nullptr, nullptr,
-                     sd, nullptr);
-      WS_CUDA(cudaEventRecord(I.e3, sd));
-      WS_CUDA(cudaMemcpyAsync(const_cast<ws_pred*>(outp), I.d_pred_d, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost,
-                              sd));
-      WS_CUDA(cudaStreamSynchronize(sd));
-      float ms = 0.f;
-      WS_CUDA(cudaEventElapsedTime(&ms, I.e2, I.e3));
-      draft_ms += ms;
-      draft_rows_fed += b.tok.size();
-      draft_forwards += 1;
-      stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (copy_src.empty() ? 0 : 1);
-      stats.d2h += n_out * sizeof(ws_pred);
+    if (jc.kind == kJobCtrlDraft) b.row_mask.resize(b.tok.size(), 0ull);
+    const std::int32_t last = static_cast<std::int32_t>(b.tok.size()) - 1;
+    rows_by_kind[jc.kind] += static_cast<std::uint64_t>(last + 1 - row0);
+    jobs_by_kind[jc.kind] += 1;
+    I.job_out[j] = static_cast<std::int32_t>(b.out_rows.size());
+    b.out_rows.push_back(last);
+    b.plant.push_back(p_->plant(I.ctx[n_ctx - 1], true));
+  }
+  flush_wg();
+  if (b.row_mask.size() != b.tok.size()) throw std::logic_error("model path: row mask bookkeeping");
+  const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
+  cudaStream_t sd = draft_stream();
+  if (n_out) {
+    p_->draft().copy_slots(I.copy_src, I.copy_dst, sd);
+    WS_CUDA(cudaEventRecord(I.e2, sd));
+    p_->draft().forward(b, cfg.plant_draft, sd);
+    row_stats_bf16(p_->draft().logits(), n_out, V, V, 1.0f, I.d_pred_d, nullptr, I.d_ws_d, 0, 0, nullptr, nullptr,
+                   sd, nullptr);
+    WS_CUDA(cudaEventRecord(I.e3, sd));
+    WS_CUDA(cudaMemcpyAsync(I.h_pred_d, I.d_pred_d, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, sd));
+    draft_ran_ = true;
+    draft_rows_fed += b.tok.size();
+    draft_forwards += 1;
+    stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (I.copy_src.empty() ? 0 : 1);
+    stats.d2h += n_out * sizeof(ws_pred);
+  }
+  WS_CUDA(cudaEventRecord(I.done[1], sd));
+  stats.draft_rows += nd;
+}
+
+cudaStream_t ModelBackend_Llama::draft_stream() const {
+  // WS_SERIAL=1 serialises the two forwards (clean per-kernel profiles); default overlaps them
+  static const bool serial = std::getenv("WS_SERIAL") != nullptr;
+  return serial ? p_->stream() : p_->stream_draft();
+}
+
+void ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t) {
+  if (verify_mode != WS_VERIFY_GREEDY)
+    throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
+  stats.rounds += 1;
+  if (lane == 0)
+    submit_verify(jobs);
+  else
+    submit_draft(jobs);
+}
+
+int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
+  ModelPair::Impl& I = *p_->impl;
+  for (;;) {
+    for (int lane = 0; lane < 2; ++lane) {
+      if (!(lane == 0 ? busy0 : busy1)) continue;
+      const cudaError_t e = cudaEventQuery(I.done[lane]);
+      if (e == cudaSuccess) return lane;
+      if (e != cudaErrorNotReady) WS_CUDA(e);
     }
-    for (std::uint32_t j = 0; j < nd; ++j) {
-      if (job_out[j] >= 0) {
-        res.draft[j] = outp[job_out[j]];
+    std::this_thread::yield();
+  }
+}
+
+void ModelBackend_Llama::complete(int lane, RoundResults& res) {
+  ModelPair::Impl& I = *p_->impl;
+  float ms = 0.f;
+  if (lane == 0) {
+    res.verify.resize(I.nv);
+    if (!I.nv) return;
+    WS_CUDA(cudaEventSynchronize(I.done[0]));
+    std::memcpy(res.verify.data(), I.h_vout, I.nv * sizeof(ws_verify_out));
+    WS_CUDA(cudaEventElapsedTime(&ms, I.e0, I.e1));
+    target_ms += ms;
+  } else {
+    res.draft.resize(I.nd);
+    if (!I.nd) return;
+    WS_CUDA(cudaEventSynchronize(I.done[1]));
+    for (std::uint32_t j = 0; j < I.nd; ++j) {
+      if (I.job_out[j] >= 0) {
+        res.draft[j] = I.h_pred_d[I.job_out[j]];
       } else {
         ws_pred e{};
         e.n = 1;
@@ -498,18 +571,20 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
         res.draft[j] = e;
       }
     }
+    if (draft_ran_) {
+      WS_CUDA(cudaEventElapsedTime(&ms, I.e2, I.e3));
+      draft_ms += ms;
+    }
   }
-  if (nv) {
-    WS_CUDA(cudaStreamSynchronize(st));
-    std::memcpy(res.verify.data(), I.h_res, nv * sizeof(ws_verify_out));
-    float ms = 0.f;
-    WS_CUDA(cudaEventElapsedTime(&ms, I.e0, I.e1));
-    target_ms += ms;
-  }
-  stats.rounds += 1;
-  stats.verify_rows += nv;
-  stats.draft_rows += nd;
   stats.kernel_ms = target_ms + draft_ms;
+}
+
+// Lockstep round (WS_LOCKSTEP=1): both lanes, then both results.
+void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t seed) {
+  submit(0, jobs, verify_mode, seed);
+  submit(1, jobs, verify_mode, seed);
+  complete(0, res);
+  complete(1, res);
 }
 
 }  // namespace wsb

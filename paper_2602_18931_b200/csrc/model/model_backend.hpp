@@ -44,15 +44,26 @@ class ModelBackend_Llama : public ModelBackend {
   ~ModelBackend_Llama() override;
   void run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t sample_seed) override;
   bool wants_context() const override { return true; }
+  // lane 0 = target stream (verify), lane 1 = draft stream (worker + controller drafts)
+  bool has_lanes() const override { return true; }
+  void submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed) override;
+  int wait_any(bool busy0, bool busy1) override;
+  void complete(int lane, RoundResults& res) override;
   double target_ms = 0, draft_ms = 0;
   std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
   std::uint64_t rows_by_kind[3] = {0, 0, 0}, jobs_by_kind[3] = {0, 0, 0};  // JobKind
 
  private:
+  void fill_ctx(const RoundJobs& jobs, std::uint32_t r, const JobCtx& c);
+  void submit_verify(const RoundJobs& jobs);
+  void submit_draft(const RoundJobs& jobs);
+  cudaStream_t draft_stream() const;
   ModelPair* p_;
   std::uint32_t L_;
   TokenId eos_;
   std::uint32_t k_;
+  std::uint64_t draft_batch_ = 0;
+  bool draft_ran_ = false;
 };
 
 // Owns both models, their KV caches and the per-request cache state on one device.

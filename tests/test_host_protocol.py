@@ -37,6 +37,18 @@ def test_golden_cases(golden):
             assert got[key] == case[key], (case["name"], key)
 
 
+def test_golden_cases_lanes_driver(golden, monkeypatch):
+    """The continuous-batching driver (two asynchronous lanes, completions returned in a
+    scrambled order) reproduces every golden case: per-request results cannot depend on how
+    jobs are grouped into batches or on which lane finishes first."""
+    monkeypatch.setenv("WS_EMULATE_LANES", "1")
+    for case in golden["cases"]:
+        c = abi.sim_cfg_from_dict(case["config"])
+        got = fingerprint(run_host(c))
+        for key in ("metrics", "ctrl_fnv", "wrk_fnv", "ctrl_len", "steps_fnv", "n_steps"):
+            assert got[key] == case[key], (case["name"], key)
+
+
 def test_config1_per_step_log(golden):
     case = next(c for c in golden["cases"] if c["name"] == "config1")
     b = run_host(abi.sim_cfg_from_dict(case["config"]))
