@@ -104,6 +104,9 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
                    (unsigned long long)backend.jobs_by_kind[1], (unsigned long long)backend.rows_by_kind[2],
                    (unsigned long long)backend.jobs_by_kind[2], (unsigned long long)backend.draft_forwards,
                    backend.draft_ms);
+    if (std::getenv("WS_DEBUG_ROWS"))
+      std::fprintf(stderr, "[ws] repeated draft contexts: ctrl %llu, worker %llu\n",
+                   (unsigned long long)backend.repeat_by_kind[1], (unsigned long long)backend.repeat_by_kind[2]);
   });
 }
 

@@ -11,7 +11,7 @@
 // Each CTA walks work units u = blockIdx.x, +gridDim.x, ...; the accumulator is double-buffered
 // in TMEM (2 x BN columns) so the epilogue of unit i overlaps the main loop of unit i+1.
 // Epilogues: bf16 store (LM head), fp32 residual accumulate (O / down projections add into the
-// fp32 residual stream), SwiGLU (gate/up rows interleaved in 32-row blocks), and QKV with RoPE
+// fp32 residual stream), SwiGLU (gate/up rows interleaved in 16-row blocks), and QKV with RoPE
 // + KV-pool scatter. Units are ordered M-fastest so all M-blocks of one weight tile run
 // concurrently and each weight byte crosses HBM once per GEMM.
 //
@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -43,46 +44,68 @@ constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kThreads = 192;
 constexpr int kNumSMs = 148;
 
-template <int BN>
-struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256;
-};
+// Runtime tile width BN (multiple of 16, 64..256): the ring depth is whatever fits in
+// shared memory, the two TMEM accumulators sit at columns 0 and 256 of a 512-column
+// allocation (one CTA per SM).
+constexpr int kSmemBudget = 232448;  // 227 KB opt-in
+constexpr int kTmemCols = 512;
+constexpr int kAccStride = 256;
+__host__ __device__ constexpr int a_bytes() { return BM * BK * 2; }
+__host__ __device__ constexpr int b_bytes(int bn) { return bn * BK * 2; }
+__host__ __device__ constexpr int stage_bytes(int bn) { return a_bytes() + b_bytes(bn); }
+inline int ring_stages(int bn) { return std::min(8, (kSmemBudget - 2048) / stage_bytes(bn)); }
+inline int smem_bytes(int bn) { return 1024 + ring_stages(bn) * stage_bytes(bn) + 256; }
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+__device__ __forceinline__ std::uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const std::uint32_t*>(&h);
+}
+// 32 bf16 (16 packed pairs) → dst[0, 32) with four 16-byte stores; every index is a constant
+// after unrolling, so nothing here touches local memory.
+__device__ __forceinline__ void store32_bf16(void* dst, const std::uint32_t (&pk)[16]) {
+  uint4* o = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+}
+__device__ __forceinline__ void store_bf16_tail(__nv_bfloat16* dst, const std::uint32_t (&pk)[16], int n) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < n) {
+      const std::uint32_t w = pk[j >> 1];
+      dst[j] = __ushort_as_bfloat16(static_cast<unsigned short>((j & 1) ? (w >> 16) : (w & 0xFFFFu)));
+    }
+}
+
 // Epilogue of one 128 x BN tile for this thread's row. fetch(col, r) yields the 32 fp32 values
 // of tile columns [col, col+32) (from TMEM, or the summed split-K partials) and must be called
 // by every lane (TMEM loads are warp-collective).
-template <int BN, int EPI, class Fetch>
-__device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int row, int M, int N, int n_blk, void* out, int ldo,
-                                              const RopeEpi& rp) {
+template <int EPI, class Fetch>
+__device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, int M, int N, int n_blk, void* out,
+                                              int ldo, const RopeEpi& rp) {
   const bool live = row < M;
   if constexpr (EPI == kEpiSwiGLU) {
-    // W rows interleaved in 32-row blocks [gate 0..31 | up 0..31 | gate 32..63 | ...]: column
-    // chunk 2j is gate and 2j+1 is up for output features f0 + 32j .. +31.
+    // W rows interleaved in 16-row blocks [gate 0..15 | up 0..15 | gate 16..31 | ...]: the
+    // 32-column chunk c holds gate and up of output features f0 + c/2 .. +15.
     const int f0 = n_blk * (BN / 2);
 #pragma unroll 1
-    for (int c = 0; c < BN / 2; c += 32) {
-      std::uint32_t g[32], u[32];
-      fetch(2 * c, g);
-      fetch(2 * c + 32, u);
-      if (live && f0 + c < N / 2) {
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + f0 + c;
-        alignas(16) __nv_bfloat162 v[16];
+    for (int c = 0; c < BN; c += 32) {
+      std::uint32_t r[32];
+      fetch(c, r);
+      if (live && f0 + c / 2 < N / 2) {
+        std::uint32_t pk[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float a0 = silu(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
-          const float a1 = silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
-          v[j] = __floats2bfloat162_rn(a0, a1);
+        for (int j = 0; j < 8; ++j) {
+          const float a0 = silu(__uint_as_float(r[2 * j])) * __uint_as_float(r[16 + 2 * j]);
+          const float a1 = silu(__uint_as_float(r[2 * j + 1])) * __uint_as_float(r[16 + 2 * j + 1]);
+          pk[j] = pack_bf16(a0, a1);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
+        uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo +
+                                            f0 + c / 2);
+        o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
     }
   } else if constexpr (EPI == kEpiQKVRope) {
@@ -111,54 +134,48 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int row, int M, int
         fetch(h0 + c, a);
         fetch(h0 + c + half, b);
         if (!live) continue;
-        alignas(16) __nv_bfloat162 lo[16], hi[16];
-        const float2* cs = rp.cs + static_cast<std::size_t>(pos) * half + c;
+        std::uint32_t lo[16], hi[16];
+        const float4* cs = reinterpret_cast<const float4*>(rp.cs + static_cast<std::size_t>(pos) * half + c);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           float x0 = __uint_as_float(a[2 * j]), x1 = __uint_as_float(a[2 * j + 1]);
           float y0 = __uint_as_float(b[2 * j]), y1 = __uint_as_float(b[2 * j + 1]);
           if (rot) {
-            const float2 c0 = cs[2 * j], c1 = cs[2 * j + 1];
-            const float rx0 = x0 * c0.x - y0 * c0.y, ry0 = y0 * c0.x + x0 * c0.y;
-            const float rx1 = x1 * c1.x - y1 * c1.y, ry1 = y1 * c1.x + x1 * c1.y;
+            const float4 cc = cs[j];  // (cos, sin) of pairs 2j and 2j + 1
+            const float rx0 = x0 * cc.x - y0 * cc.y, ry0 = y0 * cc.x + x0 * cc.y;
+            const float rx1 = x1 * cc.z - y1 * cc.w, ry1 = y1 * cc.z + x1 * cc.w;
             x0 = rx0;
             y0 = ry0;
             x1 = rx1;
             y1 = ry1;
           }
-          lo[j] = __floats2bfloat162_rn(x0, x1);
-          hi[j] = __floats2bfloat162_rn(y0, y1);
+          lo[j] = pack_bf16(x0, x1);
+          hi[j] = pack_bf16(y0, y1);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          reinterpret_cast<uint4*>(dst + c)[q] = reinterpret_cast<const uint4*>(lo)[q];
-          reinterpret_cast<uint4*>(dst + c + half)[q] = reinterpret_cast<const uint4*>(hi)[q];
-        }
+        store32_bf16(dst + c, lo);
+        store32_bf16(dst + c + half, hi);
       }
     }
   } else {
     const int n0 = n_blk * BN;
+    const int ncols = min(BN, N - n0);  // valid columns of this tile (BN % 32 == 16: last chunk is half)
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       std::uint32_t r[32];
       fetch(c, r);
-      if (!live || n0 + c >= N) continue;
+      if (!live || c >= ncols) continue;
       if constexpr (EPI == kEpiBF16) {
         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
-        alignas(16) __nv_bfloat162 v[16];
+        std::uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          v[j] = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-        if (n0 + c + 32 <= N) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(o)[q] = reinterpret_cast<const uint4*>(v)[q];
-        } else {
-          const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(v);
-          for (int j = 0; j < 32 && n0 + c + j < N; ++j) o[j] = vv[j];
-        }
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        if (c + 32 <= ncols)
+          store32_bf16(o, pk);
+        else
+          store_bf16_tail(o, pk, ncols - c);
       } else {  // kEpiAddF32: out[row, n] += acc
         float* o = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
-        if (n0 + c + 32 <= N) {
+        if (c + 32 <= ncols) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float4 x = reinterpret_cast<float4*>(o)[q];
@@ -171,7 +188,7 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int row, int M, int
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (n0 + c + j < N) o[j] += __uint_as_float(r[j]);
+            if (c + j < ncols) o[j] += __uint_as_float(r[j]);
         }
       }
     }
@@ -184,21 +201,21 @@ struct SplitArgs {
   unsigned int* tickets = nullptr;   // [m_blocks * n_tiles], zero-initialised, self-resetting
 };
 
-template <int BN, int EPI>
+template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo, const RopeEpi rope,
-                   const SplitArgs sk) {
-  using C = Cfg<BN>;
+                   const SplitArgs sk, int BN, int STAGES, int ablate) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~static_cast<std::uintptr_t>(1023));
+  const int A_BYTES = a_bytes(), B_BYTES = b_bytes(BN), STAGE_BYTES = stage_bytes(BN);
   unsigned char* sA = smem;
-  unsigned char* sB = smem + C::STAGES * C::A_BYTES;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  std::uint64_t* empty = full + C::STAGES;
-  std::uint64_t* tfull = empty + C::STAGES;  // [2]
-  std::uint64_t* tempty = tfull + 2;         // [2]
+  unsigned char* sB = smem + STAGES * A_BYTES;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + STAGES * STAGE_BYTES);
+  std::uint64_t* empty = full + STAGES;
+  std::uint64_t* tfull = empty + STAGES;  // [2]
+  std::uint64_t* tempty = tfull + 2;      // [2]
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
   std::uint32_t* last_flag = tmem_slot + 1;
 
@@ -217,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -235,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: continuous ring across units
-      int stage = 0;
+      int stage = 0, phase_count = 0;
       std::uint32_t phase = 0;
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
         int m_blk, n_blk, split;
@@ -243,10 +260,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
-          if (++stage == C::STAGES) {
+          if ((ablate & 2) && phase_count >= STAGES) {
+            mbar_arrive(&full[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          ++phase_count;
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+          if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -255,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      constexpr std::uint32_t idesc = idesc_bf16_f32(BM, BN);
+      const std::uint32_t idesc = idesc_bf16_f32(BM, static_cast<std::uint32_t>(BN));
       int stage = 0;
       std::uint32_t phase = 0;
       int local = 0;
@@ -266,17 +292,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int acc = local & 1;
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         tc_fence_after();
-        const std::uint32_t d = tmem_base + acc * BN;
+        const std::uint32_t d = tmem_base + acc * kAccStride;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const std::uint64_t da = smem_desc_sw128(sA + stage * C::A_BYTES);
-          const std::uint64_t db = smem_desc_sw128(sB + stage * C::B_BYTES);
+          const std::uint64_t da = smem_desc_sw128(sA + stage * A_BYTES);
+          const std::uint64_t db = smem_desc_sw128(sB + stage * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // advance 16 elements = 32 B = 2 descriptor units
-            mma_bf16(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+            if (!(ablate & 1)) mma_bf16(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
           mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
-          if (++stage == C::STAGES) {
+          if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -295,13 +321,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
       const int row = m_blk * BM + grp * 32 + static_cast<int>(lane);
-      const std::uint32_t t_row = tmem_base + acc * BN + (static_cast<std::uint32_t>(grp * 32) << 16);
+      const std::uint32_t t_row = tmem_base + acc * kAccStride + (static_cast<std::uint32_t>(grp * 32) << 16);
       auto tmem_fetch = [&](int col, std::uint32_t (&r)[32]) {
         tmem_ld32(t_row + col, r);
         tmem_ld_wait();
       };
       if (S == 1) {
-        epilogue_tile<BN, EPI>(tmem_fetch, row, M, N, n_blk, out, ldo, rope);
+        epilogue_tile<EPI>(tmem_fetch, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -322,7 +348,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                      make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                                  __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
           } else {
-            for (int j = 0; j < 32 && c + j < ncols; ++j) __stcg(my + c + j, __uint_as_float(r[j]));
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c + j < ncols) __stcg(my + c + j, __uint_as_float(r[j]));
           }
         }
       }
@@ -359,21 +387,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                   v[4 * q + 3] += x.w;
                 }
               } else {
-                for (int j = 0; j < 32 && col + j < ncols; ++j) v[j] += __ldcg(p + j);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (col + j < ncols) v[j] += __ldcg(p + j);
               }
             }
           }
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
         };
-        epilogue_tile<BN, EPI>(ws_fetch, row, M, N, n_blk, out, ldo, rope);
+        epilogue_tile<EPI>(ws_fetch, BN, row, M, N, n_blk, out, ldo, rope);
       }
       epi_bar();  // last_flag is reused by the next unit
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -404,43 +434,43 @@ CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, st
   return m;
 }
 
-template <int BN, int EPI>
-void launch(const GemmArgs& g, const SplitArgs& sk, cudaStream_t st) {
-  using C = Cfg<BN>;
+template <int EPI>
+void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
   });
+  static const int ablate = [] {  // WS_GEMM_ABLATE (measurement only): 1 no MMA, 2 no TMA after
+    const char* e = std::getenv("WS_GEMM_ABLATE");  // the first ring, 4 no stores
+    return e ? std::atoi(e) : 0;
+  }();
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
-  const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, BN);
+  const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, static_cast<std::uint32_t>(bn));
   const int m_blocks = (g.M + BM - 1) / BM;
-  const int n_tiles = (g.N + BN - 1) / BN;  // SwiGLU: N counts gate+up rows
+  const int n_tiles = (g.N + bn - 1) / bn;  // SwiGLU: N counts gate+up rows
   const int total = m_blocks * n_tiles * sk.splits;
   const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
-  gemm_tn_kernel<BN, EPI><<<grid, kThreads, C::SMEM, st>>>(ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo,
-                                                            g.rope, sk);
+  gemm_tn_kernel<EPI><<<grid, kThreads, smem_bytes(bn), st>>>(ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo,
+                                                               g.rope, sk, bn, ring_stages(bn), ablate);
   WS_CUDA(cudaGetLastError());
-}
-
-template <int EPI>
-void dispatch_bn(int bn, const GemmArgs& g, const SplitArgs& sk, cudaStream_t st) {
-  if (bn == 256) return launch<256, EPI>(g, sk, st);
-  if (bn == 128) return launch<128, EPI>(g, sk, st);
-  return launch<64, EPI>(g, sk, st);
 }
 
 }  // namespace
 
-int pick_bn(int M, int N) {
-  // Wave-quantisation model: time ~ ceil(tiles / 148) x (BN + per-tile overhead); wider tiles
-  // win ties (they halve A re-reads). Numerics do not depend on BN (tests: tile invariance).
+int pick_bn(int M, int N, int granule) {
+  // Measured on B200 (profiles/r01_gemm_feed.md): the main loop is bound by shared-memory
+  // bandwidth, ~128 B/cycle/SM shared by the TMA fill and the MMA operand reads, i.e. per
+  // k-block 2 x (BM + BN) x 128 B / 128 = 256 + 2 BN cycles against an MMA floor of 2 BN. A
+  // GEMM therefore costs ~ceil(tiles / 148) x (256 + 2 BN) per k-block: pick the BN (a
+  // multiple of 32 and of the epilogue's granule) minimising that, wider on ties. Numerics do
+  // not depend on BN (each output is the same K-ordered MMA chain).
+  const int step = std::max(32, granule);
   const int mb = (M + BM - 1) / BM;
-  int best = 64;
+  int best = step;
   long best_cost = -1;
-  for (int bn : {256, 128, 64}) {
-    if (N < bn && bn != 64) continue;
+  for (int bn = 256 / step * step; bn >= std::max(64, step); bn -= step) {
     const long tiles = static_cast<long>(mb) * ((N + bn - 1) / bn);
-    const long cost = ((tiles + kNumSMs - 1) / kNumSMs) * (bn + 48);
+    const long cost = ((tiles + kNumSMs - 1) / kNumSMs) * (256 + 2L * bn);
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
       best = bn;
@@ -448,6 +478,8 @@ int pick_bn(int M, int N) {
   }
   return best;
 }
+
+int pick_bn(int M, int N) { return pick_bn(M, N, 32); }
 
 int pick_splits(int N, int K) {
   // From (N, K) only — never from M — so results stay batch-invariant. Measured on B200
@@ -474,12 +506,17 @@ std::size_t gemm_workspace_bytes(int max_rows) {
 void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   if (g.K % BK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (g.lda % 8 || g.ldw % 8) throw std::invalid_argument("gemm: leading dims must be multiples of 8");
-  int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
+  // epilogue granularity: SwiGLU tiles hold whole 64-row gate/up blocks, QKV tiles whole heads
+  int granule = 16;
+  if (g.epi == kEpiSwiGLU) granule = 32;
   if (g.epi == kEpiQKVRope) {
     if (g.rope.hd != 64 && g.rope.hd != 128) throw std::invalid_argument("gemm: qkv epilogue needs hd 64/128");
-    if (bn < g.rope.hd) bn = g.rope.hd;  // a tile holds whole heads
     if (g.N != (g.rope.nq + 2 * g.rope.nkv) * g.rope.hd) throw std::invalid_argument("gemm: qkv width");
+    granule = g.rope.hd;
   }
+  const int bn = g.bn ? g.bn : pick_bn(g.M, g.N, granule);
+  if (bn < 16 || bn > 256 || bn % granule) throw std::invalid_argument("gemm: tile width must be a multiple of " +
+                                                                       std::to_string(granule) + " in [16, 256]");
   SplitArgs sk;
   sk.splits = g.splits > 0 ? g.splits : (g.ws ? pick_splits(g.N, g.K) : 1);
   if (sk.splits > 1) {
@@ -515,10 +552,10 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
     sk.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(g.ws) + kTicketBytes);
   }
   switch (g.epi) {
-    case kEpiBF16: return dispatch_bn<kEpiBF16>(bn, g, sk, st);
-    case kEpiAddF32: return dispatch_bn<kEpiAddF32>(bn, g, sk, st);
-    case kEpiSwiGLU: return dispatch_bn<kEpiSwiGLU>(bn, g, sk, st);
-    case kEpiQKVRope: return dispatch_bn<kEpiQKVRope>(bn, g, sk, st);
+    case kEpiBF16: return launch<kEpiBF16>(g, sk, bn, st);
+    case kEpiAddF32: return launch<kEpiAddF32>(g, sk, bn, st);
+    case kEpiSwiGLU: return launch<kEpiSwiGLU>(g, sk, bn, st);
+    case kEpiQKVRope: return launch<kEpiQKVRope>(g, sk, bn, st);
   }
   throw std::invalid_argument("gemm: unknown epilogue");
 }

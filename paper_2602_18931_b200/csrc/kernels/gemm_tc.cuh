@@ -9,7 +9,7 @@ namespace wsb {
 enum GemmEpi : int {
   kEpiBF16 = 0,     // out bf16 [M, ldo] = acc
   kEpiAddF32 = 1,   // out fp32 [M, ldo] += acc   (residual stream)
-  kEpiSwiGLU = 2,   // out bf16 [M, ldo] = silu(gate) * up; W rows interleaved in 32-row blocks
+  kEpiSwiGLU = 2,   // out bf16 [M, ldo] = silu(gate) * up; W rows interleaved in 16-row blocks
   kEpiQKVRope = 3,  // fused QKV epilogue: rotate-half RoPE on q/k, q → q_out, k/v → KV pool slots
 };
 
@@ -32,7 +32,7 @@ struct GemmArgs {
   int M, N, K;
   int lda, ldw, ldo;
   int epi = kEpiBF16;
-  int bn = 0;        // 0 = auto (64/128/256)
+  int bn = 0;        // 0 = auto (multiple of 32 in [64, 256]; see pick_bn)
   int max_ctas = 0;  // persistent grid cap (0 = one CTA per SM)
   RopeEpi rope{};    // kEpiQKVRope only
   // Split-K workspace (zero-initialised once; see gemm_workspace_bytes). With ws == nullptr the

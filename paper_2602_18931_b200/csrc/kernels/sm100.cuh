@@ -89,7 +89,6 @@ __device__ __forceinline__ void mma_commit(std::uint64_t* bar) {
                    static_cast<std::uint64_t>(smem_u32(bar)))
                : "memory");
 }
-
 // Instruction descriptor: bf16 x bf16 -> f32, both operands K-major, shape M x N.
 __host__ __device__ constexpr std::uint32_t idesc_bf16_f32(std::uint32_t M, std::uint32_t N) {
   return (1u << 4)            // D format f32

@@ -357,6 +357,12 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
     const std::uint32_t r = dj.seq;
     fill_ctx(jobs, r, jc);
     const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
+    static const bool debug_rows = std::getenv("WS_DEBUG_ROWS") != nullptr;
+    if (debug_rows) {
+      std::uint64_t h = 1469598103934665603ULL ^ r;
+      for (TokenId t : I.ctx) h = (h ^ static_cast<std::uint64_t>(t)) * 1099511628211ULL;
+      if (!seen_ctx_.insert(h).second) repeat_by_kind[jc.kind] += 1;
+    }
     if (forced_at(n_ctx - 1, P, L_, eos_) >= 0) {
       // Past the generation cap the prediction is a confident EOS whatever the context
       // (oracle.hpp:88-102): no forward, no KV (every descendant is forced too).

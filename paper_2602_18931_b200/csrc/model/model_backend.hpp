@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "../host/driver.hpp"
@@ -52,6 +53,8 @@ class ModelBackend_Llama : public ModelBackend {
   double target_ms = 0, draft_ms = 0;
   std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
   std::uint64_t rows_by_kind[3] = {0, 0, 0}, jobs_by_kind[3] = {0, 0, 0};  // JobKind
+  // WS_DEBUG_ROWS: draft jobs whose (request, context) was already drafted earlier in the run
+  std::uint64_t repeat_by_kind[3] = {0, 0, 0};
 
  private:
   void fill_ctx(const RoundJobs& jobs, std::uint32_t r, const JobCtx& c);
@@ -64,6 +67,7 @@ class ModelBackend_Llama : public ModelBackend {
   std::uint32_t k_;
   std::uint64_t draft_batch_ = 0;
   bool draft_ran_ = false;
+  std::unordered_set<std::uint64_t> seen_ctx_;
 };
 
 // Owns both models, their KV caches and the per-request cache state on one device.

@@ -47,8 +47,8 @@ def gemm(A, W, out=None, epi=EPI_BF16, bn=0, splits=1):
     return out
 
 
-def interleave_gate_up(w_gate, w_up, block=32):
-    """Rows [g0..g31, u0..u31, g32..g63, ...] — the SwiGLU epilogue's expected weight layout."""
+def interleave_gate_up(w_gate, w_up, block=16):
+    """Rows [g0..g15, u0..u15, g16..g31, ...] — the SwiGLU epilogue's expected weight layout."""
     import torch
     F, K = w_gate.shape
     g = w_gate.view(F // block, block, K)

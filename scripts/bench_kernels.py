@@ -58,6 +58,54 @@ def gemm():
         print(json.dumps(r))
 
 
+def gemm_model():
+    """The model path's projections at the measured mean batch rows (8B verify ~530 rows,
+    1B draft ~655 rows): every tile width (BN multiple of 16), against cuBLAS on the same
+    operands. One JSON line per shape: {bn: us}, the default pick and cuBLAS."""
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    shapes = [(530, 6144, 4096, "8B qkv"), (530, 4096, 4096, "8B o"), (530, 28672, 4096, "8B gate_up"),
+              (530, 4096, 14336, "8B down"), (655, 3072, 2048, "1B qkv"), (655, 2048, 2048, "1B o"),
+              (655, 16384, 2048, "1B gate_up"), (655, 2048, 8192, "1B down"), (300, 128256, 2048, "1B lm_head"),
+              (140, 128256, 4096, "8B lm_head")]
+    only = os.environ.get("SHAPES")
+    for (M, N, K, name) in shapes:
+        if only and name not in only.split(","):
+            continue
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        fl = 2.0 * M * N * K
+        per = {}
+        for bn in range(64, 257, 16):
+            per[bn] = round(timeit(lambda: ops.gemm(A, W, out=out, bn=bn), flush=flush) * 1e6, 1)
+        t_def = timeit(lambda: ops.gemm(A, W, out=out), flush=flush)
+        t_cub = timeit(lambda: torch.matmul(A, W.T), flush=flush)
+        best = min(per, key=per.get)
+        print(json.dumps({"shape": name, "M": M, "N": N, "K": K, "default_us": round(t_def * 1e6, 1),
+                          "cublas_us": round(t_cub * 1e6, 1), "best_bn": best, "best_us": per[best],
+                          "tflops_default": round(fl / t_def / 1e12), "per_bn": per}))
+        sys.stdout.flush()
+        del A, W, out
+
+
+def overhead():
+    """Fixed cost of one GEMM launch: K sweep at the 8B O-projection shape, with and without an
+    L2 flush (a different kernel) in front, 10 back-to-back launches per event pair."""
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    M, N = 530, 4096
+    for K in (64, 512, 4096):
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        t_f = timeit(lambda: ops.gemm(A, W, out=out, bn=160), flush=flush)
+
+        def ten():
+            for _ in range(10):
+                ops.gemm(A, W, out=out, bn=160)
+        t_10 = timeit(ten) / 10
+        print(json.dumps({"K": K, "us_after_flush": round(t_f * 1e6, 1), "us_back_to_back": round(t_10 * 1e6, 1)}))
+
+
 def rowstats():
     import ctypes as C
     import paper_2602_18931_b200 as ws
@@ -95,6 +143,26 @@ def one_gemm():
                       "tflops": 2.0 * M * N * K / t / 1e12}))
 
 
+def pair(shape="8B o"):
+    """One launch each of our GEMM and cuBLAS on one model shape (for an ncu side-by-side)."""
+    dims = {"8B o": (530, 4096, 4096), "8B gate_up": (530, 28672, 4096), "1B lm_head": (300, 128256, 2048),
+            "1B down": (655, 2048, 8192)}[shape]
+    M, N, K = dims
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    for _ in range(3):
+        ops.gemm(A, W, out=out)
+        torch.matmul(A, W.T)
+    torch.cuda.synchronize()
+    flush.fill_(0)
+    ops.gemm(A, W, out=out)
+    flush.fill_(0)
+    torch.matmul(A, W.T)
+    torch.cuda.synchronize()
+
+
 def ops_pick(M, N):
     bm = (M + 127) // 128
     if bm * ((N + 255) // 256) >= 296:
@@ -105,4 +173,7 @@ def ops_pick(M, N):
 
 
 if __name__ == "__main__":
-    {"gemm": gemm, "rowstats": rowstats, "one_gemm": one_gemm}[sys.argv[1]]()
+    if sys.argv[1] == "pair":
+        pair(" ".join(sys.argv[2:]) or "8B o")
+    else:
+        {"gemm": gemm, "gemm_model": gemm_model, "rowstats": rowstats, "one_gemm": one_gemm, "overhead": overhead}[sys.argv[1]]()

@@ -23,7 +23,7 @@ SHAPES = [(128, 256, 64), (37, 1000, 128), (200, 4096, 4096), (1280, 6144, 4096)
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("bn", [64, 80, 128, 144, 240, 256])
 def test_gemm_bf16(ops, shape, bn):
     M, N, K = shape
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
@@ -34,7 +34,7 @@ def test_gemm_bf16(ops, shape, bn):
     assert rel_err(out, ref) < 4e-3, (shape, bn)
 
 
-@pytest.mark.parametrize("bn", [64, 256])
+@pytest.mark.parametrize("bn", [64, 144, 176, 256])
 def test_gemm_add_f32(ops, bn):
     M, N, K = 300, 4096, 2048
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
@@ -45,7 +45,7 @@ def test_gemm_add_f32(ops, bn):
     assert rel_err(X, ref) < 1e-5
 
 
-@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("bn", [64, 96, 128, 192, 224, 256])
 def test_gemm_swiglu(ops, bn):
     M, F, K = 260, 1024, 1024
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
@@ -67,7 +67,7 @@ def test_gemm_batch_and_tile_invariance(ops):
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
     ref = ops.gemm(A, W, bn=256)
-    for bn in (64, 128):
+    for bn in (64, 96, 128, 144, 208, 0):
         assert torch.equal(ops.gemm(A, W, bn=bn), ref)
     for lo, hi in ((0, 1), (5, 37), (128, 300), (690, 700)):
         assert torch.equal(ops.gemm(A[lo:hi].contiguous(), W, bn=64), ref[lo:hi])

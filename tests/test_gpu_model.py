@@ -62,7 +62,7 @@ class Ref:
         self.layers = []
         for l in range(s["layers"]):
             qkv = (nq + 2 * nkv) * hd
-            wgu = get("wgu", l, 2 * ffn * d, (2 * ffn, d)).view(ffn // 32, 2, 32, d)
+            wgu = get("wgu", l, 2 * ffn * d, (2 * ffn, d)).view(ffn // 16, 2, 16, d)
             self.layers.append(dict(
                 an=get("attn_norm", l, d, (d,)), wqkv=get("wqkv", l, qkv * d, (qkv, d)),
                 wo=get("wo", l, d * nq * hd, (d, nq * hd)), mn=get("mlp_norm", l, d, (d,)),
