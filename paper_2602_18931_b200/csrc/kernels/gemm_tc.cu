@@ -84,7 +84,7 @@ __device__ __forceinline__ void store_bf16_tail(__nv_bfloat16* dst, const std::u
 // by every lane (TMEM loads are warp-collective).
 template <int EPI, class Fetch>
 __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, int M, int N, int n_blk, void* out,
-                                              int ldo, const RopeEpi& rp) {
+                                              int ldo, const RopeEpi& rp, const NormEpi& nm) {
   const bool live = row < M;
   if constexpr (EPI == kEpiSwiGLU) {
     // W rows interleaved in 16-row blocks [gate 0..15 | up 0..15 | gate 16..31 | ...]: the
@@ -173,22 +173,46 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, in
           store32_bf16(o, pk);
         else
           store_bf16_tail(o, pk, ncols - c);
-      } else {  // kEpiAddF32: out[row, n] += acc
+      } else {  // kEpiAddF32: out[row, n] += acc (+ the fused-RMSNorm outputs of the new row)
         float* o = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
+        float x[32];
         if (c + 32 <= ncols) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            float4 x = reinterpret_cast<float4*>(o)[q];
-            x.x += __uint_as_float(r[4 * q + 0]);
-            x.y += __uint_as_float(r[4 * q + 1]);
-            x.z += __uint_as_float(r[4 * q + 2]);
-            x.w += __uint_as_float(r[4 * q + 3]);
-            reinterpret_cast<float4*>(o)[q] = x;
+            float4 v = reinterpret_cast<float4*>(o)[q];
+            v.x += __uint_as_float(r[4 * q + 0]);
+            v.y += __uint_as_float(r[4 * q + 1]);
+            v.z += __uint_as_float(r[4 * q + 2]);
+            v.w += __uint_as_float(r[4 * q + 3]);
+            reinterpret_cast<float4*>(o)[q] = v;
+            x[4 * q] = v.x;
+            x[4 * q + 1] = v.y;
+            x[4 * q + 2] = v.z;
+            x[4 * q + 3] = v.w;
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c + j < ncols) o[j] += __uint_as_float(r[j]);
+          for (int j = 0; j < 32; ++j) {
+            x[j] = 0.f;
+            if (c + j < ncols) {
+              o[j] += __uint_as_float(r[j]);
+              x[j] = o[j];
+            }
+          }
+        }
+        if (nm.ss != nullptr) {
+          float t = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) t = fmaf(x[j], x[j], t);
+          nm.ss[static_cast<std::size_t>((n0 + c) / 32) * nm.ld_ss + row] = t;  // chunk-major: coalesced
+          std::uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(x[2 * j], x[2 * j + 1]);
+          __nv_bfloat16* xb = static_cast<__nv_bfloat16*>(nm.xb) + static_cast<std::size_t>(row) * nm.ld_xb + n0 + c;
+          if (c + 32 <= ncols)
+            store32_bf16(xb, pk);
+          else
+            store_bf16_tail(xb, pk, ncols - c);
         }
       }
     }
@@ -205,7 +229,7 @@ template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo, const RopeEpi rope,
-                   const SplitArgs sk, int BN, int STAGES, int ablate) {
+                   const SplitArgs sk, const NormEpi norm, int BN, int STAGES, int ablate) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~static_cast<std::uintptr_t>(1023));
@@ -318,16 +342,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       int m_blk, n_blk, split;
       decode(u, m_blk, n_blk, split);
       const int acc = local & 1;
+      const int row = m_blk * BM + grp * 32 + static_cast<int>(lane);
+      // fused RMSNorm consumer: this row's scale from the producer's chunk statistics (read
+      // coalesced, chunk-major, while the accumulator is still being computed; four partial
+      // sums combined in a fixed order — deterministic)
+      float rs = 1.f;
+      if (norm.ss_in != nullptr && row < M) {
+        const float* p = norm.ss_in + row;
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+        const int nc = K / 32;
+        int c = 0;
+        for (; c + 4 <= nc; c += 4) {
+          t0 += p[static_cast<std::size_t>(c) * norm.ld_ss];
+          t1 += p[static_cast<std::size_t>(c + 1) * norm.ld_ss];
+          t2 += p[static_cast<std::size_t>(c + 2) * norm.ld_ss];
+          t3 += p[static_cast<std::size_t>(c + 3) * norm.ld_ss];
+        }
+        for (; c < nc; ++c) t0 += p[static_cast<std::size_t>(c) * norm.ld_ss];
+        rs = rsqrtf(((t0 + t1) + (t2 + t3)) / static_cast<float>(K) + norm.eps);
+      }
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
-      const int row = m_blk * BM + grp * 32 + static_cast<int>(lane);
       const std::uint32_t t_row = tmem_base + acc * kAccStride + (static_cast<std::uint32_t>(grp * 32) << 16);
       auto tmem_fetch = [&](int col, std::uint32_t (&r)[32]) {
         tmem_ld32(t_row + col, r);
         tmem_ld_wait();
+        if (norm.ss_in != nullptr) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rs);
+        }
       };
       if (S == 1) {
-        epilogue_tile<EPI>(tmem_fetch, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope);
+        epilogue_tile<EPI>(tmem_fetch, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -396,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
         };
-        epilogue_tile<EPI>(ws_fetch, BN, row, M, N, n_blk, out, ldo, rope);
+        epilogue_tile<EPI>(ws_fetch, BN, row, M, N, n_blk, out, ldo, rope, norm);
       }
       epi_bar();  // last_flag is reused by the next unit
     }
@@ -451,7 +497,7 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   const int total = m_blocks * n_tiles * sk.splits;
   const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
   gemm_tn_kernel<EPI><<<grid, kThreads, smem_bytes(bn), st>>>(ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo,
-                                                               g.rope, sk, bn, ring_stages(bn), ablate);
+                                                               g.rope, sk, g.norm, bn, ring_stages(bn), ablate);
   WS_CUDA(cudaGetLastError());
 }
 
@@ -514,6 +560,9 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
     if (g.N != (g.rope.nq + 2 * g.rope.nkv) * g.rope.hd) throw std::invalid_argument("gemm: qkv width");
     granule = g.rope.hd;
   }
+  if (g.norm.ss_in && (g.splits > 1 || g.K % 32)) throw std::invalid_argument("gemm: fused norm needs splits 1");
+  if (g.norm.ss && (g.epi != kEpiAddF32 || !g.norm.xb)) throw std::invalid_argument("gemm: norm producer epilogue");
+  if (g.norm.ss) granule = 32;  // statistics are per 32-column chunk
   const int bn = g.bn ? g.bn : pick_bn(g.M, g.N, granule);
   if (bn < 16 || bn > 256 || bn % granule) throw std::invalid_argument("gemm: tile width must be a multiple of " +
                                                                        std::to_string(granule) + " in [16, 256]");

@@ -25,6 +25,21 @@ struct RopeEpi {
   int nq = 0, nkv = 0, hd = 0;
 };
 
+// Fused RMSNorm plumbing (the norm weight itself is folded into the consuming projection):
+//   producer (kEpiAddF32): after out += acc, also xb = bf16(out) and ss[col / 32][row] = the sum
+//     of squares of each 32-column chunk of the updated residual row (chunked, so the statistic
+//     never depends on the tile width: batch- and tile-invariant);
+//   consumer (any epilogue): accumulator row r is scaled by rsqrt(sum_c ss_in[c][r] / K + eps)
+//     (fixed summation order) before the epilogue's own op — A is then bf16(x), unnormalised.
+struct NormEpi {
+  void* xb = nullptr;            // producer: bf16 [M, ld_xb]
+  int ld_xb = 0;
+  float* ss = nullptr;           // producer: fp32 chunk-major [N / 32][ld_ss] (ld_ss >= M)
+  const float* ss_in = nullptr;  // consumer: fp32 chunk-major [K / 32][ld_ss]
+  int ld_ss = 0;
+  float eps = 0.f;
+};
+
 struct GemmArgs {
   const void* A;  // bf16 [M, K], row stride lda
   const void* W;  // bf16 [N, K], row stride ldw
@@ -35,6 +50,7 @@ struct GemmArgs {
   int bn = 0;        // 0 = auto (multiple of 32 in [64, 256]; see pick_bn)
   int max_ctas = 0;  // persistent grid cap (0 = one CTA per SM)
   RopeEpi rope{};    // kEpiQKVRope only
+  NormEpi norm{};    // fused RMSNorm producer / consumer (optional)
   // Split-K workspace (zero-initialised once; see gemm_workspace_bytes). With ws == nullptr the
   // GEMM never splits; splits = 0 picks the (N, K)-determined count.
   void* ws = nullptr;

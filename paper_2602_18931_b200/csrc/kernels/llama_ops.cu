@@ -24,16 +24,39 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// One warp per 32-column chunk of a row: x = float(emb[tok]), xb = the bf16 copy (exact), and
+// the chunk's sum of squares for the fused RMSNorm of the first projection (gemm_tc.cuh NormEpi).
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const std::int32_t* __restrict__ tok, int d,
-                             float* __restrict__ x) {
+                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ss,
+                             int ld_ss) {
   const int row = blockIdx.x;
+  const int lane = threadIdx.x & 31;
   const __nv_bfloat16* e = emb + static_cast<std::size_t>(tok[row]) * d;
-  float* o = x + static_cast<std::size_t>(row) * d;
-  for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2) {
-    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(e + i));
-    o[i] = f.x;
-    o[i + 1] = f.y;
+  for (int c = threadIdx.x / 32; c < d / 32; c += blockDim.x / 32) {
+    const int i = c * 32 + lane;
+    const __nv_bfloat16 b = e[i];
+    const float f = __bfloat162float(b);
+    x[static_cast<std::size_t>(row) * d + i] = f;
+    if (xb) xb[static_cast<std::size_t>(row) * d + i] = b;
+    if (ss) {
+      // the producer GEMM epilogue sums a chunk sequentially (fmaf chain); any fixed order is
+      // valid — this one is the lane order of a sequential chain too, done by lane 0
+      float t = 0.f;
+      for (int j = 0; j < 32; ++j) {
+        const float v = __shfl_sync(0xffffffffu, f, j);
+        t = fmaf(v, v, t);
+      }
+      if (lane == 0) ss[static_cast<std::size_t>(c) * ld_ss + row] = t;  // chunk-major
+    }
   }
+}
+
+__global__ void scale_cols_kernel(__nv_bfloat16* __restrict__ W, std::int64_t rows, int cols,
+                                  const __nv_bfloat16* __restrict__ w) {
+  const std::int64_t n = rows * cols;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    W[i] = __float2bfloat16_rn(__bfloat162float(W[i]) * __bfloat162float(w[i % cols]));
 }
 
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int ld_x, const std::int32_t* __restrict__ idx,
@@ -167,9 +190,18 @@ __global__ void fill_normal_kernel(__nv_bfloat16* out, std::int64_t n, std::uint
 
 }  // namespace
 
-void embed_rows(const void* emb, const std::int32_t* tok, int rows, int d, float* x, cudaStream_t st) {
+void embed_rows(const void* emb, const std::int32_t* tok, int rows, int d, float* x, void* xb, float* ss, int ld_ss,
+                cudaStream_t st) {
   if (rows <= 0) return;
-  embed_kernel<<<rows, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(emb), tok, d, x);
+  if (d % 32) throw std::invalid_argument("embed: d % 32");
+  embed_kernel<<<rows, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(emb), tok, d, x,
+                                     static_cast<__nv_bfloat16*>(xb), ss, ld_ss);
+  WS_CUDA(cudaGetLastError());
+}
+
+void fold_norm_weight(void* W, std::int64_t rows, int cols, const void* w, cudaStream_t st) {
+  scale_cols_kernel<<<1184, 256, 0, st>>>(static_cast<__nv_bfloat16*>(W), rows, cols,
+                                          static_cast<const __nv_bfloat16*>(w));
   WS_CUDA(cudaGetLastError());
 }
 

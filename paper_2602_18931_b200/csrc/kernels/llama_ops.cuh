@@ -30,8 +30,13 @@ struct AttnShape {
   float scale;      // 1/sqrt(hd)
 };
 
-// x[row, :] = float(emb[tok[row], :])
-void embed_rows(const void* emb_bf16, const std::int32_t* tok, int rows, int d, float* x, cudaStream_t st);
+// x[row, :] = float(emb[tok[row], :]); optionally xb = the bf16 row and ss[c][row] = sum of
+// squares of 32-column chunk c (chunk-major; the fused-RMSNorm statistics, gemm_tc.cuh NormEpi).
+void embed_rows(const void* emb_bf16, const std::int32_t* tok, int rows, int d, float* x, void* xb_bf16, float* ss,
+                int ld_ss, cudaStream_t st);
+
+// W[:, k] *= w[k] (bf16 [rows, cols]): folds an RMSNorm weight into the projection it feeds.
+void fold_norm_weight(void* W_bf16, std::int64_t rows, int cols, const void* w_bf16, cudaStream_t st);
 
 // y[r] = bf16(x[idx ? idx[r] : r] * rsqrt(mean(x^2) + eps) * w)   (x fp32, w bf16 [d])
 void rmsnorm_rows(const float* x, int ld_x, const std::int32_t* idx, const void* w, float eps, int rows, int d,

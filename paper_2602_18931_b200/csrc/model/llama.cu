@@ -102,6 +102,12 @@ LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_s
     fill_normal_bf16(*it.dst, static_cast<std::int64_t>(it.n), seed, sid++, it.std_, it.mean, nullptr);
   }
   if (s.tied) lm_head_ = embed_;
+  // RMSNorm weights are folded into the projections they feed (the GEMMs apply only the
+  // per-row rsqrt scale, gemm_tc.cuh NormEpi); the norm tensors stay for reference/tests.
+  for (int l = 0; l < s.layers; ++l) {
+    fold_norm_weight(wqkv_[l], s.qkv_dim(), s.d, attn_norm_[l], nullptr);
+    fold_norm_weight(wgu_[l], 2 * static_cast<std::int64_t>(s.ffn), s.d, mlp_norm_[l], nullptr);
+  }
   const std::vector<float> inv = llama3_inv_freq(s);
   WS_CUDA(cudaMalloc(&inv_freq_, inv.size() * sizeof(float)));
   WS_CUDA(cudaMemcpy(inv_freq_, inv.data(), inv.size() * sizeof(float), cudaMemcpyHostToDevice));
@@ -133,8 +139,8 @@ LlamaModel::~LlamaModel() {
   cudaSetDevice(device_);
   if (rope_cs_) cudaFree(rope_cs_);
   if (gemm_ws_) cudaFree(gemm_ws_);
-  for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_, static_cast<void*>(x_), xn_, qkv_,
-                  q_, attn_, h_, logits_, xo_, static_cast<void*>(d_meta_)})
+  for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_, static_cast<void*>(x_), xb_,
+                  static_cast<void*>(ss_), qkv_, q_, attn_, h_, logits_, xo_, static_cast<void*>(d_meta_)})
     if (p) cudaFree(p);
   if (h_meta_) cudaFreeHost(h_meta_);
 }
@@ -143,11 +149,12 @@ void LlamaModel::ensure_rows(int rows, int out_rows) {
   if (rows <= cap_rows_ && out_rows <= cap_out_) return;
   rows = std::max(rows, cap_rows_);
   out_rows = std::max(out_rows, cap_out_);
-  for (void* p : {static_cast<void*>(x_), xn_, qkv_, q_, attn_, h_, logits_, xo_})
+  for (void* p : {static_cast<void*>(x_), xb_, static_cast<void*>(ss_), qkv_, q_, attn_, h_, logits_, xo_})
     if (p) cudaFree(p);
   const std::size_t R = rows, O = out_rows;
   WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&x_), R * s_.d * 4));
-  WS_CUDA(cudaMalloc(&xn_, R * s_.d * 2));
+  WS_CUDA(cudaMalloc(&xb_, R * s_.d * 2));
+  WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&ss_), R * (s_.d / 32) * 4));
   WS_CUDA(cudaMalloc(&qkv_, R * s_.qkv_dim() * 2));
   WS_CUDA(cudaMalloc(&q_, R * s_.n_q * s_.hd * 2));
   WS_CUDA(cudaMalloc(&attn_, R * s_.n_q * s_.hd * 2));
@@ -257,28 +264,42 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
   const std::int64_t layer_stride = n_slots_ * s_.n_kv * s_.hd;
   const AttnShape ash{s_.n_q, s_.n_kv, s_.hd, s_.n_kv * s_.hd, 1.0f / std::sqrt(static_cast<float>(s_.hd))};
   prof_.begin(st);
-  embed_rows(embed_, I(o_tok), n, d, x_, st);
+  // Fused RMSNorm: the embedding and every residual update (O / down epilogues) also emit the
+  // bf16 row and its chunk statistics; the normed projections (QKV, gate/up) scale their
+  // accumulator rows by rsqrt(mean(x^2) + eps) — no separate norm kernels inside the stack.
+  NormEpi produce, consume;
+  produce.xb = xb_;
+  produce.ld_xb = d;
+  produce.ss = ss_;
+  produce.ld_ss = cap_rows_;
+  consume.ss_in = ss_;
+  consume.ld_ss = cap_rows_;
+  consume.eps = s_.eps;
+  embed_rows(embed_, I(o_tok), n, d, x_, xb_, ss_, cap_rows_, st);
   prof_.mark(KernelProfiler::kEmbed, st);
   for (int l = 0; l < s_.layers; ++l) {
     __nv_bfloat16* kp = static_cast<__nv_bfloat16*>(k_pool_) + l * layer_stride;
     __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(v_pool_) + l * layer_stride;
-    rmsnorm_rows(x_, d, nullptr, attn_norm_[l], s_.eps, n, d, xn_, d, st);
-    prof_.mark(KernelProfiler::kNorm, st);
-    // QKV projection with RoPE + KV append fused into the epilogue
-    GemmArgs qa{xn_, wqkv_[l], nullptr, n, s_.qkv_dim(), d, d, d, s_.qkv_dim(), kEpiQKVRope, 0};
+    // QKV projection (attention norm fused) with RoPE + KV append fused into the epilogue
+    GemmArgs qa{xb_, wqkv_[l], nullptr, n, s_.qkv_dim(), d, d, d, s_.qkv_dim(), kEpiQKVRope, 0};
     qa.rope = RopeEpi{I(o_pos), I(o_slot), rope_cs_, q_, kp, vp, s_.n_q, s_.n_kv, s_.hd};
+    qa.norm = consume;
     gemm_tn(with_ws(qa), st);
     prof_.mark(KernelProfiler::kQKV, st);
     attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()), n_small,
               I(o_ext), reinterpret_cast<const unsigned long long*>(d_meta_ + o_msk), ash, attn_, st);
     prof_.mark(KernelProfiler::kAttn, st);
-    gemm_tn(with_ws(GemmArgs{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0}), st);
+    GemmArgs oa{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0};
+    oa.norm = produce;
+    gemm_tn(with_ws(oa), st);
     prof_.mark(KernelProfiler::kO, st);
-    rmsnorm_rows(x_, d, nullptr, mlp_norm_[l], s_.eps, n, d, xn_, d, st);
-    prof_.mark(KernelProfiler::kNorm, st);
-    gemm_tn(with_ws(GemmArgs{xn_, wgu_[l], h_, n, 2 * s_.ffn, d, d, d, s_.ffn, kEpiSwiGLU, 0}), st);
+    GemmArgs ga{xb_, wgu_[l], h_, n, 2 * s_.ffn, d, d, d, s_.ffn, kEpiSwiGLU, 0};
+    ga.norm = consume;
+    gemm_tn(with_ws(ga), st);
     prof_.mark(KernelProfiler::kGateUp, st);
-    gemm_tn(with_ws(GemmArgs{h_, wdown_[l], x_, n, d, s_.ffn, s_.ffn, s_.ffn, d, kEpiAddF32, 0}), st);
+    GemmArgs da{h_, wdown_[l], x_, n, d, s_.ffn, s_.ffn, s_.ffn, d, kEpiAddF32, 0};
+    if (l + 1 < s_.layers) da.norm = produce;
+    gemm_tn(with_ws(da), st);
     prof_.mark(KernelProfiler::kDown, st);
   }
   if (n_out == 0) return;

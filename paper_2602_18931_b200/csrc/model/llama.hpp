@@ -116,8 +116,9 @@ class LlamaModel {
   void* k_pool_ = nullptr;
   void* v_pool_ = nullptr;
   // activations
-  float* x_ = nullptr;
-  void* xn_ = nullptr;
+  float* x_ = nullptr;   // fp32 residual stream [rows][d]
+  void* xb_ = nullptr;   // its bf16 copy (A of the normed projections) [rows][d]
+  float* ss_ = nullptr;  // per-32-column-chunk sums of squares (fused RMSNorm) [rows][d/32]
   void* qkv_ = nullptr;
   void* q_ = nullptr;
   void* attn_ = nullptr;

@@ -134,8 +134,15 @@ struct ModelPair::Impl {
 
 ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(device), impl(new Impl) {
   WS_CUDA(cudaSetDevice(device));
-  WS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  WS_CUDA(cudaStreamCreateWithFlags(&stream_draft_, cudaStreamNonBlocking));
+  // The draft lane is the critical path of the continuous-batching loop (requests mostly wait
+  // on draft results), so its stream gets the higher scheduling priority; the verify lane's
+  // large GEMMs fill the SMs it leaves idle. WS_DRAFT_PRIO=0 gives both lanes equal priority.
+  int prio_lo = 0, prio_hi = 0;
+  WS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  const char* dp = std::getenv("WS_DRAFT_PRIO");
+  const bool draft_first = !(dp && dp[0] == '0');
+  WS_CUDA(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_lo));
+  WS_CUDA(cudaStreamCreateWithPriority(&stream_draft_, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
   const LlamaShape ts = shape_by_name(cfg.target), ds = shape_by_name(cfg.draft);
   if (ts.vocab != ds.vocab) throw ConfigError("target and draft vocabularies differ");
   const std::int64_t R = cfg.max_requests, C = cfg.max_ctx;
