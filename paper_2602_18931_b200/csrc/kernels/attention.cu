@@ -19,6 +19,7 @@
 #include <stdexcept>
 
 #include "cuda_check.hpp"
+#include "pdl.cuh"
 #include "llama_ops.cuh"
 
 namespace wsb {
@@ -79,6 +80,8 @@ __global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* 
                                                             const unsigned long long* __restrict__ row_mask, int nq,
                                                             int nkv, float scale_log2,
                                                             __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();  // inputs come from the previous kernel of the chain
   constexpr int C = HD / 8;   // 16-byte chunks per row
   constexpr int KS = HD / 16; // k16 steps for S = Q·Kᵀ
   constexpr int NT = HD / 8;  // n8 tiles of the output
@@ -293,11 +296,10 @@ void launch_attn(const void* q, const void* k_pool, const void* v_pool, const At
                  const std::int32_t* extra, const unsigned long long* row_mask, const AttnShape& s, float sl2,
                  void* out, cudaStream_t st) {
   if (n_groups <= 0) return;
-  attn_mma_kernel<HD, NW><<<dim3(n_groups, s.n_kv), 32 * NW, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
-      static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask, s.n_q, s.n_kv, sl2,
-      static_cast<__nv_bfloat16*>(out));
-  WS_CUDA(cudaGetLastError());
+  launch_pdl(attn_mma_kernel<HD, NW>, dim3(n_groups, s.n_kv), dim3(32 * NW), 0, st, 1,
+             static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
+             static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask, s.n_q, s.n_kv, sl2,
+             static_cast<__nv_bfloat16*>(out));
 }
 
 // groups[0, n_small) hold <= 16 query vectors each (one warp per CTA), the rest use 4 warps.

@@ -31,6 +31,7 @@
 #include <string>
 
 #include "cuda_check.hpp"
+#include "pdl.cuh"
 #include "sm100.cuh"
 
 namespace wsb {
@@ -50,11 +51,13 @@ constexpr int kNumSMs = 148;
 constexpr int kSmemBudget = 232448;  // 227 KB opt-in
 constexpr int kTmemCols = 512;
 constexpr int kAccStride = 256;
+// Per-CTA smem of one ring stage: the CTA's 128 A rows + its share of the BN weight rows (all
+// of them for a single CTA, half for a CTA pair).
 __host__ __device__ constexpr int a_bytes() { return BM * BK * 2; }
-__host__ __device__ constexpr int b_bytes(int bn) { return bn * BK * 2; }
-__host__ __device__ constexpr int stage_bytes(int bn) { return a_bytes() + b_bytes(bn); }
-inline int ring_stages(int bn) { return std::min(8, (kSmemBudget - 2048) / stage_bytes(bn)); }
-inline int smem_bytes(int bn) { return 1024 + ring_stages(bn) * stage_bytes(bn) + 256; }
+__host__ __device__ constexpr int b_bytes(int bn, int cg) { return bn / cg * BK * 2; }
+__host__ __device__ constexpr int stage_bytes(int bn, int cg) { return a_bytes() + b_bytes(bn, cg); }
+inline int ring_stages(int bn, int cg) { return std::min(8, (kSmemBudget - 2048) / stage_bytes(bn, cg)); }
+inline int smem_bytes(int bn, int cg) { return 1024 + ring_stages(bn, cg) * stage_bytes(bn, cg) + 256; }
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -225,7 +228,11 @@ struct SplitArgs {
   unsigned int* tickets = nullptr;   // [m_blocks * n_tiles], zero-initialised, self-resetting
 };
 
-template <int EPI>
+// CG = 1: one CTA per 128 x BN tile. CG = 2: a CTA pair (cluster of 2, cta_group::2) per
+// 256 x BN tile — each CTA holds its 128 A rows and half of the BN weight rows, the leader's
+// single thread issues the pair MMA over both CTAs' smem, and each CTA's TMEM receives its
+// 128 rows; shared-memory traffic per MAC drops by a third (the main loop is smem-bound).
+template <int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo, const RopeEpi rope,
@@ -233,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~static_cast<std::uintptr_t>(1023));
-  const int A_BYTES = a_bytes(), B_BYTES = b_bytes(BN), STAGE_BYTES = stage_bytes(BN);
+  const int A_BYTES = a_bytes(), B_BYTES = b_bytes(BN, CG), STAGE_BYTES = stage_bytes(BN, CG);
   unsigned char* sA = smem;
   unsigned char* sB = smem + STAGES * A_BYTES;
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -244,17 +251,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint32_t* last_flag = tmem_slot + 1;
 
   const int num_k = K / BK;
-  const int S = sk.splits;
-  const int total = m_blocks * n_tiles * S;
+  const int S = sk.splits;  // 1 for pairs
+  const int m_units = CG == 2 ? (m_blocks + 1) / 2 : m_blocks;
+  const int total = m_units * n_tiles * S;
+  const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int first = CG == 2 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int step = CG == 2 ? static_cast<int>(cluster_count_x()) : static_cast<int>(gridDim.x);
+  const bool leader = rank == 0;
   const std::uint32_t warp = warp_id(), lane = lane_id();
-  // unit u → (m_blk, n_blk, split), M fastest; split s covers k-blocks [s*nk/S, (s+1)*nk/S)
+  // unit u → (M unit, n_blk, split), M fastest; this CTA's 128-row block is unit * CG + rank;
+  // split s covers k-blocks [s*nk/S, (s+1)*nk/S)
   auto decode = [&](int u, int& m_blk, int& n_blk, int& split) {
-    m_blk = u % m_blocks;
-    const int r = u / m_blocks;
+    m_blk = (u % m_units) * CG + rank;
+    const int r = u / m_units;
     split = r % S;
     n_blk = r / S;
   };
 
+  if (threadIdx.x == 0) pdl_trigger();  // the next kernel may start its prologue on free SMs
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -264,38 +278,70 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty[a], 4 * CG);  // one arrival per epilogue warp (of both CTAs for a pair)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (CG == 2)
+      tmem_alloc_pair<kTmemCols>(tmem_slot);
+    else
+      tmem_alloc<kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // the peer's barriers exist before any remote signal
   tc_fence_after();
   const std::uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: continuous ring across units
-      int stage = 0, phase_count = 0;
+      // The weight boxes of the first ring fill depend on nothing: issue them before waiting for
+      // the previous kernel (PDL), then the activation boxes.
+      const std::uint32_t fill_bytes = CG == 2 ? 2 * STAGE_BYTES : STAGE_BYTES;
+      int pre = 0;
+      if (first < total) {
+        int m_blk, n_blk, split;
+        decode(first, m_blk, n_blk, split);
+        const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
+        pre = min(STAGES, kb1 - kb0);
+        for (int i = 0; i < pre; ++i) {
+          const int kb = kb0 + i;
+          if constexpr (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(&full[i], fill_bytes);
+            tma_load_2d_pair(sB + i * B_BYTES, &tmB, &full[i], kb * BK, n_blk * BN + rank * (BN / 2));
+          } else {
+            mbar_arrive_expect_tx(&full[i], fill_bytes);
+            tma_load_2d(sB + i * B_BYTES, &tmB, &full[i], kb * BK, n_blk * BN);
+          }
+        }
+      }
+      pdl_wait();
+      int stage = 0, it = 0;
       std::uint32_t phase = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      for (int u = first; u < total; u += step) {
         int m_blk, n_blk, split;
         decode(u, m_blk, n_blk, split);
         const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if ((ablate & 2) && phase_count >= STAGES) {
-            mbar_arrive(&full[stage]);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          if (it < pre) {  // weight box already in flight
+            if constexpr (CG == 2)
+              tma_load_2d_pair(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+            else
+              tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if constexpr (CG == 2) {
+              // both CTAs' boxes complete on the leader's barrier, which expects the pair's bytes
+              if (leader) mbar_arrive_expect_tx(&full[stage], fill_bytes);
+              tma_load_2d_pair(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+              tma_load_2d_pair(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN + rank * (BN / 2));
+            } else {
+              mbar_arrive_expect_tx(&full[stage], fill_bytes);
+              tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+              tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
             }
-            continue;
           }
-          ++phase_count;
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-          tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -304,12 +350,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
-      const std::uint32_t idesc = idesc_bf16_f32(BM, static_cast<std::uint32_t>(BN));
+    if (lane == 0 && leader) {  // MMA issuer (the pair leader issues for both CTAs)
+      const std::uint32_t idesc = idesc_bf16_f32(BM * CG, static_cast<std::uint32_t>(BN));
       int stage = 0;
       std::uint32_t phase = 0;
       int local = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x, ++local) {
+      for (int u = first; u < total; u += step, ++local) {
         int m_blk, n_blk, split;
         decode(u, m_blk, n_blk, split);
         const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
@@ -318,27 +364,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const std::uint32_t d = tmem_base + acc * kAccStride;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
+          mbar_wait(&full[stage], phase);  // TMA → MMA: both async proxy, ordered by the mbarrier
           const std::uint64_t da = smem_desc_sw128(sA + stage * A_BYTES);
           const std::uint64_t db = smem_desc_sw128(sB + stage * B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)  // advance 16 elements = 32 B = 2 descriptor units
-            if (!(ablate & 1)) mma_bf16(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
-          mma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+          for (int k = 0; k < BK / 16; ++k) {  // advance 16 elements = 32 B = 2 descriptor units
+            if (ablate & 1) continue;
+            if constexpr (CG == 2)
+              mma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+            else
+              mma_bf16(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+          }
+          // frees the smem slot (in both CTAs of a pair) when these MMAs retire
+          if constexpr (CG == 2)
+            mma_commit_pair(&empty[stage], 3);
+          else
+            mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (CG == 2)
+          mma_commit_pair(&tfull[acc], 3);
+        else
+          mma_commit(&tfull[acc]);
       }
     }
   } else {  // epilogue warps 2..5 → TMEM lane groups (warp % 4)
+    pdl_wait();  // the epilogues read the residual / norm statistics / rope tables
     const int grp = static_cast<int>(warp & 3);
     const int rows_pad = m_blocks * BM;
     int local = 0;
-    for (int u = blockIdx.x; u < total; u += gridDim.x, ++local) {
+    for (int u = first; u < total; u += step, ++local) {
       int m_blk, n_blk, split;
       decode(u, m_blk, n_blk, split);
       const int acc = local & 1;
@@ -376,7 +434,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         epilogue_tile<EPI>(tmem_fetch, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {  // the accumulator is reused by the (leader's) MMA issuer
+          if constexpr (CG == 2)
+            mbar_arrive_cluster(&tempty[acc], 0);
+          else
+            mbar_arrive(&tempty[acc]);
+        }
         continue;
       }
       // split-K: publish this split's fp32 partial, release TMEM, take a ticket
@@ -449,7 +512,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  if constexpr (CG == 2) {
+    cluster_sync();  // neither CTA leaves while its peer's MMAs / signals may still target it
+    if (warp == 1) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  } else {
+    if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -480,50 +548,97 @@ CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, st
   return m;
 }
 
-template <int EPI>
+int pair_clusters() {  // co-resident CTA pairs at one CTA per SM
+  static int n = [] {
+    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<kEpiBF16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemBudget));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * 74, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = kSmemBudget;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int c = 0;
+    WS_CUDA(cudaOccupancyMaxActiveClusters(&c, gemm_tn_kernel<kEpiBF16, 2>, &cfg));
+    return std::max(1, c);
+  }();
+  return n;
+}
+
+template <int EPI, int CG>
 void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
   });
-  static const int ablate = [] {  // WS_GEMM_ABLATE (measurement only): 1 no MMA, 2 no TMA after
-    const char* e = std::getenv("WS_GEMM_ABLATE");  // the first ring, 4 no stores
+  static const int ablate = [] {  // WS_GEMM_ABLATE (measurement only): 1 no MMA,
+    const char* e = std::getenv("WS_GEMM_ABLATE");  // 4 no epilogue stores
     return e ? std::atoi(e) : 0;
   }();
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
-  const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, static_cast<std::uint32_t>(bn));
+  const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, static_cast<std::uint32_t>(bn / CG));
   const int m_blocks = (g.M + BM - 1) / BM;
   const int n_tiles = (g.N + bn - 1) / bn;  // SwiGLU: N counts gate+up rows
-  const int total = m_blocks * n_tiles * sk.splits;
-  const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
-  gemm_tn_kernel<EPI><<<grid, kThreads, smem_bytes(bn), st>>>(ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo,
-                                                               g.rope, sk, g.norm, bn, ring_stages(bn), ablate);
-  WS_CUDA(cudaGetLastError());
+  const int smem = smem_bytes(bn, CG), stages = ring_stages(bn, CG);
+  if constexpr (CG == 1) {
+    const int total = m_blocks * n_tiles * sk.splits;
+    const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
+    launch_pdl(gemm_tn_kernel<EPI, 1>, dim3(grid), dim3(kThreads), smem, st, 1, ta, tb, g.M, g.N, g.K, m_blocks,
+               n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, ablate);
+  } else {
+    const int total = (m_blocks + 1) / 2 * n_tiles;
+    int clusters = std::min(total, pair_clusters());
+    if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 2));
+    launch_pdl(gemm_tn_kernel<EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2, ta, tb, g.M, g.N, g.K,
+               m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, ablate);
+  }
+}
+
+template <int EPI>
+void launch_cg(const GemmArgs& g, const SplitArgs& sk, int bn, int cg, cudaStream_t st) {
+  if (cg == 2) return launch<EPI, 2>(g, sk, bn, st);
+  return launch<EPI, 1>(g, sk, bn, st);
 }
 
 }  // namespace
 
-int pick_bn(int M, int N, int granule) {
-  // Measured on B200 (profiles/r01_gemm_feed.md): the main loop is bound by shared-memory
-  // bandwidth, ~128 B/cycle/SM shared by the TMA fill and the MMA operand reads, i.e. per
-  // k-block 2 x (BM + BN) x 128 B / 128 = 256 + 2 BN cycles against an MMA floor of 2 BN. A
-  // GEMM therefore costs ~ceil(tiles / 148) x (256 + 2 BN) per k-block: pick the BN (a
-  // multiple of 32 and of the epilogue's granule) minimising that, wider on ties. Numerics do
-  // not depend on BN (each output is the same K-ordered MMA chain).
+// Tile choice from the measured shared-memory bound (profiles/r01_gemm_feed.md): per k-block an
+// SM moves its A rows and its share of the weight rows through smem twice (TMA fill + MMA
+// read) at ~128 B/cycle, against an MMA floor of 2 BN cycles:
+//   single CTA, 128 x BN:  256 + 2 BN cycles   (always smem-bound)
+//   CTA pair,   256 x BN:  max(2 BN, 256 + BN) (balanced at BN = 256)
+// and a GEMM costs ceil(units / slots) of those (148 SMs, 74 pairs). Pick the (mode, BN) — BN a
+// multiple of 32 and of the epilogue's granule — minimising that; wider on ties. Numerics do
+// not depend on either (each output is the same K-ordered MMA chain): batch/tile invariance.
+struct TileChoice {
+  int cg, bn;
+};
+TileChoice pick_tile(int M, int N, int granule, bool allow_pair) {
   const int step = std::max(32, granule);
   const int mb = (M + BM - 1) / BM;
-  int best = step;
+  TileChoice best{1, step};
   long best_cost = -1;
-  for (int bn = 256 / step * step; bn >= std::max(64, step); bn -= step) {
-    const long tiles = static_cast<long>(mb) * ((N + bn - 1) / bn);
-    const long cost = ((tiles + kNumSMs - 1) / kNumSMs) * (256 + 2L * bn);
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best = bn;
+  for (int cg = 1; cg <= (allow_pair && mb > 1 ? 2 : 1); ++cg) {
+    for (int bn = 256 / step * step; bn >= std::max(64, step); bn -= step) {
+      const long units = static_cast<long>((mb + cg - 1) / cg) * ((N + bn - 1) / bn);
+      const long slots = cg == 2 ? kNumSMs / 2 : kNumSMs;
+      const long per = cg == 2 ? std::max(2L * bn, 256L + bn) : 256L + 2L * bn;
+      const long cost = ((units + slots - 1) / slots) * per;
+      if (best_cost < 0 || cost < best_cost) {
+        best_cost = cost;
+        best = TileChoice{cg, bn};
+      }
     }
   }
   return best;
 }
+
+int pick_bn(int M, int N, int granule) { return pick_tile(M, N, granule, false).bn; }
 
 int pick_bn(int M, int N) { return pick_bn(M, N, 32); }
 
@@ -563,9 +678,18 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   if (g.norm.ss_in && (g.splits > 1 || g.K % 32)) throw std::invalid_argument("gemm: fused norm needs splits 1");
   if (g.norm.ss && (g.epi != kEpiAddF32 || !g.norm.xb)) throw std::invalid_argument("gemm: norm producer epilogue");
   if (g.norm.ss) granule = 32;  // statistics are per 32-column chunk
-  const int bn = g.bn ? g.bn : pick_bn(g.M, g.N, granule);
+  // WS_GEMM_PAIR: "0" keeps every GEMM on single CTAs, "2" forces CTA pairs (tests, A/B)
+  const char* pe = std::getenv("WS_GEMM_PAIR");
+  const int pair_env = pe ? std::atoi(pe) : -1;
+  const bool pair_ok = pair_env != 0 && g.splits <= 1 && g.cta_group != 1;
+  TileChoice tc = pick_tile(g.M, g.N, granule, pair_ok);
+  if (g.cta_group == 2 || (pair_env == 2 && pair_ok)) tc.cg = 2;
+  if (g.bn) tc.bn = g.bn;
+  const int bn = tc.bn;
   if (bn < 16 || bn > 256 || bn % granule) throw std::invalid_argument("gemm: tile width must be a multiple of " +
                                                                        std::to_string(granule) + " in [16, 256]");
+  if (bn % 32 && g.cta_group != 2) tc.cg = 1;  // an explicit odd-16 width runs on single CTAs
+  if (tc.cg == 2 && (bn % 32 || g.splits > 1)) throw std::invalid_argument("gemm: CTA pairs need BN % 32, no split");
   SplitArgs sk;
   sk.splits = g.splits > 0 ? g.splits : (g.ws ? pick_splits(g.N, g.K) : 1);
   if (sk.splits > 1) {
@@ -600,11 +724,12 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
     sk.tickets = static_cast<unsigned int*>(g.ws);
     sk.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(g.ws) + kTicketBytes);
   }
+  if (tc.cg == 2) sk.splits = 1;
   switch (g.epi) {
-    case kEpiBF16: return launch<kEpiBF16>(g, sk, bn, st);
-    case kEpiAddF32: return launch<kEpiAddF32>(g, sk, bn, st);
-    case kEpiSwiGLU: return launch<kEpiSwiGLU>(g, sk, bn, st);
-    case kEpiQKVRope: return launch<kEpiQKVRope>(g, sk, bn, st);
+    case kEpiBF16: return launch_cg<kEpiBF16>(g, sk, bn, tc.cg, st);
+    case kEpiAddF32: return launch_cg<kEpiAddF32>(g, sk, bn, tc.cg, st);
+    case kEpiSwiGLU: return launch_cg<kEpiSwiGLU>(g, sk, bn, tc.cg, st);
+    case kEpiQKVRope: return launch_cg<kEpiQKVRope>(g, sk, bn, tc.cg, st);
   }
   throw std::invalid_argument("gemm: unknown epilogue");
 }

@@ -8,6 +8,7 @@
 #include <stdexcept>
 
 #include "cuda_check.hpp"
+#include "pdl.cuh"
 
 namespace wsb {
 
@@ -29,6 +30,8 @@ __device__ __forceinline__ float warp_max(float v) {
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const std::int32_t* __restrict__ tok, int d,
                              float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ss,
                              int ld_ss) {
+  pdl_trigger();
+  pdl_wait();  // inputs come from the previous kernel of the chain
   const int row = blockIdx.x;
   const int lane = threadIdx.x & 31;
   const __nv_bfloat16* e = emb + static_cast<std::size_t>(tok[row]) * d;
@@ -62,6 +65,8 @@ __global__ void scale_cols_kernel(__nv_bfloat16* __restrict__ W, std::int64_t ro
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int ld_x, const std::int32_t* __restrict__ idx,
                                const __nv_bfloat16* __restrict__ w, float eps, int d, __nv_bfloat16* __restrict__ y,
                                int ld_y) {
+  pdl_trigger();
+  pdl_wait();  // inputs come from the previous kernel of the chain
   const int row = blockIdx.x;
   const int src = idx ? idx[row] : row;
   const float4* xr = reinterpret_cast<const float4*>(x + static_cast<std::size_t>(src) * ld_x);
@@ -130,6 +135,8 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int nq
 }
 
 __global__ void plant_kernel(__nv_bfloat16* logits, int ld, const std::int32_t* plant, float bias, int rows) {
+  pdl_trigger();
+  pdl_wait();  // inputs come from the previous kernel of the chain
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int t = plant[r];
@@ -194,9 +201,8 @@ void embed_rows(const void* emb, const std::int32_t* tok, int rows, int d, float
                 cudaStream_t st) {
   if (rows <= 0) return;
   if (d % 32) throw std::invalid_argument("embed: d % 32");
-  embed_kernel<<<rows, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(emb), tok, d, x,
-                                     static_cast<__nv_bfloat16*>(xb), ss, ld_ss);
-  WS_CUDA(cudaGetLastError());
+  launch_pdl(embed_kernel, dim3(rows), dim3(256), 0, st, 1, static_cast<const __nv_bfloat16*>(emb), tok, d, x,
+             static_cast<__nv_bfloat16*>(xb), ss, ld_ss);
 }
 
 void fold_norm_weight(void* W, std::int64_t rows, int cols, const void* w, cudaStream_t st) {
@@ -209,9 +215,8 @@ void rmsnorm_rows(const float* x, int ld_x, const std::int32_t* idx, const void*
                   void* y, int ld_y, cudaStream_t st) {
   if (rows <= 0) return;
   if (d % 4) throw std::invalid_argument("rmsnorm: d % 4");
-  rmsnorm_kernel<<<rows, 256, 0, st>>>(x, ld_x, idx, static_cast<const __nv_bfloat16*>(w), eps, d,
-                                       static_cast<__nv_bfloat16*>(y), ld_y);
-  WS_CUDA(cudaGetLastError());
+  launch_pdl(rmsnorm_kernel, dim3(rows), dim3(256), 0, st, 1, x, ld_x, idx, static_cast<const __nv_bfloat16*>(w), eps,
+             d, static_cast<__nv_bfloat16*>(y), ld_y);
 }
 
 void rope_kv_append(const void* qkv, int rows, int nq, int nkv, int hd, const std::int32_t* pos,
@@ -226,8 +231,8 @@ void rope_kv_append(const void* qkv, int rows, int nq, int nkv, int hd, const st
 
 void plant_bias(void* logits, int ld, const std::int32_t* plant, float bias, int rows, cudaStream_t st) {
   if (rows <= 0) return;
-  plant_kernel<<<(rows + 127) / 128, 128, 0, st>>>(static_cast<__nv_bfloat16*>(logits), ld, plant, bias, rows);
-  WS_CUDA(cudaGetLastError());
+  launch_pdl(plant_kernel, dim3((rows + 127) / 128), dim3(128), 0, st, 1, static_cast<__nv_bfloat16*>(logits), ld,
+             plant, bias, rows);
 }
 
 void copy_slots(void* k_pool, void* v_pool, const std::int32_t* src, const std::int32_t* dst, int n, int layers,

@@ -19,6 +19,7 @@
 #include <stdexcept>
 
 #include "cuda_check.hpp"
+#include "pdl.cuh"
 
 namespace wsb {
 
@@ -193,6 +194,8 @@ __global__ void __launch_bounds__(kThreads) row_stats_kernel(
     ws_pred* __restrict__ out_pred, RowStats* __restrict__ out_stats, Partial* __restrict__ partials,
     std::uint32_t* __restrict__ row_ticket, std::uint32_t k, const std::uint32_t* __restrict__ cand,
     ws_verify_out* __restrict__ vout, std::uint32_t* __restrict__ req_ticket, const std::int32_t* __restrict__ forced) {
+  pdl_trigger();
+  pdl_wait();  // inputs come from the previous kernel of the chain
   const std::uint32_t split = blockIdx.x, splits = gridDim.x, row = blockIdx.y;
   const std::uint32_t lo = split * kRowChunk;
   const std::uint32_t hi = min(vocab, lo + kRowChunk);
@@ -304,10 +307,9 @@ void row_stats_bf16(const void* logits, std::uint32_t rows, std::uint32_t vocab,
   Partial* partials = reinterpret_cast<Partial*>(ws + kTicketBytes);
   const bool vec_ok = (reinterpret_cast<std::uintptr_t>(logits) % 16 == 0) && (ld % 8 == 0);
   dim3 grid(splits, rows);
-  row_stats_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const __nv_bfloat16*>(logits), vocab, ld,
-                                                  inv_temp * kLog2e, vec_ok, out_pred, out_stats, partials,
-                                                  row_ticket, k, cand, verify_out, req_ticket, forced);
-  WS_CUDA(cudaGetLastError());
+  launch_pdl(row_stats_kernel, grid, dim3(kThreads), 0, stream, 1, static_cast<const __nv_bfloat16*>(logits), vocab,
+             ld, inv_temp * kLog2e, vec_ok, out_pred, out_stats, partials, row_ticket, k, cand, verify_out,
+             req_ticket, forced);
 }
 
 }  // namespace wsb

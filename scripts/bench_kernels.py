@@ -76,7 +76,7 @@ def gemm_model():
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         fl = 2.0 * M * N * K
         per = {}
-        for bn in range(64, 257, 16):
+        for bn in range(64, 257, 32):
             per[bn] = round(timeit(lambda: ops.gemm(A, W, out=out, bn=bn), flush=flush) * 1e6, 1)
         t_def = timeit(lambda: ops.gemm(A, W, out=out), flush=flush)
         t_cub = timeit(lambda: torch.matmul(A, W.T), flush=flush)

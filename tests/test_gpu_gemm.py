@@ -110,3 +110,32 @@ def test_gemm_large_throughput_smoke(ops):
     idx = torch.randint(0, N, (64,), device="cuda")
     ref = A.float() @ W[idx].float().T
     assert rel_err(out[:, idx], ref) < 4e-3
+
+
+@pytest.mark.parametrize("epi", [0, 1, 2])
+@pytest.mark.parametrize("shape", [(530, 4096, 4096), (655, 2048, 2048), (100, 1024, 512), (300, 3072, 1024)])
+def test_gemm_cta_pair(ops, monkeypatch, epi, shape):
+    """CTA-pair tiles (cta_group::2, 256 x BN over two SMs) against the fp32 reference and,
+    bit for bit, against single-CTA tiles: the pair issues the same K-ordered MMA chain."""
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + epi)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    if epi == 2:
+        Wg, Wu = W[:N // 2].contiguous(), W[N // 2:].contiguous()
+        W = ops.interleave_gate_up(Wg, Wu)
+        ref = torch.nn.functional.silu(A.float() @ Wg.float().T) * (A.float() @ Wu.float().T)
+    else:
+        ref = A.float() @ W.float().T
+    outs = {}
+    for mode in ("0", "2"):
+        monkeypatch.setenv("WS_GEMM_PAIR", mode)
+        if epi == 1:
+            X = torch.ones(M, N, device="cuda")
+            ops.gemm(A, W, out=X, epi=1)
+            outs[mode] = X - 1.0
+        else:
+            outs[mode] = ops.gemm(A, W, epi=epi)
+        torch.cuda.synchronize()
+    assert rel_err(outs["2"], ref) < 6e-3
+    assert torch.equal(outs["2"], outs["0"])
