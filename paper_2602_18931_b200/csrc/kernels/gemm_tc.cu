@@ -295,16 +295,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const std::uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer: continuous ring across units
-      // The weight boxes of the first ring fill depend on nothing: issue them before waiting for
-      // the previous kernel (PDL), then the activation boxes.
-      const std::uint32_t fill_bytes = CG == 2 ? 2 * STAGE_BYTES : STAGE_BYTES;
-      int pre = 0;
-      if (first < total) {
-        int m_blk, n_blk, split;
-        decode(first, m_blk, n_blk, split);
-        const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
-        pre = min(STAGES, kb1 - kb0);
+    // TMA producer: the whole warp runs the ring (operands stay warp-uniform), one elected lane
+    // issues. The weight boxes of the first ring fill depend on nothing: they go out before the
+    // wait for the previous kernel (PDL), the activation boxes after it.
+    const std::uint32_t fill_bytes = CG == 2 ? 2 * STAGE_BYTES : STAGE_BYTES;
+    int pre = 0;
+    if (first < total) {
+      int m_blk, n_blk, split;
+      decode(first, m_blk, n_blk, split);
+      const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
+      pre = min(STAGES, kb1 - kb0);
+      if (elect_one()) {
         for (int i = 0; i < pre; ++i) {
           const int kb = kb0 + i;
           if constexpr (CG == 2) {
@@ -316,42 +317,42 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      pdl_wait();
-      int stage = 0, it = 0;
-      std::uint32_t phase = 0;
-      for (int u = first; u < total; u += step) {
-        int m_blk, n_blk, split;
-        decode(u, m_blk, n_blk, split);
-        const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          if (it < pre) {  // weight box already in flight
-            if constexpr (CG == 2)
-              tma_load_2d_pair(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-            else
-              tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-          } else {
-            mbar_wait(&empty[stage], phase ^ 1);
-            if constexpr (CG == 2) {
-              // both CTAs' boxes complete on the leader's barrier, which expects the pair's bytes
-              if (leader) mbar_arrive_expect_tx(&full[stage], fill_bytes);
-              tma_load_2d_pair(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+      __syncwarp();
+    }
+    pdl_wait();
+    int stage = 0, it = 0;
+    std::uint32_t phase = 0;
+    for (int u = first; u < total; u += step) {
+      int m_blk, n_blk, split;
+      decode(u, m_blk, n_blk, split);
+      const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const bool prefilled = it < pre;  // weight box already in flight
+        if (!prefilled) mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          if constexpr (CG == 2) {
+            // both CTAs' boxes complete on the leader's barrier, which expects the pair's bytes
+            if (!prefilled && leader) mbar_arrive_expect_tx(&full[stage], fill_bytes);
+            tma_load_2d_pair(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+            if (!prefilled)
               tma_load_2d_pair(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN + rank * (BN / 2));
-            } else {
-              mbar_arrive_expect_tx(&full[stage], fill_bytes);
-              tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-              tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
-            }
+          } else {
+            if (!prefilled) mbar_arrive_expect_tx(&full[stage], fill_bytes);
+            tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+            if (!prefilled) tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
           }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // MMA issuer (the pair leader issues for both CTAs)
+    if (leader) {  // MMA issuer: the whole warp runs the loop, one elected lane issues
       const std::uint32_t idesc = idesc_bf16_f32(BM * CG, static_cast<std::uint32_t>(BN));
+      const std::uint64_t da0 = smem_desc_sw128(sA), db0 = smem_desc_sw128(sB);
       int stage = 0;
       std::uint32_t phase = 0;
       int local = 0;
@@ -365,30 +366,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         const std::uint32_t d = tmem_base + acc * kAccStride;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);  // TMA → MMA: both async proxy, ordered by the mbarrier
-          const std::uint64_t da = smem_desc_sw128(sA + stage * A_BYTES);
-          const std::uint64_t db = smem_desc_sw128(sB + stage * B_BYTES);
+          // descriptor start-address field is addr >> 4 (stage offsets are 16-byte multiples)
+          const std::uint64_t da = da0 + static_cast<std::uint64_t>((stage * A_BYTES) >> 4);
+          const std::uint64_t db = db0 + static_cast<std::uint64_t>((stage * B_BYTES) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {  // advance 16 elements = 32 B = 2 descriptor units
-            if (ablate & 1) continue;
+            for (int k = 0; k < BK / 16; ++k) {  // advance 16 elements = 32 B = 2 descriptor units
+              if (ablate & 1) continue;
+              if constexpr (CG == 2)
+                mma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+              else
+                mma_bf16(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+            }
+            // frees the smem slot (in both CTAs of a pair) when these MMAs retire
             if constexpr (CG == 2)
-              mma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+              mma_commit_pair(&empty[stage], 3);
             else
-              mma_bf16(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+              mma_commit(&empty[stage]);
           }
-          // frees the smem slot (in both CTAs of a pair) when these MMAs retire
-          if constexpr (CG == 2)
-            mma_commit_pair(&empty[stage], 3);
-          else
-            mma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if constexpr (CG == 2)
-          mma_commit_pair(&tfull[acc], 3);
-        else
-          mma_commit(&tfull[acc]);
+        if (elect_one()) {
+          if constexpr (CG == 2)
+            mma_commit_pair(&tfull[acc], 3);
+          else
+            mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
       }
     }
   } else {  // epilogue warps 2..5 → TMEM lane groups (warp % 4)

@@ -15,6 +15,21 @@ __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
 }
 
 __device__ __forceinline__ std::uint32_t warp_id() { return threadIdx.x / 32; }
+// One lane of the (converged) warp. Issuing tcgen05 / TMA ops under elect_one() from a loop
+// the whole warp runs keeps their operands warp-uniform, so they live in uniform registers —
+// a lane-0-only loop makes the compiler wrap every issue in an ELECT + R2UR.BROADCAST retry
+// loop (~50-100 cycles per MMA, which starves the tensor core at BN < 256).
+__device__ __forceinline__ bool elect_one() {
+  std::uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ std::uint32_t lane_id() { return threadIdx.x % 32; }
 
 // ---- mbarrier ----

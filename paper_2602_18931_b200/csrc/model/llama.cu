@@ -259,6 +259,7 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
   auto with_ws = [&](GemmArgs g) {
     g.ws = gemm_ws_;
     g.ws_bytes = gemm_ws_bytes_;
+    g.max_ctas = max_ctas_;
     return g;
   };
   const std::int64_t layer_stride = n_slots_ * s_.n_kv * s_.hd;

@@ -73,6 +73,8 @@ class KernelProfiler {
 class LlamaModel {
  public:
   KernelProfiler& profiler() { return prof_; }
+  // Cap on the persistent GEMM grids (0 = every SM): leaves SMs to a concurrent forward.
+  void set_max_ctas(int n) { max_ctas_ = n; }
   LlamaModel(const LlamaShape& shape, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device);
   ~LlamaModel();
   LlamaModel(const LlamaModel&) = delete;
@@ -96,6 +98,7 @@ class LlamaModel {
  private:
   void ensure_rows(int rows, int out_rows);
   KernelProfiler prof_;
+  int max_ctas_ = 0;
   LlamaShape s_;
   int device_;
   std::int64_t n_slots_;

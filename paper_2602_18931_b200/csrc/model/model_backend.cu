@@ -150,6 +150,8 @@ ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(d
   target_.reset(new LlamaModel(ts, cfg.seed * 2 + 1, R * C, max_rows, device));
   draft_.reset(new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows, device));
   prompts_.resize(cfg.max_requests);
+  if (const char* e = std::getenv("WS_TARGET_CTAS")) target_->set_max_ctas(std::atoi(e));
+  if (const char* e = std::getenv("WS_DRAFT_CTAS")) draft_->set_max_ctas(std::atoi(e));
   WS_CUDA(cudaEventCreate(&impl->e0));
   WS_CUDA(cudaEventCreate(&impl->e1));
   WS_CUDA(cudaEventCreate(&impl->e2));
