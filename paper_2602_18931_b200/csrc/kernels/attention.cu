@@ -16,6 +16,7 @@
 // kernel is HBM-bound on KV bytes; tensor-core throughput is not the limiter at these shapes.
 #include <cuda_bf16.h>
 
+#include <mutex>
 #include <stdexcept>
 
 #include "cuda_check.hpp"
@@ -69,54 +70,65 @@ __device__ __forceinline__ int swz(int row, int chunk) {
   return row * C + (chunk ^ (row & 7));
 }
 
-// NW warps per CTA (16 query vectors each): NW = 4 for verify / catch-up groups, NW = 1 for the
-// small tree groups of the draft (<= 16 vectors), so those do not idle three warps per CTA.
-template <int HD, int NW>
-__global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* __restrict__ q,
-                                                            const __nv_bfloat16* __restrict__ kp,
-                                                            const __nv_bfloat16* __restrict__ vp,
-                                                            const AttnGroup* __restrict__ groups,
-                                                            const std::int32_t* __restrict__ extra,
-                                                            const unsigned long long* __restrict__ row_mask, int nq,
-                                                            int nkv, float scale_log2,
-                                                            __nv_bfloat16* __restrict__ out) {
+// VW x KS warps per CTA: VW vector warps (16 query vectors each) times KS key slices. Slice
+// ks streams the K/V tiles t = ks, ks + KS, ... through its own double buffer, so a CTA keeps
+// KS tiles in flight; at the end of a pass the slices' softmax states merge in slice order.
+// KS is fixed per head dim (never chosen from the group), so a row's result is the same in any
+// group of any batch (batch invariance: speculative stream == greedy stream).
+template <int HD, int VW, int KS>
+__global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloat16* __restrict__ q,
+                                                                 const __nv_bfloat16* __restrict__ kp,
+                                                                 const __nv_bfloat16* __restrict__ vp,
+                                                                 const AttnGroup* __restrict__ groups,
+                                                                 const std::int32_t* __restrict__ extra,
+                                                                 const unsigned long long* __restrict__ row_mask,
+                                                                 int nq, int nkv, float scale_log2,
+                                                                 __nv_bfloat16* __restrict__ out) {
   pdl_trigger();
   pdl_wait();  // inputs come from the previous kernel of the chain
   constexpr int C = HD / 8;   // 16-byte chunks per row
-  constexpr int KS = HD / 16; // k16 steps for S = Q·Kᵀ
+  constexpr int KST = HD / 16; // k16 steps for S = Q·Kᵀ
   constexpr int NT = HD / 8;  // n8 tiles of the output
-  constexpr int kThreads = 32 * NW;
-  constexpr int kVecPerPass = 16 * NW;
-  __shared__ __align__(128) uint4 sQ[kVecPerPass * C];
-  __shared__ __align__(128) uint4 sK[2][kTile * C];
-  __shared__ __align__(128) uint4 sV[2][kTile * C];
+  constexpr int kSliceThreads = 32 * VW;
+  constexpr int kVecPerPass = 16 * VW;
+  constexpr int kMergeFloats = 4 + 4 * NT;  // m_lo, m_hi, l_lo, l_hi, o[NT][4] per lane
+  static_assert((KS - 1) * VW * 32 * kMergeFloats * 4 <= KS * 2 * 2 * kTile * C * 16, "merge scratch");
+  // dynamic smem: Q tile, then [slice][buffer][K | V] tiles (attn_smem_bytes)
+  extern __shared__ __align__(128) uint4 smem_dyn[];
+  uint4* sQ = smem_dyn;
+  uint4* sKV0 = smem_dyn + kVecPerPass * C;
+  auto kv_tile = [&](int slice, int buf, int which) { return sKV0 + ((slice * 2 + buf) * 2 + which) * (kTile * C); };
 
   const AttnGroup g = groups[blockIdx.x];
   const int kvh = blockIdx.y;
   const int G = nq / nkv;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int vw = warp % VW, ks = warp / VW;
+  const int st = threadIdx.x % kSliceThreads;  // thread index within the slice
   const int nvec = g.n_rows * G;
   const int ctx = g.prefix_len + g.extra_len;
   const std::size_t slot_stride = static_cast<std::size_t>(nkv) * HD;
   const int n_tiles = (ctx + kTile - 1) / kTile;
+  const int n_iter = (n_tiles + KS - 1) / KS;
 
   auto slot_of = [&](int p) -> int {
     return p < g.prefix_len ? g.prefix_slot + p : (p < ctx ? extra[g.extra_off + p - g.prefix_len] : -1);
   };
-  auto load_tile = [&](int t, int buf) {
-    for (int i = threadIdx.x; i < kTile * C; i += kThreads) {
+  auto load_tile = [&](int t, int buf) {  // by the threads of this slice
+    if (t >= n_tiles) return;
+    for (int i = st; i < kTile * C; i += kSliceThreads) {
       const int r = i / C, c = i % C;
       const int s = slot_of(t * kTile + r);
       const std::size_t base = static_cast<std::size_t>(s < 0 ? 0 : s) * slot_stride + static_cast<std::size_t>(kvh) * HD;
-      cp_async16(&sK[buf][swz<HD>(r, c)], kp + base + c * 8, s >= 0);
-      cp_async16(&sV[buf][swz<HD>(r, c)], vp + base + c * 8, s >= 0);
+      cp_async16(kv_tile(ks, buf, 0) + swz<HD>(r, c), kp + base + c * 8, s >= 0);
+      cp_async16(kv_tile(ks, buf, 1) + swz<HD>(r, c), vp + base + c * 8, s >= 0);
     }
   };
 
   for (int pass0 = 0; pass0 < nvec; pass0 += kVecPerPass) {
     __syncthreads();
     // Q for this pass: vector v -> (row j = v / G, head kvh*G + v % G), zero past nvec
-    for (int i = threadIdx.x; i < kVecPerPass * C; i += kThreads) {
+    for (int i = threadIdx.x; i < kVecPerPass * C; i += 32 * VW * KS) {
       const int vv = i / C, c = i % C, v = pass0 + vv;
       uint4 val = make_uint4(0, 0, 0, 0);
       if (v < nvec) {
@@ -125,12 +137,12 @@ __global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* 
       }
       sQ[swz<HD>(vv, c)] = val;
     }
-    load_tile(0, 0);
+    load_tile(ks, 0);
     cp_async_commit();
     __syncthreads();
 
     // this warp's 16 query vectors; the thread's two accumulator rows
-    const int wv0 = pass0 + warp * 16;
+    const int wv0 = pass0 + vw * 16;
     const bool warp_live = wv0 < nvec;
     const int r_lo = lane / 4, r_hi = r_lo + 8;
     int last_lo = -1, last_hi = -1;
@@ -150,14 +162,14 @@ __global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* 
       }
     }
     // Q fragments (A operand) for all k16 steps
-    std::uint32_t qa[KS][4];
+    std::uint32_t qa[KST][4];
     if (warp_live) {
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        // lanes 0-15 rows 0-15 chunk 2ks, lanes 16-31 rows 0-15 chunk 2ks+1
-        const int row = warp * 16 + (lane % 16);
-        const int chunk = 2 * ks + lane / 16;
-        ldsm_x4(qa[ks], &sQ[swz<HD>(row, chunk)]);
+      for (int kk = 0; kk < KST; ++kk) {
+        // lanes 0-15 rows 0-15 chunk 2kk, lanes 16-31 rows 0-15 chunk 2kk+1
+        const int row = vw * 16 + (lane % 16);
+        const int chunk = 2 * kk + lane / 16;
+        ldsm_x4(qa[kk], &sQ[swz<HD>(row, chunk)]);
       }
     }
     float o[NT][4];
@@ -165,32 +177,33 @@ __global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* 
     for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
     float mx_lo = -INFINITY, mx_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
-    for (int t = 0; t < n_tiles; ++t) {
-      const int buf = t & 1;
-      if (t + 1 < n_tiles) {
-        load_tile(t + 1, buf ^ 1);
+    for (int it = 0; it < n_iter; ++it) {
+      const int t = it * KS + ks;  // this slice's tile
+      const int buf = it & 1;
+      if (it + 1 < n_iter) {
+        load_tile(t + KS, buf ^ 1);
         cp_async_commit();
         cp_async_wait1();
       } else {
         cp_async_wait0();
       }
       __syncthreads();
-      if (warp_live) {
+      if (warp_live && t < n_tiles) {
         // S = Q·Kᵀ over 32 positions: 4 n8 tiles
         float s[4][4];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int kk = 0; kk < KST; ++kk) {
 #pragma unroll
           for (int np = 0; np < 2; ++np) {  // pairs of n8 tiles (16 positions) per ldmatrix.x4
             std::uint32_t kb[4];
             // matrices: (pos 0-7, k lo), (pos 0-7, k hi), (pos 8-15, k lo), (pos 8-15, k hi)
             const int pos = np * 16 + (lane % 8) + ((lane / 16) * 8);
-            const int chunk = 2 * ks + ((lane / 8) & 1);
-            ldsm_x4(kb, &sK[buf][swz<HD>(pos, chunk)]);
-            mma16816(s[2 * np], qa[ks], kb[0], kb[1]);
-            mma16816(s[2 * np + 1], qa[ks], kb[2], kb[3]);
+            const int chunk = 2 * kk + ((lane / 8) & 1);
+            ldsm_x4(kb, kv_tile(ks, buf, 0) + swz<HD>(pos, chunk));
+            mma16816(s[2 * np], qa[kk], kb[0], kb[1]);
+            mma16816(s[2 * np + 1], qa[kk], kb[2], kb[3]);
           }
         }
         // visibility + scale (exp2 domain)
@@ -234,9 +247,9 @@ __global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* 
           const float p2v = exp2f(s[nt][2] - base_hi), p3v = exp2f(s[nt][3] - base_hi);
           rs_lo += p0v + p1v;
           rs_hi += p2v + p3v;
-          const int ks = nt / 2, half = nt % 2;
-          pa[ks][half * 2 + 0] = pack_bf16(p0v, p1v);
-          pa[ks][half * 2 + 1] = pack_bf16(p2v, p3v);
+          const int kk = nt / 2, half = nt % 2;
+          pa[kk][half * 2 + 0] = pack_bf16(p0v, p1v);
+          pa[kk][half * 2 + 1] = pack_bf16(p2v, p3v);
         }
         rs_lo += __shfl_xor_sync(0xffffffffu, rs_lo, 1);
         rs_lo += __shfl_xor_sync(0xffffffffu, rs_lo, 2);
@@ -253,23 +266,61 @@ __global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* 
         }
         // O += P·V: A = P (16 x 32 positions), B = V (32 positions x HD) via ldmatrix.trans
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
+        for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
           for (int np = 0; np < NT / 2; ++np) {  // pairs of n8 output tiles (16 dims)
             std::uint32_t vb[4];
             // matrices: (pos lo 0-7, dims np*16+0-7), (pos 8-15, same), (pos 0-7, dims +8), (pos 8-15, +8)
-            const int pos = ks * 16 + (lane % 8) + ((lane / 8) & 1) * 8;
+            const int pos = kk * 16 + (lane % 8) + ((lane / 8) & 1) * 8;
             const int chunk = 2 * np + (lane / 16);
-            ldsm_x4_t(vb, &sV[buf][swz<HD>(pos, chunk)]);
-            mma16816(o[2 * np], pa[ks], vb[0], vb[1]);
-            mma16816(o[2 * np + 1], pa[ks], vb[2], vb[3]);
+            ldsm_x4_t(vb, kv_tile(ks, buf, 1) + swz<HD>(pos, chunk));
+            mma16816(o[2 * np], pa[kk], vb[0], vb[1]);
+            mma16816(o[2 * np + 1], pa[kk], vb[2], vb[3]);
           }
         }
       }
-      __syncthreads();  // buffer `buf` is refilled two tiles later
+      __syncthreads();  // buffer `buf` of every slice is refilled two iterations later
     }
-    // epilogue: normalise and store this warp's rows
-    if (warp_live) {
+    // merge the KS slices' states (slice order, in the K/V scratch), then normalise + store
+    if constexpr (KS > 1) {
+      float* scratch = reinterpret_cast<float*>(sKV0);
+      if (ks > 0 && warp_live) {
+        float* my = scratch + ((static_cast<std::size_t>(ks - 1) * VW + vw) * 32 + lane) * kMergeFloats;
+        my[0] = mx_lo;
+        my[1] = mx_hi;
+        my[2] = l_lo;
+        my[3] = l_hi;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) my[4 + nt * 4 + e] = o[nt][e];
+      }
+      __syncthreads();
+      if (ks == 0 && warp_live) {
+#pragma unroll 1
+        for (int sl = 1; sl < KS; ++sl) {
+          const float* ot = scratch + ((static_cast<std::size_t>(sl - 1) * VW + vw) * 32 + lane) * kMergeFloats;
+          const float om_lo = ot[0], om_hi = ot[1];
+          const float nm_lo = fmaxf(mx_lo, om_lo), nm_hi = fmaxf(mx_hi, om_hi);
+          const float b_lo = nm_lo == -INFINITY ? 0.f : nm_lo, b_hi = nm_hi == -INFINITY ? 0.f : nm_hi;
+          const float ca_lo = exp2f(mx_lo - b_lo), cb_lo = exp2f(om_lo - b_lo);
+          const float ca_hi = exp2f(mx_hi - b_hi), cb_hi = exp2f(om_hi - b_hi);
+          l_lo = l_lo * ca_lo + ot[2] * cb_lo;
+          l_hi = l_hi * ca_hi + ot[3] * cb_hi;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            o[nt][0] = o[nt][0] * ca_lo + ot[4 + nt * 4 + 0] * cb_lo;
+            o[nt][1] = o[nt][1] * ca_lo + ot[4 + nt * 4 + 1] * cb_lo;
+            o[nt][2] = o[nt][2] * ca_hi + ot[4 + nt * 4 + 2] * cb_hi;
+            o[nt][3] = o[nt][3] * ca_hi + ot[4 + nt * 4 + 3] * cb_hi;
+          }
+          mx_lo = nm_lo;
+          mx_hi = nm_hi;
+        }
+      }
+    }
+    // epilogue: normalise and store this warp's rows (slice 0 holds the merged state)
+    if (warp_live && ks == 0) {
       const float inv_lo = l_lo > 0.f ? 1.f / l_lo : 0.f, inv_hi = l_hi > 0.f ? 1.f / l_hi : 0.f;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -291,29 +342,45 @@ __global__ void __launch_bounds__(32 * NW) attn_mma_kernel(const __nv_bfloat16* 
 
 }  // namespace
 
-template <int HD, int NW>
+template <int HD, int VW, int KS>
 void launch_attn(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
                  const std::int32_t* extra, const unsigned long long* row_mask, const AttnShape& s, float sl2,
                  void* out, cudaStream_t st) {
   if (n_groups <= 0) return;
-  launch_pdl(attn_mma_kernel<HD, NW>, dim3(n_groups, s.n_kv), dim3(32 * NW), 0, st, 1,
+  constexpr int C = HD / 8;
+  constexpr int kSmem = (16 * VW * C + KS * 4 * kTile * C) * 16;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    WS_CUDA(cudaFuncSetAttribute(attn_mma_kernel<HD, VW, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+  });
+  launch_pdl(attn_mma_kernel<HD, VW, KS>, dim3(n_groups, s.n_kv), dim3(32 * VW * KS), kSmem, st, 1,
              static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
              static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask, s.n_q, s.n_kv, sl2,
              static_cast<__nv_bfloat16*>(out));
 }
 
-// groups[0, n_small) hold <= 16 query vectors each (one warp per CTA), the rest use 4 warps.
+// groups[0, n_vw1) hold <= 16 query vectors each (one vector warp per CTA), the next n_vw2
+// <= 32 (two), the rest use four. Every launch uses the same key-slice count, so numerics never
+// depend on the grouping.
 void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
-               int n_small, const std::int32_t* extra, const unsigned long long* row_mask, const AttnShape& s,
-               void* out, cudaStream_t st) {
+               int n_vw1, int n_vw2, const std::int32_t* extra, const unsigned long long* row_mask,
+               const AttnShape& s, void* out, cudaStream_t st) {
   if (n_groups <= 0) return;
   const float sl2 = s.scale * 1.4426950408889634f;
+  // key slices per head dim (measured: two slices help the 64-wide draft heads, not the
+  // 128-wide target heads, whose CTAs then fit fewer per SM)
+  constexpr int KS128 = 1, KS64 = 2;
+  const int n_vw4 = n_groups - n_vw1 - n_vw2;
+  const AttnGroup* g2 = groups + n_vw1;
+  const AttnGroup* g4 = g2 + n_vw2;
   if (s.hd == 128) {
-    launch_attn<128, 1>(q, k_pool, v_pool, groups, n_small, extra, row_mask, s, sl2, out, st);
-    launch_attn<128, 4>(q, k_pool, v_pool, groups + n_small, n_groups - n_small, extra, row_mask, s, sl2, out, st);
+    launch_attn<128, 1, KS128>(q, k_pool, v_pool, groups, n_vw1, extra, row_mask, s, sl2, out, st);
+    launch_attn<128, 2, KS128>(q, k_pool, v_pool, g2, n_vw2, extra, row_mask, s, sl2, out, st);
+    launch_attn<128, 4, KS128>(q, k_pool, v_pool, g4, n_vw4, extra, row_mask, s, sl2, out, st);
   } else if (s.hd == 64) {
-    launch_attn<64, 1>(q, k_pool, v_pool, groups, n_small, extra, row_mask, s, sl2, out, st);
-    launch_attn<64, 4>(q, k_pool, v_pool, groups + n_small, n_groups - n_small, extra, row_mask, s, sl2, out, st);
+    launch_attn<64, 1, KS64>(q, k_pool, v_pool, groups, n_vw1, extra, row_mask, s, sl2, out, st);
+    launch_attn<64, 2, KS64>(q, k_pool, v_pool, g2, n_vw2, extra, row_mask, s, sl2, out, st);
+    launch_attn<64, 4, KS64>(q, k_pool, v_pool, g4, n_vw4, extra, row_mask, s, sl2, out, st);
   } else {
     throw std::invalid_argument("attention: head dim must be 64 or 128");
   }

@@ -50,9 +50,10 @@ void rope_kv_append(const void* qkv, int rows, int nq, int nkv, int hd, const st
                     cudaStream_t st);
 
 // Grouped attention (causal or masked groups) over the slot pools → out bf16 [rows, nq * hd].
-// groups[0, n_small) must hold at most 16 query vectors (n_rows * n_q / n_kv) each.
+// groups[0, n_vw1) hold at most 16 query vectors (n_rows * n_q / n_kv) each, the next n_vw2 at
+// most 32, the rest any number.
 void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
-               int n_small, const std::int32_t* extra_slots, const unsigned long long* row_mask,
+               int n_vw1, int n_vw2, const std::int32_t* extra_slots, const unsigned long long* row_mask,
                const AttnShape& shape, void* out, cudaStream_t st);
 
 // logits[row, plant[row]] += bias (plant < 0: none) — the planted shared bigram bias.

@@ -238,14 +238,17 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
   const std::size_t o_tok = put(b.tok.data(), n * 4, s_tok);
   const std::size_t o_pos = put(b.pos.data(), n * 4, s_tok);
   const std::size_t o_slot = put(b.slot.data(), n * 4, s_tok);
-  // small groups (<= 16 query vectors: one warp per CTA) first, then the rest (four warps)
+  // groups by query-vector count: <= 16 (one vector warp per CTA), <= 32 (two), more (four)
   const int G = s_.n_q / s_.n_kv;
   grp_sorted_.clear();
   for (const AttnGroup& g : b.groups)
     if (g.n_rows * G <= 16) grp_sorted_.push_back(g);
-  const int n_small = static_cast<int>(grp_sorted_.size());
+  const int n_vw1 = static_cast<int>(grp_sorted_.size());
   for (const AttnGroup& g : b.groups)
-    if (g.n_rows * G > 16) grp_sorted_.push_back(g);
+    if (g.n_rows * G > 16 && g.n_rows * G <= 32) grp_sorted_.push_back(g);
+  const int n_vw2 = static_cast<int>(grp_sorted_.size()) - n_vw1;
+  for (const AttnGroup& g : b.groups)
+    if (g.n_rows * G > 32) grp_sorted_.push_back(g);
   const std::size_t o_grp = put(grp_sorted_.data(), grp_sorted_.size() * sizeof(AttnGroup), s_grp);
   const std::size_t o_ext = put(b.extra.data(), b.extra.size() * 4, s_ext);
   const std::size_t o_out = put(b.out_rows.data(), n_out * 4, s_out);
@@ -287,7 +290,7 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
     qa.norm = consume;
     gemm_tn(with_ws(qa), st);
     prof_.mark(KernelProfiler::kQKV, st);
-    attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()), n_small,
+    attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()), n_vw1, n_vw2,
               I(o_ext), reinterpret_cast<const unsigned long long*>(d_meta_ + o_msk), ash, attn_, st);
     prof_.mark(KernelProfiler::kAttn, st);
     GemmArgs oa{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0};
