@@ -197,17 +197,21 @@ class CallbackBackend : public wsb::ModelBackend {
   }
 
   // WS_EMULATE_LANES=1: the two-lane continuous-batching driver over the callback (CPU tests
-  // of the lanes driver); completions are returned in a scrambled but seeded order.
+  // of the lanes driver); completions are returned in a scrambled but seeded order, and every
+  // batch of more than one job is cut in half (the rest stays pending — partial takes).
   bool has_lanes() const override { return lanes_; }
-  void submit(int lane, const wsb::RoundJobs& jobs, int mode, std::uint64_t seed) override {
+  std::size_t submit(int lane, const wsb::RoundJobs& jobs, int mode, std::uint64_t seed) override {
     wsb::RoundJobs one;
+    const std::size_t n = lane == 0 ? jobs.verify.size() : jobs.draft.size();
+    const std::size_t take = n > 1 ? (n + 1) / 2 : n;
     if (lane == 0) {
-      one.verify = jobs.verify;
+      one.verify.assign(jobs.verify.begin(), jobs.verify.begin() + take);
       one.cands = jobs.cands;
     } else {
-      one.draft = jobs.draft;
+      one.draft.assign(jobs.draft.begin(), jobs.draft.begin() + take);
     }
     run_round(one, done_[lane], mode, seed);
+    return take;
   }
   int wait_any(bool busy0, bool busy1) override {
     if (busy0 && busy1) {

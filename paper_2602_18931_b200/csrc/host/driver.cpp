@@ -419,6 +419,48 @@ class RequestRun {
   std::vector<TokenId> path_tmp_;
 };
 
+// A backend took only jobs [0, took) of a lane batch: the rest go back to the (empty) pending
+// list in order — they lead the lane's next batch, so nothing is deferred twice in a row.
+void requeue_verify(RoundJobs& fly, std::vector<RequestRun*>& fly_slots, std::size_t took, RoundJobs& pend,
+                    std::vector<RequestRun*>& pend_slots) {
+  for (std::size_t j = took; j < fly.verify.size(); ++j) {
+    VerifyJob v = fly.verify[j];
+    const std::uint32_t off = v.cand_off;
+    v.cand_off = static_cast<std::uint32_t>(pend.cands.size());
+    pend.cands.insert(pend.cands.end(), fly.cands.begin() + off, fly.cands.begin() + off + v.k);
+    pend.verify.push_back(v);
+    if (fly.want_ctx) {
+      JobCtx c = fly.verify_ctx[j];
+      const std::uint32_t o = c.off;
+      c.off = static_cast<std::uint32_t>(pend.ctx_tokens.size());
+      pend.ctx_tokens.insert(pend.ctx_tokens.end(), fly.ctx_tokens.begin() + o, fly.ctx_tokens.begin() + o + c.len);
+      pend.verify_ctx.push_back(c);
+    }
+    pend_slots.push_back(fly_slots[j]);
+  }
+  fly.verify.resize(took);
+  if (fly.want_ctx) fly.verify_ctx.resize(took);
+  fly_slots.resize(took);
+}
+
+void requeue_draft(RoundJobs& fly, std::vector<RequestRun::DraftSlot>& fly_slots, std::size_t took, RoundJobs& pend,
+                   std::vector<RequestRun::DraftSlot>& pend_slots) {
+  for (std::size_t j = took; j < fly.draft.size(); ++j) {
+    pend.draft.push_back(fly.draft[j]);
+    if (fly.want_ctx) {
+      JobCtx c = fly.draft_ctx[j];
+      const std::uint32_t o = c.off;
+      c.off = static_cast<std::uint32_t>(pend.ctx_tokens.size());
+      pend.ctx_tokens.insert(pend.ctx_tokens.end(), fly.ctx_tokens.begin() + o, fly.ctx_tokens.begin() + o + c.len);
+      pend.draft_ctx.push_back(c);
+    }
+    pend_slots.push_back(fly_slots[j]);
+  }
+  fly.draft.resize(took);
+  if (fly.want_ctx) fly.draft_ctx.resize(took);
+  fly_slots.resize(took);
+}
+
 // Continuous batching over the backend's two lanes (see ModelBackend).
 void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::size_t n, ModelBackend& backend,
                         RequestOutput* outs, bool log_steps) {
@@ -464,7 +506,8 @@ void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::s
       std::swap(vslots, vslots_fly);
       pend_v.clear();
       vslots.clear();
-      backend.submit(0, fly_v, cfg.verify, cfg.sample_seed);
+      const std::size_t took = backend.submit(0, fly_v, cfg.verify, cfg.sample_seed);
+      if (took < fly_v.verify.size()) requeue_verify(fly_v, vslots_fly, took, pend_v, vslots);
       busy[0] = true;
     }
     if (!busy[1] && !pend_d.draft.empty()) {
@@ -472,7 +515,8 @@ void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::s
       std::swap(dslots, dslots_fly);
       pend_d.clear();
       dslots.clear();
-      backend.submit(1, fly_d, cfg.verify, cfg.sample_seed);
+      const std::size_t took = backend.submit(1, fly_d, cfg.verify, cfg.sample_seed);
+      if (took < fly_d.draft.size()) requeue_draft(fly_d, dslots_fly, took, pend_d, dslots);
       busy[1] = true;
     }
     if (!busy[0] && !busy[1]) throw std::logic_error("driver: requests blocked with no pending model step");
@@ -499,7 +543,7 @@ void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::s
 
 }  // namespace
 
-void ModelBackend::submit(int, const RoundJobs&, int, std::uint64_t) {
+std::size_t ModelBackend::submit(int, const RoundJobs&, int, std::uint64_t) {
   throw std::logic_error("backend has no asynchronous lanes");
 }
 int ModelBackend::wait_any(bool, bool) { throw std::logic_error("backend has no asynchronous lanes"); }

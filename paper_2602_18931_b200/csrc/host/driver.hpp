@@ -93,8 +93,10 @@ class ModelBackend {
   virtual bool wants_context() const { return false; }
   virtual bool has_lanes() const { return false; }
   // lane 0 reads jobs.verify/cands/verify_ctx, lane 1 jobs.draft/draft_ctx (+ ctx_tokens);
-  // `jobs` must stay alive and unchanged until complete(lane).
-  virtual void submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed);
+  // `jobs` must stay alive and unchanged until complete(lane). Returns how many of the lane's
+  // jobs (a prefix) it took; the driver keeps the rest pending for the lane's next batch (a
+  // backend may trim a batch to a tile-friendly size).
+  virtual std::size_t submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed);
   virtual int wait_any(bool busy0, bool busy1);        // blocks until a busy lane is done
   virtual void complete(int lane, RoundResults& res);  // fills res.verify (0) / res.draft (1)
   BackendStats stats;

@@ -225,14 +225,55 @@ void ModelBackend_Llama::fill_ctx(const RoundJobs& jobs, std::uint32_t r, const 
 
 // Lane 0: one target forward over every pending verify row, then the fused K3/K4 greedy
 // verify epilogue; verify outs land in pinned memory.
-void ModelBackend_Llama::submit_verify(const RoundJobs& jobs) {
+// Padding-aware trim of a verify batch: the GEMMs tile rows by 256 (CTA pairs), so a batch a
+// few rows past a multiple of 256 pays a whole extra row block in every projection. When the
+// overflow is at most kSlack rows, the trailing jobs are left for the lane's next batch (they
+// lead it). Rows per job = the context tokens missing from its cache (a read-only LCP pass).
+// WS_VERIFY_TRIM=0 disables.
+std::size_t ModelBackend_Llama::verify_take(const RoundJobs& jobs) {
+  static const bool on = [] {
+    const char* e = std::getenv("WS_VERIFY_TRIM");
+    return !(e && e[0] == '0');
+  }();
+  const std::size_t nv = jobs.verify.size();
+  if (!on || nv < 2) return nv;
+  constexpr std::size_t kUnit = 256, kSlack = 64;
+  ModelPair::Impl& I = *p_->impl;
+  const std::int32_t P = static_cast<std::int32_t>(p_->cfg().prompt_len);
+  std::vector<std::size_t> rows(nv);
+  std::size_t total = 0;
+  for (std::size_t j = 0; j < nv; ++j) {
+    const VerifyJob& vj = jobs.verify[j];
+    const JobCtx& c = jobs.verify_ctx[j];
+    const std::uint32_t r = static_cast<std::uint32_t>(vj.request);
+    const std::vector<TokenId>& prompt = p_->prompt(r);
+    const std::int32_t n_ctx = P + static_cast<std::int32_t>(c.len) + static_cast<std::int32_t>(vj.k);
+    const std::int32_t first = n_ctx - static_cast<std::int32_t>(k_) - 1;
+    const std::vector<TokenId>& valid = I.tgt[r].valid;
+    std::int32_t lcp = 0;
+    auto tok_at = [&](std::int32_t p) -> TokenId {
+      return p < P ? prompt[p] : jobs.ctx_tokens[c.off + (p - P)];
+    };
+    while (lcp < first && lcp < static_cast<std::int32_t>(valid.size()) && valid[lcp] == tok_at(lcp)) ++lcp;
+    rows[j] = static_cast<std::size_t>(n_ctx - lcp);
+    total += rows[j];
+  }
+  const std::size_t over = total % kUnit;
+  if (total <= kUnit || over == 0 || over > kSlack) return nv;
+  const std::size_t cap = total - over;
+  std::size_t acc = 0, take = 0;
+  while (take < nv && acc + rows[take] <= cap) acc += rows[take++];
+  return std::max<std::size_t>(1, take);
+}
+
+void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_take) {
   ModelPair::Impl& I = *p_->impl;
   const ModelPairCfg& cfg = p_->cfg();
   cudaStream_t st = p_->stream();
   const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
   const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
   const std::int32_t V = p_->target().shape().vocab;
-  const std::uint32_t nv = static_cast<std::uint32_t>(jobs.verify.size());
+  const std::uint32_t nv = static_cast<std::uint32_t>(nv_take);
   I.nv = nv;
   if (!nv) return;
   const std::size_t need = static_cast<std::size_t>(nv) * (k_ + 1) + 16;
@@ -538,14 +579,17 @@ cudaStream_t ModelBackend_Llama::draft_stream() const {
   return serial ? p_->stream() : p_->stream_draft();
 }
 
-void ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t) {
+std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t) {
   if (verify_mode != WS_VERIFY_GREEDY)
     throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
   stats.rounds += 1;
-  if (lane == 0)
-    submit_verify(jobs);
-  else
-    submit_draft(jobs);
+  if (lane == 0) {
+    const std::size_t take = verify_take(jobs);
+    submit_verify(jobs, take);
+    return take;
+  }
+  submit_draft(jobs);
+  return jobs.draft.size();
 }
 
 int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
@@ -595,9 +639,12 @@ void ModelBackend_Llama::complete(int lane, RoundResults& res) {
 }
 
 // Lockstep round (WS_LOCKSTEP=1): both lanes, then both results.
-void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t seed) {
-  submit(0, jobs, verify_mode, seed);
-  submit(1, jobs, verify_mode, seed);
+void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t) {
+  if (verify_mode != WS_VERIFY_GREEDY)
+    throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
+  stats.rounds += 1;
+  submit_verify(jobs, jobs.verify.size());  // lockstep rounds take every job
+  submit_draft(jobs);
   complete(0, res);
   complete(1, res);
 }

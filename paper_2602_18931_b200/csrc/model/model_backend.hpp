@@ -47,7 +47,7 @@ class ModelBackend_Llama : public ModelBackend {
   bool wants_context() const override { return true; }
   // lane 0 = target stream (verify), lane 1 = draft stream (worker + controller drafts)
   bool has_lanes() const override { return true; }
-  void submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed) override;
+  std::size_t submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed) override;
   int wait_any(bool busy0, bool busy1) override;
   void complete(int lane, RoundResults& res) override;
   double target_ms = 0, draft_ms = 0;
@@ -58,7 +58,8 @@ class ModelBackend_Llama : public ModelBackend {
 
  private:
   void fill_ctx(const RoundJobs& jobs, std::uint32_t r, const JobCtx& c);
-  void submit_verify(const RoundJobs& jobs);
+  std::size_t verify_take(const RoundJobs& jobs);  // padding-aware batch trim (lanes driver)
+  void submit_verify(const RoundJobs& jobs, std::size_t nv);
   void submit_draft(const RoundJobs& jobs);
   cudaStream_t draft_stream() const;
   ModelPair* p_;
