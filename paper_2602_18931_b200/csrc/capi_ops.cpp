@@ -80,4 +80,12 @@ int ws_op_verify_greedy_bf16(const void* logits, uint32_t n_req, uint32_t k, uin
   });
 }
 
+// Diagnostics (not part of the public header): the K1 timeline recorded under WS_GEMM_ABLATE & 8.
+int ws_debug_gemm_trace(unsigned long long* out8) {
+  return op_guarded("ws_debug_gemm_trace", [&] {
+    if (!out8) throw std::invalid_argument("null argument");
+    wsb::gemm_debug_trace(out8);
+  });
+}
+
 }  // extern "C"

@@ -222,6 +222,18 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, in
   }
 }
 
+// WS_GEMM_ABLATE bit 8: CTA 0 records a %globaltimer timeline of its first unit (diagnostics,
+// read back with ws_debug_gemm_trace): entry, prologue done, dependency wait done, first ring
+// slot full, last MMA of the unit issued, accumulator ready in the epilogue, epilogue done, exit.
+__device__ unsigned long long g_gemm_trace[8];
+__device__ __forceinline__ void trace_point(int ablate, int i) {
+  if ((ablate & 8) && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_trace[i] = t;
+  }
+}
+
 struct SplitArgs {
   int splits = 1;
   float* ws = nullptr;               // fp32 partials [splits][m_blocks*BM][N]
@@ -268,7 +280,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     n_blk = r / S;
   };
 
-  if (threadIdx.x == 0) pdl_trigger();  // the next kernel may start its prologue on free SMs
+  if (threadIdx.x == 0) {
+    pdl_trigger();  // (no-op unless WS_PDL_EARLY)
+    trace_point(ablate, 0);
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -293,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync();  // the peer's barriers exist before any remote signal
   tc_fence_after();
   const std::uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) trace_point(ablate, 1);
 
   if (warp == 0) {
     // TMA producer: the whole warp runs the ring (operands stay warp-uniform), one elected lane
@@ -320,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
     pdl_wait();
+    if (lane == 0) trace_point(ablate, 2);
     int stage = 0, it = 0;
     std::uint32_t phase = 0;
     for (int u = first; u < total; u += step) {
@@ -366,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const std::uint32_t d = tmem_base + acc * kAccStride;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);  // TMA → MMA: both async proxy, ordered by the mbarrier
+          if (local == 0 && kb == kb0 && lane == 0) trace_point(ablate, 3);
           // descriptor start-address field is addr >> 4 (stage offsets are 16-byte multiples)
           const std::uint64_t da = da0 + static_cast<std::uint64_t>((stage * A_BYTES) >> 4);
           const std::uint64_t db = db0 + static_cast<std::uint64_t>((stage * B_BYTES) >> 4);
@@ -396,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             mma_commit(&tfull[acc]);
         }
+        if (local == 0 && lane == 0) trace_point(ablate, 4);
         __syncwarp();
       }
     }
@@ -428,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         rs = rsqrtf(((t0 + t1) + (t2 + t3)) / static_cast<float>(K) + norm.eps);
       }
       mbar_wait(&tfull[acc], (local >> 1) & 1);
+      if (local == 0 && warp == 2 && lane == 0) trace_point(ablate, 5);
       tc_fence_after();
       const std::uint32_t t_row = tmem_base + acc * kAccStride + (static_cast<std::uint32_t>(grp * 32) << 16);
       auto tmem_fetch = [&](int col, std::uint32_t (&r)[32]) {
@@ -440,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       if (S == 1) {
         epilogue_tile<EPI>(tmem_fetch, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
+        if (local == 0 && warp == 2 && lane == 0) trace_point(ablate, 6);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // the accumulator is reused by the (leader's) MMA issuer
@@ -456,7 +477,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         std::uint32_t r[32];
-        tmem_fetch(c, r);
+        tmem_ld32(t_row + c, r);  // raw partial: the norm scale applies once, after the ordered sum
+        tmem_ld_wait();
         if (c < ncols) {
           if (c + 32 <= ncols) {
 #pragma unroll
@@ -511,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(norm.ss_in != nullptr ? v[j] * rs : v[j]);
         };
         epilogue_tile<EPI>(ws_fetch, BN, row, M, N, n_blk, out, ldo, rope, norm);
       }
@@ -520,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_point(ablate, 7);
   if constexpr (CG == 2) {
     cluster_sync();  // neither CTA leaves while its peer's MMAs / signals may still target it
     if (warp == 1) tmem_dealloc_pair<kTmemCols>(tmem_base);
@@ -650,6 +673,10 @@ int pick_bn(int M, int N, int granule) { return pick_tile(M, N, granule, false).
 
 int pick_bn(int M, int N) { return pick_bn(M, N, 32); }
 
+void gemm_debug_trace(unsigned long long* out8) {
+  WS_CUDA(cudaMemcpyFromSymbol(out8, g_gemm_trace, sizeof(unsigned long long) * 8));
+}
+
 int pick_splits(int N, int K) {
   // From (N, K) only — never from M — so results stay batch-invariant. Measured on B200
   // (profiles/r01_splitk.md): at the verify/draft batch sizes the extra partial traffic and the
@@ -683,7 +710,7 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
     if (g.N != (g.rope.nq + 2 * g.rope.nkv) * g.rope.hd) throw std::invalid_argument("gemm: qkv width");
     granule = g.rope.hd;
   }
-  if (g.norm.ss_in && (g.splits > 1 || g.K % 32)) throw std::invalid_argument("gemm: fused norm needs splits 1");
+  if (g.norm.ss_in && g.K % 32) throw std::invalid_argument("gemm: fused norm needs K % 32 == 0");
   if (g.norm.ss && (g.epi != kEpiAddF32 || !g.norm.xb)) throw std::invalid_argument("gemm: norm producer epilogue");
   if (g.norm.ss) granule = 32;  // statistics are per 32-column chunk
   // WS_GEMM_PAIR: "0" keeps every GEMM on single CTAs, "2" forces CTA pairs (tests, A/B)

@@ -62,6 +62,7 @@ struct GemmArgs {
 // C = A · W^T on tcgen05 (sm_100a). Throws on bad shapes / CUDA errors.
 void gemm_tn(const GemmArgs& g, cudaStream_t stream);
 int pick_bn(int M, int N);
+void gemm_debug_trace(unsigned long long* out8);  // WS_GEMM_ABLATE & 8 timeline (diagnostics)
 int pick_splits(int N, int K);
 // Bytes of a split-K workspace serving GEMMs of up to max_rows rows per launch slice.
 std::size_t gemm_workspace_bytes(int max_rows);

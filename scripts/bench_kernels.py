@@ -172,8 +172,57 @@ def ops_pick(M, N):
     return 64
 
 
+def timeline():
+    """WS_GEMM_ABLATE=8: per-phase timeline (ns from kernel entry) of CTA 0's first unit, for
+    small and large M at the 1B O / 8B gate-up shapes, back to back after a warm-up."""
+    import ctypes as C
+    import paper_2602_18931_b200 as ws
+    L = ws.lib()
+    L.ws_debug_gemm_trace.argtypes = [C.c_void_p]
+    names = ["entry", "prologue", "dep_wait", "first_full", "last_mma", "acc_ready", "epi_done", "exit"]
+    for (M, N, K, epi, name) in [(160, 2048, 2048, 1, "1B o M=160"), (655, 2048, 2048, 1, "1B o M=655"),
+                                 (160, 28672, 4096, 2, "8B gate_up M=160"), (530, 28672, 4096, 2, "8B gate_up M=530")]:
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+        out = torch.zeros(M, N, device="cuda", dtype=torch.float32) if epi == 1 else None
+        for _ in range(3):
+            ops.gemm(A, W, out=out, epi=epi)
+        torch.cuda.synchronize()
+        ops.gemm(A, W, out=out, epi=epi)
+        torch.cuda.synchronize()
+        buf = (C.c_ulonglong * 8)()
+        assert L.ws_debug_gemm_trace(buf) == 0
+        t0 = buf[0]
+        print(json.dumps({"gemm": name, **{n: (buf[i] - t0) for i, n in enumerate(names)}}))
+
+
+def splitk():
+    """Deterministic split-K (fixed split count, last split sums the partials in order) vs one
+    pass, for the narrow projections at small (N = 8 GPUs) and full (N = 1) batch rows."""
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    for (N, K, name) in [(2048, 2048, "1B o"), (2048, 8192, "1B down"), (4096, 4096, "8B o"),
+                         (4096, 14336, "8B down")]:
+        for M in (80, 160, 530, 655):
+            A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+            W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+            X = torch.zeros(M, N, device="cuda")
+            res = {}
+            for sp in (1, 2, 4, 8):
+                if K // 64 < 2 * sp:
+                    continue
+                best = None
+                for bn in (64, 128, 256) if sp > 1 else (0,):
+                    t = timeit(lambda: ops.gemm(A, W, out=X, epi=1, bn=bn, splits=sp), flush=flush) * 1e6
+                    best = t if best is None or t < best[0] else best
+                    best = (t, bn) if isinstance(best, float) else best
+                res[sp] = (round(best[0], 1), best[1])
+            print(json.dumps({"shape": name, "M": M, "split_us_bn": res}))
+            sys.stdout.flush()
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "pair":
         pair(" ".join(sys.argv[2:]) or "8B o")
     else:
-        {"gemm": gemm, "gemm_model": gemm_model, "rowstats": rowstats, "one_gemm": one_gemm, "overhead": overhead}[sys.argv[1]]()
+        {"gemm": gemm, "gemm_model": gemm_model, "rowstats": rowstats, "one_gemm": one_gemm, "overhead": overhead,
+         "timeline": timeline, "splitk": splitk}[sys.argv[1]]()
