@@ -39,6 +39,8 @@ def parse():
     p.add_argument("--requests", type=int, default=LLAMA_REQUESTS)
     p.add_argument("--verify", choices=["greedy", "rejection"], default="greedy")
     p.add_argument("--host-threads", type=int, default=0)
+    p.add_argument("--shards", type=int, default=int(os.environ.get("WS_SHARDS", "1")),
+                   help="llama: protocol threads per GPU, each with its own verify/draft streams")
     p.add_argument("--cpu-sample-s", type=float, default=6.0)
     return p.parse_args()
 
@@ -260,6 +262,7 @@ def main():
 
     if args.workload == "llama":
         cfg = llama_cfg(args, world, rank)
+        cfg.host_threads = max(1, args.shards)
         ctx.load_models(abi.model_cfg(max_requests=args.requests))
 
         def run_once(tokens_out=False):

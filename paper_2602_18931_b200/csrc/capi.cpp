@@ -256,6 +256,11 @@ SimCfg sim_cfg_from_abi(const ws_sim_cfg& c) {
 void run_shard(const ws_sim_cfg* c, const SimCfg& cfg, ModelBackend& backend, ws_run_out* out, int device) {
   execute(c, cfg, 1, [&](std::uint32_t) -> ModelBackend& { return backend; }, out, device);
 }
+void run_shard_threads(const ws_sim_cfg* c, const SimCfg& cfg, const std::vector<ModelBackend*>& backends,
+                       ws_run_out* out, int device) {
+  execute(c, cfg, static_cast<std::uint32_t>(backends.size()),
+          [&](std::uint32_t t) -> ModelBackend& { return *backends[t]; }, out, device);
+}
 }  // namespace wsb
 
 extern "C" {

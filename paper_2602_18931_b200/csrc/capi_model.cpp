@@ -1,12 +1,14 @@
 // C ABI of the real-model path (include/wanspec_b200.h "real-model pair").
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "context.hpp"
 #include "kernels/cuda_check.hpp"
@@ -54,6 +56,7 @@ int ws_model_load(ws_ctx* ctx, const ws_model_cfg* c) {
     m.draft_plant_rate = c->draft_plant_rate;
     if (m.prompt_len < 1) throw wsb::ConfigError("prompt_len must be >= 1");
     WS_CUDA(cudaSetDevice(ctx->device));
+    ctx->model_lanes.clear();
     ctx->models.reset();
     ctx->models.reset(new wsb::ModelPair(m, ctx->device));
   });
@@ -74,39 +77,71 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
     WS_CUDA(cudaSetDevice(ctx->device));
     mp.reset_requests();
     const bool prof = std::getenv("WS_PROFILE") != nullptr;
-    mp.target().profiler().enable(prof);
-    mp.draft().profiler().enable(prof);
-    wsb::ModelBackend_Llama backend(&mp, c->oracle.sequence_length, c->oracle.eos_id, c->k);
-    wsb::run_shard(c, cfg, backend, out, ctx->device);
+    // host_threads protocol threads, each with its own backend (streams, workspaces) over a
+    // contiguous range of the shard's requests: small per-thread batches still keep the GPU
+    // busy because the threads' forwards run concurrently.
+    const std::uint32_t local = c->local_requests ? c->local_requests : c->num_requests - c->first_request;
+    const std::uint32_t threads = std::min(std::max<std::uint32_t>(1, c->host_threads), local);
+    auto& owned = ctx->model_lanes;  // created once per thread index, reused across runs
+    while (owned.size() < threads)
+      owned.emplace_back(new wsb::ModelBackend_Llama(&mp, c->oracle.sequence_length, c->oracle.eos_id, c->k));
+    std::vector<wsb::ModelBackend*> backends;
+    std::vector<wsb::ModelBackend_Llama*> used;
+    for (std::uint32_t t = 0; t < threads; ++t) {
+      owned[t]->reset_run(c->oracle.sequence_length, c->oracle.eos_id, c->k);
+      owned[t]->profiler(0).enable(prof);
+      owned[t]->profiler(1).enable(prof);
+      backends.push_back(owned[t].get());
+      used.push_back(owned[t].get());
+    }
+    wsb::run_shard_threads(c, cfg, backends, out, ctx->device);
     if (prof) {
       for (int which = 0; which < 2; ++which) {
-        wsb::KernelProfiler& p = which == 0 ? mp.target().profiler() : mp.draft().profiler();
-        p.collect();
+        double ms[wsb::KernelProfiler::kClasses] = {};
+        unsigned long long cnt[wsb::KernelProfiler::kClasses] = {};
+        for (auto* bk : used) {
+          wsb::KernelProfiler& p = bk->profiler(which);
+          p.collect();
+          for (int k = 0; k < wsb::KernelProfiler::kClasses; ++k) {
+            ms[k] += p.ms[k];
+            cnt[k] += p.count[k];
+            p.ms[k] = 0;
+            p.count[k] = 0;
+          }
+        }
         std::fprintf(stderr, "[ws-profile] {\"model\": \"%s\"", which == 0 ? "target" : "draft");
         for (int k = 0; k < wsb::KernelProfiler::kClasses; ++k)
-          std::fprintf(stderr, ", \"%s\": [%.3f, %llu]", wsb::KernelProfiler::name(k), p.ms[k],
-                       static_cast<unsigned long long>(p.count[k]));
+          std::fprintf(stderr, ", \"%s\": [%.3f, %llu]", wsb::KernelProfiler::name(k), ms[k], cnt[k]);
         std::fprintf(stderr, "}\n");
-        for (int k = 0; k < wsb::KernelProfiler::kClasses; ++k) {
-          p.ms[k] = 0;
-          p.count[k] = 0;
-        }
       }
     }
-    g_last = LastStats{backend.target_ms, backend.draft_ms, backend.target_rows, backend.draft_rows_fed,
-                       backend.target_forwards, backend.draft_forwards};
-    if (std::getenv("WS_DEBUG_ROWS"))
+    LastStats st;
+    std::uint64_t rows_kind[3] = {0, 0, 0}, jobs_kind[3] = {0, 0, 0}, rep_kind[3] = {0, 0, 0};
+    for (auto* bk : used) {
+      st.target_ms += bk->target_ms;
+      st.draft_ms += bk->draft_ms;
+      st.target_rows += bk->target_rows;
+      st.draft_rows += bk->draft_rows_fed;
+      st.target_forwards += bk->target_forwards;
+      st.draft_forwards += bk->draft_forwards;
+      for (int k = 0; k < 3; ++k) {
+        rows_kind[k] += bk->rows_by_kind[k];
+        jobs_kind[k] += bk->jobs_by_kind[k];
+        rep_kind[k] += bk->repeat_by_kind[k];
+      }
+    }
+    g_last = st;
+    if (std::getenv("WS_DEBUG_ROWS")) {
       std::fprintf(stderr,
                    "[ws] target rows %llu in %llu fwd (%.1f ms) | draft rows ctrl %llu / %llu jobs, worker %llu / "
                    "%llu jobs in %llu fwd (%.1f ms)\n",
-                   (unsigned long long)backend.target_rows, (unsigned long long)backend.target_forwards,
-                   backend.target_ms, (unsigned long long)backend.rows_by_kind[1],
-                   (unsigned long long)backend.jobs_by_kind[1], (unsigned long long)backend.rows_by_kind[2],
-                   (unsigned long long)backend.jobs_by_kind[2], (unsigned long long)backend.draft_forwards,
-                   backend.draft_ms);
-    if (std::getenv("WS_DEBUG_ROWS"))
-      std::fprintf(stderr, "[ws] repeated draft contexts: ctrl %llu, worker %llu\n",
-                   (unsigned long long)backend.repeat_by_kind[1], (unsigned long long)backend.repeat_by_kind[2]);
+                   (unsigned long long)st.target_rows, (unsigned long long)st.target_forwards, st.target_ms,
+                   (unsigned long long)rows_kind[1], (unsigned long long)jobs_kind[1],
+                   (unsigned long long)rows_kind[2], (unsigned long long)jobs_kind[2],
+                   (unsigned long long)st.draft_forwards, st.draft_ms);
+      std::fprintf(stderr, "[ws] repeated draft contexts: ctrl %llu, worker %llu\n", (unsigned long long)rep_kind[1],
+                   (unsigned long long)rep_kind[2]);
+    }
   });
 }
 

@@ -15,6 +15,8 @@ struct ws_ctx {
   wsb::DevTables tables;
   std::vector<std::unique_ptr<wsb::OracleLane>> lanes;
   std::unique_ptr<wsb::ModelPair> models;
+  // real-model protocol threads' backends (streams, workspaces), kept across runs
+  std::vector<std::unique_ptr<wsb::ModelBackend_Llama>> model_lanes;
 
   wsb::OracleLane& lane(std::size_t i) {
     while (lanes.size() <= i) lanes.emplace_back(new wsb::OracleLane(&tables, device));
@@ -27,4 +29,7 @@ int ops_guarded_rc(const char* what, const std::exception& e);
 // Shared by capi.cpp / capi_model.cpp: SimConfig validation + conversion and the shard runner.
 SimCfg sim_cfg_from_abi(const ws_sim_cfg& c);
 void run_shard(const ws_sim_cfg* c, const SimCfg& cfg, ModelBackend& backend, ws_run_out* out, int device);
+// One protocol thread per backend, each over a contiguous range of the shard's requests.
+void run_shard_threads(const ws_sim_cfg* c, const SimCfg& cfg, const std::vector<ModelBackend*>& backends,
+                       ws_run_out* out, int device);
 }  // namespace wsb

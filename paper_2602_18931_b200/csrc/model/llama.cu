@@ -128,41 +128,55 @@ LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_s
   WS_CUDA(cudaMalloc(&v_pool_, pool));
   WS_CUDA(cudaMemset(k_pool_, 0, pool));
   WS_CUDA(cudaMemset(v_pool_, 0, pool));
-  ensure_rows(max_rows, max_rows);
-  gemm_ws_bytes_ = gemm_workspace_bytes(4096);  // split-K partials (row-sliced beyond 4096 rows)
-  WS_CUDA(cudaMalloc(&gemm_ws_, gemm_ws_bytes_));
-  WS_CUDA(cudaMemset(gemm_ws_, 0, gemm_ws_bytes_));
+  ws0_ = make_workspace(max_rows);
   WS_CUDA(cudaDeviceSynchronize());
+}
+
+std::unique_ptr<ForwardWorkspace> LlamaModel::make_workspace(int max_rows) const {
+  WS_CUDA(cudaSetDevice(device_));
+  std::unique_ptr<ForwardWorkspace> ws(new ForwardWorkspace(device_));
+  ensure_rows(*ws, max_rows, max_rows);
+  ws->gemm_ws_bytes = gemm_workspace_bytes(4096);  // split-K partials (row-sliced beyond 4096 rows)
+  WS_CUDA(cudaMalloc(&ws->gemm_ws, ws->gemm_ws_bytes));
+  WS_CUDA(cudaMemset(ws->gemm_ws, 0, ws->gemm_ws_bytes));
+  return ws;
+}
+
+ForwardWorkspace::~ForwardWorkspace() {
+  cudaSetDevice(device);
+  for (void* p : {static_cast<void*>(x), xb, static_cast<void*>(ss), qkv, q, attn, h, logits, xo,
+                  static_cast<void*>(d_meta), gemm_ws})
+    if (p) cudaFree(p);
+  if (h_meta) cudaFreeHost(h_meta);
 }
 
 LlamaModel::~LlamaModel() {
   cudaSetDevice(device_);
   if (rope_cs_) cudaFree(rope_cs_);
-  if (gemm_ws_) cudaFree(gemm_ws_);
-  for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_, static_cast<void*>(x_), xb_,
-                  static_cast<void*>(ss_), qkv_, q_, attn_, h_, logits_, xo_, static_cast<void*>(d_meta_)})
+  ws0_.reset();
+  for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_})
     if (p) cudaFree(p);
-  if (h_meta_) cudaFreeHost(h_meta_);
 }
 
-void LlamaModel::ensure_rows(int rows, int out_rows) {
-  if (rows <= cap_rows_ && out_rows <= cap_out_) return;
-  rows = std::max(rows, cap_rows_);
-  out_rows = std::max(out_rows, cap_out_);
-  for (void* p : {static_cast<void*>(x_), xb_, static_cast<void*>(ss_), qkv_, q_, attn_, h_, logits_, xo_})
+void LlamaModel::ensure_rows(ForwardWorkspace& ws, int rows, int out_rows) const {
+  if (rows <= ws.cap_rows && out_rows <= ws.cap_out) return;
+  rows = std::max(rows, ws.cap_rows);
+  out_rows = std::max(out_rows, ws.cap_out);
+  for (void* p : {static_cast<void*>(ws.x), ws.xb, static_cast<void*>(ws.ss), ws.qkv, ws.q, ws.attn, ws.h, ws.logits,
+                  ws.xo})
     if (p) cudaFree(p);
   const std::size_t R = rows, O = out_rows;
-  WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&x_), R * s_.d * 4));
-  WS_CUDA(cudaMalloc(&xb_, R * s_.d * 2));
-  WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&ss_), R * (s_.d / 32) * 4));
-  WS_CUDA(cudaMalloc(&qkv_, R * s_.qkv_dim() * 2));
-  WS_CUDA(cudaMalloc(&q_, R * s_.n_q * s_.hd * 2));
-  WS_CUDA(cudaMalloc(&attn_, R * s_.n_q * s_.hd * 2));
-  WS_CUDA(cudaMalloc(&h_, R * s_.ffn * 2));
-  WS_CUDA(cudaMalloc(&xo_, O * s_.d * 2));
-  WS_CUDA(cudaMalloc(&logits_, O * static_cast<std::size_t>(s_.vocab) * 2));
-  cap_rows_ = rows;
-  cap_out_ = out_rows;
+  WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&ws.x), R * s_.d * 4));
+  WS_CUDA(cudaMalloc(&ws.xb, R * s_.d * 2));
+  WS_CUDA(cudaMalloc(reinterpret_cast<void**>(&ws.ss), R * (s_.d / 32) * 4));
+  WS_CUDA(cudaMalloc(&ws.qkv, R * s_.qkv_dim() * 2));
+  WS_CUDA(cudaMalloc(&ws.q, R * s_.n_q * s_.hd * 2));
+  WS_CUDA(cudaMalloc(&ws.attn, R * s_.n_q * s_.hd * 2));
+  WS_CUDA(cudaMalloc(&ws.h, R * s_.ffn * 2));
+  WS_CUDA(cudaMalloc(&ws.xo, O * s_.d * 2));
+  WS_CUDA(cudaMalloc(&ws.logits, O * static_cast<std::size_t>(s_.vocab) * 2));
+  ws.cap_rows = rows;
+  ws.cap_out = out_rows;
 }
 
 void* LlamaModel::weight(const std::string& w, int l, std::int64_t* numel) {
@@ -185,8 +199,12 @@ void* LlamaModel::weight(const std::string& w, int l, std::int64_t* numel) {
 }
 
 void LlamaModel::copy_slots(const std::vector<std::int32_t>& src, const std::vector<std::int32_t>& dst,
-                            cudaStream_t st) {
+                            cudaStream_t st, ForwardWorkspace& ws) {
   if (src.empty()) return;
+  unsigned char*& d_meta_ = ws.d_meta;
+  unsigned char*& h_meta_ = ws.h_meta;
+  std::size_t& cap_meta_ = ws.cap_meta;
+  std::size_t& h2d_ = ws.h2d;
   const std::size_t n = src.size();
   const std::size_t need = 2 * n * 4;
   if (need > cap_meta_) {
@@ -207,14 +225,31 @@ void LlamaModel::copy_slots(const std::vector<std::int32_t>& src, const std::vec
   WS_CUDA(cudaStreamSynchronize(st));
 }
 
-void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st) {
+void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, ForwardWorkspace& ws) {
   const int n = static_cast<int>(b.tok.size());
   const int n_out = static_cast<int>(b.out_rows.size());
   if (n == 0) return;
   if (b.pos.size() != b.tok.size() || b.slot.size() != b.tok.size()) throw std::invalid_argument("forward: ragged rows");
   for (std::int32_t p : b.pos)
     if (p < 0 || p >= kMaxPos) throw std::invalid_argument("forward: position out of the RoPE table range");
-  ensure_rows(n, n_out);
+  ensure_rows(ws, n, n_out);
+  float* const x_ = ws.x;
+  void* const xb_ = ws.xb;
+  float* const ss_ = ws.ss;
+  void* const q_ = ws.q;
+  void* const attn_ = ws.attn;
+  void* const h_ = ws.h;
+  void* const logits_ = ws.logits;
+  void* const xo_ = ws.xo;
+  unsigned char*& d_meta_ = ws.d_meta;
+  unsigned char*& h_meta_ = ws.h_meta;
+  std::size_t& cap_meta_ = ws.cap_meta;
+  std::size_t& h2d_ = ws.h2d;
+  std::vector<AttnGroup>& grp_sorted_ = ws.grp_sorted;
+  KernelProfiler& prof_ = ws.prof;
+  const int cap_rows_ = ws.cap_rows;
+  void* const gemm_ws_ = ws.gemm_ws;
+  const std::size_t gemm_ws_bytes_ = ws.gemm_ws_bytes;
   // ---- one packed H2D for all metadata ----
   const std::size_t s_tok = al(n * 4), s_grp = al(b.groups.size() * sizeof(AttnGroup)), s_ext = al(b.extra.size() * 4 + 4),
                     s_out = al(n_out * 4 + 4);

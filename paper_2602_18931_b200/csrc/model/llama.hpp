@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -70,9 +71,38 @@ class KernelProfiler {
   std::vector<std::pair<int, cudaEvent_t>> marks_;
 };
 
+// Activation state of one caller's forwards: several callers (protocol threads, each with its
+// own streams) run forwards of the same model concurrently — weights and KV pools are shared,
+// these buffers are not.
+struct ForwardWorkspace {
+  explicit ForwardWorkspace(int dev) : device(dev) {}
+  ~ForwardWorkspace();
+  ForwardWorkspace(const ForwardWorkspace&) = delete;
+  ForwardWorkspace& operator=(const ForwardWorkspace&) = delete;
+  int device;
+  int cap_rows = 0, cap_out = 0;
+  float* x = nullptr;   // fp32 residual stream [rows][d]
+  void* xb = nullptr;   // its bf16 copy (A of the normed projections) [rows][d]
+  float* ss = nullptr;  // per-32-column-chunk sums of squares (fused RMSNorm), chunk-major
+  void* qkv = nullptr;
+  void* q = nullptr;
+  void* attn = nullptr;
+  void* h = nullptr;
+  void* logits = nullptr;
+  void* xo = nullptr;
+  unsigned char* d_meta = nullptr;  // batch metadata (device) + pinned staging
+  unsigned char* h_meta = nullptr;
+  std::size_t cap_meta = 0;
+  void* gemm_ws = nullptr;  // split-K workspace (K1)
+  std::size_t gemm_ws_bytes = 0;
+  std::vector<AttnGroup> grp_sorted;
+  std::size_t h2d = 0;
+  KernelProfiler prof;
+};
+
 class LlamaModel {
  public:
-  KernelProfiler& profiler() { return prof_; }
+  KernelProfiler& profiler() { return ws0_->prof; }
   // Cap on the persistent GEMM grids (0 = every SM): leaves SMs to a concurrent forward.
   void set_max_ctas(int n) { max_ctas_ = n; }
   LlamaModel(const LlamaShape& shape, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device);
@@ -84,11 +114,17 @@ class LlamaModel {
   std::int64_t n_slots() const { return n_slots_; }
 
   // Uploads the batch (one H2D of a packed block) and runs the forward; logits of the
-  // out_rows (bf16 [n_out, vocab]) land in logits(). plant_bias > 0 adds the planted bias.
-  void forward(const ForwardBatch& b, float plant_bias, cudaStream_t st);
-  const void* logits() const { return logits_; }
-  std::size_t h2d_bytes() const { return h2d_; }
-  void copy_slots(const std::vector<std::int32_t>& src, const std::vector<std::int32_t>& dst, cudaStream_t st);
+  // out_rows (bf16 [n_out, vocab]) land in ws.logits. plant_bias > 0 adds the planted bias.
+  void forward(const ForwardBatch& b, float plant_bias, cudaStream_t st, ForwardWorkspace& ws);
+  void forward(const ForwardBatch& b, float plant_bias, cudaStream_t st) { forward(b, plant_bias, st, *ws0_); }
+  const void* logits() const { return ws0_->logits; }
+  std::size_t h2d_bytes() const { return ws0_->h2d; }
+  void copy_slots(const std::vector<std::int32_t>& src, const std::vector<std::int32_t>& dst, cudaStream_t st,
+                  ForwardWorkspace& ws);
+  void copy_slots(const std::vector<std::int32_t>& src, const std::vector<std::int32_t>& dst, cudaStream_t st) {
+    copy_slots(src, dst, st, *ws0_);
+  }
+  std::unique_ptr<ForwardWorkspace> make_workspace(int max_rows) const;
 
   // weight access for tests: which = "embed","attn_norm","wqkv","wo","mlp_norm","wgu","wdown","final_norm","lm_head"
   void* weight(const std::string& which, int layer, std::int64_t* numel);
@@ -96,13 +132,12 @@ class LlamaModel {
   void* v_pool() const { return v_pool_; }
 
  private:
-  void ensure_rows(int rows, int out_rows);
-  KernelProfiler prof_;
+  void ensure_rows(ForwardWorkspace& ws, int rows, int out_rows) const;
+  std::unique_ptr<ForwardWorkspace> ws0_;  // the model's own workspace (test / single-caller API)
   int max_ctas_ = 0;
   LlamaShape s_;
   int device_;
   std::int64_t n_slots_;
-  int cap_rows_ = 0, cap_out_ = 0;
   // weights
   void* embed_ = nullptr;
   void* lm_head_ = nullptr;
@@ -111,28 +146,10 @@ class LlamaModel {
   void* weight_block_ = nullptr;
   float* inv_freq_ = nullptr;
   float2* rope_cs_ = nullptr;  // [kMaxPos][hd/2] cos/sin
-  std::vector<AttnGroup> grp_sorted_;
-  void* gemm_ws_ = nullptr;    // split-K workspace (K1)
-  std::size_t gemm_ws_bytes_ = 0;
   static constexpr int kMaxPos = 4096;
   // KV pools [layer][slot][n_kv][hd]
   void* k_pool_ = nullptr;
   void* v_pool_ = nullptr;
-  // activations
-  float* x_ = nullptr;   // fp32 residual stream [rows][d]
-  void* xb_ = nullptr;   // its bf16 copy (A of the normed projections) [rows][d]
-  float* ss_ = nullptr;  // per-32-column-chunk sums of squares (fused RMSNorm) [rows][d/32]
-  void* qkv_ = nullptr;
-  void* q_ = nullptr;
-  void* attn_ = nullptr;
-  void* h_ = nullptr;
-  void* logits_ = nullptr;
-  void* xo_ = nullptr;
-  // batch metadata (device) + pinned staging
-  unsigned char* d_meta_ = nullptr;
-  unsigned char* h_meta_ = nullptr;
-  std::size_t cap_meta_ = 0;
-  std::size_t h2d_ = 0;
 };
 
 }  // namespace wsb

@@ -110,7 +110,16 @@ struct TreeCache {
 struct ModelPair::Impl {
   std::vector<LinearCache> tgt, ctrl;
   std::vector<TreeCache> wrk;
-  // verify lane (target stream): K3/K4 buffers, pinned staging and results
+};
+
+// One protocol thread's GPU state: its two lanes' streams and forward workspaces, K3/K4
+// buffers, pinned staging and results. Several backends share one ModelPair (weights, KV
+// pools, per-request caches) and serve disjoint request ranges concurrently.
+struct ModelBackend_Llama::Lanes {
+  int device = 0;
+  cudaStream_t st_t = nullptr, st_d = nullptr;  // verify (target) / draft streams
+  std::unique_ptr<ForwardWorkspace> ws_t, ws_d;
+  // verify lane
   ws_pred* d_pred = nullptr;
   ws_verify_out* d_vout = nullptr;
   std::uint32_t* d_cands = nullptr;
@@ -119,7 +128,7 @@ struct ModelPair::Impl {
   unsigned char* h_stage = nullptr;
   ws_verify_out* h_vout = nullptr;
   std::size_t cap_v = 0;
-  // draft lane (draft stream): the two lanes run concurrently, so nothing is shared
+  // draft lane
   ws_pred* d_pred_d = nullptr;
   void* d_ws_d = nullptr;
   ws_pred* h_pred_d = nullptr;
@@ -130,51 +139,40 @@ struct ModelPair::Impl {
   std::uint32_t nv = 0, nd = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   cudaEvent_t done[2] = {nullptr, nullptr};  // after each lane's result D2H
+  ~Lanes() {
+    cudaSetDevice(device);
+    for (void* q : {static_cast<void*>(d_pred), static_cast<void*>(d_vout), static_cast<void*>(d_cands),
+                    static_cast<void*>(d_forced), d_ws, static_cast<void*>(d_pred_d), d_ws_d})
+      if (q) cudaFree(q);
+    for (void* q : {static_cast<void*>(h_stage), static_cast<void*>(h_vout), static_cast<void*>(h_pred_d)})
+      if (q) cudaFreeHost(q);
+    for (cudaEvent_t e : {e0, e1, e2, e3, done[0], done[1]})
+      if (e) cudaEventDestroy(e);
+    ws_t.reset();
+    ws_d.reset();
+    if (st_t) cudaStreamDestroy(st_t);
+    if (st_d) cudaStreamDestroy(st_d);
+  }
 };
 
 ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(device), impl(new Impl) {
   WS_CUDA(cudaSetDevice(device));
-  // The draft lane is the critical path of the continuous-batching loop (requests mostly wait
-  // on draft results), so its stream gets the higher scheduling priority; the verify lane's
-  // large GEMMs fill the SMs it leaves idle. WS_DRAFT_PRIO=0 gives both lanes equal priority.
-  int prio_lo = 0, prio_hi = 0;
-  WS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  const char* dp = std::getenv("WS_DRAFT_PRIO");
-  const bool draft_first = !(dp && dp[0] == '0');
-  WS_CUDA(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_lo));
-  WS_CUDA(cudaStreamCreateWithPriority(&stream_draft_, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
   const LlamaShape ts = shape_by_name(cfg.target), ds = shape_by_name(cfg.draft);
   if (ts.vocab != ds.vocab) throw ConfigError("target and draft vocabularies differ");
   const std::int64_t R = cfg.max_requests, C = cfg.max_ctx;
-  const int max_rows = static_cast<int>(std::min<std::int64_t>(R * 20, 8192));
-  target_.reset(new LlamaModel(ts, cfg.seed * 2 + 1, R * C, max_rows, device));
-  draft_.reset(new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows, device));
+  max_rows_ = static_cast<int>(std::min<std::int64_t>(R * 20, 8192));
+  target_.reset(new LlamaModel(ts, cfg.seed * 2 + 1, R * C, max_rows_, device));
+  draft_.reset(new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows_, device));
   prompts_.resize(cfg.max_requests);
   if (const char* e = std::getenv("WS_TARGET_CTAS")) target_->set_max_ctas(std::atoi(e));
   if (const char* e = std::getenv("WS_DRAFT_CTAS")) draft_->set_max_ctas(std::atoi(e));
-  WS_CUDA(cudaEventCreate(&impl->e0));
-  WS_CUDA(cudaEventCreate(&impl->e1));
-  WS_CUDA(cudaEventCreate(&impl->e2));
-  WS_CUDA(cudaEventCreate(&impl->e3));
-  WS_CUDA(cudaEventCreateWithFlags(&impl->done[0], cudaEventDisableTiming));
-  WS_CUDA(cudaEventCreateWithFlags(&impl->done[1], cudaEventDisableTiming));
   reset_requests();
 }
 
 ModelPair::~ModelPair() {
   cudaSetDevice(device_);
-  Impl& I = *impl;
-  for (void* p : {static_cast<void*>(I.d_pred), static_cast<void*>(I.d_vout), static_cast<void*>(I.d_cands),
-                  static_cast<void*>(I.d_forced), I.d_ws, static_cast<void*>(I.d_pred_d), I.d_ws_d})
-    if (p) cudaFree(p);
-  for (void* p : {static_cast<void*>(I.h_stage), static_cast<void*>(I.h_vout), static_cast<void*>(I.h_pred_d)})
-    if (p) cudaFreeHost(p);
-  for (cudaEvent_t e : {I.e0, I.e1, I.e2, I.e3, I.done[0], I.done[1]})
-    if (e) cudaEventDestroy(e);
   target_.reset();
   draft_.reset();
-  if (stream_) cudaStreamDestroy(stream_);
-  if (stream_draft_) cudaStreamDestroy(stream_draft_);
 }
 
 void ModelPair::reset_requests() {
@@ -205,8 +203,45 @@ std::int32_t ModelPair::plant(TokenId t, bool is_draft) const {
 }
 
 ModelBackend_Llama::ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, TokenId eos, std::uint32_t k)
-    : p_(pair), L_(seq_len), eos_(eos), k_(k) {}
+    : p_(pair), L_(seq_len), eos_(eos), k_(k), ln_(new Lanes) {
+  Lanes& L = *ln_;
+  L.device = pair->device();
+  WS_CUDA(cudaSetDevice(L.device));
+  // The draft lane is the critical path of the continuous-batching loop (requests mostly wait
+  // on draft results), so its stream gets the higher scheduling priority; the verify lane's
+  // large GEMMs fill the SMs it leaves idle. WS_DRAFT_PRIO=0 gives both lanes equal priority.
+  int prio_lo = 0, prio_hi = 0;
+  WS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  const char* dp = std::getenv("WS_DRAFT_PRIO");
+  const bool draft_first = !(dp && dp[0] == '0');
+  WS_CUDA(cudaStreamCreateWithPriority(&L.st_t, cudaStreamNonBlocking, prio_lo));
+  WS_CUDA(cudaStreamCreateWithPriority(&L.st_d, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
+  // workspaces grow to the batch sizes actually seen (a cap of max_rows each would be GBs of
+  // logits per protocol thread)
+  L.ws_t = pair->target().make_workspace(64);
+  L.ws_d = pair->draft().make_workspace(64);
+  WS_CUDA(cudaEventCreate(&L.e0));
+  WS_CUDA(cudaEventCreate(&L.e1));
+  WS_CUDA(cudaEventCreate(&L.e2));
+  WS_CUDA(cudaEventCreate(&L.e3));
+  WS_CUDA(cudaEventCreateWithFlags(&L.done[0], cudaEventDisableTiming));
+  WS_CUDA(cudaEventCreateWithFlags(&L.done[1], cudaEventDisableTiming));
+}
 ModelBackend_Llama::~ModelBackend_Llama() = default;
+
+void ModelBackend_Llama::reset_run(std::uint32_t seq_len, TokenId eos, std::uint32_t k) {
+  L_ = seq_len;
+  eos_ = eos;
+  if (k != k_) ln_->cap_v = 0;  // candidate staging is sized by k: regrow on the next batch
+  k_ = k;
+  stats = BackendStats{};
+  target_ms = draft_ms = 0;
+  target_rows = draft_rows_fed = target_forwards = draft_forwards = 0;
+  for (int i = 0; i < 3; ++i) rows_by_kind[i] = jobs_by_kind[i] = repeat_by_kind[i] = 0;
+  seen_ctx_.clear();
+}
+
+KernelProfiler& ModelBackend_Llama::profiler(int which) { return which == 0 ? ln_->ws_t->prof : ln_->ws_d->prof; }
 
 namespace {
 // Row at context position pos predicts committed index pos + 1 - P; past the generation cap
@@ -218,9 +253,10 @@ inline std::int32_t forced_at(std::int32_t pos, std::int32_t P, std::uint32_t L,
 
 void ModelBackend_Llama::fill_ctx(const RoundJobs& jobs, std::uint32_t r, const JobCtx& c) {
   ModelPair::Impl& I = *p_->impl;
+  Lanes& L = *ln_;
   const std::vector<TokenId>& prompt = p_->prompt(r);
-  I.ctx.assign(prompt.begin(), prompt.end());
-  I.ctx.insert(I.ctx.end(), jobs.ctx_tokens.begin() + c.off, jobs.ctx_tokens.begin() + c.off + c.len);
+  L.ctx.assign(prompt.begin(), prompt.end());
+  L.ctx.insert(L.ctx.end(), jobs.ctx_tokens.begin() + c.off, jobs.ctx_tokens.begin() + c.off + c.len);
 }
 
 // Lane 0: one target forward over every pending verify row, then the fused K3/K4 greedy
@@ -239,6 +275,7 @@ std::size_t ModelBackend_Llama::verify_take(const RoundJobs& jobs) {
   if (!on || nv < 2) return nv;
   constexpr std::size_t kUnit = 256, kSlack = 64;
   ModelPair::Impl& I = *p_->impl;
+  Lanes& L = *ln_;
   const std::int32_t P = static_cast<std::int32_t>(p_->cfg().prompt_len);
   std::vector<std::size_t> rows(nv);
   std::size_t total = 0;
@@ -268,54 +305,55 @@ std::size_t ModelBackend_Llama::verify_take(const RoundJobs& jobs) {
 
 void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_take) {
   ModelPair::Impl& I = *p_->impl;
+  Lanes& L = *ln_;
   const ModelPairCfg& cfg = p_->cfg();
-  cudaStream_t st = p_->stream();
+  cudaStream_t st = L.st_t;
   const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
   const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
   const std::int32_t V = p_->target().shape().vocab;
   const std::uint32_t nv = static_cast<std::uint32_t>(nv_take);
-  I.nv = nv;
+  L.nv = nv;
   if (!nv) return;
   const std::size_t need = static_cast<std::size_t>(nv) * (k_ + 1) + 16;
-  if (need > I.cap_v) {  // the lane is idle here (the driver submits only to idle lanes)
-    for (void* q : {static_cast<void*>(I.d_pred), static_cast<void*>(I.d_vout), static_cast<void*>(I.d_cands),
-                    static_cast<void*>(I.d_forced), I.d_ws})
+  if (need > L.cap_v) {  // the lane is idle here (the driver submits only to idle lanes)
+    for (void* q : {static_cast<void*>(L.d_pred), static_cast<void*>(L.d_vout), static_cast<void*>(L.d_cands),
+                    static_cast<void*>(L.d_forced), L.d_ws})
       if (q) cudaFree(q);
-    for (void* q : {static_cast<void*>(I.h_stage), static_cast<void*>(I.h_vout)})
+    for (void* q : {static_cast<void*>(L.h_stage), static_cast<void*>(L.h_vout)})
       if (q) cudaFreeHost(q);
-    I.cap_v = need * 2;
-    WS_CUDA(cudaMalloc(&I.d_pred, I.cap_v * sizeof(ws_pred)));
-    WS_CUDA(cudaMalloc(&I.d_vout, I.cap_v * sizeof(ws_verify_out)));
-    WS_CUDA(cudaMalloc(&I.d_cands, I.cap_v * k_ * 4 + 64));
-    WS_CUDA(cudaMalloc(&I.d_forced, I.cap_v * 4));
-    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(I.cap_v), V,
-                                                      static_cast<std::uint32_t>(I.cap_v));
-    WS_CUDA(cudaMalloc(&I.d_ws, wsb_));
-    WS_CUDA(cudaMemset(I.d_ws, 0, wsb_));
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_vout), I.cap_v * sizeof(ws_verify_out),
+    L.cap_v = need * 2;
+    WS_CUDA(cudaMalloc(&L.d_pred, L.cap_v * sizeof(ws_pred)));
+    WS_CUDA(cudaMalloc(&L.d_vout, L.cap_v * sizeof(ws_verify_out)));
+    WS_CUDA(cudaMalloc(&L.d_cands, L.cap_v * k_ * 4 + 64));
+    WS_CUDA(cudaMalloc(&L.d_forced, L.cap_v * 4));
+    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(L.cap_v), V,
+                                                      static_cast<std::uint32_t>(L.cap_v));
+    WS_CUDA(cudaMalloc(&L.d_ws, wsb_));
+    WS_CUDA(cudaMemset(L.d_ws, 0, wsb_));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&L.h_vout), L.cap_v * sizeof(ws_verify_out),
                           cudaHostAllocDefault));
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_stage), I.cap_v * (k_ * 4 + 8) + 256, cudaHostAllocDefault));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&L.h_stage), L.cap_v * (k_ * 4 + 8) + 256, cudaHostAllocDefault));
   }
-  ForwardBatch& b = I.tb;
+  ForwardBatch& b = L.tb;
   b.clear();
-  I.forced.assign(static_cast<std::size_t>(nv) * (k_ + 1), -1);
-  std::uint32_t* hc = reinterpret_cast<std::uint32_t*>(I.h_stage);
+  L.forced.assign(static_cast<std::size_t>(nv) * (k_ + 1), -1);
+  std::uint32_t* hc = reinterpret_cast<std::uint32_t*>(L.h_stage);
   for (std::uint32_t j = 0; j < nv; ++j) {
     const VerifyJob& vj = jobs.verify[j];
     const std::uint32_t r = static_cast<std::uint32_t>(vj.request);
     fill_ctx(jobs, r, jobs.verify_ctx[j]);
-    I.ctx.insert(I.ctx.end(), jobs.cands.begin() + vj.cand_off, jobs.cands.begin() + vj.cand_off + vj.k);
-    const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
+    L.ctx.insert(L.ctx.end(), jobs.cands.begin() + vj.cand_off, jobs.cands.begin() + vj.cand_off + vj.k);
+    const std::int32_t n_ctx = static_cast<std::int32_t>(L.ctx.size());
     const std::int32_t first = n_ctx - static_cast<std::int32_t>(k_) - 1;  // = P + base - 1
     if (n_ctx > MC) throw ConfigError("model path: verify context " + std::to_string(n_ctx) + " exceeds max_ctx");
     LinearCache& c = I.tgt[r];
     std::int32_t lcp = 0;
-    while (lcp < first && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
+    while (lcp < first && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == L.ctx[lcp]) ++lcp;
     const std::int32_t base_slot = static_cast<std::int32_t>(r) * MC;
     const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
     const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
     for (std::int32_t p = lcp; p < n_ctx; ++p) {
-      b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
+      b.tok.push_back(static_cast<std::int32_t>(L.ctx[p]));
       b.pos.push_back(p);
       b.slot.push_back(base_slot + p);
       b.extra.push_back(base_slot + p);
@@ -324,26 +362,26 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
     b.row_mask.resize(b.tok.size(), 0ull);
     for (std::int32_t p = first; p < n_ctx; ++p) {
       b.out_rows.push_back(row0 + p - lcp);
-      b.plant.push_back(p_->plant(I.ctx[p], false));
-      I.forced[j * (k_ + 1) + (p - first)] = forced_at(p, P, L_, eos_);
+      b.plant.push_back(p_->plant(L.ctx[p], false));
+      L.forced[j * (k_ + 1) + (p - first)] = forced_at(p, P, L_, eos_);
     }
-    c.valid.assign(I.ctx.begin(), I.ctx.end());
+    c.valid.assign(L.ctx.begin(), L.ctx.end());
     std::memcpy(hc + j * k_, jobs.cands.data() + vj.cand_off, k_ * 4);
   }
-  std::memcpy(hc + nv * k_, I.forced.data(), I.forced.size() * 4);
-  WS_CUDA(cudaMemcpyAsync(I.d_cands, hc, nv * k_ * 4, cudaMemcpyHostToDevice, st));
-  WS_CUDA(cudaMemcpyAsync(I.d_forced, hc + nv * k_, I.forced.size() * 4, cudaMemcpyHostToDevice, st));
-  WS_CUDA(cudaEventRecord(I.e0, st));
-  p_->target().forward(b, cfg.plant_target, st);
-  row_stats_bf16(p_->target().logits(), nv * (k_ + 1), V, V, 1.0f, I.d_pred, nullptr, I.d_ws, nv, k_, I.d_cands,
-                 I.d_vout, st, I.d_forced);
-  WS_CUDA(cudaEventRecord(I.e1, st));
-  WS_CUDA(cudaMemcpyAsync(I.h_vout, I.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
-  WS_CUDA(cudaEventRecord(I.done[0], st));
+  std::memcpy(hc + nv * k_, L.forced.data(), L.forced.size() * 4);
+  WS_CUDA(cudaMemcpyAsync(L.d_cands, hc, nv * k_ * 4, cudaMemcpyHostToDevice, st));
+  WS_CUDA(cudaMemcpyAsync(L.d_forced, hc + nv * k_, L.forced.size() * 4, cudaMemcpyHostToDevice, st));
+  WS_CUDA(cudaEventRecord(L.e0, st));
+  p_->target().forward(b, cfg.plant_target, st, *L.ws_t);
+  row_stats_bf16(L.ws_t->logits, nv * (k_ + 1), V, V, 1.0f, L.d_pred, nullptr, L.d_ws, nv, k_, L.d_cands,
+                 L.d_vout, st, L.d_forced);
+  WS_CUDA(cudaEventRecord(L.e1, st));
+  WS_CUDA(cudaMemcpyAsync(L.h_vout, L.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaEventRecord(L.done[0], st));
   target_rows += b.tok.size();
   target_forwards += 1;
   stats.launches += 1 + 8ull * p_->target().shape().layers + 4;
-  stats.h2d += nv * k_ * 4 + I.forced.size() * 4;
+  stats.h2d += nv * k_ * 4 + L.forced.size() * 4;
   stats.d2h += nv * sizeof(ws_verify_out);
   stats.verify_rows += nv;
 }
@@ -352,32 +390,33 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
 // groups, controller local drafts / catch-up as causal groups), then K3/K4 row statistics.
 void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
   ModelPair::Impl& I = *p_->impl;
+  Lanes& L = *ln_;
   const ModelPairCfg& cfg = p_->cfg();
   const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
   const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
   const std::int32_t V = p_->draft().shape().vocab;
   const std::uint32_t nd = static_cast<std::uint32_t>(jobs.draft.size());
-  I.nd = nd;
+  L.nd = nd;
   draft_ran_ = false;
   if (!nd) return;
   ++draft_batch_;
   const std::size_t need = static_cast<std::size_t>(nd) + 16;
-  if (need > I.cap_d) {
-    for (void* q : {static_cast<void*>(I.d_pred_d), I.d_ws_d})
+  if (need > L.cap_d) {
+    for (void* q : {static_cast<void*>(L.d_pred_d), L.d_ws_d})
       if (q) cudaFree(q);
-    if (I.h_pred_d) cudaFreeHost(I.h_pred_d);
-    I.cap_d = need * 2;
-    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(I.cap_d), V, 0);
-    WS_CUDA(cudaMalloc(&I.d_ws_d, wsb_));
-    WS_CUDA(cudaMemset(I.d_ws_d, 0, wsb_));
-    WS_CUDA(cudaMalloc(&I.d_pred_d, I.cap_d * sizeof(ws_pred)));
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&I.h_pred_d), I.cap_d * sizeof(ws_pred), cudaHostAllocDefault));
+    if (L.h_pred_d) cudaFreeHost(L.h_pred_d);
+    L.cap_d = need * 2;
+    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(L.cap_d), V, 0);
+    WS_CUDA(cudaMalloc(&L.d_ws_d, wsb_));
+    WS_CUDA(cudaMemset(L.d_ws_d, 0, wsb_));
+    WS_CUDA(cudaMalloc(&L.d_pred_d, L.cap_d * sizeof(ws_pred)));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&L.h_pred_d), L.cap_d * sizeof(ws_pred), cudaHostAllocDefault));
   }
-  ForwardBatch& b = I.db;
+  ForwardBatch& b = L.db;
   b.clear();
-  I.job_out.assign(nd, -1);
-  I.copy_src.clear();
-  I.copy_dst.clear();
+  L.job_out.assign(nd, -1);
+  L.copy_src.clear();
+  L.copy_dst.clear();
   // the open shared-prefix tree group of one request's worker leaves (masked attention group)
   struct TreeGroup {
     bool active = false;
@@ -406,17 +445,17 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
     const JobCtx& jc = jobs.draft_ctx[j];
     const std::uint32_t r = dj.seq;
     fill_ctx(jobs, r, jc);
-    const std::int32_t n_ctx = static_cast<std::int32_t>(I.ctx.size());
+    const std::int32_t n_ctx = static_cast<std::int32_t>(L.ctx.size());
     static const bool debug_rows = std::getenv("WS_DEBUG_ROWS") != nullptr;
     if (debug_rows) {
       std::uint64_t h = 1469598103934665603ULL ^ r;
-      for (TokenId t : I.ctx) h = (h ^ static_cast<std::uint64_t>(t)) * 1099511628211ULL;
+      for (TokenId t : L.ctx) h = (h ^ static_cast<std::uint64_t>(t)) * 1099511628211ULL;
       if (!seen_ctx_.insert(h).second) repeat_by_kind[jc.kind] += 1;
     }
     if (forced_at(n_ctx - 1, P, L_, eos_) >= 0) {
       // Past the generation cap the prediction is a confident EOS whatever the context
       // (oracle.hpp:88-102): no forward, no KV (every descendant is forced too).
-      I.job_out[j] = -1;
+      L.job_out[j] = -1;
       continue;
     }
     if (n_ctx > MC)
@@ -429,16 +468,16 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
     if (jc.kind == kJobCtrlDraft) {  // controller local draft + catch-up prefill (controller.hpp:194-208)
       LinearCache& c = I.ctrl[r];
       std::int32_t lcp = 0;
-      while (lcp < n_ctx - 1 && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == I.ctx[lcp]) ++lcp;
+      while (lcp < n_ctx - 1 && lcp < static_cast<std::int32_t>(c.valid.size()) && c.valid[lcp] == L.ctx[lcp]) ++lcp;
       const std::int32_t base_slot = static_cast<std::int32_t>(r) * S;
       for (std::int32_t p = lcp; p < n_ctx; ++p) {
-        b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
+        b.tok.push_back(static_cast<std::int32_t>(L.ctx[p]));
         b.pos.push_back(p);
         b.slot.push_back(base_slot + p);
         b.extra.push_back(base_slot + p);
       }
       b.groups.push_back(AttnGroup{row0, n_ctx - lcp, base_slot, lcp, eoff, n_ctx - lcp});
-      c.valid.assign(I.ctx.begin(), I.ctx.end());
+      c.valid.assign(L.ctx.begin(), L.ctx.end());
     } else {  // worker leaf: committed prefix + trie
       TreeCache& t = I.wrk[r];
       const std::int32_t pre_base = static_cast<std::int32_t>(r) * S + MC;
@@ -447,7 +486,7 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
       // prefix must agree with the context (committed is append-only; defensive check)
       std::int32_t pl = static_cast<std::int32_t>(t.prefix.size());
       std::int32_t agree = 0;
-      while (agree < pl && agree < n_comm && t.prefix[agree] == I.ctx[agree]) ++agree;
+      while (agree < pl && agree < n_comm && t.prefix[agree] == L.ctx[agree]) ++agree;
       if (agree < pl) {
         t.prefix.resize(agree);
         t.drop_all();
@@ -456,11 +495,11 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
       // migrate speculative nodes that became committed into the prefix
       std::int32_t cur = -1;
       while (pl < n_comm) {
-        const std::int32_t c = t.find(cur, I.ctx[pl]);
+        const std::int32_t c = t.find(cur, L.ctx[pl]);
         if (c < 0) break;
-        I.copy_src.push_back(t.nodes[c].slot);
-        I.copy_dst.push_back(pre_base + pl);
-        t.prefix.push_back(I.ctx[pl]);
+        L.copy_src.push_back(t.nodes[c].slot);
+        L.copy_dst.push_back(pre_base + pl);
+        t.prefix.push_back(L.ctx[pl]);
         ++pl;
         cur = c;
       }
@@ -484,7 +523,7 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
       const bool leaf_job = q == n_comm && n_ctx > n_comm;
       if (leaf_job) {
         while (q < n_ctx - 1) {
-          const std::int32_t c = t.find(node, I.ctx[q]);
+          const std::int32_t c = t.find(node, L.ctx[q]);
           if (c < 0) break;
           anc.push_back(t.nodes[c].slot);
           node = c;
@@ -498,20 +537,20 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
         if (p < n_comm) {
           slot = pre_base + p;
         } else {
-          std::int32_t c = t.find(node, I.ctx[p]);
+          std::int32_t c = t.find(node, L.ctx[p]);
           if (c < 0) {
-            c = t.add(node, I.ctx[p]);
+            c = t.add(node, L.ctx[p]);
             t.last_alloc_round = draft_batch_;
           }
           slot = t.nodes[c].slot;
           node = c;
         }
-        b.tok.push_back(static_cast<std::int32_t>(I.ctx[p]));
+        b.tok.push_back(static_cast<std::int32_t>(L.ctx[p]));
         b.pos.push_back(p);
         b.slot.push_back(slot);
         row_slots.push_back(slot);
       }
-      for (std::int32_t p = pl; p < std::min(n_comm, n_ctx); ++p) t.prefix.push_back(I.ctx[p]);
+      for (std::int32_t p = pl; p < std::min(n_comm, n_ctx); ++p) t.prefix.push_back(L.ctx[p]);
       if (!leaf_job || anc.size() + row_slots.size() > 64) {
         // root / catch-up job: its own causal group
         flush_wg();
@@ -547,36 +586,36 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
     const std::int32_t last = static_cast<std::int32_t>(b.tok.size()) - 1;
     rows_by_kind[jc.kind] += static_cast<std::uint64_t>(last + 1 - row0);
     jobs_by_kind[jc.kind] += 1;
-    I.job_out[j] = static_cast<std::int32_t>(b.out_rows.size());
+    L.job_out[j] = static_cast<std::int32_t>(b.out_rows.size());
     b.out_rows.push_back(last);
-    b.plant.push_back(p_->plant(I.ctx[n_ctx - 1], true));
+    b.plant.push_back(p_->plant(L.ctx[n_ctx - 1], true));
   }
   flush_wg();
   if (b.row_mask.size() != b.tok.size()) throw std::logic_error("model path: row mask bookkeeping");
   const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
   cudaStream_t sd = draft_stream();
   if (n_out) {
-    p_->draft().copy_slots(I.copy_src, I.copy_dst, sd);
-    WS_CUDA(cudaEventRecord(I.e2, sd));
-    p_->draft().forward(b, cfg.plant_draft, sd);
-    row_stats_bf16(p_->draft().logits(), n_out, V, V, 1.0f, I.d_pred_d, nullptr, I.d_ws_d, 0, 0, nullptr, nullptr,
+    p_->draft().copy_slots(L.copy_src, L.copy_dst, sd, *L.ws_d);
+    WS_CUDA(cudaEventRecord(L.e2, sd));
+    p_->draft().forward(b, cfg.plant_draft, sd, *L.ws_d);
+    row_stats_bf16(L.ws_d->logits, n_out, V, V, 1.0f, L.d_pred_d, nullptr, L.d_ws_d, 0, 0, nullptr, nullptr,
                    sd, nullptr);
-    WS_CUDA(cudaEventRecord(I.e3, sd));
-    WS_CUDA(cudaMemcpyAsync(I.h_pred_d, I.d_pred_d, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, sd));
+    WS_CUDA(cudaEventRecord(L.e3, sd));
+    WS_CUDA(cudaMemcpyAsync(L.h_pred_d, L.d_pred_d, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, sd));
     draft_ran_ = true;
     draft_rows_fed += b.tok.size();
     draft_forwards += 1;
-    stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (I.copy_src.empty() ? 0 : 1);
+    stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (L.copy_src.empty() ? 0 : 1);
     stats.d2h += n_out * sizeof(ws_pred);
   }
-  WS_CUDA(cudaEventRecord(I.done[1], sd));
+  WS_CUDA(cudaEventRecord(L.done[1], sd));
   stats.draft_rows += nd;
 }
 
 cudaStream_t ModelBackend_Llama::draft_stream() const {
   // WS_SERIAL=1 serialises the two forwards (clean per-kernel profiles); default overlaps them
   static const bool serial = std::getenv("WS_SERIAL") != nullptr;
-  return serial ? p_->stream() : p_->stream_draft();
+  return serial ? ln_->st_t : ln_->st_d;
 }
 
 std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t) {
@@ -594,10 +633,11 @@ std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int veri
 
 int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
   ModelPair::Impl& I = *p_->impl;
+  Lanes& L = *ln_;
   for (;;) {
     for (int lane = 0; lane < 2; ++lane) {
       if (!(lane == 0 ? busy0 : busy1)) continue;
-      const cudaError_t e = cudaEventQuery(I.done[lane]);
+      const cudaError_t e = cudaEventQuery(L.done[lane]);
       if (e == cudaSuccess) return lane;
       if (e != cudaErrorNotReady) WS_CUDA(e);
     }
@@ -607,21 +647,22 @@ int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
 
 void ModelBackend_Llama::complete(int lane, RoundResults& res) {
   ModelPair::Impl& I = *p_->impl;
+  Lanes& L = *ln_;
   float ms = 0.f;
   if (lane == 0) {
-    res.verify.resize(I.nv);
-    if (!I.nv) return;
-    WS_CUDA(cudaEventSynchronize(I.done[0]));
-    std::memcpy(res.verify.data(), I.h_vout, I.nv * sizeof(ws_verify_out));
-    WS_CUDA(cudaEventElapsedTime(&ms, I.e0, I.e1));
+    res.verify.resize(L.nv);
+    if (!L.nv) return;
+    WS_CUDA(cudaEventSynchronize(L.done[0]));
+    std::memcpy(res.verify.data(), L.h_vout, L.nv * sizeof(ws_verify_out));
+    WS_CUDA(cudaEventElapsedTime(&ms, L.e0, L.e1));
     target_ms += ms;
   } else {
-    res.draft.resize(I.nd);
-    if (!I.nd) return;
-    WS_CUDA(cudaEventSynchronize(I.done[1]));
-    for (std::uint32_t j = 0; j < I.nd; ++j) {
-      if (I.job_out[j] >= 0) {
-        res.draft[j] = I.h_pred_d[I.job_out[j]];
+    res.draft.resize(L.nd);
+    if (!L.nd) return;
+    WS_CUDA(cudaEventSynchronize(L.done[1]));
+    for (std::uint32_t j = 0; j < L.nd; ++j) {
+      if (L.job_out[j] >= 0) {
+        res.draft[j] = L.h_pred_d[L.job_out[j]];
       } else {
         ws_pred e{};
         e.n = 1;
@@ -631,7 +672,7 @@ void ModelBackend_Llama::complete(int lane, RoundResults& res) {
       }
     }
     if (draft_ran_) {
-      WS_CUDA(cudaEventElapsedTime(&ms, I.e2, I.e3));
+      WS_CUDA(cudaEventElapsedTime(&ms, L.e2, L.e3));
       draft_ms += ms;
     }
   }

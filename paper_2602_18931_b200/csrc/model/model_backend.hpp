@@ -50,6 +50,10 @@ class ModelBackend_Llama : public ModelBackend {
   std::size_t submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed) override;
   int wait_any(bool busy0, bool busy1) override;
   void complete(int lane, RoundResults& res) override;
+  KernelProfiler& profiler(int which);  // 0 = target forwards, 1 = draft forwards of this backend
+  // New run on the same pair (the caller reset the per-request caches): run parameters, zeroed
+  // counters; streams, workspaces and device buffers are kept.
+  void reset_run(std::uint32_t seq_len, TokenId eos, std::uint32_t k);
   double target_ms = 0, draft_ms = 0;
   std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
   std::uint64_t rows_by_kind[3] = {0, 0, 0}, jobs_by_kind[3] = {0, 0, 0};  // JobKind
@@ -68,6 +72,8 @@ class ModelBackend_Llama : public ModelBackend {
   std::uint32_t k_;
   std::uint64_t draft_batch_ = 0;
   bool draft_ran_ = false;
+  struct Lanes;
+  std::unique_ptr<Lanes> ln_;
   std::unordered_set<std::uint64_t> seen_ctx_;
 };
 
@@ -82,8 +88,8 @@ class ModelPair {
   LlamaModel& draft() { return *draft_; }
   const std::vector<TokenId>& prompt(std::uint32_t r);
   std::int32_t plant(TokenId t, bool draft) const;
-  cudaStream_t stream() const { return stream_; }
-  cudaStream_t stream_draft() const { return stream_draft_; }
+  int device() const { return device_; }
+  int max_rows() const { return max_rows_; }
 
   struct Impl;
   std::unique_ptr<Impl> impl;
@@ -93,8 +99,7 @@ class ModelPair {
   int device_;
   std::unique_ptr<LlamaModel> target_, draft_;
   std::vector<std::vector<TokenId>> prompts_;
-  cudaStream_t stream_ = nullptr;        // target (verify)
-  cudaStream_t stream_draft_ = nullptr;  // draft (worker + controller local)
+  int max_rows_ = 0;
 };
 
 }  // namespace wsb

@@ -161,6 +161,20 @@ def test_model_sim_speculative_equals_greedy(tiny_pair):
     assert st["target_forwards"] > 0 and st["draft_forwards"] > 0
 
 
+def test_model_sim_protocol_threads_equal_one_thread(tiny_pair):
+    """host_threads protocol threads (each its own verify/draft streams and workspaces over a
+    contiguous request range, forwards running concurrently) give the one-thread results."""
+    from paper_2602_18931_b200 import abi
+    c1 = abi.config3(num_requests=8, k=4, seq_len=30, vocab=1000, eos=999)
+    one = tiny_pair.run_model_sim(c1)
+    for t in (2, 3):
+        ct = abi.config3(num_requests=8, k=4, seq_len=30, vocab=1000, eos=999)
+        ct.host_threads = t
+        many = tiny_pair.run_model_sim(ct)
+        assert many.metrics_list() == one.metrics_list()
+        assert many.ctrl_outputs() == one.ctrl_outputs()
+
+
 def test_model_sim_k8_and_accept_stats(tiny_pair):
     from paper_2602_18931_b200 import abi
     c = abi.config3(num_requests=8, k=8, seq_len=36, vocab=1000, eos=999)
