@@ -41,6 +41,9 @@ def parse():
     p.add_argument("--host-threads", type=int, default=0)
     p.add_argument("--shards", type=int, default=int(os.environ.get("WS_SHARDS", "1")),
                    help="llama: protocol threads per GPU, each with its own verify/draft streams")
+    p.add_argument("--placement", choices=["shared", "split"], default=os.environ.get("WS_PLACEMENT", "shared"),
+                   help="llama, N >= 2: 'split' puts the draft model on its own GPU (ranks < N/2 drive "
+                        "target GPU r + draft GPU r + N/2; SURVEY §8e), 'shared' shards requests over all GPUs")
     p.add_argument("--cpu-sample-s", type=float, default=6.0)
     return p.parse_args()
 
@@ -129,7 +132,10 @@ def config_block(args, world, host_threads):
                             f"{args.requests} requests, k={args.k}, b=2, s=4, theta=phi=0.5, RTT 20 ms "
                             "(virtual), greedy verify, planted shared bigram bias (match ~0.8)",
                 "model": "llama3-8b + llama3.2-1b", "global_batch": args.requests, "seq_len": 128 + 100,
-                "parallelism": f"requests sharded over {world} GPU(s) (strong scaling), no collective",
+                "parallelism": (f"split placement: requests sharded over {world // 2} target GPU(s), each "
+                                f"paired with its own draft GPU (SURVEY §8e), no collective"
+                                if args.placement == "split" and world >= 2 and world % 2 == 0 else
+                                f"requests sharded over {world} GPU(s) (strong scaling), no collective"),
                 "l2": "weights (18.5 GB) and KV (>126 MB) exceed L2; no explicit flush needed"}
     return {"workload": "BASELINE configs[1]: tiny draft/target pair (oracle tables, V=32768), "
                         f"{TINY_REQ_PER_GPU} requests/GPU, k=8, b=2, s=4, theta=phi=0.5, RTT 20 ms, "
@@ -260,10 +266,17 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     peak_bw, peak_tf, peak_kind = peaks()
 
+    split = args.workload == "llama" and args.placement == "split" and world >= 2 and world % 2 == 0
+    active = not split or rank < world // 2
     if args.workload == "llama":
-        cfg = llama_cfg(args, world, rank)
+        if split:  # requests sharded over the target GPUs; GPU r + N/2 runs rank r's drafts
+            cfg = llama_cfg(args, world // 2, min(rank, world // 2 - 1))
+        else:
+            cfg = llama_cfg(args, world, rank)
         cfg.host_threads = max(1, args.shards)
-        ctx.load_models(abi.model_cfg(max_requests=args.requests))
+        if active:
+            ctx.load_models(abi.model_cfg(max_requests=args.requests),
+                            draft_device=local_rank + world // 2 if split else -1)
 
         def run_once(tokens_out=False):
             return ctx.run_model_sim(cfg, with_tokens=tokens_out, with_steps=False)
@@ -276,14 +289,14 @@ def main():
         def run_once(tokens_out=False):
             return ctx.run_sim_full(cfg, with_tokens=tokens_out, with_steps=False, resident=True)
 
-    for _ in range(args.warmup):
+    for _ in range(args.warmup if active else 0):
         run_once()
     tokens, total_ms, launches, kernel_ms, h2d, d2h = 0, 0.0, 0, 0.0, 0, 0
     mstats = {"target_ms": 0.0, "draft_ms": 0.0, "target_rows": 0, "draft_rows": 0, "target_forwards": 0,
               "draft_forwards": 0}
     barrier()
     with ClockSampler(local_rank) as clk:
-        for _ in range(args.steps):
+        for _ in range(args.steps if active else 0):
             if args.workload == "tiny":
                 flush.fill_(1.0)
             torch.cuda.synchronize()
@@ -303,7 +316,9 @@ def main():
                     mstats[kk] += v
     barrier()
 
-    stats = torch.tensor([total_ms, float(tokens), float(launches)], dtype=torch.float64, device="cuda")
+    torch.cuda.set_device(local_rank)
+    stats = torch.tensor([total_ms, float(tokens), float(launches)], dtype=torch.float64,
+                         device=torch.device("cuda", local_rank))
     if dist:
         mx, sm = stats.clone(), stats.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)

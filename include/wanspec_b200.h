@@ -270,6 +270,11 @@ typedef struct ws_model_cfg {
   uint32_t pad;
 } ws_model_cfg;
 int ws_model_load(ws_ctx* ctx, const ws_model_cfg* cfg);
+/* Split placement: the target (verify) model on the context's GPU and the draft
+ * model — the worker's rollout and the controller's local drafts — on `draft_device`, each lane
+ * on its own GPU; requests' proposals and verify results meet in the host driver. A negative
+ * draft_device is ws_model_load. */
+int ws_model_load_split(ws_ctx* ctx, const ws_model_cfg* cfg, int draft_device);
 /* run_sim_full (sim.hpp:429-442) with the verify / draft model calls on the loaded models;
  * cfg->oracle supplies vocab_size (must equal the models'), eos_id and sequence_length. */
 int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);

@@ -66,6 +66,7 @@ def lib():
     L.ws_run_sim_resident.argtypes = [C.c_void_p, _P(abi.SimCfg), _P(abi.RunOut)]
     L.ws_run_sim_with_model.argtypes = [_P(abi.SimCfg), MODEL_ROUND_FN, C.c_void_p, _P(abi.RunOut)]
     L.ws_model_load.argtypes = [C.c_void_p, _P(abi.ModelCfg)]
+    L.ws_model_load_split.argtypes = [C.c_void_p, _P(abi.ModelCfg), C.c_int]
     L.ws_run_model_sim.argtypes = [C.c_void_p, _P(abi.SimCfg), _P(abi.RunOut)]
     L.ws_model_stats.argtypes = [C.c_void_p, _P(C.c_double), _P(C.c_double), _P(C.c_uint64), _P(C.c_uint64),
                                  _P(C.c_uint64), _P(C.c_uint64)]
@@ -157,10 +158,11 @@ class Context:
         return [(o.n, tuple(o.id[:o.n]), tuple(o.prob[:o.n]), o.entropy) for o in out]
 
     # -- real-model pair (config 3) --
-    def load_models(self, mcfg):
-        """Allocate + seed-initialise the target/draft models and their KV pools on this GPU."""
+    def load_models(self, mcfg, draft_device=-1):
+        """Allocate + seed-initialise the target/draft models and their KV pools on this GPU
+        (the draft model on `draft_device` under split placement)."""
         self._mcfg = mcfg  # keep the C strings alive
-        _check(lib().ws_model_load(self._h, C.byref(mcfg)))
+        _check(lib().ws_model_load_split(self._h, C.byref(mcfg), int(draft_device)))
 
     def run_model_sim(self, cfg, with_tokens=True, with_steps=True):
         """run_sim_full with the verify/draft model calls on the loaded models."""

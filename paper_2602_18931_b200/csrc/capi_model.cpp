@@ -40,8 +40,10 @@ LastStats g_last;
 
 extern "C" {
 
-int ws_model_load(ws_ctx* ctx, const ws_model_cfg* c) {
-  return guard("ws_model_load", [&] {
+int ws_model_load(ws_ctx* ctx, const ws_model_cfg* c) { return ws_model_load_split(ctx, c, -1); }
+
+int ws_model_load_split(ws_ctx* ctx, const ws_model_cfg* c, int draft_device) {
+  return guard("ws_model_load_split", [&] {
     if (!ctx || !c || !c->target || !c->draft) throw std::invalid_argument("null argument");
     wsb::ModelPairCfg m;
     m.target = c->target;
@@ -54,7 +56,13 @@ int ws_model_load(ws_ctx* ctx, const ws_model_cfg* c) {
     m.plant_target = c->plant_target;
     m.plant_draft = c->plant_draft;
     m.draft_plant_rate = c->draft_plant_rate;
+    m.draft_device = draft_device;
     if (m.prompt_len < 1) throw wsb::ConfigError("prompt_len must be >= 1");
+    if (draft_device >= 0) {
+      int n = 0;
+      WS_CUDA(cudaGetDeviceCount(&n));
+      if (draft_device >= n) throw wsb::ConfigError("draft_device out of range");
+    }
     WS_CUDA(cudaSetDevice(ctx->device));
     ctx->model_lanes.clear();
     ctx->models.reset();
@@ -141,6 +149,9 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
                    (unsigned long long)st.draft_forwards, st.draft_ms);
       std::fprintf(stderr, "[ws] repeated draft contexts: ctrl %llu, worker %llu\n", (unsigned long long)rep_kind[1],
                    (unsigned long long)rep_kind[2]);
+      for (auto* bk : used)
+        std::fprintf(stderr, "[ws] host ms: submit verify %.1f, submit draft %.1f, wait %.1f\n", bk->host_submit_ms[0],
+                     bk->host_submit_ms[1], bk->host_wait_ms);
     }
   });
 }

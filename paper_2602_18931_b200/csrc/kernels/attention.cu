@@ -349,8 +349,8 @@ void launch_attn(const void* q, const void* k_pool, const void* v_pool, const At
   if (n_groups <= 0) return;
   constexpr int C = HD / 8;
   constexpr int kSmem = (16 * VW * C + KS * 4 * kTile * C) * 16;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static std::atomic<std::uint32_t> attr_done{0};
+  once_per_device(attr_done, [] {
     WS_CUDA(cudaFuncSetAttribute(attn_mma_kernel<HD, VW, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
   });
   launch_pdl(attn_mma_kernel<HD, VW, KS>, dim3(n_groups, s.n_kv), dim3(32 * VW * KS), kSmem, st, 1,

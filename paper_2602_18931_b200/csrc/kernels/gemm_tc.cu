@@ -226,6 +226,7 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, in
 // read back with ws_debug_gemm_trace): entry, prologue done, dependency wait done, first ring
 // slot full, last MMA of the unit issued, accumulator ready in the epilogue, epilogue done, exit.
 __device__ unsigned long long g_gemm_trace[8];
+constexpr int kEarlyTrigger = 1 << 16;  // (flag bit in `ablate`) trigger dependents at entry
 __device__ __forceinline__ void trace_point(int ablate, int i) {
   if ((ablate & 8) && blockIdx.x == 0) {
     unsigned long long t;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   if (threadIdx.x == 0) {
-    pdl_trigger();  // (no-op unless WS_PDL_EARLY)
+    if (ablate & kEarlyTrigger) pdl_trigger_now();  // small grid: dependents may use the idle SMs
     trace_point(ablate, 0);
   }
   if (warp == 0 && lane == 0) {
@@ -579,7 +580,7 @@ CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, st
   return m;
 }
 
-int pair_clusters() {  // co-resident CTA pairs at one CTA per SM
+int pair_clusters() {  // co-resident CTA pairs at one CTA per SM (same on every B200)
   static int n = [] {
     WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<kEpiBF16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemBudget));
@@ -603,12 +604,18 @@ int pair_clusters() {  // co-resident CTA pairs at one CTA per SM
 
 template <int EPI, int CG>
 void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
+  static std::atomic<std::uint32_t> attr_done{0};
+  once_per_device(attr_done, [] {
     WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
   });
   static const int ablate = [] {  // WS_GEMM_ABLATE (measurement only): 1 no MMA,
     const char* e = std::getenv("WS_GEMM_ABLATE");  // 4 no epilogue stores
+    return e ? std::atoi(e) : 0;
+  }();
+  // grids at or below WS_PDL_EARLY_GRID CTAs trigger their dependents at entry (default 0 = off:
+  // measured 1.28 -> 1.33 s per step at 64 requests with 96, no gain at 256)
+  static const int early_grid = [] {
+    const char* e = std::getenv("WS_PDL_EARLY_GRID");
     return e ? std::atoi(e) : 0;
   }();
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
@@ -619,14 +626,16 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   if constexpr (CG == 1) {
     const int total = m_blocks * n_tiles * sk.splits;
     const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
+    const int flags = ablate | (grid <= early_grid ? kEarlyTrigger : 0);
     launch_pdl(gemm_tn_kernel<EPI, 1>, dim3(grid), dim3(kThreads), smem, st, 1, ta, tb, g.M, g.N, g.K, m_blocks,
-               n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, ablate);
+               n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
   } else {
     const int total = (m_blocks + 1) / 2 * n_tiles;
     int clusters = std::min(total, pair_clusters());
     if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 2));
+    const int flags = ablate | (2 * clusters <= early_grid ? kEarlyTrigger : 0);
     launch_pdl(gemm_tn_kernel<EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2, ta, tb, g.M, g.N, g.K,
-               m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, ablate);
+               m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
   }
 }
 

@@ -25,6 +25,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 #else
 __device__ __forceinline__ void pdl_trigger() {}
 #endif
+// Unconditional early trigger, for grids that leave SMs idle (small-batch GEMMs): the next
+// kernel's CTAs start their prologue and weight prefetch on those SMs.
+__device__ __forceinline__ void pdl_trigger_now() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 inline bool pdl_enabled() {
   static const bool on = [] {

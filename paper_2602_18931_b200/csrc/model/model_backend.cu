@@ -6,6 +6,7 @@
 #include <cstring>
 #include <random>
 #include <stdexcept>
+#include <chrono>
 #include <thread>
 
 #include "../kernels/cuda_check.hpp"
@@ -116,7 +117,8 @@ struct ModelPair::Impl {
 // buffers, pinned staging and results. Several backends share one ModelPair (weights, KV
 // pools, per-request caches) and serve disjoint request ranges concurrently.
 struct ModelBackend_Llama::Lanes {
-  int device = 0;
+  int device = 0;    // verify lane (target model)
+  int device_d = 0;  // draft lane (the same GPU, or another under split placement)
   cudaStream_t st_t = nullptr, st_d = nullptr;  // verify (target) / draft streams
   std::unique_ptr<ForwardWorkspace> ws_t, ws_d;
   // verify lane
@@ -140,18 +142,22 @@ struct ModelBackend_Llama::Lanes {
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   cudaEvent_t done[2] = {nullptr, nullptr};  // after each lane's result D2H
   ~Lanes() {
-    cudaSetDevice(device);
+    cudaSetDevice(device);  // (frees / destroys below work for either device's objects)
     for (void* q : {static_cast<void*>(d_pred), static_cast<void*>(d_vout), static_cast<void*>(d_cands),
                     static_cast<void*>(d_forced), d_ws, static_cast<void*>(d_pred_d), d_ws_d})
       if (q) cudaFree(q);
     for (void* q : {static_cast<void*>(h_stage), static_cast<void*>(h_vout), static_cast<void*>(h_pred_d)})
       if (q) cudaFreeHost(q);
-    for (cudaEvent_t e : {e0, e1, e2, e3, done[0], done[1]})
+    for (cudaEvent_t e : {e0, e1, done[0]})
       if (e) cudaEventDestroy(e);
     ws_t.reset();
-    ws_d.reset();
     if (st_t) cudaStreamDestroy(st_t);
+    cudaSetDevice(device_d);
+    for (cudaEvent_t e : {e2, e3, done[1]})
+      if (e) cudaEventDestroy(e);
+    ws_d.reset();
     if (st_d) cudaStreamDestroy(st_d);
+    cudaSetDevice(device);
   }
 };
 
@@ -161,8 +167,10 @@ ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(d
   if (ts.vocab != ds.vocab) throw ConfigError("target and draft vocabularies differ");
   const std::int64_t R = cfg.max_requests, C = cfg.max_ctx;
   max_rows_ = static_cast<int>(std::min<std::int64_t>(R * 20, 8192));
+  draft_device_ = cfg.draft_device >= 0 ? cfg.draft_device : device;
   target_.reset(new LlamaModel(ts, cfg.seed * 2 + 1, R * C, max_rows_, device));
-  draft_.reset(new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows_, device));
+  draft_.reset(new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows_, draft_device_));
+  WS_CUDA(cudaSetDevice(device));
   prompts_.resize(cfg.max_requests);
   if (const char* e = std::getenv("WS_TARGET_CTAS")) target_->set_max_ctas(std::atoi(e));
   if (const char* e = std::getenv("WS_DRAFT_CTAS")) draft_->set_max_ctas(std::atoi(e));
@@ -206,6 +214,7 @@ ModelBackend_Llama::ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, T
     : p_(pair), L_(seq_len), eos_(eos), k_(k), ln_(new Lanes) {
   Lanes& L = *ln_;
   L.device = pair->device();
+  L.device_d = pair->draft_device();
   WS_CUDA(cudaSetDevice(L.device));
   // The draft lane is the critical path of the continuous-batching loop (requests mostly wait
   // on draft results), so its stream gets the higher scheduling priority; the verify lane's
@@ -215,17 +224,19 @@ ModelBackend_Llama::ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, T
   const char* dp = std::getenv("WS_DRAFT_PRIO");
   const bool draft_first = !(dp && dp[0] == '0');
   WS_CUDA(cudaStreamCreateWithPriority(&L.st_t, cudaStreamNonBlocking, prio_lo));
-  WS_CUDA(cudaStreamCreateWithPriority(&L.st_d, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
+  WS_CUDA(cudaEventCreate(&L.e0));
+  WS_CUDA(cudaEventCreate(&L.e1));
+  WS_CUDA(cudaEventCreateWithFlags(&L.done[0], cudaEventDisableTiming));
   // workspaces grow to the batch sizes actually seen (a cap of max_rows each would be GBs of
   // logits per protocol thread)
   L.ws_t = pair->target().make_workspace(64);
-  L.ws_d = pair->draft().make_workspace(64);
-  WS_CUDA(cudaEventCreate(&L.e0));
-  WS_CUDA(cudaEventCreate(&L.e1));
+  WS_CUDA(cudaSetDevice(L.device_d));
+  WS_CUDA(cudaStreamCreateWithPriority(&L.st_d, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
   WS_CUDA(cudaEventCreate(&L.e2));
   WS_CUDA(cudaEventCreate(&L.e3));
-  WS_CUDA(cudaEventCreateWithFlags(&L.done[0], cudaEventDisableTiming));
   WS_CUDA(cudaEventCreateWithFlags(&L.done[1], cudaEventDisableTiming));
+  L.ws_d = pair->draft().make_workspace(64);
+  WS_CUDA(cudaSetDevice(L.device));
 }
 ModelBackend_Llama::~ModelBackend_Llama() = default;
 
@@ -238,6 +249,7 @@ void ModelBackend_Llama::reset_run(std::uint32_t seq_len, TokenId eos, std::uint
   target_ms = draft_ms = 0;
   target_rows = draft_rows_fed = target_forwards = draft_forwards = 0;
   for (int i = 0; i < 3; ++i) rows_by_kind[i] = jobs_by_kind[i] = repeat_by_kind[i] = 0;
+  host_submit_ms[0] = host_submit_ms[1] = host_wait_ms = 0;
   seen_ctx_.clear();
 }
 
@@ -306,6 +318,7 @@ std::size_t ModelBackend_Llama::verify_take(const RoundJobs& jobs) {
 void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_take) {
   ModelPair::Impl& I = *p_->impl;
   Lanes& L = *ln_;
+  DeviceGuard dg(L.device);
   const ModelPairCfg& cfg = p_->cfg();
   cudaStream_t st = L.st_t;
   const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
@@ -391,6 +404,7 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
 void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
   ModelPair::Impl& I = *p_->impl;
   Lanes& L = *ln_;
+  DeviceGuard dg(L.device_d);
   const ModelPairCfg& cfg = p_->cfg();
   const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
   const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
@@ -615,28 +629,40 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
 cudaStream_t ModelBackend_Llama::draft_stream() const {
   // WS_SERIAL=1 serialises the two forwards (clean per-kernel profiles); default overlaps them
   static const bool serial = std::getenv("WS_SERIAL") != nullptr;
-  return serial ? ln_->st_t : ln_->st_d;
+  return serial && ln_->device_d == ln_->device ? ln_->st_t : ln_->st_d;
 }
 
 std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t) {
   if (verify_mode != WS_VERIFY_GREEDY)
     throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
   stats.rounds += 1;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::size_t took;
   if (lane == 0) {
-    const std::size_t take = verify_take(jobs);
-    submit_verify(jobs, take);
-    return take;
+    took = verify_take(jobs);
+    submit_verify(jobs, took);
+  } else {
+    submit_draft(jobs);
+    took = jobs.draft.size();
   }
-  submit_draft(jobs);
-  return jobs.draft.size();
+  host_submit_ms[lane] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return took;
 }
 
 int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
   ModelPair::Impl& I = *p_->impl;
   Lanes& L = *ln_;
+  const auto t0 = std::chrono::steady_clock::now();
+  struct Acc {
+    double& ms;
+    std::chrono::steady_clock::time_point t0;
+    ~Acc() { ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+  } acc{host_wait_ms, t0};
   for (;;) {
     for (int lane = 0; lane < 2; ++lane) {
       if (!(lane == 0 ? busy0 : busy1)) continue;
+      // each event is queried with its own GPU current (split placement: two devices)
+      DeviceGuard dg(lane == 0 ? L.device : L.device_d);
       const cudaError_t e = cudaEventQuery(L.done[lane]);
       if (e == cudaSuccess) return lane;
       if (e != cudaErrorNotReady) WS_CUDA(e);
@@ -648,6 +674,7 @@ int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
 void ModelBackend_Llama::complete(int lane, RoundResults& res) {
   ModelPair::Impl& I = *p_->impl;
   Lanes& L = *ln_;
+  DeviceGuard dg(lane == 0 ? L.device : L.device_d);
   float ms = 0.f;
   if (lane == 0) {
     res.verify.resize(L.nv);

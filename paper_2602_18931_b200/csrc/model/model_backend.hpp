@@ -35,6 +35,7 @@ struct ModelPairCfg {
   float plant_target = 16.f;       // planted shared bigram bias (logit units)
   float plant_draft = 16.f;
   float draft_plant_rate = 0.8f;   // fraction of input tokens whose plant the draft also sees
+  int draft_device = -1;           // split placement: the draft model on another GPU (-1: same)
 };
 
 class ModelPair;
@@ -59,6 +60,7 @@ class ModelBackend_Llama : public ModelBackend {
   std::uint64_t rows_by_kind[3] = {0, 0, 0}, jobs_by_kind[3] = {0, 0, 0};  // JobKind
   // WS_DEBUG_ROWS: draft jobs whose (request, context) was already drafted earlier in the run
   std::uint64_t repeat_by_kind[3] = {0, 0, 0};
+  double host_submit_ms[2] = {0, 0}, host_wait_ms = 0;  // host time in submit (per lane) / wait_any
 
  private:
   void fill_ctx(const RoundJobs& jobs, std::uint32_t r, const JobCtx& c);
@@ -88,7 +90,8 @@ class ModelPair {
   LlamaModel& draft() { return *draft_; }
   const std::vector<TokenId>& prompt(std::uint32_t r);
   std::int32_t plant(TokenId t, bool draft) const;
-  int device() const { return device_; }
+  int device() const { return device_; }  // the target model's GPU
+  int draft_device() const { return draft_device_; }
   int max_rows() const { return max_rows_; }
 
   struct Impl;
@@ -100,6 +103,7 @@ class ModelPair {
   std::unique_ptr<LlamaModel> target_, draft_;
   std::vector<std::vector<TokenId>> prompts_;
   int max_rows_ = 0;
+  int draft_device_ = 0;
 };
 
 }  // namespace wsb

@@ -72,9 +72,9 @@ def draft_batch(n_wrk=256, leaves=2, n_ctrl=150, slots_per_req=1024):
     return tok, pos, slot, groups, extra, mask, outr
 
 
-def run(L, name, batch, n_slots, iters):
+def run(L, name, batch, n_slots, iters, device=0):
     h = C.c_void_p()
-    rc = L.ws_model_create(name.encode(), 7, n_slots, 2048, 0, C.byref(h))
+    rc = L.ws_model_create(name.encode(), 7, n_slots, 2048, device, C.byref(h))
     assert rc == 0, L.ws_last_error()
     tok, pos, slot, groups, extra, mask, outr = batch
     i32 = lambda v: torch.tensor(v, dtype=torch.int32)  # noqa: E731
@@ -82,8 +82,8 @@ def run(L, name, batch, n_slots, iters):
     t_grp = i32([x for g in groups for x in g])
     t_ext, t_out = i32(extra), i32(outr)
     t_msk = torch.tensor(mask, dtype=torch.int64)
-    logits = torch.empty(len(outr), V, dtype=torch.bfloat16, device="cuda")
-    st = torch.cuda.current_stream()
+    logits = torch.empty(len(outr), V, dtype=torch.bfloat16, device=torch.device("cuda", device))
+    st = torch.cuda.current_stream(device)
 
     def fwd():
         rc = L.ws_model_forward(h, len(tok), t_tok.data_ptr(), t_pos.data_ptr(), t_slot.data_ptr(), len(groups),
@@ -93,25 +93,28 @@ def run(L, name, batch, n_slots, iters):
 
     for _ in range(2):
         fwd()
-    torch.cuda.synchronize()
+    torch.cuda.synchronize(device)
     ms = []
     for _ in range(iters):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        fwd()
-        e1.record()
-        torch.cuda.synchronize()
+        with torch.cuda.device(device):
+            e0.record(st)
+            fwd()
+            e1.record(st)
+        torch.cuda.synchronize(device)
         ms.append(e0.elapsed_time(e1))
     L.ws_model_destroy(h)
-    return {"model": name, "rows": len(tok), "groups": len(groups), "out_rows": len(outr),
+    return {"model": name, "device": device, "rows": len(tok), "groups": len(groups), "out_rows": len(outr),
             "ms_median": sorted(ms)[len(ms) // 2], "ms_all": [round(x, 3) for x in ms]}
 
 
 def main():
     iters = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     L = bind()
-    print(json.dumps(run(L, "llama3-8b", verify_batch(), 105 * 256, iters)))
-    print(json.dumps(run(L, "llama3.2-1b", draft_batch(), 256 * 1024, iters)))
+    devs = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0"])]
+    for dev in devs:
+        print(json.dumps(run(L, "llama3-8b", verify_batch(), 105 * 256, iters, dev)))
+        print(json.dumps(run(L, "llama3.2-1b", draft_batch(), 256 * 1024, iters, dev)))
 
 
 if __name__ == "__main__":

@@ -223,3 +223,22 @@ def test_forward_prefill_verify_tree(L, name):
         check(got[1:2], ref.logits(A + [B[0], Y])[7:8])
     finally:
         L.ws_model_destroy(h)
+
+
+def test_model_sim_split_placement_equals_shared():
+    """Split placement (draft model on a second GPU) gives the same per-request
+    results as both models on one GPU. Needs two GPUs."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_2602_18931_b200 as ws
+    from paper_2602_18931_b200 import abi
+    outs = []
+    for draft_dev in (-1, 1):
+        ctx = ws.Context(0)
+        ctx.load_models(abi.model_cfg("tiny", "tiny-draft", prompt_len=16, max_requests=8, max_ctx=64,
+                                      plant_target=6.0, plant_draft=6.0, draft_plant_rate=0.8),
+                        draft_device=draft_dev)
+        b = ctx.run_model_sim(abi.config3(num_requests=8, k=4, seq_len=30, vocab=1000, eos=999))
+        outs.append((b.metrics_list(), b.ctrl_outputs()))
+        ctx.close()
+    assert outs[0] == outs[1]
