@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
     }
   };
 
-  for (int pass0 = 0; pass0 < nvec; pass0 += kVecPerPass) {
+  // one pass: the entry's query vectors [g.pad, g.pad + 16 VW) (large groups come as several
+  // entries — attention_vectors_per_cta())
+  for (int pass0 = g.pad; pass0 < nvec && pass0 < g.pad + kVecPerPass; pass0 += kVecPerPass) {
     __syncthreads();
     // Q for this pass: vector v -> (row j = v / G, head kvh*G + v % G), zero past nvec
     for (int i = threadIdx.x; i < kVecPerPass * C; i += 32 * VW * KS) {
@@ -359,31 +361,24 @@ void launch_attn(const void* q, const void* k_pool, const void* v_pool, const At
              static_cast<__nv_bfloat16*>(out));
 }
 
-// groups[0, n_vw1) hold <= 16 query vectors each (one vector warp per CTA), the next n_vw2
-// <= 32 (two), the rest use four. Every launch uses the same key-slice count, so numerics never
-// depend on the grouping.
-void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
-               int n_vw1, int n_vw2, const std::int32_t* extra, const unsigned long long* row_mask,
-               const AttnShape& s, void* out, cudaStream_t st) {
-  if (n_groups <= 0) return;
+// One launch: every entry is one CTA's pass over <= attention_vectors_per_cta(hd) query vectors
+// of its group (AttnGroup.pad = first vector). The vector-warp count and the key-slice count
+// are fixed per head dim, so numerics never depend on the grouping.
+int attention_vectors_per_cta(int hd) { return hd == 128 ? 32 : 16; }
+
+void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* entries, int n_entries,
+               const std::int32_t* extra, const unsigned long long* row_mask, const AttnShape& s, void* out,
+               cudaStream_t st) {
+  if (n_entries <= 0) return;
   const float sl2 = s.scale * 1.4426950408889634f;
   // key slices per head dim (measured: two slices help the 64-wide draft heads, not the
   // 128-wide target heads, whose CTAs then fit fewer per SM)
-  constexpr int KS128 = 1, KS64 = 2;
-  const int n_vw4 = n_groups - n_vw1 - n_vw2;
-  const AttnGroup* g2 = groups + n_vw1;
-  const AttnGroup* g4 = g2 + n_vw2;
-  if (s.hd == 128) {
-    launch_attn<128, 1, KS128>(q, k_pool, v_pool, groups, n_vw1, extra, row_mask, s, sl2, out, st);
-    launch_attn<128, 2, KS128>(q, k_pool, v_pool, g2, n_vw2, extra, row_mask, s, sl2, out, st);
-    launch_attn<128, 4, KS128>(q, k_pool, v_pool, g4, n_vw4, extra, row_mask, s, sl2, out, st);
-  } else if (s.hd == 64) {
-    launch_attn<64, 1, KS64>(q, k_pool, v_pool, groups, n_vw1, extra, row_mask, s, sl2, out, st);
-    launch_attn<64, 2, KS64>(q, k_pool, v_pool, g2, n_vw2, extra, row_mask, s, sl2, out, st);
-    launch_attn<64, 4, KS64>(q, k_pool, v_pool, g4, n_vw4, extra, row_mask, s, sl2, out, st);
-  } else {
+  if (s.hd == 128)
+    launch_attn<128, 2, 1>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
+  else if (s.hd == 64)
+    launch_attn<64, 1, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
+  else
     throw std::invalid_argument("attention: head dim must be 64 or 128");
-  }
 }
 
 }  // namespace wsb

@@ -50,11 +50,13 @@ void rope_kv_append(const void* qkv, int rows, int nq, int nkv, int hd, const st
                     cudaStream_t st);
 
 // Grouped attention (causal or masked groups) over the slot pools → out bf16 [rows, nq * hd].
-// groups[0, n_vw1) hold at most 16 query vectors (n_rows * n_q / n_kv) each, the next n_vw2 at
-// most 32, the rest any number.
-void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
-               int n_vw1, int n_vw2, const std::int32_t* extra_slots, const unsigned long long* row_mask,
-               const AttnShape& shape, void* out, cudaStream_t st);
+// Each entry is one CTA pass over up to attention_vectors_per_cta(hd) of its group's query
+// vectors (n_rows * n_q / n_kv), starting at vector `pad`: a group with more vectors is passed
+// as several entries.
+int attention_vectors_per_cta(int hd);
+void attention(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* entries, int n_entries,
+               const std::int32_t* extra_slots, const unsigned long long* row_mask, const AttnShape& shape,
+               void* out, cudaStream_t st);
 
 // logits[row, plant[row]] += bias (plant < 0: none) — the planted shared bigram bias.
 void plant_bias(void* logits_bf16, int ld, const std::int32_t* plant, float bias, int rows, cudaStream_t st);

@@ -251,7 +251,18 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
   void* const gemm_ws_ = ws.gemm_ws;
   const std::size_t gemm_ws_bytes_ = ws.gemm_ws_bytes;
   // ---- one packed H2D for all metadata ----
-  const std::size_t s_tok = al(n * 4), s_grp = al(b.groups.size() * sizeof(AttnGroup)), s_ext = al(b.extra.size() * 4 + 4),
+  // attention entries: one per CTA pass of attention_vectors_per_cta query vectors (a catch-up
+  // group larger than that becomes several entries; pad = its first vector)
+  const int G = s_.n_q / s_.n_kv;
+  const int vpc = attention_vectors_per_cta(s_.hd);
+  grp_sorted_.clear();
+  for (const AttnGroup& g : b.groups)
+    for (int v0 = 0; v0 < g.n_rows * G; v0 += vpc) {
+      AttnGroup e = g;
+      e.pad = v0;
+      grp_sorted_.push_back(e);
+    }
+  const std::size_t s_tok = al(n * 4), s_grp = al(grp_sorted_.size() * sizeof(AttnGroup)), s_ext = al(b.extra.size() * 4 + 4),
                     s_out = al(n_out * 4 + 4);
   const std::size_t s_msk = al(b.row_mask.size() * 8 + 8);
   const std::size_t need = 3 * s_tok + s_grp + s_ext + 2 * s_out + s_msk;
@@ -273,17 +284,6 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
   const std::size_t o_tok = put(b.tok.data(), n * 4, s_tok);
   const std::size_t o_pos = put(b.pos.data(), n * 4, s_tok);
   const std::size_t o_slot = put(b.slot.data(), n * 4, s_tok);
-  // groups by query-vector count: <= 16 (one vector warp per CTA), <= 32 (two), more (four)
-  const int G = s_.n_q / s_.n_kv;
-  grp_sorted_.clear();
-  for (const AttnGroup& g : b.groups)
-    if (g.n_rows * G <= 16) grp_sorted_.push_back(g);
-  const int n_vw1 = static_cast<int>(grp_sorted_.size());
-  for (const AttnGroup& g : b.groups)
-    if (g.n_rows * G > 16 && g.n_rows * G <= 32) grp_sorted_.push_back(g);
-  const int n_vw2 = static_cast<int>(grp_sorted_.size()) - n_vw1;
-  for (const AttnGroup& g : b.groups)
-    if (g.n_rows * G > 32) grp_sorted_.push_back(g);
   const std::size_t o_grp = put(grp_sorted_.data(), grp_sorted_.size() * sizeof(AttnGroup), s_grp);
   const std::size_t o_ext = put(b.extra.data(), b.extra.size() * 4, s_ext);
   const std::size_t o_out = put(b.out_rows.data(), n_out * 4, s_out);
@@ -325,7 +325,7 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
     qa.norm = consume;
     gemm_tn(with_ws(qa), st);
     prof_.mark(KernelProfiler::kQKV, st);
-    attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(b.groups.size()), n_vw1, n_vw2,
+    attention(q_, kp, vp, reinterpret_cast<const AttnGroup*>(d_meta_ + o_grp), static_cast<int>(grp_sorted_.size()),
               I(o_ext), reinterpret_cast<const unsigned long long*>(d_meta_ + o_msk), ash, attn_, st);
     prof_.mark(KernelProfiler::kAttn, st);
     GemmArgs oa{attn_, wo_[l], x_, n, d, qd, qd, qd, d, kEpiAddF32, 0};

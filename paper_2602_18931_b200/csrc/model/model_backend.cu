@@ -277,11 +277,12 @@ void ModelBackend_Llama::fill_ctx(const RoundJobs& jobs, std::uint32_t r, const 
 // few rows past a multiple of 256 pays a whole extra row block in every projection. When the
 // overflow is at most kSlack rows, the trailing jobs are left for the lane's next batch (they
 // lead it). Rows per job = the context tokens missing from its cache (a read-only LCP pass).
-// WS_VERIFY_TRIM=0 disables.
+// Off by default (WS_VERIFY_TRIM=1 enables): measured on config 3 it turns 129 verify forwards
+// into 150 smaller ones at the same step time (2.70 s both ways).
 std::size_t ModelBackend_Llama::verify_take(const RoundJobs& jobs) {
   static const bool on = [] {
     const char* e = std::getenv("WS_VERIFY_TRIM");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   const std::size_t nv = jobs.verify.size();
   if (!on || nv < 2) return nv;
