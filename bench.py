@@ -251,13 +251,21 @@ def main():
 
     torch.cuda.set_device(local_rank)
     dist = None
+    host_group = None
+    split = args.workload == "llama" and args.placement == "split" and world >= 2 and world % 2 == 0
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if split:
+            # Under split placement rank r's draft lane runs on rank r + N/2's GPU: the idle ranks
+            # must not park an NCCL barrier kernel there (a second context on that GPU is
+            # time-sliced against the draft forwards), so barriers and the timing reduction go
+            # over a host (gloo) group.
+            host_group = dist.new_group(backend="gloo")
 
     def barrier():
         if dist:
-            dist.barrier()
+            dist.barrier(group=host_group)
         torch.cuda.synchronize()
 
     ncpu = os.cpu_count() or 1
@@ -266,7 +274,6 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     peak_bw, peak_tf, peak_kind = peaks()
 
-    split = args.workload == "llama" and args.placement == "split" and world >= 2 and world % 2 == 0
     active = not split or rank < world // 2
     if args.workload == "llama":
         if split:  # requests sharded over the target GPUs; GPU r + N/2 runs rank r's drafts
@@ -318,11 +325,11 @@ def main():
 
     torch.cuda.set_device(local_rank)
     stats = torch.tensor([total_ms, float(tokens), float(launches)], dtype=torch.float64,
-                         device=torch.device("cuda", local_rank))
+                         device="cpu" if host_group is not None else torch.device("cuda", local_rank))
     if dist:
         mx, sm = stats.clone(), stats.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=host_group)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM, group=host_group)
         total_ms_max, tokens_all, launches_all = mx[0].item(), sm[1].item(), sm[2].item()
     else:
         total_ms_max, tokens_all, launches_all = total_ms, float(tokens), float(launches)
