@@ -275,6 +275,13 @@ int ws_model_load(ws_ctx* ctx, const ws_model_cfg* cfg);
  * on its own GPU; requests' proposals and verify results meet in the host driver. A negative
  * draft_device is ws_model_load. */
 int ws_model_load_split(ws_ctx* ctx, const ws_model_cfg* cfg, int draft_device);
+/* Teacher-forced trace export (the reference's docs/trace_format.md records):
+ * for requests [first_request, first_request + n) of the loaded pair, the target's greedy
+ * continuation of each prompt for `length` positions; every record holds the target's and the
+ * draft's top-2 and entropy on the same committed context (the reference's TokenRecord,
+ * oracle.hpp:52-70). out: n * length records, request-major. Resets the pair's KV caches. */
+int ws_model_export_trace(ws_ctx* ctx, uint32_t first_request, uint32_t n, uint32_t length,
+                          ws_token_record* out);
 /* run_sim_full (sim.hpp:429-442) with the verify / draft model calls on the loaded models;
  * cfg->oracle supplies vocab_size (must equal the models'), eos_id and sequence_length. */
 int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);

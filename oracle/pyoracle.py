@@ -72,6 +72,9 @@ def _load_ref():
     lib.ref_draft_prediction.argtypes = [_P(abi.TokenRecord), C.c_uint32, C.c_uint32,
                                          C.c_uint64, _P(abi.Pred)]
     lib.ref_entropy_of.argtypes = [_P(C.c_double), C.c_size_t, _P(C.c_double)]
+    lib.ref_set_trace_path.argtypes = [C.c_char_p]
+    lib.ref_trace_deal.argtypes = [_P(abi.OracleCfg), C.c_char_p, C.c_uint32, C.c_uint32, _P(abi.TokenRecord),
+                                   _P(C.c_uint32), C.c_char_p, C.c_size_t]
     return lib
 
 
@@ -188,6 +191,28 @@ def ref_run_sim(cfg, threads=1, with_tokens=True, with_steps=True):
     if rc != 0:
         raise RuntimeError(f"ref_run_sim rc={rc}: {err.value.decode()}")
     return bufs
+
+
+def ref_run_sim_trace(cfg, path, threads=1, with_tokens=True, with_steps=True):
+    """run_sim_full with the reference's trace oracle (OracleKind::trace) replaying `path`."""
+    lib = ref_lib()
+    lib.ref_set_trace_path(path.encode())
+    try:
+        return ref_run_sim(cfg, threads, with_tokens, with_steps)
+    finally:
+        lib.ref_set_trace_path(None)
+
+
+def ref_trace_deal(ocfg, path, n, max_len):
+    """The first n sequences the reference's trace oracle deals from `path` (its validation and
+    seeded shuffle): (records n * max_len, lengths)."""
+    recs = (abi.TokenRecord * (n * max_len))()
+    lens = (C.c_uint32 * n)()
+    err = C.create_string_buffer(512)
+    rc = ref_lib().ref_trace_deal(C.byref(ocfg), path.encode(), n, max_len, recs, lens, err, 512)
+    if rc != 0:
+        raise RuntimeError(f"ref_trace_deal rc={rc}: {err.value.decode()}")
+    return recs, list(lens)
 
 
 def model_round_fn(cfg):

@@ -66,6 +66,10 @@ void to_record(const wanspec::TokenRecord& r, ws_token_record* o) {
   o->draft_entropy = r.draft_prediction.entropy;
 }
 
+// When set (ref_set_trace_path), runs use the reference's trace oracle on that NDJSON file
+// (OracleKind::trace, oracle.hpp:258-290) instead of the stochastic tiny pair.
+std::string g_trace_path;
+
 wanspec::SimConfig to_sim(const ws_sim_cfg* c) {
   wanspec::SimConfig s;
   s.mode = c->mode == WS_MODE_BASELINE ? wanspec::SimMode::baseline : wanspec::SimMode::wanspec;
@@ -153,6 +157,10 @@ extern "C" {
 int ref_run_sim(const ws_sim_cfg* c, int threads, ws_run_out* out, char* err, std::size_t errlen) {
   try {
     wanspec::SimConfig cfg = to_sim(c);
+    if (!g_trace_path.empty()) {
+      cfg.oracle.kind = wanspec::OracleKind::trace;
+      cfg.oracle.trace_path = g_trace_path;
+    }
     cfg.validate();
     if (c->first_request >= c->num_requests) throw wanspec::ConfigError("shard out of range");
     std::uint32_t local = c->local_requests ? c->local_requests : c->num_requests - c->first_request;
@@ -235,6 +243,37 @@ int ref_run_sim(const ws_sim_cfg* c, int threads, ws_run_out* out, char* err, st
   } catch (const std::exception& e) {
     set_err(err, errlen, e.what());
     return WS_ELOGIC;
+  }
+}
+
+// Trace oracle selection for ref_run_sim / ref_trace_deal (nullptr or "" = stochastic).
+void ref_set_trace_path(const char* path) { g_trace_path = path ? path : ""; }
+
+// The reference's trace oracle over `path` (validation, seeded shuffle, oracle.hpp:183-290):
+// the first n dealt sequences as records, n * max_len, positions past a sequence's length left
+// zero; lens[s] = its stored length.
+int ref_trace_deal(const ws_oracle_cfg* c, const char* path, std::uint32_t n, std::uint32_t max_len,
+                   ws_token_record* out, std::uint32_t* lens, char* err, std::size_t errlen) {
+  try {
+    wanspec::OracleConfig oc;
+    oc.kind = wanspec::OracleKind::trace;
+    oc.trace_path = path;
+    oc.seed = c->seed;
+    oc.vocab_size = c->vocab_size;
+    oc.eos_id = c->eos_id;
+    oc.sequence_length = c->sequence_length;
+    wanspec::Oracle o = wanspec::Oracle::open(oc);
+    for (std::uint32_t s = 0; s < n; ++s) {
+      wanspec::SequenceTrace t = o.next_sequence();
+      if (t.length() > max_len) throw wanspec::ConfigError("trace sequence longer than max_len");
+      lens[s] = static_cast<std::uint32_t>(t.length());
+      for (std::size_t i = 0; i < t.length(); ++i)
+        to_record(t.records()[i], &out[static_cast<std::size_t>(s) * max_len + i]);
+    }
+    return WS_OK;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return WS_ECONFIG;
   }
 }
 

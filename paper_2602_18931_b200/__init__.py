@@ -67,6 +67,7 @@ def lib():
     L.ws_run_sim_with_model.argtypes = [_P(abi.SimCfg), MODEL_ROUND_FN, C.c_void_p, _P(abi.RunOut)]
     L.ws_model_load.argtypes = [C.c_void_p, _P(abi.ModelCfg)]
     L.ws_model_load_split.argtypes = [C.c_void_p, _P(abi.ModelCfg), C.c_int]
+    L.ws_model_export_trace.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, _P(abi.TokenRecord)]
     L.ws_run_model_sim.argtypes = [C.c_void_p, _P(abi.SimCfg), _P(abi.RunOut)]
     L.ws_model_stats.argtypes = [C.c_void_p, _P(C.c_double), _P(C.c_double), _P(C.c_uint64), _P(C.c_uint64),
                                  _P(C.c_uint64), _P(C.c_uint64)]
@@ -163,6 +164,13 @@ class Context:
         (the draft model on `draft_device` under split placement)."""
         self._mcfg = mcfg  # keep the C strings alive
         _check(lib().ws_model_load_split(self._h, C.byref(mcfg), int(draft_device)))
+
+    def export_trace(self, first_request, n, length):
+        """Teacher-forced records of the loaded pair (ws_model_export_trace): n * length
+        TokenRecords, request-major (see trace.py for the reference's NDJSON format)."""
+        recs = (abi.TokenRecord * (n * length))()
+        _check(lib().ws_model_export_trace(self._h, first_request, n, length, recs))
+        return recs
 
     def run_model_sim(self, cfg, with_tokens=True, with_steps=True):
         """run_sim_full with the verify/draft model calls on the loaded models."""

@@ -156,6 +156,15 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
   });
 }
 
+int ws_model_export_trace(ws_ctx* ctx, uint32_t first_request, uint32_t n, uint32_t length, ws_token_record* out) {
+  return guard("ws_model_export_trace", [&] {
+    if (!ctx || !out) throw std::invalid_argument("null argument");
+    if (!ctx->models) throw wsb::ConfigError("no model loaded (ws_model_load)");
+    wsb::DeviceGuard dg(ctx->device);
+    ctx->models->export_trace(first_request, n, length, out);
+  });
+}
+
 int ws_model_stats(ws_ctx*, double* target_ms, double* draft_ms, uint64_t* target_rows, uint64_t* draft_rows,
                    uint64_t* target_forwards, uint64_t* draft_forwards) {
   if (target_ms) *target_ms = g_last.target_ms;

@@ -189,6 +189,98 @@ void ModelPair::reset_requests() {
   impl->wrk.assign(cfg_.max_requests, TreeCache{});
 }
 
+void ModelPair::export_trace(std::uint32_t first, std::uint32_t n, std::uint32_t length, ws_token_record* out) {
+  if (first + n > cfg_.max_requests) throw ConfigError("export_trace: requests exceed max_requests");
+  if (cfg_.prompt_len + length > cfg_.max_ctx) throw ConfigError("export_trace: prompt + length exceeds max_ctx");
+  if (n == 0 || length == 0) return;
+  const std::int32_t P = static_cast<std::int32_t>(cfg_.prompt_len), MC = static_cast<std::int32_t>(cfg_.max_ctx);
+  const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg_.trie_slots);
+  const std::uint32_t V = static_cast<std::uint32_t>(target_->shape().vocab);
+  reset_requests();
+  struct Side {
+    LlamaModel* m;
+    int dev;
+    bool draft;
+    std::int32_t stride;
+    cudaStream_t st = nullptr;
+    std::unique_ptr<ForwardWorkspace> ws;
+    ws_pred* d_pred = nullptr;
+    void* d_rs = nullptr;
+    std::vector<ws_pred> h;
+  } sides[2] = {{target_.get(), device_, false, MC}, {draft_.get(), draft_device_, true, S}};
+  const std::uint32_t rows_max = n * static_cast<std::uint32_t>(P);
+  for (Side& sd : sides) {
+    DeviceGuard dg(sd.dev);
+    WS_CUDA(cudaStreamCreateWithFlags(&sd.st, cudaStreamNonBlocking));
+    sd.ws = sd.m->make_workspace(static_cast<int>(rows_max));
+    WS_CUDA(cudaMalloc(&sd.d_pred, n * sizeof(ws_pred)));
+    const std::size_t wb = rowstats_workspace_bytes(n, V, 0);
+    WS_CUDA(cudaMalloc(&sd.d_rs, wb));
+    WS_CUDA(cudaMemset(sd.d_rs, 0, wb));
+    sd.h.resize(n);
+  }
+  std::vector<TokenId> last(n);  // the token fed at each step (prompt tail, then greedy)
+  for (std::uint32_t i = 0; i < length; ++i) {
+    for (Side& sd : sides) {
+      DeviceGuard dg(sd.dev);
+      ForwardBatch b;
+      for (std::uint32_t j = 0; j < n; ++j) {
+        const std::uint32_t r = first + j;
+        const std::vector<TokenId>& pr = prompt(r);
+        const std::int32_t base = static_cast<std::int32_t>(r) * sd.stride;
+        const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
+        const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
+        // step 0 prefills the prompt; step i feeds the greedy token of position i - 1
+        const std::int32_t p0 = i == 0 ? 0 : P + static_cast<std::int32_t>(i) - 1;
+        const std::int32_t p1 = i == 0 ? P : p0 + 1;
+        for (std::int32_t p = p0; p < p1; ++p) {
+          const TokenId t = i == 0 ? pr[p] : last[j];
+          b.tok.push_back(static_cast<std::int32_t>(t));
+          b.pos.push_back(p);
+          b.slot.push_back(base + p);
+          b.extra.push_back(base + p);
+        }
+        b.groups.push_back(AttnGroup{row0, p1 - p0, base, p0, eoff, p1 - p0});
+        b.out_rows.push_back(static_cast<std::int32_t>(b.tok.size()) - 1);
+        b.plant.push_back(plant(static_cast<TokenId>(b.tok.back()), sd.draft));
+      }
+      b.row_mask.assign(b.tok.size(), 0ull);
+      sd.m->forward(b, sd.draft ? cfg_.plant_draft : cfg_.plant_target, sd.st, *sd.ws);
+      row_stats_bf16(sd.ws->logits, n, V, V, 1.0f, sd.d_pred, nullptr, sd.d_rs, 0, 0, nullptr, nullptr, sd.st,
+                     nullptr);
+      WS_CUDA(cudaMemcpyAsync(sd.h.data(), sd.d_pred, n * sizeof(ws_pred), cudaMemcpyDeviceToHost, sd.st));
+    }
+    for (Side& sd : sides) {
+      DeviceGuard dg(sd.dev);
+      WS_CUDA(cudaStreamSynchronize(sd.st));
+    }
+    for (std::uint32_t j = 0; j < n; ++j) {
+      const ws_pred& t = sides[0].h[j];
+      const ws_pred& d = sides[1].h[j];
+      ws_token_record& rec = out[static_cast<std::size_t>(j) * length + i];
+      rec.target_token = t.id[0];
+      rec.target_top2 = t.id[1];
+      rec.target_p1 = t.prob[0];
+      rec.target_p2 = t.n > 1 ? t.prob[1] : 0.0;
+      rec.target_entropy = t.entropy;
+      rec.draft_top1 = d.id[0];
+      rec.draft_top2 = d.id[1];
+      rec.draft_p1 = d.prob[0];
+      rec.draft_p2 = d.n > 1 ? d.prob[1] : 0.0;
+      rec.draft_entropy = d.entropy;
+      last[j] = t.id[0];  // teacher forcing along the target's greedy path
+    }
+  }
+  for (Side& sd : sides) {
+    DeviceGuard dg(sd.dev);
+    sd.ws.reset();
+    cudaFree(sd.d_pred);
+    cudaFree(sd.d_rs);
+    cudaStreamDestroy(sd.st);
+  }
+  reset_requests();  // the requests' KV regions were overwritten
+}
+
 const std::vector<TokenId>& ModelPair::prompt(std::uint32_t r) {
   if (r >= prompts_.size()) throw ConfigError("request index exceeds max_requests");
   std::vector<TokenId>& p = prompts_[r];

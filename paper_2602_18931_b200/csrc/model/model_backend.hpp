@@ -85,6 +85,11 @@ class ModelPair {
   ModelPair(const ModelPairCfg& cfg, int device);
   ~ModelPair();
   void reset_requests();  // forget all cached KV state (new run)
+  // Teacher-forced trace export: for requests [first, first + n), the target's
+  // greedy continuation of the prompt for `length` positions; at every position the target's
+  // and the draft's top-2 / entropy on the same (committed) context. out: n * length records,
+  // request-major. Overwrites the requests' KV (the caches are reset).
+  void export_trace(std::uint32_t first, std::uint32_t n, std::uint32_t length, ws_token_record* out);
   const ModelPairCfg& cfg() const { return cfg_; }
   LlamaModel& target() { return *target_; }
   LlamaModel& draft() { return *draft_; }
