@@ -350,7 +350,15 @@ def main():
             local = cfg.local_requests
             avg_ctx = 128 + 50 + args.k / 2
             roof, rows, fl, by, t_meas = llama_roofline(mstats, args.k, peak_bw, peak_tf, avg_ctx)
-            roof.update({"traffic": None, "kernel": "verify step (target forward + K3/K4)",
+            traffic = None
+            tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_verify_traffic.json")
+            if os.path.exists(tpath):  # ncu dram bytes of one verify forward (committed capture)
+                with open(tpath) as f:
+                    tj = json.load(f)
+                traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
+                roof["traffic_rows"] = tj["rows"]
+                roof["traffic_source"] = "profiles/r01_verify_traffic.json (ncu, verify forward at %d rows)" % tj["rows"]
+            roof.update({"traffic": traffic, "kernel": "verify step (target forward + K3/K4)",
                          "peak_kind": peak_kind, "rows_per_verify": rows, "ms_per_verify": t_meas * 1e3,
                          "alg_flops_per_verify": fl, "alg_bytes_per_verify": by})
             line["roofline"] = roof
