@@ -625,13 +625,15 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   const int smem = smem_bytes(bn, CG), stages = ring_stages(bn, CG);
   if constexpr (CG == 1) {
     const int total = m_blocks * n_tiles * sk.splits;
-    const int grid = std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
+    // max_ctas < 0: one CTA per unit (not persistent: SMs free up between units, so a
+    // concurrent higher-priority stream's kernels get scheduled sooner)
+    const int grid = g.max_ctas < 0 ? total : std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
     const int flags = ablate | (grid <= early_grid ? kEarlyTrigger : 0);
     launch_pdl(gemm_tn_kernel<EPI, 1>, dim3(grid), dim3(kThreads), smem, st, 1, ta, tb, g.M, g.N, g.K, m_blocks,
                n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
   } else {
     const int total = (m_blocks + 1) / 2 * n_tiles;
-    int clusters = std::min(total, pair_clusters());
+    int clusters = g.max_ctas < 0 ? total : std::min(total, pair_clusters());
     if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 2));
     const int flags = ablate | (2 * clusters <= early_grid ? kEarlyTrigger : 0);
     launch_pdl(gemm_tn_kernel<EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2, ta, tb, g.M, g.N, g.K,

@@ -48,7 +48,7 @@ struct GemmArgs {
   int lda, ldw, ldo;
   int epi = kEpiBF16;
   int bn = 0;        // 0 = auto (multiple of 32 in [64, 256]; see pick_bn)
-  int max_ctas = 0;  // persistent grid cap (0 = one CTA per SM)
+  int max_ctas = 0;  // persistent grid cap (0 = one CTA per SM; < 0 = one CTA per tile, not persistent)
   int cta_group = 0; // 0 = auto, 1 = single CTAs, 2 = CTA pairs (256-row tiles, cta_group::2)
   RopeEpi rope{};    // kEpiQKVRope only
   NormEpi norm{};    // fused RMSNorm producer / consumer (optional)

@@ -314,8 +314,9 @@ ModelBackend_Llama::ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, T
   int prio_lo = 0, prio_hi = 0;
   WS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   const char* dp = std::getenv("WS_DRAFT_PRIO");
-  const bool draft_first = !(dp && dp[0] == '0');
-  WS_CUDA(cudaStreamCreateWithPriority(&L.st_t, cudaStreamNonBlocking, prio_lo));
+  const bool draft_first = !(dp && (dp[0] == '0' || dp[0] == '-'));
+  const bool target_first = dp && dp[0] == '-';  // WS_DRAFT_PRIO=-1: the verify lane first
+  WS_CUDA(cudaStreamCreateWithPriority(&L.st_t, cudaStreamNonBlocking, target_first ? prio_hi : prio_lo));
   WS_CUDA(cudaEventCreate(&L.e0));
   WS_CUDA(cudaEventCreate(&L.e1));
   WS_CUDA(cudaEventCreateWithFlags(&L.done[0], cudaEventDisableTiming));
