@@ -10,6 +10,8 @@
 // can change a rounding: results are bit-identical to oracle/restate.c (-ffp-contract=off).
 #include "k9_oracle.cuh"
 
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 
 #include "cuda_check.hpp"
@@ -188,7 +190,9 @@ __global__ void __launch_bounds__(128) k9_round(KTables t, const VerifyJob* __re
                                                 const std::uint32_t* __restrict__ cands,
                                                 const DraftJob* __restrict__ dj, std::uint32_t nd,
                                                 VerifyOut* __restrict__ vo, ws_pred* __restrict__ dout,
-                                                int mode, std::uint32_t key0, std::uint32_t key1) {
+                                                int mode, std::uint32_t key0, std::uint32_t key1,
+                                                unsigned int* __restrict__ blocks_done,
+                                                unsigned long long* round_flag, unsigned long long round_id) {
   const std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g < nv) {
     const VerifyJob j = vj[g];
@@ -260,6 +264,17 @@ __global__ void __launch_bounds__(128) k9_round(KTables t, const VerifyJob* __re
     p.pad = 0;
     dout[g - nv] = p;
   }
+  // Completion without a driver call: every block's results are system-visible before it
+  // counts itself; the last block publishes the round id to the mapped flag the host spins on.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(blocks_done, 1u) == gridDim.x - 1) {
+      *blocks_done = 0;
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned long long*>(round_flag) = round_id;
+    }
+  }
 }
 
 KTables ktables(const DevTables& t) {
@@ -328,6 +343,11 @@ OracleLane::OracleLane(const DevTables* tables, int device) : t_(tables), device
   WS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   WS_CUDA(cudaEventCreate(&ev0_));
   WS_CUDA(cudaEventCreate(&ev1_));
+  WS_CUDA(cudaMalloc(&d_blocks_done_, sizeof(unsigned int)));
+  WS_CUDA(cudaMemset(d_blocks_done_, 0, sizeof(unsigned int)));
+  WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_flag_), sizeof(unsigned long long), cudaHostAllocMapped));
+  WS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_flag_), h_flag_, 0));
+  *h_flag_ = 0;
 }
 
 OracleLane::~OracleLane() {
@@ -335,6 +355,8 @@ OracleLane::~OracleLane() {
   if (h_out_) cudaFreeHost(h_out_);  // d_in_/d_out_ alias these mapped allocations
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
+  if (d_blocks_done_) cudaFree(d_blocks_done_);
+  if (h_flag_) cudaFreeHost(h_flag_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -374,18 +396,35 @@ void OracleLane::run_round(const RoundJobs& jobs, RoundResults& res, int verify_
   std::memcpy(h_in_ + sv, jobs.cands.data(), jobs.cands.size() * sizeof(std::uint32_t));
   std::memcpy(h_in_ + sv + sc, jobs.draft.data(), nd * sizeof(DraftJob));
   const std::uint32_t total = nv + nd;
-  const std::uint32_t threads = 128, blocks = (total + threads - 1) / threads;
-  WS_CUDA(cudaEventRecord(ev0_, stream_));
+  const std::uint32_t threads = 128, blocks = std::max<std::uint32_t>(1, (total + threads - 1) / threads);
+  // A round is one launch and a spin on the mapped completion flag (no sync call: with several
+  // protocol threads per GPU, driver calls serialise on the context). WS_PROFILE adds events.
+  static const bool timed = std::getenv("WS_PROFILE") != nullptr;
+  if (timed) WS_CUDA(cudaEventRecord(ev0_, stream_));
+  const unsigned long long id = ++round_id_;
   k9_round<<<blocks, threads, 0, stream_>>>(
       ktables(*t_), reinterpret_cast<const VerifyJob*>(d_in_), nv,
       reinterpret_cast<const std::uint32_t*>(d_in_ + sv), reinterpret_cast<const DraftJob*>(d_in_ + sv + sc), nd,
       reinterpret_cast<VerifyOut*>(d_out_), reinterpret_cast<ws_pred*>(d_out_ + ov), verify_mode,
-      static_cast<std::uint32_t>(sample_seed), static_cast<std::uint32_t>(sample_seed >> 32));
+      static_cast<std::uint32_t>(sample_seed), static_cast<std::uint32_t>(sample_seed >> 32), d_blocks_done_, d_flag_,
+      id);
   WS_CUDA(cudaGetLastError());
-  WS_CUDA(cudaEventRecord(ev1_, stream_));
-  WS_CUDA(cudaStreamSynchronize(stream_));
   float ms = 0.f;
-  WS_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  if (timed) WS_CUDA(cudaEventRecord(ev1_, stream_));
+  for (std::uint64_t spin = 1;; ++spin) {
+    if (*reinterpret_cast<volatile unsigned long long*>(h_flag_) == id) break;
+    if ((spin & 0xFFFFF) == 0) {  // surface a failed launch instead of spinning forever
+      const cudaError_t e = cudaStreamQuery(stream_);
+      if (e != cudaSuccess && e != cudaErrorNotReady) WS_CUDA(e);
+      if (e == cudaSuccess && *reinterpret_cast<volatile unsigned long long*>(h_flag_) != id)
+        throw CudaError("K9: round finished without publishing its completion flag");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  if (timed) {
+    WS_CUDA(cudaStreamSynchronize(stream_));
+    WS_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  }
   res.verify.resize(nv);
   res.draft.resize(nd);
   std::memcpy(res.verify.data(), h_out_, nv * sizeof(VerifyOut));

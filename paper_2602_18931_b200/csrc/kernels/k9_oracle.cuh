@@ -49,6 +49,10 @@ class OracleLane : public ModelBackend {
   int device_;
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  unsigned int* d_blocks_done_ = nullptr;      // last-block detection (device, self-resetting)
+  unsigned long long* h_flag_ = nullptr;       // mapped completion flag the host spins on
+  unsigned long long* d_flag_ = nullptr;
+  unsigned long long round_id_ = 0;
   unsigned char* h_in_ = nullptr;
   unsigned char* h_out_ = nullptr;
   unsigned char* d_in_ = nullptr;
