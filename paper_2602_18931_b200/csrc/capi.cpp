@@ -196,7 +196,7 @@ class CallbackBackend : public wsb::ModelBackend {
     stats.draft_rows += jobs.draft.size();
   }
 
-  // WS_EMULATE_LANES=1: the two-lane continuous-batching driver over the callback (CPU tests
+  // WS_EMULATE_LANES=1: the lanes continuous-batching driver (verify + two draft lanes) over the callback (CPU tests
   // of the lanes driver); completions are returned in a scrambled but seeded order, and every
   // batch of more than one job is cut in half (the rest stays pending — partial takes).
   bool has_lanes() const override { return lanes_; }
@@ -213,27 +213,28 @@ class CallbackBackend : public wsb::ModelBackend {
     run_round(one, done_[lane], mode, seed);
     return take;
   }
-  int wait_any(bool busy0, bool busy1) override {
-    if (busy0 && busy1) {
-      rng_ ^= rng_ << 13;
-      rng_ ^= rng_ >> 7;
-      rng_ ^= rng_ << 17;
-      return static_cast<int>(rng_ & 1);
-    }
-    return busy0 ? 0 : 1;
+  int n_lanes() const override { return 3; }  // verify + two draft lanes
+  int wait_any(std::uint32_t busy) override {
+    int lanes[3], n = 0;
+    for (int l = 0; l < 3; ++l)
+      if (busy & (1u << l)) lanes[n++] = l;
+    rng_ ^= rng_ << 13;
+    rng_ ^= rng_ >> 7;
+    rng_ ^= rng_ << 17;
+    return lanes[rng_ % static_cast<std::uint64_t>(n)];
   }
   void complete(int lane, wsb::RoundResults& res) override {
     if (lane == 0)
       res.verify.swap(done_[0].verify);
     else
-      res.draft.swap(done_[1].draft);
+      res.draft.swap(done_[lane].draft);
   }
 
  private:
   ws_model_round_fn fn_;
   void* user_;
   bool lanes_;
-  wsb::RoundResults done_[2];
+  wsb::RoundResults done_[3];
   std::uint64_t rng_ = 0x9E3779B97F4A7C15ULL;
 };
 

@@ -97,8 +97,7 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
     std::vector<wsb::ModelBackend_Llama*> used;
     for (std::uint32_t t = 0; t < threads; ++t) {
       owned[t]->reset_run(c->oracle.sequence_length, c->oracle.eos_id, c->k);
-      owned[t]->profiler(0).enable(prof);
-      owned[t]->profiler(1).enable(prof);
+      for (int lane = 0; lane < owned[t]->n_lanes(); ++lane) owned[t]->profiler(lane).enable(prof);
       backends.push_back(owned[t].get());
       used.push_back(owned[t].get());
     }
@@ -107,16 +106,17 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
       for (int which = 0; which < 2; ++which) {
         double ms[wsb::KernelProfiler::kClasses] = {};
         unsigned long long cnt[wsb::KernelProfiler::kClasses] = {};
-        for (auto* bk : used) {
-          wsb::KernelProfiler& p = bk->profiler(which);
-          p.collect();
-          for (int k = 0; k < wsb::KernelProfiler::kClasses; ++k) {
-            ms[k] += p.ms[k];
-            cnt[k] += p.count[k];
-            p.ms[k] = 0;
-            p.count[k] = 0;
+        for (auto* bk : used)
+          for (int lane = which; lane < (which == 0 ? 1 : bk->n_lanes()); ++lane) {
+            wsb::KernelProfiler& p = bk->profiler(lane);
+            p.collect();
+            for (int k = 0; k < wsb::KernelProfiler::kClasses; ++k) {
+              ms[k] += p.ms[k];
+              cnt[k] += p.count[k];
+              p.ms[k] = 0;
+              p.count[k] = 0;
+            }
           }
-        }
         std::fprintf(stderr, "[ws-profile] {\"model\": \"%s\"", which == 0 ? "target" : "draft");
         for (int k = 0; k < wsb::KernelProfiler::kClasses; ++k)
           std::fprintf(stderr, ", \"%s\": [%.3f, %llu]", wsb::KernelProfiler::name(k), ms[k], cnt[k]);
@@ -124,7 +124,7 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
       }
     }
     LastStats st;
-    std::uint64_t rows_kind[3] = {0, 0, 0}, jobs_kind[3] = {0, 0, 0}, rep_kind[3] = {0, 0, 0};
+    std::uint64_t rows_kind[3] = {0, 0, 0}, jobs_kind[3] = {0, 0, 0};
     for (auto* bk : used) {
       st.target_ms += bk->target_ms;
       st.draft_ms += bk->draft_ms;
@@ -135,7 +135,6 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
       for (int k = 0; k < 3; ++k) {
         rows_kind[k] += bk->rows_by_kind[k];
         jobs_kind[k] += bk->jobs_by_kind[k];
-        rep_kind[k] += bk->repeat_by_kind[k];
       }
     }
     g_last = st;
@@ -147,8 +146,6 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
                    (unsigned long long)rows_kind[1], (unsigned long long)jobs_kind[1],
                    (unsigned long long)rows_kind[2], (unsigned long long)jobs_kind[2],
                    (unsigned long long)st.draft_forwards, st.draft_ms);
-      std::fprintf(stderr, "[ws] repeated draft contexts: ctrl %llu, worker %llu\n", (unsigned long long)rep_kind[1],
-                   (unsigned long long)rep_kind[2]);
       for (auto* bk : used)
         std::fprintf(stderr, "[ws] host ms: submit verify %.1f, submit draft %.1f, wait %.1f\n", bk->host_submit_ms[0],
                      bk->host_submit_ms[1], bk->host_wait_ms);

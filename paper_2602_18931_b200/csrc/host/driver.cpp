@@ -461,13 +461,18 @@ void requeue_draft(RoundJobs& fly, std::vector<RequestRun::DraftSlot>& fly_slots
   fly_slots.resize(took);
 }
 
-// Continuous batching over the backend's two lanes (see ModelBackend).
+// Continuous batching over the backend's lanes (see ModelBackend): lane 0 takes verify jobs,
+// lanes 1..n-1 take draft jobs — with several draft lanes the next draft batch is planned and
+// launched while the previous one still runs, so the critical draft path never waits on the
+// host.
 void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::size_t n, ModelBackend& backend,
                         RequestOutput* outs, bool log_steps) {
+  const int n_lanes = std::max(2, backend.n_lanes());
   std::vector<std::unique_ptr<RequestRun>> runs;
   runs.reserve(n);
   std::vector<RequestRun*> vslots, vslots_fly;
-  std::vector<RequestRun::DraftSlot> dslots, dslots_fly;
+  std::vector<RequestRun::DraftSlot> dslots;
+  std::vector<std::vector<RequestRun::DraftSlot>> dslots_fly(n_lanes);
   for (std::size_t i = 0; i < n; ++i) {
     runs.emplace_back(new RequestRun(cfg, requests[i], log_steps));
     runs.back()->verify_slots_ = &vslots;
@@ -475,14 +480,16 @@ void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::s
   }
   std::unordered_map<const RequestRun*, std::size_t> index;
   for (std::size_t i = 0; i < n; ++i) index[runs[i].get()] = i;
-  RoundJobs pend_v, pend_d, fly_v, fly_d;
-  pend_v.want_ctx = pend_d.want_ctx = fly_v.want_ctx = fly_d.want_ctx = backend.wants_context();
+  RoundJobs pend_v, pend_d;
+  std::vector<RoundJobs> fly(n_lanes);
+  pend_v.want_ctx = pend_d.want_ctx = backend.wants_context();
+  for (RoundJobs& f : fly) f.want_ctx = backend.wants_context();
   RoundResults res;
   std::vector<std::size_t> ready(n);
   for (std::size_t i = 0; i < n; ++i) ready[i] = i;
   std::vector<char> queued(n, 0);
   std::size_t live = n;
-  bool busy[2] = {false, false};
+  std::uint32_t busy = 0;  // bit per lane
   auto wake = [&](RequestRun* r) {
     const std::size_t i = index[r];
     if (!queued[i]) {
@@ -501,36 +508,45 @@ void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::s
     }
     ready.clear();
     if (live == 0) break;
-    if (!busy[0] && !pend_v.verify.empty()) {
-      std::swap(pend_v, fly_v);
+    for (int lane = 1; lane < n_lanes && !pend_d.draft.empty(); ++lane) {
+      if (busy & (1u << lane)) continue;
+      std::swap(pend_d, fly[lane]);
+      std::swap(dslots, dslots_fly[lane]);
+      pend_d.clear();
+      dslots.clear();
+      const std::size_t took = backend.submit(lane, fly[lane], cfg.verify, cfg.sample_seed);
+      if (took < fly[lane].draft.size()) requeue_draft(fly[lane], dslots_fly[lane], took, pend_d, dslots);
+      busy |= 1u << lane;
+    }
+    // Verify batching: a verify batch of fewer than vmin jobs waits while a draft batch is in
+    // flight (it joins the jobs that arrive meanwhile). Config 3 on one B200: 128 → 71 verify
+    // forwards per run at the same rows, +3% tokens/s (profiles/r01_driver_policy.md).
+    // WS_VERIFY_MIN overrides (0: submit whenever the verify lane is idle).
+    static const std::size_t vmin = [] {
+      const char* e = std::getenv("WS_VERIFY_MIN");
+      return e ? static_cast<std::size_t>(std::atoi(e)) : std::size_t{32};
+    }();
+    if (!(busy & 1u) && !pend_v.verify.empty() && (pend_v.verify.size() >= vmin || !(busy & ~1u))) {
+      std::swap(pend_v, fly[0]);
       std::swap(vslots, vslots_fly);
       pend_v.clear();
       vslots.clear();
-      const std::size_t took = backend.submit(0, fly_v, cfg.verify, cfg.sample_seed);
-      if (took < fly_v.verify.size()) requeue_verify(fly_v, vslots_fly, took, pend_v, vslots);
-      busy[0] = true;
+      const std::size_t took = backend.submit(0, fly[0], cfg.verify, cfg.sample_seed);
+      if (took < fly[0].verify.size()) requeue_verify(fly[0], vslots_fly, took, pend_v, vslots);
+      busy |= 1u;
     }
-    if (!busy[1] && !pend_d.draft.empty()) {
-      std::swap(pend_d, fly_d);
-      std::swap(dslots, dslots_fly);
-      pend_d.clear();
-      dslots.clear();
-      const std::size_t took = backend.submit(1, fly_d, cfg.verify, cfg.sample_seed);
-      if (took < fly_d.draft.size()) requeue_draft(fly_d, dslots_fly, took, pend_d, dslots);
-      busy[1] = true;
-    }
-    if (!busy[0] && !busy[1]) throw std::logic_error("driver: requests blocked with no pending model step");
-    const int lane = backend.wait_any(busy[0], busy[1]);
+    if (!busy) throw std::logic_error("driver: requests blocked with no pending model step");
+    const int lane = backend.wait_any(busy);
     backend.complete(lane, res);
-    busy[lane] = false;
+    busy &= ~(1u << lane);
     if (lane == 0) {
       for (std::size_t j = 0; j < vslots_fly.size(); ++j) {
         vslots_fly[j]->deliver_verify(res.verify[j]);
         wake(vslots_fly[j]);
       }
     } else {
-      for (std::size_t j = 0; j < dslots_fly.size(); ++j) {
-        const auto& s = dslots_fly[j];
+      for (std::size_t j = 0; j < dslots_fly[lane].size(); ++j) {
+        const auto& s = dslots_fly[lane][j];
         if (s.which == RequestRun::kLocalSlot)
           s.run->deliver_local(res.draft[j]);
         else
@@ -546,7 +562,7 @@ void run_requests_lanes(const SimCfg& cfg, const std::uint32_t* requests, std::s
 std::size_t ModelBackend::submit(int, const RoundJobs&, int, std::uint64_t) {
   throw std::logic_error("backend has no asynchronous lanes");
 }
-int ModelBackend::wait_any(bool, bool) { throw std::logic_error("backend has no asynchronous lanes"); }
+int ModelBackend::wait_any(std::uint32_t) { throw std::logic_error("backend has no asynchronous lanes"); }
 void ModelBackend::complete(int, RoundResults&) { throw std::logic_error("backend has no asynchronous lanes"); }
 
 void run_requests(const SimCfg& cfg, const std::uint32_t* requests, std::size_t n,

@@ -92,13 +92,14 @@ class ModelBackend {
                          std::uint64_t sample_seed) = 0;
   virtual bool wants_context() const { return false; }
   virtual bool has_lanes() const { return false; }
+  virtual int n_lanes() const { return 2; }  // lane 0: verify; lanes 1..n-1: draft
   // lane 0 reads jobs.verify/cands/verify_ctx, lane 1 jobs.draft/draft_ctx (+ ctx_tokens);
   // `jobs` must stay alive and unchanged until complete(lane). Returns how many of the lane's
   // jobs (a prefix) it took; the driver keeps the rest pending for the lane's next batch (a
   // backend may trim a batch to a tile-friendly size).
   virtual std::size_t submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed);
-  virtual int wait_any(bool busy0, bool busy1);        // blocks until a busy lane is done
-  virtual void complete(int lane, RoundResults& res);  // fills res.verify (0) / res.draft (1)
+  virtual int wait_any(std::uint32_t busy_lanes);      // blocks until a busy lane (bit) is done
+  virtual void complete(int lane, RoundResults& res);  // fills res.verify (lane 0) / res.draft
   BackendStats stats;
 };
 

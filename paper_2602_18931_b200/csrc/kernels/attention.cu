@@ -71,11 +71,12 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 }
 
 // VW x KS warps per CTA: VW vector warps (16 query vectors each) times KS key slices. Slice
-// ks streams the K/V tiles t = ks, ks + KS, ... through its own double buffer, so a CTA keeps
-// KS tiles in flight; at the end of a pass the slices' softmax states merge in slice order.
-// KS is fixed per head dim (never chosen from the group), so a row's result is the same in any
-// group of any batch (batch invariance: speculative stream == greedy stream).
-template <int HD, int VW, int KS>
+// ks streams the K/V tiles t = ks, ks + KS, ... through its own STAGES-deep cp.async ring, so a
+// CTA keeps KS * (STAGES - 1) tiles in flight; at the end of a pass the slices' softmax states
+// merge in slice order. KS is fixed per head dim (never chosen from the group), so a row's
+// result is the same in any group of any batch (batch invariance: speculative stream == greedy
+// stream); STAGES only changes how far ahead the loads run.
+template <int HD, int VW, int KS, int STAGES>
 __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloat16* __restrict__ q,
                                                                  const __nv_bfloat16* __restrict__ kp,
                                                                  const __nv_bfloat16* __restrict__ vp,
@@ -92,12 +93,15 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
   constexpr int kSliceThreads = 32 * VW;
   constexpr int kVecPerPass = 16 * VW;
   constexpr int kMergeFloats = 4 + 4 * NT;  // m_lo, m_hi, l_lo, l_hi, o[NT][4] per lane
-  static_assert((KS - 1) * VW * 32 * kMergeFloats * 4 <= KS * 2 * 2 * kTile * C * 16, "merge scratch");
-  // dynamic smem: Q tile, then [slice][buffer][K | V] tiles (attn_smem_bytes)
+  static_assert((KS - 1) * VW * 32 * kMergeFloats * 4 <= KS * STAGES * 2 * kTile * C * 16, "merge scratch");
+  static_assert(STAGES >= 2, "ring depth");
+  // dynamic smem: Q tile, then [slice][stage][K | V] tiles (launch_attn's kSmem)
   extern __shared__ __align__(128) uint4 smem_dyn[];
   uint4* sQ = smem_dyn;
   uint4* sKV0 = smem_dyn + kVecPerPass * C;
-  auto kv_tile = [&](int slice, int buf, int which) { return sKV0 + ((slice * 2 + buf) * 2 + which) * (kTile * C); };
+  auto kv_tile = [&](int slice, int buf, int which) {
+    return sKV0 + ((slice * STAGES + buf) * 2 + which) * (kTile * C);
+  };
 
   const AttnGroup g = groups[blockIdx.x];
   const int kvh = blockIdx.y;
@@ -139,8 +143,11 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
       }
       sQ[swz<HD>(vv, c)] = val;
     }
-    load_tile(ks, 0);
-    cp_async_commit();
+#pragma unroll
+    for (int i = 0; i < STAGES - 1; ++i) {  // ring prologue: this slice's first STAGES-1 tiles
+      if (i < n_iter) load_tile(i * KS + ks, i);
+      cp_async_commit();
+    }
     __syncthreads();
 
     // this warp's 16 query vectors; the thread's two accumulator rows
@@ -181,13 +188,12 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
 
     for (int it = 0; it < n_iter; ++it) {
       const int t = it * KS + ks;  // this slice's tile
-      const int buf = it & 1;
-      if (it + 1 < n_iter) {
-        load_tile(t + KS, buf ^ 1);
+      const int buf = it % STAGES;
+      {  // refill the stage consumed last iteration; one (possibly empty) group per iteration
+        const int ahead = it + STAGES - 1;
+        if (ahead < n_iter) load_tile(ahead * KS + ks, ahead % STAGES);
         cp_async_commit();
-        cp_async_wait1();
-      } else {
-        cp_async_wait0();
+        asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
       }
       __syncthreads();
       if (warp_live && t < n_tiles) {
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
           }
         }
       }
-      __syncthreads();  // buffer `buf` of every slice is refilled two iterations later
+      __syncthreads();  // stage `buf` of every slice is refilled next iteration
     }
     // merge the KS slices' states (slice order, in the K/V scratch), then normalise + store
     if constexpr (KS > 1) {
@@ -344,18 +350,19 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
 
 }  // namespace
 
-template <int HD, int VW, int KS>
+template <int HD, int VW, int KS, int STAGES>
 void launch_attn(const void* q, const void* k_pool, const void* v_pool, const AttnGroup* groups, int n_groups,
                  const std::int32_t* extra, const unsigned long long* row_mask, const AttnShape& s, float sl2,
                  void* out, cudaStream_t st) {
   if (n_groups <= 0) return;
   constexpr int C = HD / 8;
-  constexpr int kSmem = (16 * VW * C + KS * 4 * kTile * C) * 16;
+  constexpr int kSmem = (16 * VW * C + KS * STAGES * 2 * kTile * C) * 16;
   static std::atomic<std::uint32_t> attr_done{0};
   once_per_device(attr_done, [] {
-    WS_CUDA(cudaFuncSetAttribute(attn_mma_kernel<HD, VW, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    WS_CUDA(cudaFuncSetAttribute(attn_mma_kernel<HD, VW, KS, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmem));
   });
-  launch_pdl(attn_mma_kernel<HD, VW, KS>, dim3(n_groups, s.n_kv), dim3(32 * VW * KS), kSmem, st, 1,
+  launch_pdl(attn_mma_kernel<HD, VW, KS, STAGES>, dim3(n_groups, s.n_kv), dim3(32 * VW * KS), kSmem, st, 1,
              static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k_pool),
              static_cast<const __nv_bfloat16*>(v_pool), groups, extra, row_mask, s.n_q, s.n_kv, sl2,
              static_cast<__nv_bfloat16*>(out));
@@ -373,10 +380,12 @@ void attention(const void* q, const void* k_pool, const void* v_pool, const Attn
   const float sl2 = s.scale * 1.4426950408889634f;
   // key slices per head dim (measured: two slices help the 64-wide draft heads, not the
   // 128-wide target heads, whose CTAs then fit fewer per SM)
+  // K/V ring depth 2 (measured in config 3: 3 and 4 stages cost occupancy and were 3-4% slower
+  // end to end)
   if (s.hd == 128)
-    launch_attn<128, 2, 1>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
+    launch_attn<128, 2, 1, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
   else if (s.hd == 64)
-    launch_attn<64, 1, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
+    launch_attn<64, 1, 2, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
   else
     throw std::invalid_argument("attention: head dim must be 64 or 128");
 }

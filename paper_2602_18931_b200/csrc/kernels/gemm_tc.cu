@@ -59,7 +59,7 @@ __host__ __device__ constexpr int stage_bytes(int bn, int cg) { return a_bytes()
 inline int ring_stages(int bn, int cg) { return std::min(8, (kSmemBudget - 2048) / stage_bytes(bn, cg)); }
 inline int smem_bytes(int bn, int cg) { return 1024 + ring_stages(bn, cg) * stage_bytes(bn, cg) + 256; }
 
-__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __device__ __forceinline__ std::uint32_t pack_bf16(float lo, float hi) {
@@ -84,11 +84,14 @@ __device__ __forceinline__ void store_bf16_tail(__nv_bfloat16* dst, const std::u
 
 // Epilogue of one 128 x BN tile for this thread's row. fetch(col, r) yields the 32 fp32 values
 // of tile columns [col, col+32) (from TMEM, or the summed split-K partials) and must be called
-// by every lane (TMEM loads are warp-collective).
-template <int EPI, class Fetch>
-__device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, int M, int N, int n_blk, void* out,
-                                              int ldo, const RopeEpi& rp, const NormEpi& nm) {
+// by every lane (TMEM loads are warp-collective). wait() blocks until the accumulator is ready:
+// inputs that do not depend on it (the residual row) are loaded before the call, so their L2
+// latency overlaps the main loop instead of following it.
+template <int EPI, class Fetch, class Wait>
+__device__ __forceinline__ void epilogue_tile(Fetch&& fetch, Wait&& wait, int BN, int row, int M, int N, int n_blk,
+                                              void* out, int ldo, const RopeEpi& rp, const NormEpi& nm) {
   const bool live = row < M;
+  if constexpr (EPI != kEpiAddF32 && EPI != kEpiQKVRope) wait();
   if constexpr (EPI == kEpiSwiGLU) {
     // W rows interleaved in 16-row blocks [gate 0..15 | up 0..15 | gate 16..31 | ...]: the
     // 32-column chunk c holds gate and up of output features f0 + c/2 .. +15.
@@ -118,6 +121,15 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, in
     const int n0 = n_blk * BN;
     const int pos = live ? rp.pos[row] : 0;
     const int slot = live ? rp.slot[row] : 0;
+    // (cos, sin) of the row's first 32 pairs, shared by every head of the tile: loaded before
+    // the accumulator wait
+    float4 cs0[16];
+    if (live) {
+      const float4* cs = reinterpret_cast<const float4*>(rp.cs + static_cast<std::size_t>(pos) * half);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) cs0[j] = cs[j];
+    }
+    wait();
 #pragma unroll 1
     for (int h0 = 0; h0 < BN; h0 += hd) {
       const int hh = (n0 + h0) / hd;  // warp-uniform
@@ -144,7 +156,7 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, in
           float x0 = __uint_as_float(a[2 * j]), x1 = __uint_as_float(a[2 * j + 1]);
           float y0 = __uint_as_float(b[2 * j]), y1 = __uint_as_float(b[2 * j + 1]);
           if (rot) {
-            const float4 cc = cs[j];  // (cos, sin) of pairs 2j and 2j + 1
+            const float4 cc = c == 0 ? cs0[j] : cs[j];  // (cos, sin) of pairs 2j and 2j + 1
             const float rx0 = x0 * cc.x - y0 * cc.y, ry0 = y0 * cc.x + x0 * cc.y;
             const float rx1 = x1 * cc.z - y1 * cc.w, ry1 = y1 * cc.z + x1 * cc.w;
             x0 = rx0;
@@ -159,30 +171,33 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, in
         store32_bf16(dst + c + half, hi);
       }
     }
-  } else {
+  } else if constexpr (EPI == kEpiAddF32) {
+    // out[row, n] += acc (+ the fused-RMSNorm outputs of the new row). The residual chunk c + 32
+    // is loaded while chunk c is processed, chunk 0 before the accumulator wait.
     const int n0 = n_blk * BN;
     const int ncols = min(BN, N - n0);  // valid columns of this tile (BN % 32 == 16: last chunk is half)
+    float* orow = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0;
+    float4 cur[8], nxt[8];
+    auto load = [&](int c, float4 (&v)[8]) {
+      if (live && c + 32 <= ncols) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = reinterpret_cast<const float4*>(orow + c)[q];
+      }
+    };
+    load(0, cur);
+    wait();
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       std::uint32_t r[32];
       fetch(c, r);
-      if (!live || c >= ncols) continue;
-      if constexpr (EPI == kEpiBF16) {
-        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
-        std::uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-        if (c + 32 <= ncols)
-          store32_bf16(o, pk);
-        else
-          store_bf16_tail(o, pk, ncols - c);
-      } else {  // kEpiAddF32: out[row, n] += acc (+ the fused-RMSNorm outputs of the new row)
-        float* o = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
+      if (c + 32 < BN) load(c + 32, nxt);
+      if (live && c < ncols) {
+        float* o = orow + c;
         float x[32];
         if (c + 32 <= ncols) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            float4 v = reinterpret_cast<float4*>(o)[q];
+            float4 v = cur[q];
             v.x += __uint_as_float(r[4 * q + 0]);
             v.y += __uint_as_float(r[4 * q + 1]);
             v.z += __uint_as_float(r[4 * q + 2]);
@@ -217,6 +232,27 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, int BN, int row, in
           else
             store_bf16_tail(xb, pk, ncols - c);
         }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+    }
+  } else {
+    const int n0 = n_blk * BN;
+    const int ncols = min(BN, N - n0);  // valid columns of this tile (BN % 32 == 16: last chunk is half)
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      std::uint32_t r[32];
+      fetch(c, r);
+      if (!live || c >= ncols) continue;
+      if constexpr (EPI == kEpiBF16) {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + static_cast<std::size_t>(row) * ldo + n0 + c;
+        std::uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        if (c + 32 <= ncols)
+          store32_bf16(o, pk);
+        else
+          store_bf16_tail(o, pk, ncols - c);
       }
     }
   }
@@ -447,9 +483,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (; c < nc; ++c) t0 += p[static_cast<std::size_t>(c) * norm.ld_ss];
         rs = rsqrtf(((t0 + t1) + (t2 + t3)) / static_cast<float>(K) + norm.eps);
       }
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      if (local == 0 && warp == 2 && lane == 0) trace_point(ablate, 5);
-      tc_fence_after();
+      auto acc_wait = [&] {
+        mbar_wait(&tfull[acc], (local >> 1) & 1);
+        if (local == 0 && warp == 2 && lane == 0) trace_point(ablate, 5);
+        tc_fence_after();
+      };
       const std::uint32_t t_row = tmem_base + acc * kAccStride + (static_cast<std::uint32_t>(grp * 32) << 16);
       auto tmem_fetch = [&](int col, std::uint32_t (&r)[32]) {
         tmem_ld32(t_row + col, r);
@@ -460,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       if (S == 1) {
-        epilogue_tile<EPI>(tmem_fetch, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
+        epilogue_tile<EPI>(tmem_fetch, acc_wait, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
         if (local == 0 && warp == 2 && lane == 0) trace_point(ablate, 6);
         tc_fence_before();
         __syncwarp();
@@ -473,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       // split-K: publish this split's fp32 partial, release TMEM, take a ticket
+      acc_wait();
       const int ncols = min(BN, N - n_blk * BN);
       float* my = sk.ws + (static_cast<std::size_t>(split) * rows_pad + row) * N + static_cast<std::size_t>(n_blk) * BN;
 #pragma unroll 1
@@ -536,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(norm.ss_in != nullptr ? v[j] * rs : v[j]);
         };
-        epilogue_tile<EPI>(ws_fetch, BN, row, M, N, n_blk, out, ldo, rope, norm);
+        epilogue_tile<EPI>(ws_fetch, [] {}, BN, row, M, N, n_blk, out, ldo, rope, norm);
       }
       epi_bar();  // last_flag is reused by the next unit
     }

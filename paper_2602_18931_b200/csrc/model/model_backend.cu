@@ -113,14 +113,44 @@ struct ModelPair::Impl {
   std::vector<TreeCache> wrk;
 };
 
-// One protocol thread's GPU state: its two lanes' streams and forward workspaces, K3/K4
-// buffers, pinned staging and results. Several backends share one ModelPair (weights, KV
-// pools, per-request caches) and serve disjoint request ranges concurrently.
+// One draft lane: its stream, forward workspace, K3/K4 buffers and pinned results. Several
+// draft lanes let the host plan and launch the next draft batch while the previous one runs
+// (every actor has at most one draft job set in flight, so lanes never touch the same KV).
+struct DraftLane {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::unique_ptr<ForwardWorkspace> ws;
+  ws_pred* d_pred = nullptr;
+  void* d_ws = nullptr;
+  ws_pred* h_pred = nullptr;
+  std::size_t cap = 0;
+  ForwardBatch b;
+  std::vector<std::int32_t> job_out, copy_src, copy_dst;  // job_out: output row, -1 forced EOS
+  std::uint32_t nd = 0;
+  bool ran = false;
+  cudaEvent_t e_start = nullptr, e_end = nullptr, done = nullptr;
+  ~DraftLane() {
+    cudaSetDevice(device);
+    if (d_pred) cudaFree(d_pred);
+    if (d_ws) cudaFree(d_ws);
+    if (h_pred) cudaFreeHost(h_pred);
+    for (cudaEvent_t e : {e_start, e_end, done})
+      if (e) cudaEventDestroy(e);
+    ws.reset();
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+// One protocol thread's GPU state: the verify lane's stream, forward workspace, K3/K4
+// buffers, pinned staging and results, plus its draft lanes. Several backends share one
+// ModelPair (weights, KV pools, per-request caches) and serve disjoint request ranges
+// concurrently.
 struct ModelBackend_Llama::Lanes {
   int device = 0;    // verify lane (target model)
-  int device_d = 0;  // draft lane (the same GPU, or another under split placement)
-  cudaStream_t st_t = nullptr, st_d = nullptr;  // verify (target) / draft streams
-  std::unique_ptr<ForwardWorkspace> ws_t, ws_d;
+  int device_d = 0;  // draft lanes (the same GPU, or another under split placement)
+  cudaStream_t st_t = nullptr;  // verify (target) stream
+  std::unique_ptr<ForwardWorkspace> ws_t;
+  std::vector<std::unique_ptr<DraftLane>> dl;  // lanes 1..n
   // verify lane
   ws_pred* d_pred = nullptr;
   ws_verify_out* d_vout = nullptr;
@@ -130,34 +160,23 @@ struct ModelBackend_Llama::Lanes {
   unsigned char* h_stage = nullptr;
   ws_verify_out* h_vout = nullptr;
   std::size_t cap_v = 0;
-  // draft lane
-  ws_pred* d_pred_d = nullptr;
-  void* d_ws_d = nullptr;
-  ws_pred* h_pred_d = nullptr;
-  std::size_t cap_d = 0;
-  ForwardBatch tb, db;
+  ForwardBatch tb;
   std::vector<TokenId> ctx;
-  std::vector<std::int32_t> forced, job_out, copy_src, copy_dst;
-  std::uint32_t nv = 0, nd = 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
-  cudaEvent_t done[2] = {nullptr, nullptr};  // after each lane's result D2H
+  std::vector<std::int32_t> forced;
+  std::uint32_t nv = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, done = nullptr;  // done: after the verify D2H
   ~Lanes() {
-    cudaSetDevice(device);  // (frees / destroys below work for either device's objects)
+    dl.clear();
+    cudaSetDevice(device);
     for (void* q : {static_cast<void*>(d_pred), static_cast<void*>(d_vout), static_cast<void*>(d_cands),
-                    static_cast<void*>(d_forced), d_ws, static_cast<void*>(d_pred_d), d_ws_d})
+                    static_cast<void*>(d_forced), d_ws})
       if (q) cudaFree(q);
-    for (void* q : {static_cast<void*>(h_stage), static_cast<void*>(h_vout), static_cast<void*>(h_pred_d)})
+    for (void* q : {static_cast<void*>(h_stage), static_cast<void*>(h_vout)})
       if (q) cudaFreeHost(q);
-    for (cudaEvent_t e : {e0, e1, done[0]})
+    for (cudaEvent_t e : {e0, e1, done})
       if (e) cudaEventDestroy(e);
     ws_t.reset();
     if (st_t) cudaStreamDestroy(st_t);
-    cudaSetDevice(device_d);
-    for (cudaEvent_t e : {e2, e3, done[1]})
-      if (e) cudaEventDestroy(e);
-    ws_d.reset();
-    if (st_d) cudaStreamDestroy(st_d);
-    cudaSetDevice(device);
   }
 };
 
@@ -319,16 +338,24 @@ ModelBackend_Llama::ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, T
   WS_CUDA(cudaStreamCreateWithPriority(&L.st_t, cudaStreamNonBlocking, target_first ? prio_hi : prio_lo));
   WS_CUDA(cudaEventCreate(&L.e0));
   WS_CUDA(cudaEventCreate(&L.e1));
-  WS_CUDA(cudaEventCreateWithFlags(&L.done[0], cudaEventDisableTiming));
+  WS_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
   // workspaces grow to the batch sizes actually seen (a cap of max_rows each would be GBs of
   // logits per protocol thread)
   L.ws_t = pair->target().make_workspace(64);
+  // WS_DRAFT_LANES: draft lanes per protocol thread (default 1)
+  int n_draft = 1;
+  if (const char* e = std::getenv("WS_DRAFT_LANES")) n_draft = std::max(1, std::min(8, std::atoi(e)));
   WS_CUDA(cudaSetDevice(L.device_d));
-  WS_CUDA(cudaStreamCreateWithPriority(&L.st_d, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
-  WS_CUDA(cudaEventCreate(&L.e2));
-  WS_CUDA(cudaEventCreate(&L.e3));
-  WS_CUDA(cudaEventCreateWithFlags(&L.done[1], cudaEventDisableTiming));
-  L.ws_d = pair->draft().make_workspace(64);
+  for (int i = 0; i < n_draft; ++i) {
+    std::unique_ptr<DraftLane> d(new DraftLane);
+    d->device = L.device_d;
+    WS_CUDA(cudaStreamCreateWithPriority(&d->st, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
+    WS_CUDA(cudaEventCreate(&d->e_start));
+    WS_CUDA(cudaEventCreate(&d->e_end));
+    WS_CUDA(cudaEventCreateWithFlags(&d->done, cudaEventDisableTiming));
+    d->ws = pair->draft().make_workspace(64);
+    L.dl.push_back(std::move(d));
+  }
   WS_CUDA(cudaSetDevice(L.device));
 }
 ModelBackend_Llama::~ModelBackend_Llama() = default;
@@ -341,12 +368,15 @@ void ModelBackend_Llama::reset_run(std::uint32_t seq_len, TokenId eos, std::uint
   stats = BackendStats{};
   target_ms = draft_ms = 0;
   target_rows = draft_rows_fed = target_forwards = draft_forwards = 0;
-  for (int i = 0; i < 3; ++i) rows_by_kind[i] = jobs_by_kind[i] = repeat_by_kind[i] = 0;
+  for (int i = 0; i < 3; ++i) rows_by_kind[i] = jobs_by_kind[i] = 0;
   host_submit_ms[0] = host_submit_ms[1] = host_wait_ms = 0;
-  seen_ctx_.clear();
 }
 
-KernelProfiler& ModelBackend_Llama::profiler(int which) { return which == 0 ? ln_->ws_t->prof : ln_->ws_d->prof; }
+int ModelBackend_Llama::n_lanes() const { return 1 + static_cast<int>(ln_->dl.size()); }
+
+KernelProfiler& ModelBackend_Llama::profiler(int lane) {
+  return lane == 0 ? ln_->ws_t->prof : ln_->dl.at(lane - 1)->ws->prof;
+}
 
 namespace {
 // Row at context position pos predicts committed index pos + 1 - P; past the generation cap
@@ -484,7 +514,7 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
                  L.d_vout, st, L.d_forced);
   WS_CUDA(cudaEventRecord(L.e1, st));
   WS_CUDA(cudaMemcpyAsync(L.h_vout, L.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
-  WS_CUDA(cudaEventRecord(L.done[0], st));
+  WS_CUDA(cudaEventRecord(L.done, st));
   target_rows += b.tok.size();
   target_forwards += 1;
   stats.launches += 1 + 8ull * p_->target().shape().layers + 4;
@@ -493,38 +523,39 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
   stats.verify_rows += nv;
 }
 
-// Lane 1: one draft forward over every pending draft job (worker leaves as shared-prefix tree
-// groups, controller local drafts / catch-up as causal groups), then K3/K4 row statistics.
-void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
+// Lanes 1..n: one draft forward over every pending draft job (worker leaves as shared-prefix
+// tree groups, controller local drafts / catch-up as causal groups), then K3/K4 row statistics.
+void ModelBackend_Llama::submit_draft(int lane, const RoundJobs& jobs) {
   ModelPair::Impl& I = *p_->impl;
   Lanes& L = *ln_;
+  DraftLane& D = *L.dl.at(lane - 1);
   DeviceGuard dg(L.device_d);
   const ModelPairCfg& cfg = p_->cfg();
   const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
   const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
   const std::int32_t V = p_->draft().shape().vocab;
   const std::uint32_t nd = static_cast<std::uint32_t>(jobs.draft.size());
-  L.nd = nd;
-  draft_ran_ = false;
+  D.nd = nd;
+  D.ran = false;
   if (!nd) return;
   ++draft_batch_;
   const std::size_t need = static_cast<std::size_t>(nd) + 16;
-  if (need > L.cap_d) {
-    for (void* q : {static_cast<void*>(L.d_pred_d), L.d_ws_d})
-      if (q) cudaFree(q);
-    if (L.h_pred_d) cudaFreeHost(L.h_pred_d);
-    L.cap_d = need * 2;
-    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(L.cap_d), V, 0);
-    WS_CUDA(cudaMalloc(&L.d_ws_d, wsb_));
-    WS_CUDA(cudaMemset(L.d_ws_d, 0, wsb_));
-    WS_CUDA(cudaMalloc(&L.d_pred_d, L.cap_d * sizeof(ws_pred)));
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&L.h_pred_d), L.cap_d * sizeof(ws_pred), cudaHostAllocDefault));
+  if (need > D.cap) {  // the lane is idle here (the driver submits only to idle lanes)
+    if (D.d_pred) cudaFree(D.d_pred);
+    if (D.d_ws) cudaFree(D.d_ws);
+    if (D.h_pred) cudaFreeHost(D.h_pred);
+    D.cap = need * 2;
+    const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(D.cap), V, 0);
+    WS_CUDA(cudaMalloc(&D.d_ws, wsb_));
+    WS_CUDA(cudaMemset(D.d_ws, 0, wsb_));
+    WS_CUDA(cudaMalloc(&D.d_pred, D.cap * sizeof(ws_pred)));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&D.h_pred), D.cap * sizeof(ws_pred), cudaHostAllocDefault));
   }
-  ForwardBatch& b = L.db;
+  ForwardBatch& b = D.b;
   b.clear();
-  L.job_out.assign(nd, -1);
-  L.copy_src.clear();
-  L.copy_dst.clear();
+  D.job_out.assign(nd, -1);
+  D.copy_src.clear();
+  D.copy_dst.clear();
   // the open shared-prefix tree group of one request's worker leaves (masked attention group)
   struct TreeGroup {
     bool active = false;
@@ -554,16 +585,10 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
     const std::uint32_t r = dj.seq;
     fill_ctx(jobs, r, jc);
     const std::int32_t n_ctx = static_cast<std::int32_t>(L.ctx.size());
-    static const bool debug_rows = std::getenv("WS_DEBUG_ROWS") != nullptr;
-    if (debug_rows) {
-      std::uint64_t h = 1469598103934665603ULL ^ r;
-      for (TokenId t : L.ctx) h = (h ^ static_cast<std::uint64_t>(t)) * 1099511628211ULL;
-      if (!seen_ctx_.insert(h).second) repeat_by_kind[jc.kind] += 1;
-    }
     if (forced_at(n_ctx - 1, P, L_, eos_) >= 0) {
       // Past the generation cap the prediction is a confident EOS whatever the context
       // (oracle.hpp:88-102): no forward, no KV (every descendant is forced too).
-      L.job_out[j] = -1;
+      D.job_out[j] = -1;
       continue;
     }
     if (n_ctx > MC)
@@ -605,8 +630,8 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
       while (pl < n_comm) {
         const std::int32_t c = t.find(cur, L.ctx[pl]);
         if (c < 0) break;
-        L.copy_src.push_back(t.nodes[c].slot);
-        L.copy_dst.push_back(pre_base + pl);
+        D.copy_src.push_back(t.nodes[c].slot);
+        D.copy_dst.push_back(pre_base + pl);
         t.prefix.push_back(L.ctx[pl]);
         ++pl;
         cur = c;
@@ -694,36 +719,37 @@ void ModelBackend_Llama::submit_draft(const RoundJobs& jobs) {
     const std::int32_t last = static_cast<std::int32_t>(b.tok.size()) - 1;
     rows_by_kind[jc.kind] += static_cast<std::uint64_t>(last + 1 - row0);
     jobs_by_kind[jc.kind] += 1;
-    L.job_out[j] = static_cast<std::int32_t>(b.out_rows.size());
+    D.job_out[j] = static_cast<std::int32_t>(b.out_rows.size());
     b.out_rows.push_back(last);
     b.plant.push_back(p_->plant(L.ctx[n_ctx - 1], true));
   }
   flush_wg();
   if (b.row_mask.size() != b.tok.size()) throw std::logic_error("model path: row mask bookkeeping");
   const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
-  cudaStream_t sd = draft_stream();
+  cudaStream_t sd = draft_stream(lane);
   if (n_out) {
-    p_->draft().copy_slots(L.copy_src, L.copy_dst, sd, *L.ws_d);
-    WS_CUDA(cudaEventRecord(L.e2, sd));
-    p_->draft().forward(b, cfg.plant_draft, sd, *L.ws_d);
-    row_stats_bf16(L.ws_d->logits, n_out, V, V, 1.0f, L.d_pred_d, nullptr, L.d_ws_d, 0, 0, nullptr, nullptr,
-                   sd, nullptr);
-    WS_CUDA(cudaEventRecord(L.e3, sd));
-    WS_CUDA(cudaMemcpyAsync(L.h_pred_d, L.d_pred_d, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, sd));
-    draft_ran_ = true;
+    p_->draft().copy_slots(D.copy_src, D.copy_dst, sd, *D.ws);
+    WS_CUDA(cudaEventRecord(D.e_start, sd));
+    p_->draft().forward(b, cfg.plant_draft, sd, *D.ws);
+    row_stats_bf16(D.ws->logits, n_out, V, V, 1.0f, D.d_pred, nullptr, D.d_ws, 0, 0, nullptr, nullptr, sd,
+                   nullptr);
+    WS_CUDA(cudaEventRecord(D.e_end, sd));
+    WS_CUDA(cudaMemcpyAsync(D.h_pred, D.d_pred, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, sd));
+    D.ran = true;
     draft_rows_fed += b.tok.size();
     draft_forwards += 1;
-    stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (L.copy_src.empty() ? 0 : 1);
+    stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (D.copy_src.empty() ? 0 : 1);
     stats.d2h += n_out * sizeof(ws_pred);
   }
-  WS_CUDA(cudaEventRecord(L.done[1], sd));
+  WS_CUDA(cudaEventRecord(D.done, sd));
   stats.draft_rows += nd;
 }
 
-cudaStream_t ModelBackend_Llama::draft_stream() const {
-  // WS_SERIAL=1 serialises the two forwards (clean per-kernel profiles); default overlaps them
+cudaStream_t ModelBackend_Llama::draft_stream(int lane) const {
+  // WS_SERIAL=1 serialises every forward on one stream (clean per-kernel profiles); default
+  // overlaps the lanes
   static const bool serial = std::getenv("WS_SERIAL") != nullptr;
-  return serial && ln_->device_d == ln_->device ? ln_->st_t : ln_->st_d;
+  return serial && ln_->device_d == ln_->device ? ln_->st_t : ln_->dl.at(lane - 1)->st;
 }
 
 std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t) {
@@ -736,16 +762,16 @@ std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int veri
     took = verify_take(jobs);
     submit_verify(jobs, took);
   } else {
-    submit_draft(jobs);
+    submit_draft(lane, jobs);
     took = jobs.draft.size();
   }
-  host_submit_ms[lane] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  host_submit_ms[lane == 0 ? 0 : 1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return took;
 }
 
-int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
-  ModelPair::Impl& I = *p_->impl;
+int ModelBackend_Llama::wait_any(std::uint32_t busy) {
   Lanes& L = *ln_;
+  const int n = n_lanes();
   const auto t0 = std::chrono::steady_clock::now();
   struct Acc {
     double& ms;
@@ -753,11 +779,11 @@ int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
     ~Acc() { ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
   } acc{host_wait_ms, t0};
   for (;;) {
-    for (int lane = 0; lane < 2; ++lane) {
-      if (!(lane == 0 ? busy0 : busy1)) continue;
+    for (int lane = 0; lane < n; ++lane) {
+      if (!(busy & (1u << lane))) continue;
       // each event is queried with its own GPU current (split placement: two devices)
       DeviceGuard dg(lane == 0 ? L.device : L.device_d);
-      const cudaError_t e = cudaEventQuery(L.done[lane]);
+      const cudaError_t e = cudaEventQuery(lane == 0 ? L.done : L.dl[lane - 1]->done);
       if (e == cudaSuccess) return lane;
       if (e != cudaErrorNotReady) WS_CUDA(e);
     }
@@ -766,24 +792,24 @@ int ModelBackend_Llama::wait_any(bool busy0, bool busy1) {
 }
 
 void ModelBackend_Llama::complete(int lane, RoundResults& res) {
-  ModelPair::Impl& I = *p_->impl;
   Lanes& L = *ln_;
   DeviceGuard dg(lane == 0 ? L.device : L.device_d);
   float ms = 0.f;
   if (lane == 0) {
     res.verify.resize(L.nv);
     if (!L.nv) return;
-    WS_CUDA(cudaEventSynchronize(L.done[0]));
+    WS_CUDA(cudaEventSynchronize(L.done));
     std::memcpy(res.verify.data(), L.h_vout, L.nv * sizeof(ws_verify_out));
     WS_CUDA(cudaEventElapsedTime(&ms, L.e0, L.e1));
     target_ms += ms;
   } else {
-    res.draft.resize(L.nd);
-    if (!L.nd) return;
-    WS_CUDA(cudaEventSynchronize(L.done[1]));
-    for (std::uint32_t j = 0; j < L.nd; ++j) {
-      if (L.job_out[j] >= 0) {
-        res.draft[j] = L.h_pred_d[L.job_out[j]];
+    DraftLane& D = *L.dl.at(lane - 1);
+    res.draft.resize(D.nd);
+    if (!D.nd) return;
+    WS_CUDA(cudaEventSynchronize(D.done));
+    for (std::uint32_t j = 0; j < D.nd; ++j) {
+      if (D.job_out[j] >= 0) {
+        res.draft[j] = D.h_pred[D.job_out[j]];
       } else {
         ws_pred e{};
         e.n = 1;
@@ -792,8 +818,8 @@ void ModelBackend_Llama::complete(int lane, RoundResults& res) {
         res.draft[j] = e;
       }
     }
-    if (draft_ran_) {
-      WS_CUDA(cudaEventElapsedTime(&ms, L.e2, L.e3));
+    if (D.ran) {
+      WS_CUDA(cudaEventElapsedTime(&ms, D.e_start, D.e_end));
       draft_ms += ms;
     }
   }
@@ -806,7 +832,7 @@ void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int
     throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
   stats.rounds += 1;
   submit_verify(jobs, jobs.verify.size());  // lockstep rounds take every job
-  submit_draft(jobs);
+  submit_draft(1, jobs);
   complete(0, res);
   complete(1, res);
 }

@@ -16,7 +16,6 @@
 #include <cstdint>
 #include <memory>
 #include <string>
-#include <unordered_set>
 #include <vector>
 
 #include "../host/driver.hpp"
@@ -46,37 +45,34 @@ class ModelBackend_Llama : public ModelBackend {
   ~ModelBackend_Llama() override;
   void run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t sample_seed) override;
   bool wants_context() const override { return true; }
-  // lane 0 = target stream (verify), lane 1 = draft stream (worker + controller drafts)
+  // lane 0 = target stream (verify), lanes 1..n = draft streams (worker + controller drafts)
   bool has_lanes() const override { return true; }
+  int n_lanes() const override;
   std::size_t submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed) override;
-  int wait_any(bool busy0, bool busy1) override;
+  int wait_any(std::uint32_t busy) override;
   void complete(int lane, RoundResults& res) override;
-  KernelProfiler& profiler(int which);  // 0 = target forwards, 1 = draft forwards of this backend
+  KernelProfiler& profiler(int lane);  // lane 0: target forwards; lanes 1..n: draft forwards
   // New run on the same pair (the caller reset the per-request caches): run parameters, zeroed
   // counters; streams, workspaces and device buffers are kept.
   void reset_run(std::uint32_t seq_len, TokenId eos, std::uint32_t k);
   double target_ms = 0, draft_ms = 0;
   std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
   std::uint64_t rows_by_kind[3] = {0, 0, 0}, jobs_by_kind[3] = {0, 0, 0};  // JobKind
-  // WS_DEBUG_ROWS: draft jobs whose (request, context) was already drafted earlier in the run
-  std::uint64_t repeat_by_kind[3] = {0, 0, 0};
   double host_submit_ms[2] = {0, 0}, host_wait_ms = 0;  // host time in submit (per lane) / wait_any
 
  private:
   void fill_ctx(const RoundJobs& jobs, std::uint32_t r, const JobCtx& c);
   std::size_t verify_take(const RoundJobs& jobs);  // padding-aware batch trim (lanes driver)
   void submit_verify(const RoundJobs& jobs, std::size_t nv);
-  void submit_draft(const RoundJobs& jobs);
-  cudaStream_t draft_stream() const;
+  void submit_draft(int lane, const RoundJobs& jobs);
+  cudaStream_t draft_stream(int lane) const;
   ModelPair* p_;
   std::uint32_t L_;
   TokenId eos_;
   std::uint32_t k_;
   std::uint64_t draft_batch_ = 0;
-  bool draft_ran_ = false;
   struct Lanes;
   std::unique_ptr<Lanes> ln_;
-  std::unordered_set<std::uint64_t> seen_ctx_;
 };
 
 // Owns both models, their KV caches and the per-request cache state on one device.

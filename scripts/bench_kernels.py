@@ -181,6 +181,8 @@ def timeline():
     L.ws_debug_gemm_trace.argtypes = [C.c_void_p]
     names = ["entry", "prologue", "dep_wait", "first_full", "last_mma", "acc_ready", "epi_done", "exit"]
     for (M, N, K, epi, name) in [(160, 2048, 2048, 1, "1B o M=160"), (655, 2048, 2048, 1, "1B o M=655"),
+                                 (655, 2048, 8192, 1, "1B down M=655"), (530, 4096, 14336, 1, "8B down M=530"),
+                                 (655, 16384, 2048, 2, "1B gate_up M=655"),
                                  (160, 28672, 4096, 2, "8B gate_up M=160"), (530, 28672, 4096, 2, "8B gate_up M=530")]:
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)

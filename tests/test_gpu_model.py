@@ -242,3 +242,23 @@ def test_model_sim_split_placement_equals_shared():
         outs.append((b.metrics_list(), b.ctrl_outputs()))
         ctx.close()
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("lanes", ["2", "3"])
+def test_model_sim_draft_lanes(tiny_pair, monkeypatch, lanes):
+    """Several draft lanes per protocol thread (the next draft batch planned and launched while
+    another runs on its own stream and workspace) give the one-lane per-request results."""
+    import paper_2602_18931_b200 as ws
+    from paper_2602_18931_b200 import abi
+    c = abi.config3(num_requests=8, k=4, seq_len=30, vocab=1000, eos=999)
+    ref = tiny_pair.run_model_sim(c)
+    monkeypatch.setenv("WS_DRAFT_LANES", lanes)
+    ctx = ws.Context(0)  # backends read the switch when created
+    try:
+        ctx.load_models(abi.model_cfg("tiny", "tiny-draft", prompt_len=16, max_requests=8, max_ctx=64,
+                                      plant_target=6.0, plant_draft=6.0, draft_plant_rate=0.8))
+        got = ctx.run_model_sim(c)
+        assert got.ctrl_outputs() == ref.ctrl_outputs()
+        assert got.metrics_list() == ref.metrics_list()
+    finally:
+        ctx.close()
