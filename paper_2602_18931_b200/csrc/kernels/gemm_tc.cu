@@ -458,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {  // epilogue warps 2..5 → TMEM lane groups (warp % 4)
     pdl_wait();  // the epilogues read the residual / norm statistics / rope tables
     const int grp = static_cast<int>(warp & 3);
-    const int rows_pad = m_blocks * BM;
+    const int m_slots = m_units * CG;  // 128-row blocks incl. a pair's padding block
+    const int rows_pad = m_slots * BM;
     int local = 0;
     for (int u = first; u < total; u += step, ++local) {
       int m_blk, n_blk, split;
@@ -535,10 +536,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {  // the accumulator is reused by the (leader's) MMA issuer
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(&tempty[acc], 0);
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       __threadfence();
       epi_bar();
-      const int tile = n_blk * m_blocks + m_blk;
+      const int tile = n_blk * m_slots + m_blk;
       if (threadIdx.x == 64) {
         const unsigned int t = atomicAdd(&sk.tickets[tile], 1u);
         *last_flag = t == static_cast<unsigned int>(S - 1) ? 1u : 0u;
@@ -766,7 +772,7 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   // WS_GEMM_PAIR: "0" keeps every GEMM on single CTAs, "2" forces CTA pairs (tests, A/B)
   const char* pe = std::getenv("WS_GEMM_PAIR");
   const int pair_env = pe ? std::atoi(pe) : -1;
-  const bool pair_ok = pair_env != 0 && g.splits <= 1 && g.cta_group != 1;
+  const bool pair_ok = pair_env != 0 && g.cta_group != 1;
   TileChoice tc = pick_tile(g.M, g.N, granule, pair_ok);
   if (g.cta_group == 2 || (pair_env == 2 && pair_ok)) tc.cg = 2;
   if (g.bn) tc.bn = g.bn;
@@ -774,19 +780,21 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   if (bn < 16 || bn > 256 || bn % granule) throw std::invalid_argument("gemm: tile width must be a multiple of " +
                                                                        std::to_string(granule) + " in [16, 256]");
   if (bn % 32 && g.cta_group != 2) tc.cg = 1;  // an explicit odd-16 width runs on single CTAs
-  if (tc.cg == 2 && (bn % 32 || g.splits > 1)) throw std::invalid_argument("gemm: CTA pairs need BN % 32, no split");
+  if (tc.cg == 2 && bn % 32) throw std::invalid_argument("gemm: CTA pairs need BN % 32");
   SplitArgs sk;
   sk.splits = g.splits > 0 ? g.splits : (g.ws ? pick_splits(g.N, g.K) : 1);
   if (sk.splits > 1) {
     if (!g.ws) throw std::invalid_argument("gemm: split-K needs a workspace");
     const int m_blocks = (g.M + BM - 1) / BM;
+    const int m_slots = tc.cg == 2 ? (m_blocks + 1) / 2 * 2 : m_blocks;  // as in the kernel
     const int n_tiles = (g.N + bn - 1) / bn;
-    const std::size_t need = kTicketBytes + static_cast<std::size_t>(sk.splits) * m_blocks * BM * g.N * sizeof(float);
-    if (need > g.ws_bytes || static_cast<std::size_t>(m_blocks) * n_tiles > kMaxTiles) {
+    const std::size_t need = kTicketBytes + static_cast<std::size_t>(sk.splits) * m_slots * BM * g.N * sizeof(float);
+    if (need > g.ws_bytes || static_cast<std::size_t>(m_slots) * n_tiles > kMaxTiles) {
       // Rows are independent: run the GEMM in row slices that fit the workspace.
       if (g.ws_bytes <= kTicketBytes) throw std::invalid_argument("gemm: split-K workspace too small");
       const std::size_t per_row = static_cast<std::size_t>(sk.splits) * g.N * sizeof(float);
-      const int per = std::max<int>(BM, static_cast<int>((g.ws_bytes - kTicketBytes) / per_row / BM * BM));
+      const int unit = tc.cg == 2 ? 2 * BM : BM;  // pair slices keep whole CTA pairs
+      const int per = std::max<int>(unit, static_cast<int>((g.ws_bytes - kTicketBytes) / per_row / unit * unit));
       if (per >= g.M) throw std::invalid_argument("gemm: split-K workspace too small");
       for (int r0 = 0; r0 < g.M; r0 += per) {
         GemmArgs s = g;
@@ -802,6 +810,7 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
           s.out = static_cast<__nv_bfloat16*>(g.out) + static_cast<std::size_t>(r0) * g.ldo;
         s.bn = bn;
         s.splits = sk.splits;
+        s.cta_group = tc.cg;
         gemm_tn(s, st);
       }
       return;
@@ -809,7 +818,6 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
     sk.tickets = static_cast<unsigned int*>(g.ws);
     sk.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(g.ws) + kTicketBytes);
   }
-  if (tc.cg == 2) sk.splits = 1;
   switch (g.epi) {
     case kEpiBF16: return launch_cg<kEpiBF16>(g, sk, bn, tc.cg, st);
     case kEpiAddF32: return launch_cg<kEpiAddF32>(g, sk, bn, tc.cg, st);

@@ -143,6 +143,45 @@ def one_gemm():
                       "tflops": 2.0 * M * N * K / t / 1e12}))
 
 
+def one_add():
+    """One residual-epilogue GEMM (1B down projection at 655 rows, out fp32 += acc), for ncu."""
+    M, N, K = 655, 2048, 8192
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    for _ in range(4):
+        ops.gemm(A, W, out=out, epi=1)
+    torch.cuda.synchronize()
+    t = timeit(lambda: ops.gemm(A, W, out=out, epi=1))
+    ob = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    tb = timeit(lambda: ops.gemm(A, W, out=ob))
+    print(json.dumps({"kernel": "gemm down+residual", "M": M, "N": N, "K": K, "us": t * 1e6,
+                      "bf16_out_us": tb * 1e6}))
+
+
+def splitk_pair():
+    """Split-K on CTA pairs vs one pass (default tile pick), residual epilogue, L2 flushed: the
+    narrow projections are L2-throughput-bound (every N tile re-reads the activation rows)."""
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    for (M, N, K, name) in [(655, 2048, 8192, "1B down"), (655, 2048, 2048, "1B o"), (530, 4096, 14336, "8B down"),
+                            (530, 4096, 4096, "8B o"), (160, 2048, 8192, "1B down M=160"),
+                            (150, 4096, 14336, "8B down M=150")]:
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+        X = torch.zeros(M, N, device="cuda")
+        os.environ.pop("WS_GEMM_PAIR", None)
+        res = {"1": round(timeit(lambda: ops.gemm(A, W, out=X, epi=1), flush=flush) * 1e6, 1)}
+        os.environ["WS_GEMM_PAIR"] = "2"
+        for sp in (2, 3, 4):
+            for bn in (128, 192, 256):
+                res[f"{sp}x{bn}"] = round(timeit(lambda: ops.gemm(A, W, out=X, epi=1, bn=bn, splits=sp),
+                                                 flush=flush) * 1e6, 1)
+        os.environ.pop("WS_GEMM_PAIR", None)
+        best = min(res, key=res.get)
+        print(json.dumps({"shape": name, "M": M, "N": N, "K": K, "best": best, "us": res}))
+        sys.stdout.flush()
+
+
 def pair(shape="8B o"):
     """One launch each of our GEMM and cuBLAS on one model shape (for an ncu side-by-side)."""
     dims = {"8B o": (530, 4096, 4096), "8B gate_up": (530, 28672, 4096), "1B lm_head": (300, 128256, 2048),
@@ -227,4 +266,4 @@ if __name__ == "__main__":
         pair(" ".join(sys.argv[2:]) or "8B o")
     else:
         {"gemm": gemm, "gemm_model": gemm_model, "rowstats": rowstats, "one_gemm": one_gemm, "overhead": overhead,
-         "timeline": timeline, "splitk": splitk}[sys.argv[1]]()
+         "timeline": timeline, "splitk": splitk, "one_add": one_add, "splitk_pair": splitk_pair}[sys.argv[1]]()

@@ -17,7 +17,7 @@ def label(n):
     m = re.search(r"gemm_tn_kernel<(\d), (\d)>", n)
     if m:
         return f"K1 gemm {EPI[m.group(1)]}, {'CTA pair' if m.group(2) == '2' else 'single CTA'}"
-    m = re.search(r"attn_mma_kernel<(\d+), (\d), (\d)>", n)
+    m = re.search(r"attn_mma_kernel<(\d+), (\d), (\d)(?:, \d)?>", n)
     if m:
         return f"K2 attention hd{m.group(1)}, {m.group(2)} vector warp(s), {m.group(3)} key slice(s)"
     return re.sub(r"\(.*", "", n).replace("unnamed>::", "").replace("wsb::", "")
