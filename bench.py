@@ -344,7 +344,10 @@ def main():
                 # the public C-ABI call is already end to end: host protocol → per-round H2D of the
                 # batch (tokens, positions, slots, groups, candidates) → forwards → D2H of results
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d // max(1, args.steps),
-                        "d2h_bytes_per_step": d2h // max(1, args.steps)},
+                        "d2h_bytes_per_step": d2h // max(1, args.steps),
+                        "note": "the timed step is the public call (ws_run_model_sim / ws_run_sim) from host "
+                                "buffers: every round's job tables go H2D and its results D2H inside the timed "
+                                "region, so value and e2e are one measurement"},
                 "gpu_launches": int(launches_all), "clocks": clk.summary()}
         if args.workload == "llama":
             local = cfg.local_requests
