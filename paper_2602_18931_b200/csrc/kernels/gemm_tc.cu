@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
@@ -56,8 +57,15 @@ constexpr int kAccStride = 256;
 __host__ __device__ constexpr int a_bytes() { return BM * BK * 2; }
 __host__ __device__ constexpr int b_bytes(int bn, int cg) { return bn / cg * BK * 2; }
 __host__ __device__ constexpr int stage_bytes(int bn, int cg) { return a_bytes() + b_bytes(bn, cg); }
-inline int ring_stages(int bn, int cg) { return std::min(8, (kSmemBudget - 2048) / stage_bytes(bn, cg)); }
-inline int smem_bytes(int bn, int cg) { return 1024 + ring_stages(bn, cg) * stage_bytes(bn, cg) + 256; }
+// cluster split-K (CS = 2): the receiving CTA's two 128 x 33 fp32 chunk buffers, after the ring
+constexpr int kCsStride = 36;  // floats per row of a chunk buffer (16-byte rows, spread banks)
+constexpr int kCsBufBytes = 2 * 128 * kCsStride * 4;
+inline int ring_stages(int bn, int cg, int cs = 1) {
+  return std::min(8, (kSmemBudget - 2048 - (cs == 2 ? kCsBufBytes : 0)) / stage_bytes(bn, cg));
+}
+inline int smem_bytes(int bn, int cg, int cs = 1) {
+  return 1024 + ring_stages(bn, cg, cs) * stage_bytes(bn, cg) + 256 + (cs == 2 ? kCsBufBytes : 0);
+}
 
 __device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -273,6 +281,7 @@ __device__ __forceinline__ void trace_point(int ablate, int i) {
 
 struct SplitArgs {
   int splits = 1;
+  bool cluster = false;              // splits == 2 on CTA pairs: reduce through DSMEM (CS = 2)
   float* ws = nullptr;               // fp32 partials [splits][m_blocks*BM][N]
   unsigned int* tickets = nullptr;   // [m_blocks * n_tiles], zero-initialised, self-resetting
 };
@@ -281,7 +290,12 @@ struct SplitArgs {
 // 256 x BN tile — each CTA holds its 128 A rows and half of the BN weight rows, the leader's
 // single thread issues the pair MMA over both CTAs' smem, and each CTA's TMEM receives its
 // 128 rows; shared-memory traffic per MAC drops by a third (the main loop is smem-bound).
-template <int EPI, int CG>
+// CS = 2 (CTA pairs only): cluster split-K. A cluster of four CTAs is two pairs computing the
+// same 256 x BN tile over the two halves of K; the second pair streams its fp32 accumulator
+// through distributed shared memory into the first pair's CTAs, which add it to their own
+// (split 0 + split 1, the order of the ordered global split-K sum) and run the epilogue. Half
+// the K loop per SM, twice the tiles in flight, no partial traffic through L2.
+template <int EPI, int CG, int CS = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo, const RopeEpi rope,
@@ -298,22 +312,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* tempty = tfull + 2;      // [2]
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
   std::uint32_t* last_flag = tmem_slot + 1;
+  std::uint64_t* rfull = reinterpret_cast<std::uint64_t*>(tmem_slot + 2);  // [2] CS == 2: peer chunk landed
+  std::uint64_t* sfree = rfull + 2;                                         // [2] CS == 2: chunk buffer consumed
+  float* rbuf = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // CS == 2: [2][128][36]
 
   const int num_k = K / BK;
   const int S = sk.splits;  // 1 for pairs
   const int m_units = CG == 2 ? (m_blocks + 1) / 2 : m_blocks;
   const int total = m_units * n_tiles * S;
-  const int rank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int crank = CG == 2 ? static_cast<int>(cluster_ctarank()) : 0;  // rank in the cluster
+  const int rank = crank & 1;                      // role in the CTA pair (0 = leader)
+  const int pair_base = crank & ~1;                // the pair's leader rank in the cluster
+  const int ksplit = CS == 2 ? crank >> 1 : 0;     // cluster split-K: which half of K
+  const std::uint16_t pair_mask = static_cast<std::uint16_t>(3u << pair_base);
   const int first = CG == 2 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
   const int step = CG == 2 ? static_cast<int>(cluster_count_x()) : static_cast<int>(gridDim.x);
   const bool leader = rank == 0;
   const std::uint32_t warp = warp_id(), lane = lane_id();
   // unit u → (M unit, n_blk, split), M fastest; this CTA's 128-row block is unit * CG + rank;
   // split s covers k-blocks [s*nk/S, (s+1)*nk/S)
+  const int KSPLITS = CS == 2 ? 2 : S;  // K ranges per tile
   auto decode = [&](int u, int& m_blk, int& n_blk, int& split) {
     m_blk = (u % m_units) * CG + rank;
     const int r = u / m_units;
-    split = r % S;
+    split = CS == 2 ? ksplit : r % S;
     n_blk = r / S;
   };
 
@@ -331,6 +353,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);  // one arrival per epilogue warp (of both CTAs for a pair)
+      if constexpr (CS == 2) {
+        mbar_init(&rfull[a], 4);  // one per sending epilogue warp, after the warp's stores
+        mbar_init(&sfree[a], 4);  // one per receiving epilogue warp, after the warp's reads
+      }
     }
     fence_barrier_init();
   }
@@ -356,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (first < total) {
       int m_blk, n_blk, split;
       decode(first, m_blk, n_blk, split);
-      const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
+      const int kb0 = split * num_k / KSPLITS, kb1 = (split + 1) * num_k / KSPLITS;
       pre = min(STAGES, kb1 - kb0);
       if (elect_one()) {
         for (int i = 0; i < pre; ++i) {
@@ -379,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = first; u < total; u += step) {
       int m_blk, n_blk, split;
       decode(u, m_blk, n_blk, split);
-      const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
+      const int kb0 = split * num_k / KSPLITS, kb1 = (split + 1) * num_k / KSPLITS;
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         const bool prefilled = it < pre;  // weight box already in flight
         if (!prefilled) mbar_wait(&empty[stage], phase ^ 1);
@@ -413,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = first; u < total; u += step, ++local) {
         int m_blk, n_blk, split;
         decode(u, m_blk, n_blk, split);
-        const int kb0 = split * num_k / S, kb1 = (split + 1) * num_k / S;
+        const int kb0 = split * num_k / KSPLITS, kb1 = (split + 1) * num_k / KSPLITS;
         const int acc = local & 1;
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         tc_fence_after();
@@ -435,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // frees the smem slot (in both CTAs of a pair) when these MMAs retire
             if constexpr (CG == 2)
-              mma_commit_pair(&empty[stage], 3);
+              mma_commit_pair(&empty[stage], pair_mask);
             else
               mma_commit(&empty[stage]);
           }
@@ -447,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) {
           if constexpr (CG == 2)
-            mma_commit_pair(&tfull[acc], 3);
+            mma_commit_pair(&tfull[acc], pair_mask);
           else
             mma_commit(&tfull[acc]);
         }
@@ -461,6 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int m_slots = m_units * CG;  // 128-row blocks incl. a pair's padding block
     const int rows_pad = m_slots * BM;
     int local = 0;
+    int cs_q = 0;  // CS == 2: chunks exchanged so far (buffer = cs_q & 1)
     for (int u = first; u < total; u += step, ++local) {
       int m_blk, n_blk, split;
       decode(u, m_blk, n_blk, split);
@@ -498,6 +525,63 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rs);
         }
       };
+      if constexpr (CS == 2) {
+        const int rl = grp * 32 + static_cast<int>(lane);  // row within this CTA's 128
+        if (ksplit == 1) {
+          // sender: this CTA's accumulator, 32 columns at a time, into the split-0 CTA with the
+          // same role (cluster rank - 2), double-buffered
+          acc_wait();
+          const std::uint32_t dst = static_cast<std::uint32_t>(crank - 2);
+          const std::uint32_t rb = mapa_u32(rbuf, dst);
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32, ++cs_q) {
+            const int b = cs_q & 1;
+            mbar_wait_cluster(&sfree[b], ((cs_q >> 1) & 1) ^ 1);
+            std::uint32_t r[32];
+            tmem_ld32(t_row + c, r);
+            tmem_ld_wait();
+            const std::uint32_t a = rb + static_cast<std::uint32_t>((b * 128 * kCsStride + rl * kCsStride) * 4);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) st_cluster_v4(a + 4 * j, r[j], r[j + 1], r[j + 2], r[j + 3]);
+            __syncwarp();  // orders the lanes' stores before lane 0's cluster-scope release
+            if (lane == 0) mbar_arrive_cluster(&rfull[b], dst);
+          }
+        } else {
+          // receiver: own (split 0) + peer (split 1), the ordered global split-K sum
+          auto cs_fetch = [&](int col, std::uint32_t (&r)[32]) {
+            tmem_ld32(t_row + col, r);
+            tmem_ld_wait();
+            const int b = cs_q & 1;
+            mbar_wait_cluster(&rfull[b], (cs_q >> 1) & 1);
+            const float4* pb = reinterpret_cast<const float4*>(rbuf + b * 128 * kCsStride + rl * kCsStride);
+            float pv[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 t = pb[j];
+              pv[4 * j] = t.x;
+              pv[4 * j + 1] = t.y;
+              pv[4 * j + 2] = t.z;
+              pv[4 * j + 3] = t.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float v = __uint_as_float(r[j]) + pv[j];
+              if (norm.ss_in != nullptr) v *= rs;
+              r[j] = __float_as_uint(v);
+            }
+            // relaxed: the values are already consumed, and a release would first drain this
+            // thread's residual stores of the previous chunk
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(&sfree[b], static_cast<std::uint32_t>(crank + 2));
+            ++cs_q;
+          };
+          epilogue_tile<EPI>(cs_fetch, acc_wait, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[acc], pair_base);
+        continue;
+      }
       if (S == 1) {
         epilogue_tile<EPI>(tmem_fetch, acc_wait, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
         if (local == 0 && warp == 2 && lane == 0) trace_point(ablate, 6);
@@ -505,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {  // the accumulator is reused by the (leader's) MMA issuer
           if constexpr (CG == 2)
-            mbar_arrive_cluster(&tempty[acc], 0);
+            mbar_arrive_cluster(&tempty[acc], pair_base);
           else
             mbar_arrive(&tempty[acc]);
         }
@@ -538,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {  // the accumulator is reused by the (leader's) MMA issuer
         if constexpr (CG == 2)
-          mbar_arrive_cluster(&tempty[acc], 0);
+          mbar_arrive_cluster(&tempty[acc], pair_base);
         else
           mbar_arrive(&tempty[acc]);
       }
@@ -625,33 +709,36 @@ CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, st
   return m;
 }
 
-int pair_clusters() {  // co-resident CTA pairs at one CTA per SM (same on every B200)
+template <int CSZ>
+int max_clusters() {  // co-resident clusters of CSZ CTAs at one CTA per SM (same on every B200)
   static int n = [] {
-    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<kEpiBF16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<kEpiBF16, 2, CSZ / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemBudget));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * 74, 1, 1);
+    cfg.gridDim = dim3(CSZ * (kNumSMs / CSZ), 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = kSmemBudget;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = CSZ;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int c = 0;
-    WS_CUDA(cudaOccupancyMaxActiveClusters(&c, gemm_tn_kernel<kEpiBF16, 2>, &cfg));
+    WS_CUDA(cudaOccupancyMaxActiveClusters(&c, gemm_tn_kernel<kEpiBF16, 2, CSZ / 2>, &cfg));
     return std::max(1, c);
   }();
   return n;
 }
+int pair_clusters() { return max_clusters<2>(); }
 
-template <int EPI, int CG>
+template <int EPI, int CG, int CS = 1>
 void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   static std::atomic<std::uint32_t> attr_done{0};
   once_per_device(attr_done, [] {
-    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI, CG, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemBudget));
   });
   static const int ablate = [] {  // WS_GEMM_ABLATE (measurement only): 1 no MMA,
     const char* e = std::getenv("WS_GEMM_ABLATE");  // 4 no epilogue stores
@@ -667,7 +754,7 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, static_cast<std::uint32_t>(bn / CG));
   const int m_blocks = (g.M + BM - 1) / BM;
   const int n_tiles = (g.N + bn - 1) / bn;  // SwiGLU: N counts gate+up rows
-  const int smem = smem_bytes(bn, CG), stages = ring_stages(bn, CG);
+  const int smem = smem_bytes(bn, CG, CS), stages = ring_stages(bn, CG, CS);
   if constexpr (CG == 1) {
     const int total = m_blocks * n_tiles * sk.splits;
     // max_ctas < 0: one CTA per unit (not persistent: SMs free up between units, so a
@@ -676,8 +763,18 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
     const int flags = ablate | (grid <= early_grid ? kEarlyTrigger : 0);
     launch_pdl(gemm_tn_kernel<EPI, 1>, dim3(grid), dim3(kThreads), smem, st, 1, ta, tb, g.M, g.N, g.K, m_blocks,
                n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
+  } else if constexpr (CS == 2) {
+    const int total = (m_blocks + 1) / 2 * n_tiles;  // tiles; each cluster of 4 holds both K halves
+    static const bool dbg = std::getenv("WS_GEMM_DEBUG") != nullptr;
+    if (dbg) std::fprintf(stderr, "[gemm] cluster split: %d tiles, %d co-resident clusters of 4, bn %d, %d stages\n",
+                          total, max_clusters<4>(), bn, stages);
+    int clusters = g.max_ctas < 0 ? total : std::min(total, max_clusters<4>());
+    if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 4));
+    const int flags = ablate | (4 * clusters <= early_grid ? kEarlyTrigger : 0);
+    launch_pdl(gemm_tn_kernel<EPI, 2, 2>, dim3(4 * clusters), dim3(kThreads), smem, st, 4, ta, tb, g.M, g.N, g.K,
+               m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
   } else {
-    const int total = (m_blocks + 1) / 2 * n_tiles;
+    const int total = (m_blocks + 1) / 2 * n_tiles * sk.splits;
     int clusters = g.max_ctas < 0 ? total : std::min(total, pair_clusters());
     if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 2));
     const int flags = ablate | (2 * clusters <= early_grid ? kEarlyTrigger : 0);
@@ -688,7 +785,16 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
 
 template <int EPI>
 void launch_cg(const GemmArgs& g, const SplitArgs& sk, int bn, int cg, cudaStream_t st) {
-  if (cg == 2) return launch<EPI, 2>(g, sk, bn, st);
+  if (cg == 2) {
+    if constexpr (EPI != kEpiQKVRope) {  // (the QKV epilogue reads chunks out of order)
+      if (sk.splits == 2 && sk.cluster) {
+        SplitArgs one = sk;
+        one.splits = 1;  // the K halves live in the cluster, not in the unit index
+        return launch<EPI, 2, 2>(g, one, bn, st);
+      }
+    }
+    return launch<EPI, 2>(g, sk, bn, st);
+  }
   return launch<EPI, 1>(g, sk, bn, st);
 }
 
@@ -783,7 +889,11 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   if (tc.cg == 2 && bn % 32) throw std::invalid_argument("gemm: CTA pairs need BN % 32");
   SplitArgs sk;
   sk.splits = g.splits > 0 ? g.splits : (g.ws ? pick_splits(g.N, g.K) : 1);
-  if (sk.splits > 1) {
+  // two K halves on CTA pairs reduce through distributed shared memory (no workspace);
+  // WS_GEMM_DSMEM=0 keeps them on the global-partials path (tests compare the two bit for bit)
+  const char* de = std::getenv("WS_GEMM_DSMEM");
+  sk.cluster = sk.splits == 2 && tc.cg == 2 && g.epi != kEpiQKVRope && !(de && de[0] == '0');
+  if (sk.splits > 1 && !sk.cluster) {
     if (!g.ws) throw std::invalid_argument("gemm: split-K needs a workspace");
     const int m_blocks = (g.M + BM - 1) / BM;
     const int m_slots = tc.cg == 2 ? (m_blocks + 1) / 2 * 2 : m_blocks;  // as in the kernel

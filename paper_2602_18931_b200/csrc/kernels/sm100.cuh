@@ -99,6 +99,42 @@ __device__ __forceinline__ void mbar_arrive_cluster(std::uint64_t* bar, std::uin
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// try_wait with cluster-scope acquire: the arrivals come from another CTA of the cluster that
+// released its distributed-shared-memory stores with them.
+__device__ __forceinline__ void mbar_wait_cluster(std::uint64_t* bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAITC:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONEC;\n"
+      "bra LAB_WAITC;\n"
+      "DONEC:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Address of this CTA's smem location `p` in CTA `rank` of the cluster (shared::cluster window).
+__device__ __forceinline__ std::uint32_t mapa_u32(const void* p, std::uint32_t rank) {
+  std::uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f32(std::uint32_t addr, std::uint32_t v) {
+  asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(std::uint32_t addr, std::uint32_t a, std::uint32_t b, std::uint32_t c,
+                                              std::uint32_t d) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+// Relaxed remote arrive: no ordering of this thread's earlier memory operations (its global
+// stores need not drain first). For a consumer that has already used the values it read.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(std::uint64_t* bar, std::uint32_t rank) {
+  std::uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 // CTA-pair TMA: the box lands in this CTA's smem, its bytes complete on the pair LEADER's
 // mbarrier (same offset, rank bit cleared) — the leader's MMA waits for both halves.
 __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, std::uint64_t* bar,

@@ -1,5 +1,2 @@
-python bench.py --steps 2 --warmup 3 > gpurun_out/s_n1.log 2>&1; echo "n1 $(grep -o '"value": [0-9.]*' gpurun_out/s_n1.log | head -1)"
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 3 > gpurun_out/s_n2.log 2>&1; echo "n2 $(grep -o '"value": [0-9.]*' gpurun_out/s_n2.log | head -1)"
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 4 --steps 2 --warmup 3 > gpurun_out/s_n4.log 2>&1; echo "n4 $(grep -o '"value": [0-9.]*' gpurun_out/s_n4.log | head -1)"
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 4 --placement split --steps 2 --warmup 3 > gpurun_out/s_n4split.log 2>&1; echo "n4 split $(grep -o '"value": [0-9.]*' gpurun_out/s_n4split.log | head -1)"
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29514 bench.py --gpus 4 --impl reference --steps 1 --warmup 3 > gpurun_out/s_n4ref.log 2>&1; echo "n4 ref $(grep -o '"value": [0-9.]*' gpurun_out/s_n4ref.log | head -1)"
+timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q -k "split" 2>&1 | tail -2
+timeout 300 python scripts/bench_kernels.py splitk_pair 2>&1 | tail -6

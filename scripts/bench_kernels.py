@@ -237,6 +237,33 @@ def timeline():
         print(json.dumps({"gemm": name, **{n: (buf[i] - t0) for i, n in enumerate(names)}}))
 
 
+def timeline_split():
+    """WS_GEMM_ABLATE=8 timeline of CTA 0 for the cluster split-K (pairs, 2 K halves) vs one pass."""
+    import ctypes as C
+    import paper_2602_18931_b200 as ws
+    L = ws.lib()
+    L.ws_debug_gemm_trace.argtypes = [C.c_void_p]
+    names = ["entry", "prologue", "dep_wait", "first_full", "last_mma", "acc_ready", "epi_done", "exit"]
+    for (M, N, K, sp, bn, name) in [(160, 2048, 8192, 1, 0, "1B down M=160 one pass"),
+                                    (160, 2048, 8192, 2, 128, "1B down M=160 split 2 bn128"),
+                                    (655, 2048, 8192, 1, 0, "1B down M=655 one pass"),
+                                    (655, 2048, 8192, 2, 192, "1B down M=655 split 2 bn192")]:
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+        out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+        os.environ["WS_GEMM_PAIR"] = "2"
+        for _ in range(3):
+            ops.gemm(A, W, out=out, epi=1, bn=bn, splits=sp)
+        torch.cuda.synchronize()
+        ops.gemm(A, W, out=out, epi=1, bn=bn, splits=sp)
+        torch.cuda.synchronize()
+        buf = (C.c_ulonglong * 8)()
+        assert L.ws_debug_gemm_trace(buf) == 0
+        t0 = buf[0]
+        print(json.dumps({"gemm": name, **{n: (buf[i] - t0) for i, n in enumerate(names)}}))
+        os.environ.pop("WS_GEMM_PAIR", None)
+
+
 def splitk():
     """Deterministic split-K (fixed split count, last split sums the partials in order) vs one
     pass, for the narrow projections at small (N = 8 GPUs) and full (N = 1) batch rows."""
@@ -266,4 +293,4 @@ if __name__ == "__main__":
         pair(" ".join(sys.argv[2:]) or "8B o")
     else:
         {"gemm": gemm, "gemm_model": gemm_model, "rowstats": rowstats, "one_gemm": one_gemm, "overhead": overhead,
-         "timeline": timeline, "splitk": splitk, "one_add": one_add, "splitk_pair": splitk_pair}[sys.argv[1]]()
+         "timeline": timeline, "splitk": splitk, "one_add": one_add, "splitk_pair": splitk_pair, "timeline_split": timeline_split}[sys.argv[1]]()

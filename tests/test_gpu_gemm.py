@@ -144,25 +144,28 @@ def test_gemm_cta_pair(ops, monkeypatch, epi, shape):
 @pytest.mark.parametrize("epi", [0, 1])
 @pytest.mark.parametrize("splits", [2, 3])
 def test_gemm_cta_pair_split_k(ops, monkeypatch, epi, splits):
-    """Split-K on CTA pairs (each CTA publishes its rows' partial, the last split of a tile sums
-    them in split order): bit for bit the single-CTA split-K result at the same split count,
-    also with an odd number of 128-row blocks (the pair's padding block)."""
+    """Split-K on CTA pairs: two K halves in a cluster of four reduced through distributed shared
+    memory, or (other counts / WS_GEMM_DSMEM=0) each CTA publishing its rows' partial and the
+    last split summing them in split order — bit for bit the single-CTA split-K result at the
+    same split count, also with an odd number of 128-row blocks (the pair's padding block)."""
     M, N, K = 655, 2048, 8192
     g = torch.Generator(device="cuda").manual_seed(splits * 7 + epi)
     A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
     ref = A.float() @ W.float().T
     outs = {}
-    for mode, bn in (("0", 128), ("2", 256), ("2", 96)):
+    for mode, bn, dsmem in (("0", 128, "1"), ("2", 256, "1"), ("2", 96, "1"), ("2", 128, "0"), ("2", 192, "1")):
+        # splits == 2 on pairs reduces through distributed shared memory unless WS_GEMM_DSMEM=0
         monkeypatch.setenv("WS_GEMM_PAIR", mode)
+        monkeypatch.setenv("WS_GEMM_DSMEM", dsmem)
         if epi == 1:
             X = torch.ones(M, N, device="cuda")
             ops.gemm(A, W, out=X, epi=1, splits=splits, bn=bn)
-            outs[(mode, bn)] = X - 1.0
+            outs[(mode, bn, dsmem)] = X - 1.0
         else:
-            outs[(mode, bn)] = ops.gemm(A, W, epi=epi, splits=splits, bn=bn)
+            outs[(mode, bn, dsmem)] = ops.gemm(A, W, epi=epi, splits=splits, bn=bn)
         torch.cuda.synchronize()
-    base = outs[("0", 128)]
+    base = outs[("0", 128, "1")]
     assert rel_err(base, ref) < 6e-3
     for k, v in outs.items():
         assert torch.equal(v, base), k
