@@ -882,13 +882,36 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   TileChoice tc = pick_tile(g.M, g.N, granule, pair_ok);
   if (g.cta_group == 2 || (pair_env == 2 && pair_ok)) tc.cg = 2;
   if (g.bn) tc.bn = g.bn;
+  bool csplit_now = false;
+  // WS_GEMM_CSPLIT=1 (experiment): residual-epilogue projections (O, down) run as cluster
+  // split-K on CTA pairs — a fixed split count whatever M, so results stay batch-invariant —
+  // with BN from the pair cost model over 33 co-resident clusters of four.
+  static const bool csplit = [] {
+    const char* e = std::getenv("WS_GEMM_CSPLIT");
+    return e && e[0] == '1';
+  }();
+  if (csplit && g.splits == 0 && g.epi == kEpiAddF32 && g.cta_group != 1 && !g.bn && g.K / BK >= 16) {
+    csplit_now = true;
+    tc.cg = 2;
+    const int mu = ((g.M + BM - 1) / BM + 1) / 2;
+    long best = -1;
+    for (int b = 256; b >= 128; b -= 32) {
+      const long tiles = static_cast<long>(mu) * ((g.N + b - 1) / b);
+      const long cost = (tiles + 32) / 33 * std::max(2L * b, 256L + b);
+      if (best < 0 || cost < best) {
+        best = cost;
+        tc.bn = b;
+      }
+    }
+  }
   const int bn = tc.bn;
   if (bn < 16 || bn > 256 || bn % granule) throw std::invalid_argument("gemm: tile width must be a multiple of " +
                                                                        std::to_string(granule) + " in [16, 256]");
   if (bn % 32 && g.cta_group != 2) tc.cg = 1;  // an explicit odd-16 width runs on single CTAs
   if (tc.cg == 2 && bn % 32) throw std::invalid_argument("gemm: CTA pairs need BN % 32");
   SplitArgs sk;
-  sk.splits = g.splits > 0 ? g.splits : (g.ws ? pick_splits(g.N, g.K) : 1);
+  sk.splits = csplit_now ? 2 : g.splits > 0 ? g.splits : (g.ws ? pick_splits(g.N, g.K) : 1);
+
   // two K halves on CTA pairs reduce through distributed shared memory (no workspace);
   // WS_GEMM_DSMEM=0 keeps them on the global-partials path (tests compare the two bit for bit)
   const char* de = std::getenv("WS_GEMM_DSMEM");

@@ -143,6 +143,23 @@ def one_gemm():
                       "tflops": 2.0 * M * N * K / t / 1e12}))
 
 
+def one_split():
+    """One cluster split-K GEMM (1B down at 655 rows, 2 K halves, BN 192) and its one-pass
+    counterpart, for ncu side by side."""
+    M, N, K = 655, 2048, 8192
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    os.environ["WS_GEMM_PAIR"] = "2"
+    for _ in range(3):
+        ops.gemm(A, W, out=out, epi=1, bn=192, splits=2)
+        ops.gemm(A, W, out=out, epi=1)
+    torch.cuda.synchronize()
+    ops.gemm(A, W, out=out, epi=1, bn=192, splits=2)
+    ops.gemm(A, W, out=out, epi=1)
+    torch.cuda.synchronize()
+
+
 def one_add():
     """One residual-epilogue GEMM (1B down projection at 655 rows, out fp32 += acc), for ncu."""
     M, N, K = 655, 2048, 8192
@@ -293,4 +310,4 @@ if __name__ == "__main__":
         pair(" ".join(sys.argv[2:]) or "8B o")
     else:
         {"gemm": gemm, "gemm_model": gemm_model, "rowstats": rowstats, "one_gemm": one_gemm, "overhead": overhead,
-         "timeline": timeline, "splitk": splitk, "one_add": one_add, "splitk_pair": splitk_pair, "timeline_split": timeline_split}[sys.argv[1]]()
+         "timeline": timeline, "splitk": splitk, "one_add": one_add, "splitk_pair": splitk_pair, "timeline_split": timeline_split, "one_split": one_split}[sys.argv[1]]()
