@@ -130,8 +130,9 @@ def rowstats():
 
 
 def one_gemm():
-    """One realistic verify-batch GEMM (8B gate/up + SwiGLU at 526 rows), for ncu --set full."""
-    M, N, K = 526, 28672, 4096
+    """One realistic verify-batch GEMM (8B gate/up + SwiGLU; M = the mean verify batch, 990 rows
+    under verify batching, override with WS_ONE_GEMM_M), for ncu --set full."""
+    M, N, K = int(os.environ.get("WS_ONE_GEMM_M", "990")), 28672, 4096
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
     out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
