@@ -170,15 +170,20 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
         if (g.masked) m_hi = row_mask[g.row0 + j]; else last_hi = g.extra_len - g.n_rows + j;
       }
     }
-    // Q fragments (A operand) for all k16 steps
-    std::uint32_t qa[KST][4];
-    if (warp_live) {
+    // Q fragments (A operand) for all k16 steps: held in registers for hd 64; for hd 128 they
+    // are re-read from smem per tile (32 fewer registers → one more CTA per SM)
+    constexpr bool kQReg = HD <= 64;
+    std::uint32_t qa[kQReg ? KST : 1][4];
+    auto q_frag = [&](int kk, std::uint32_t (&f)[4]) {
+      // lanes 0-15 rows 0-15 chunk 2kk, lanes 16-31 rows 0-15 chunk 2kk+1
+      const int row = vw * 16 + (lane % 16);
+      const int chunk = 2 * kk + lane / 16;
+      ldsm_x4(f, &sQ[swz<HD>(row, chunk)]);
+    };
+    if constexpr (kQReg) {
+      if (warp_live) {
 #pragma unroll
-      for (int kk = 0; kk < KST; ++kk) {
-        // lanes 0-15 rows 0-15 chunk 2kk, lanes 16-31 rows 0-15 chunk 2kk+1
-        const int row = vw * 16 + (lane % 16);
-        const int chunk = 2 * kk + lane / 16;
-        ldsm_x4(qa[kk], &sQ[swz<HD>(row, chunk)]);
+        for (int kk = 0; kk < KST; ++kk) q_frag(kk, qa[kk]);
       }
     }
     float o[NT][4];
@@ -203,6 +208,13 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
         for (int nt = 0; nt < 4; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
 #pragma unroll
         for (int kk = 0; kk < KST; ++kk) {
+          std::uint32_t qf[4];
+          if constexpr (kQReg) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) qf[e] = qa[kk][e];
+          } else {
+            q_frag(kk, qf);
+          }
 #pragma unroll
           for (int np = 0; np < 2; ++np) {  // pairs of n8 tiles (16 positions) per ldmatrix.x4
             std::uint32_t kb[4];
@@ -210,8 +222,8 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
             const int pos = np * 16 + (lane % 8) + ((lane / 16) * 8);
             const int chunk = 2 * kk + ((lane / 8) & 1);
             ldsm_x4(kb, kv_tile(ks, buf, 0) + swz<HD>(pos, chunk));
-            mma16816(s[2 * np], qa[kk], kb[0], kb[1]);
-            mma16816(s[2 * np + 1], qa[kk], kb[2], kb[3]);
+            mma16816(s[2 * np], qf, kb[0], kb[1]);
+            mma16816(s[2 * np + 1], qf, kb[2], kb[3]);
           }
         }
         // visibility + scale (exp2 domain)

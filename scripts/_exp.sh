@@ -1,1 +1,2 @@
-python scripts/bench_kernels.py one_gemm && ncu --set full --import-source on --clock-control none -k regex:gemm_tn_kernel -s 8 -c 1 -o gpurun_out/r01_ncu_gemm_gateup_990 python scripts/bench_kernels.py one_gemm > gpurun_out/ncu_gu.log 2>&1; tail -1 gpurun_out/ncu_gu.log
+timeout 600 python -m pytest tests/test_gpu_model.py -x -q 2>&1 | tail -2
+python scripts/forward_probe.py 1 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_att.csv python scripts/forward_probe.py 1 > /dev/null 2>&1; wc -l gpurun_out/launches_att.csv
