@@ -133,19 +133,19 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
   // entries — attention_vectors_per_cta())
   for (int pass0 = g.pad; pass0 < nvec && pass0 < g.pad + kVecPerPass; pass0 += kVecPerPass) {
     __syncthreads();
-    // Q for this pass: vector v -> (row j = v / G, head kvh*G + v % G), zero past nvec
-    for (int i = threadIdx.x; i < kVecPerPass * C; i += 32 * VW * KS) {
-      const int vv = i / C, c = i % C, v = pass0 + vv;
-      uint4 val = make_uint4(0, 0, 0, 0);
-      if (v < nvec) {
-        const int j = v / G, h = kvh * G + v % G;
-        val = *reinterpret_cast<const uint4*>(q + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD + c * 8);
-      }
-      sQ[swz<HD>(vv, c)] = val;
-    }
 #pragma unroll
     for (int i = 0; i < STAGES - 1; ++i) {  // ring prologue: this slice's first STAGES-1 tiles
       if (i < n_iter) load_tile(i * KS + ks, i);
+      if (i == 0) {
+        // Q for this pass, in the first group so its latency overlaps the first K/V tiles:
+        // vector v -> (row j = v / G, head kvh*G + v % G), zero-filled past nvec
+        for (int e = threadIdx.x; e < kVecPerPass * C; e += 32 * VW * KS) {
+          const int vv = e / C, c = e % C, v = pass0 + vv;
+          const bool ok = v < nvec;
+          const int j = ok ? v / G : 0, h = ok ? kvh * G + v % G : 0;
+          cp_async16(&sQ[swz<HD>(vv, c)], q + (static_cast<std::size_t>(g.row0 + j) * nq + h) * HD + c * 8, ok);
+        }
+      }
       cp_async_commit();
     }
     __syncthreads();
@@ -180,12 +180,7 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
       const int chunk = 2 * kk + lane / 16;
       ldsm_x4(f, &sQ[swz<HD>(row, chunk)]);
     };
-    if constexpr (kQReg) {
-      if (warp_live) {
-#pragma unroll
-        for (int kk = 0; kk < KST; ++kk) q_frag(kk, qa[kk]);
-      }
-    }
+    // (hd 64: the fragments are read once Q has landed, at the first tile)
     float o[NT][4];
 #pragma unroll
     for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
@@ -201,6 +196,12 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
         asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
       }
       __syncthreads();
+      if constexpr (kQReg) {
+        if (it == 0 && warp_live) {  // Q landed with the first group
+#pragma unroll
+          for (int kk = 0; kk < KST; ++kk) q_frag(kk, qa[kk]);
+        }
+      }
       if (warp_live && t < n_tiles) {
         // S = Q·Kᵀ over 32 positions: 4 n8 tiles
         float s[4][4];
