@@ -391,14 +391,14 @@ void attention(const void* q, const void* k_pool, const void* v_pool, const Attn
                cudaStream_t st) {
   if (n_entries <= 0) return;
   const float sl2 = s.scale * 1.4426950408889634f;
-  // key slices per head dim (measured: two slices help the 64-wide draft heads, not the
-  // 128-wide target heads, whose CTAs then fit fewer per SM)
-  // K/V ring depth 2 (measured in config 3: 3 and 4 stages cost occupancy and were 3-4% slower
-  // end to end)
+  // One key slice and a 2-deep K/V ring for both head dims (ncu launch lists of
+  // scripts/forward_probe.py, profiles/r01_driver_policy.md): with Q riding in the first
+  // cp.async group, hd 64 runs 32.2 µs per layer with one slice against 37.2 with two and 47.7
+  // with a 3-deep ring; deeper rings cost occupancy.
   if (s.hd == 128)
     launch_attn<128, 2, 1, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
   else if (s.hd == 64)
-    launch_attn<64, 1, 2, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
+    launch_attn<64, 1, 1, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
   else
     throw std::invalid_argument("attention: head dim must be 64 or 128");
 }
