@@ -45,6 +45,9 @@ def parse():
                    help="llama, N >= 2: 'split' puts the draft model on its own GPU (ranks < N/2 drive "
                         "target GPU r + draft GPU r + N/2; SURVEY §8e), 'shared' shards requests over all GPUs")
     p.add_argument("--cpu-sample-s", type=float, default=6.0)
+    p.add_argument("--target", choices=["llama3-8b", "llama3-70b"], default="llama3-8b",
+                   help="llama: the target model shape; llama3-70b (BASELINE config 5's model) runs whole on "
+                        "one GPU per rank (141 GB of bf16 weights; use --requests 128), no tensor parallelism")
     return p.parse_args()
 
 
@@ -127,16 +130,19 @@ def tiny_cfg(args, world, rank):
 
 def config_block(args, world, host_threads):
     if args.workload == "llama":
-        return {"workload": "BASELINE configs[2]: Llama-3.1-8B-shape target / Llama-3.2-1B-shape draft "
+        tname = {"llama3-8b": "Llama-3.1-8B", "llama3-70b": "Llama-3.1-70B"}[args.target]
+        return {"workload": ("BASELINE configs[2]: " if args.target == "llama3-8b" else
+                             "BASELINE configs[4]'s model, whole on one GPU per rank (no TP): ") +
+                            f"{tname}-shape target / Llama-3.2-1B-shape draft "
                             "(random-init bf16), 128-token seeded prompts, 100 generated tokens, "
                             f"{args.requests} requests, k={args.k}, b=2, s=4, theta=phi=0.5, RTT 20 ms "
                             "(virtual), greedy verify, planted shared bigram bias (match ~0.8)",
-                "model": "llama3-8b + llama3.2-1b", "global_batch": args.requests, "seq_len": 128 + 100,
+                "model": f"{args.target} + llama3.2-1b", "global_batch": args.requests, "seq_len": 128 + 100,
                 "parallelism": (f"split placement: requests sharded over {world // 2} target GPU(s), each "
                                 f"paired with its own draft GPU (SURVEY §8e), no collective"
                                 if args.placement == "split" and world >= 2 and world % 2 == 0 else
                                 f"requests sharded over {world} GPU(s) (strong scaling), no collective"),
-                "l2": "weights (18.5 GB) and KV (>126 MB) exceed L2; no explicit flush needed"}
+                "l2": "weights (>=18.5 GB) and KV (>126 MB) exceed L2; no explicit flush needed"}
     return {"workload": "BASELINE configs[1]: tiny draft/target pair (oracle tables, V=32768), "
                         f"{TINY_REQ_PER_GPU} requests/GPU, k=8, b=2, s=4, theta=phi=0.5, RTT 20 ms, "
                         "max_nodes=256", "verify": args.verify,
@@ -145,11 +151,15 @@ def config_block(args, world, host_threads):
             "l2": "tables are L2-resident by design; L2 flushed (256 MB write) before every timed step"}
 
 
-def llama_roofline(stats, k, peak_bw, peak_tf, avg_ctx):
+def llama_roofline(stats, k, peak_bw, peak_tf, avg_ctx, target="llama3-8b"):
     """Verify-step roofline (SURVEY §8d units): FLOPs = 2 P_mm rows + 4 L rows ctx n_q hd;
     bytes = 2 P_mm + R ctx KVB + rows KVB + rows V 2 (+ K3 read of the logits)."""
-    P_mm = 7.505e9  # Llama-3.1-8B matmul params incl. LM head
-    L, nq, hd, V, kvb = 32, 32, 128, 128256, 32 * 2 * 8 * 128 * 2
+    if target == "llama3-70b":
+        P_mm, L, nq = 69.50e9, 80, 64  # Llama-3.1-70B matmul params incl. LM head (SURVEY §8d)
+    else:
+        P_mm, L, nq = 7.505e9, 32, 32  # Llama-3.1-8B
+    hd, V = 128, 128256
+    kvb = L * 2 * 8 * 128 * 2
     fw = max(1, stats["target_forwards"])
     rows = stats["target_rows"] / fw
     reqs = rows / (k + 1)
@@ -282,7 +292,7 @@ def main():
             cfg = llama_cfg(args, world, rank)
         cfg.host_threads = max(1, args.shards)
         if active:
-            ctx.load_models(abi.model_cfg(max_requests=args.requests),
+            ctx.load_models(abi.model_cfg(target=args.target, max_requests=args.requests),
                             draft_device=local_rank + world // 2 if split else -1)
 
         def run_once(tokens_out=False):
@@ -352,10 +362,10 @@ def main():
         if args.workload == "llama":
             local = cfg.local_requests
             avg_ctx = 128 + 50 + args.k / 2
-            roof, rows, fl, by, t_meas = llama_roofline(mstats, args.k, peak_bw, peak_tf, avg_ctx)
+            roof, rows, fl, by, t_meas = llama_roofline(mstats, args.k, peak_bw, peak_tf, avg_ctx, args.target)
             traffic = None
             tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_verify_traffic.json")
-            if os.path.exists(tpath):  # ncu dram bytes of one verify forward (committed capture)
+            if os.path.exists(tpath) and args.target == "llama3-8b":  # ncu dram bytes of one verify forward
                 with open(tpath) as f:
                     tj = json.load(f)
                 traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
@@ -367,7 +377,10 @@ def main():
             line["roofline"] = roof
             line["model_time"] = {k: (v / args.steps if isinstance(v, float) else v // args.steps)
                                   for k, v in mstats.items()}
-            if world == 1:
+            if world == 1 and args.target != "llama3-8b":
+                line["cpu_baseline"] = {"value": None, "unavailable": "the numpy-port sample is defined for the "
+                                                                      "config-3 (8B) target"}
+            elif world == 1:
                 try:
                     line["cpu_baseline"] = cpu_port_sample(args, args.k)
                 except Exception as e:  # the CPU port needs ~2 GB of host RAM per 8B layer
