@@ -6,7 +6,7 @@
 // (online rescaling when the running max grows), fp32 accumulation. Top-2 follows the
 // Prediction tie rule (types.hpp:54-55): descending value, ties to the lower id.
 //
-// Layout: grid (splits, rows); a CTA streams one fixed 32768-wide vocab chunk of one row with
+// Layout: grid (splits, rows); a CTA streams one fixed 65536-wide vocab chunk of one row with
 // 16-byte vector loads (4 in flight per thread), reduces warp → CTA, and the last CTA of a row
 // (atomic ticket) merges the chunk partials in chunk order → deterministic and batch-invariant.
 // With the verify epilogue enabled, the last row of a request to finish runs run_target_step
@@ -33,7 +33,22 @@ struct State {
   float m, z, s;  // log2-domain running max, sum, sum e*d
   float v1, v2;   // raw top-2 logits
   std::uint32_t i1, i2;
+  float2 z2, s2;  // the vector path's (z, s) as even/odd-element lanes (packed f32x2 math)
 };
+
+// The vector path's top-2 is found in two steps. The stream keeps, branch-free, the thread's
+// two best 8-element vectors ranked by (vector max desc, vector index asc). A per-element insert
+// there would diverge at warp level on almost every vector (profiles/r01_ncu_rowstats.md: 27
+// issued instructions per element). Then only those two vectors are rescanned with insert().
+// This is exact: the best element lies in the best vector. The second-best element is either in
+// that vector too or it is the maximum of its own vector, and then that vector ranks second.
+// Ids grow with the vector index inside a thread, so a tie keeps the earlier vector, matching
+// the Prediction tie rule (ties to the lower id).
+struct Best2 {
+  float m1, m2;
+  std::uint32_t i1, i2;  // element id of the vector's first lane; kNone if unset
+};
+constexpr std::uint32_t kNone = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void init(State& a) {
   a.m = -INFINITY;
@@ -41,6 +56,21 @@ __device__ __forceinline__ void init(State& a) {
   a.s = 0.f;
   a.v1 = a.v2 = -INFINITY;
   a.i1 = a.i2 = 0xFFFFFFFFu;
+  a.z2 = a.s2 = make_float2(0.f, 0.f);
+}
+
+__device__ __forceinline__ void init(Best2& b) {
+  b.m1 = b.m2 = -INFINITY;
+  b.i1 = b.i2 = kNone;
+}
+
+__device__ __forceinline__ void track(Best2& b, float mx, std::uint32_t id0) {
+  const bool p1 = mx > b.m1 || b.i1 == kNone;
+  const bool p2 = mx > b.m2 || b.i2 == kNone;
+  b.m2 = p1 ? b.m1 : (p2 ? mx : b.m2);
+  b.i2 = p1 ? b.i1 : (p2 ? id0 : b.i2);
+  b.m1 = p1 ? mx : b.m1;
+  b.i1 = p1 ? id0 : b.i1;
 }
 
 __device__ __forceinline__ bool better(float v, std::uint32_t i, float w, std::uint32_t j) {
@@ -100,7 +130,7 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__device__ __forceinline__ void absorb8(State& a, const uint4& q, std::uint32_t id0, float cl) {
+__device__ __forceinline__ void absorb8(State& a, Best2& b, const uint4& q, std::uint32_t id0, float cl) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
   float x[8];
 #pragma unroll
@@ -114,23 +144,34 @@ __device__ __forceinline__ void absorb8(State& a, const uint4& q, std::uint32_t 
   for (int j = 1; j < 8; ++j) mx = fmaxf(mx, x[j]);
   const float lm = mx * cl;
   if (lm > a.m) {
-    if (a.z > 0.f) {
-      const float f = exp2f(a.m - lm);
-      a.s = f * (a.s + a.z * (a.m - lm));
-      a.z *= f;
+    if (a.z2.x > 0.f || a.z2.y > 0.f) {
+      const float f = exp2f(a.m - lm), dm = a.m - lm;
+      const float2 f2 = make_float2(f, f);
+      a.s2 = __fmul2_rn(f2, __ffma2_rn(a.z2, make_float2(dm, dm), a.s2));
+      a.z2 = __fmul2_rn(a.z2, f2);
     }
     a.m = lm;
   }
+  // two elements per packed FFMA2/FADD2 (sm_100): 1.5 instead of 3 FP32 issues per element
+  const float2 c2 = make_float2(cl, cl), n2 = make_float2(-a.m, -a.m);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float d = fmaf(x[j], cl, -a.m);
-    const float e = ex2(d);
-    a.z += e;
-    a.s = fmaf(e, d, a.s);
+  for (int j = 0; j < 4; ++j) {
+    const float2 d = __ffma2_rn(make_float2(x[2 * j], x[2 * j + 1]), c2, n2);
+    const float2 e = make_float2(ex2(d.x), ex2(d.y));
+    a.z2 = __fadd2_rn(a.z2, e);
+    a.s2 = __ffma2_rn(e, d, a.s2);
   }
-  if (mx >= a.v2) {
+  track(b, mx, id0);
+}
+
+// exact top-2 over one 8-element vector of the row (the rescan of a Best2 entry)
+__device__ __forceinline__ void insert8(State& a, const uint4& q, std::uint32_t id0) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) insert(a, x[j], id0 + j);
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __bfloat1622float2(h[j]);
+    insert(a, f.x, id0 + 2 * j);
+    insert(a, f.y, id0 + 2 * j + 1);
   }
 }
 
@@ -205,17 +246,23 @@ __global__ void __launch_bounds__(kThreads) row_stats_kernel(
   if (vec_ok) {
     const uint4* v = reinterpret_cast<const uint4*>(x + lo);
     const std::uint32_t nvec = (hi - lo) / 8;
+    Best2 best;
+    init(best);
     std::uint32_t i = threadIdx.x;
     for (; i + 3 * kThreads < nvec; i += 4 * kThreads) {
       uint4 q[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) q[u] = __ldcs(v + i + u * kThreads);
-      // (absorb32's tree form measured slower on B200 — 188 vs 158 µs at 1280x128256 — from
-      // register pressure; the per-vector update is kept)
+      // (loads of the next four issued before these are absorbed measured slower: 62 registers)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) absorb8(a, q[u], lo + 8 * (i + u * kThreads), cl);
+      for (int u = 0; u < 4; ++u) absorb8(a, best, q[u], lo + 8 * (i + u * kThreads), cl);
     }
-    for (; i < nvec; i += kThreads) absorb8(a, __ldcs(v + i), lo + 8 * i, cl);
+    for (; i < nvec; i += kThreads) absorb8(a, best, __ldcs(v + i), lo + 8 * i, cl);
+    a.z = a.z2.x + a.z2.y;  // fold the lanes (same running max) before the scalar tail
+    a.s = a.s2.x + a.s2.y;
+    // rescan the two best vectors (32 B per thread, L2 hits)
+    if (best.i1 != kNone) insert8(a, v[(best.i1 - lo) / 8], best.i1);
+    if (best.i2 != kNone) insert8(a, v[(best.i2 - lo) / 8], best.i2);
     for (std::uint32_t t = lo + nvec * 8 + threadIdx.x; t < hi; t += kThreads)
       absorb1(a, __bfloat162float(x[t]), t, cl);
   } else {
