@@ -174,6 +174,43 @@ def llama_roofline(stats, k, peak_bw, peak_tf, avg_ctx, target="llama3-8b"):
             "frac": t_hbm / t_meas}, rows, flops, byts, t_meas
 
 
+def k3_sample(rows, peak_bw, iters=20):
+    """K3 (fused softmax + entropy + top-2; the K4 accept walk is fused behind it) timed alone
+    on a verify-shaped bf16 logits block: CUDA events on the launching stream, L2 flushed
+    (256 MB write) before every launch. Algorithmic bytes = rows x V x 2 (logits read once)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2602_18931_b200 as ws
+    L, V = ws.lib(), 128256
+    L.ws_op_row_stats_workspace_bytes.restype = C.c_size_t
+    L.ws_op_row_stats_workspace_bytes.argtypes = [C.c_uint32] * 3
+    L.ws_op_row_stats_bf16.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = (torch.randn(rows, V, device="cuda", generator=g) * 2).to(torch.bfloat16)
+    wsb = torch.zeros(L.ws_op_row_stats_workspace_bytes(rows, V, 0), dtype=torch.uint8, device="cuda")
+    out = torch.zeros(rows * 40, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream()
+    tot = 0.0
+    for it in range(iters + 3):
+        flush.fill_(0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        L.ws_op_row_stats_bf16(x.data_ptr(), rows, V, V, 1.0, out.data_ptr(), None, wsb.data_ptr(), st.cuda_stream)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if it >= 3:
+            tot += e0.elapsed_time(e1) / 1e3
+    t = tot / iters
+    gbs = rows * V * 2 / t / 1e9
+    return {"kernel": "K3 row_stats (softmax + entropy + top-2, K4 accept fused)", "rows": rows, "vocab": V,
+            "us": t * 1e6, "bound": "hbm", "achieved": gbs, "peak": peak_bw, "unit": "GB/s", "frac": gbs / peak_bw,
+            "timing": "CUDA events, L2 flushed before each launch, verify-shaped rows (mean verify batch)"}
+
+
 def cpu_reference_llama(k, requests, samples=1):
     """The reference's CPU implementation of the config-3 path: the reference protocol itself
     (run_sim_full via oracle/_ref — or the restatement when the reference is absent — on its
@@ -375,6 +412,10 @@ def main():
                          "peak_kind": peak_kind, "rows_per_verify": rows, "ms_per_verify": t_meas * 1e3,
                          "alg_flops_per_verify": fl, "alg_bytes_per_verify": by})
             line["roofline"] = roof
+            try:
+                line["k3"] = k3_sample(max(1, int(round(rows))), peak_bw)
+            except Exception as e:  # a secondary figure: never fail the bench line over it
+                line["k3"] = {"unavailable": str(e)}
             line["model_time"] = {k: (v / args.steps if isinstance(v, float) else v // args.steps)
                                   for k, v in mstats.items()}
             if world == 1 and args.target != "llama3-8b":
