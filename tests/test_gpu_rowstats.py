@@ -82,6 +82,39 @@ def test_ties_resolve_to_lower_id(L):
     assert got[2][3] == pytest.approx(np.log(V), rel=1e-4)
 
 
+def test_top2_vector_and_thread_placements(L):
+    """K3 finds each thread's top-2 from its two best 8-element vectors (by vector maximum),
+    then rescans those two. Plant the top-2 where that could go wrong: both in one vector, in two
+    vectors of one thread (ids 2048 apart inside a 65536-wide chunk), ties inside one thread,
+    ties between a same-vector element and another thread's, and across chunks."""
+    V = 128256
+    x = (torch.randn(8, V, device="cuda", generator=torch.Generator(device="cuda").manual_seed(11)) * 0.1)
+    plants = [
+        {100: 5.0, 103: 4.0},                      # same vector
+        {5: 5.0, 5 + 2048 * 3: 4.0},               # same thread, different vectors
+        {7: 5.0, 7 + 2048: 5.0, 3: 4.5},           # tie for first in one thread; 3rd in 1st's vector
+        {1 + 2048 * 5: 5.0, 1 + 2048 * 2: 5.0, 1: 5.0},  # three-way tie in one thread
+        {16: 5.0, 17: 4.0, 24: 4.0},               # tie for second: same vector (17) vs thread 3 (24)
+        {40: 5.0, 47: 4.0, 8: 4.0},                # tie for second: lower id in another thread wins
+        {65536 + 10: 5.0, 10: 5.0},                # tie across chunks
+        {128255: 5.0, 128254: 5.0},                # last vector of the row
+    ]
+    want = [(100, 103), (5, 5 + 2048 * 3), (7, 7 + 2048), (1, 1 + 2048 * 2), (16, 17), (40, 8),
+            (10, 65546), (128254, 128255)]
+    for r, pl in enumerate(plants):
+        for i, v in pl.items():
+            x[r, i] = v
+    x = x.to(torch.bfloat16)
+    got, _ = run_stats(L, x)
+    xf = x.float().cpu().numpy()
+    for r in range(len(plants)):
+        assert got[r][1] == want[r], (r, got[r][1])
+        _, ids, probs, h = po.row_stats(xf[r])
+        assert ids == want[r]
+        assert got[r][2] == pytest.approx(probs, rel=1e-3)
+        assert got[r][3] == pytest.approx(h, rel=1e-3)
+
+
 def test_temperature(L):
     x = make_logits(16, 32000, 2.0, 5)
     got, _ = run_stats(L, x, inv_temp=1.0 / 0.7)
