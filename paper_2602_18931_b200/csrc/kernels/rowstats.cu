@@ -111,18 +111,6 @@ __device__ __forceinline__ void merge(State& a, const State& b) {
   insert(a, b.v2, b.i2);
 }
 
-__device__ __forceinline__ State shfl_state(const State& a, int off) {
-  State b;
-  b.m = __shfl_xor_sync(0xffffffffu, a.m, off);
-  b.z = __shfl_xor_sync(0xffffffffu, a.z, off);
-  b.s = __shfl_xor_sync(0xffffffffu, a.s, off);
-  b.v1 = __shfl_xor_sync(0xffffffffu, a.v1, off);
-  b.v2 = __shfl_xor_sync(0xffffffffu, a.v2, off);
-  b.i1 = __shfl_xor_sync(0xffffffffu, a.i1, off);
-  b.i2 = __shfl_xor_sync(0xffffffffu, a.i2, off);
-  return b;
-}
-
 // MUFU.EX2 directly (rel. error ~2^-22): the per-element exponential of the streaming pass.
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -131,13 +119,13 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 __device__ __forceinline__ void absorb8(State& a, Best2& b, const uint4& q, std::uint32_t id0, float cl) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+  // bf16 -> f32 is a 16-bit shift: one integer op per element (low half: shift, high: mask)
+  const std::uint32_t wd[4] = {q.x, q.y, q.z, q.w};
   float x[8];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const float2 f = __bfloat1622float2(h[j]);
-    x[2 * j] = f.x;
-    x[2 * j + 1] = f.y;
+    x[2 * j] = __uint_as_float(wd[j] << 16);
+    x[2 * j + 1] = __uint_as_float(wd[j] & 0xFFFF0000u);
   }
   float mx = x[0];
 #pragma unroll
@@ -268,11 +256,32 @@ __global__ void __launch_bounds__(kThreads) row_stats_kernel(
   } else {
     for (std::uint32_t t = lo + threadIdx.x; t < hi; t += kThreads) absorb1(a, __bfloat162float(x[t]), t, cl);
   }
-  // warp → CTA reduction (fixed order → deterministic)
+  // warp → CTA reduction (fixed order → deterministic): the warp max first, then every lane
+  // rescales its (z, s) to it once, so the butterfly levels are plain sums plus the top-2
+  // inserts (one exp2 per lane instead of two per level)
+  {
+    float mw = a.m;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const State b = shfl_state(a, off);
-    merge(a, b);
+    for (int off = 16; off > 0; off >>= 1) mw = fmaxf(mw, __shfl_xor_sync(0xffffffffu, mw, off));
+    if (a.z > 0.f) {
+      const float f = exp2f(a.m - mw);
+      a.s = f * (a.s + a.z * (a.m - mw));
+      a.z *= f;
+    }
+    a.m = mw;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float z = __shfl_xor_sync(0xffffffffu, a.z, off);
+      const float sv = __shfl_xor_sync(0xffffffffu, a.s, off);
+      const float v1 = __shfl_xor_sync(0xffffffffu, a.v1, off);
+      const float v2 = __shfl_xor_sync(0xffffffffu, a.v2, off);
+      const std::uint32_t i1 = __shfl_xor_sync(0xffffffffu, a.i1, off);
+      const std::uint32_t i2 = __shfl_xor_sync(0xffffffffu, a.i2, off);
+      a.z += z;
+      a.s += sv;
+      insert(a, v1, i1);
+      insert(a, v2, i2);
+    }
   }
   __shared__ State warp_states[kThreads / 32];
   __shared__ bool is_last;
