@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) row_stats_kernel(
     for (; i < nvec; i += kThreads) absorb8(a, best, __ldcs(v + i), lo + 8 * i, cl);
     a.z = a.z2.x + a.z2.y;  // fold the lanes (same running max) before the scalar tail
     a.s = a.s2.x + a.s2.y;
-    // rescan the two best vectors (32 B per thread, L2 hits)
+    // rescan the two best vectors (32 B per thread, mostly L2 hits)
     if (best.i1 != kNone) insert8(a, v[(best.i1 - lo) / 8], best.i1);
     if (best.i2 != kNone) insert8(a, v[(best.i2 - lo) / 8], best.i2);
     for (std::uint32_t t = lo + nvec * 8 + threadIdx.x; t < hi; t += kThreads)
