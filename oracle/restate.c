@@ -456,7 +456,7 @@ void or_row_stats(const float* x, uint32_t vocab, double it, ws_pred* out) {
     double d = (double)x[v] * it - m;
     double e = exp(d);
     z += e;
-    s += e * d;
+    if (e > 0.0) s += e * d; /* entropy_of's 0 ln 0 = 0 (oracle.hpp:21-33): -inf logits add nothing */
   }
   out->n = vocab >= 2 ? 2 : 1;
   out->id[0] = i1;

@@ -31,11 +31,6 @@ int guard(const char* what, F&& f) {
     return wsb::ops_guarded_rc(what, e);
   }
 }
-struct LastStats {
-  double target_ms = 0, draft_ms = 0;
-  std::uint64_t target_rows = 0, draft_rows = 0, target_forwards = 0, draft_forwards = 0;
-};
-LastStats g_last;
 }  // namespace
 
 extern "C" {
@@ -123,7 +118,7 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
         std::fprintf(stderr, "}\n");
       }
     }
-    LastStats st;
+    ws_ctx::ModelStats st;
     std::uint64_t rows_kind[3] = {0, 0, 0}, jobs_kind[3] = {0, 0, 0};
     for (auto* bk : used) {
       st.target_ms += bk->target_ms;
@@ -137,7 +132,7 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
         jobs_kind[k] += bk->jobs_by_kind[k];
       }
     }
-    g_last = st;
+    ctx->last_stats = st;
     if (std::getenv("WS_DEBUG_ROWS")) {
       std::fprintf(stderr,
                    "[ws] target rows %llu in %llu fwd (%.1f ms) | draft rows ctrl %llu / %llu jobs, worker %llu / "
@@ -162,8 +157,10 @@ int ws_model_export_trace(ws_ctx* ctx, uint32_t first_request, uint32_t n, uint3
   });
 }
 
-int ws_model_stats(ws_ctx*, double* target_ms, double* draft_ms, uint64_t* target_rows, uint64_t* draft_rows,
+int ws_model_stats(ws_ctx* ctx, double* target_ms, double* draft_ms, uint64_t* target_rows, uint64_t* draft_rows,
                    uint64_t* target_forwards, uint64_t* draft_forwards) {
+  if (!ctx) return WS_EARG;
+  const ws_ctx::ModelStats& g_last = ctx->last_stats;
   if (target_ms) *target_ms = g_last.target_ms;
   if (draft_ms) *draft_ms = g_last.draft_ms;
   if (target_rows) *target_rows = g_last.target_rows;

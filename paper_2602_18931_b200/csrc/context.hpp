@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <memory>
 #include <vector>
 
@@ -17,6 +18,11 @@ struct ws_ctx {
   std::unique_ptr<wsb::ModelPair> models;
   // real-model protocol threads' backends (streams, workspaces), kept across runs
   std::vector<std::unique_ptr<wsb::ModelBackend_Llama>> model_lanes;
+  // model-step statistics of this context's last ws_run_model_sim (ws_model_stats)
+  struct ModelStats {
+    double target_ms = 0, draft_ms = 0;
+    std::uint64_t target_rows = 0, draft_rows = 0, target_forwards = 0, draft_forwards = 0;
+  } last_stats;
 
   wsb::OracleLane& lane(std::size_t i) {
     while (lanes.size() <= i) lanes.emplace_back(new wsb::OracleLane(&tables, device));

@@ -932,6 +932,10 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
       for (int r0 = 0; r0 < g.M; r0 += per) {
         GemmArgs s = g;
         s.M = std::min(per, g.M - r0);
+        // the fused-norm statistics and the bf16 row copy are indexed by the launch-local row
+        if (g.norm.ss_in) s.norm.ss_in = g.norm.ss_in + r0;
+        if (g.norm.ss) s.norm.ss = g.norm.ss + r0;
+        if (g.norm.xb) s.norm.xb = static_cast<__nv_bfloat16*>(g.norm.xb) + static_cast<std::size_t>(r0) * g.norm.ld_xb;
         s.A = static_cast<const __nv_bfloat16*>(g.A) + static_cast<std::size_t>(r0) * g.lda;
         if (g.epi == kEpiAddF32)
           s.out = static_cast<float*>(g.out) + static_cast<std::size_t>(r0) * g.ldo;

@@ -28,6 +28,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kFloor = -1.2676506002282294e30f;  // -2^100: exp weight 0, products finite
 
 struct State {
   float m, z, s;  // log2-domain running max, sum, sum e*d
@@ -120,7 +121,17 @@ __device__ __forceinline__ float ex2(float x) {
 
 __device__ __forceinline__ void absorb8(State& a, Best2& b, const uint4& q, std::uint32_t id0, float cl) {
   // bf16 -> f32 is a 16-bit shift: one integer op per element (low half: shift, high: mask)
-  const std::uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+  // -inf logits (masked vocabulary) are clamped to -2^100 for the softmax sums: their weight
+  // is still exactly 0, but e*d stays 0 instead of 0*(-inf) = NaN (entropy_of's 0 ln 0 = 0,
+  // oracle.hpp:21-33). One packed bf16x2 max per two elements; the top-2 rescan reads the raw
+  // vector, so a -inf second candidate keeps its value.
+  std::uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&wd[j]);
+    h = __hmax2(h, __floats2bfloat162_rn(kFloor, kFloor));
+    wd[j] = *reinterpret_cast<const std::uint32_t*>(&h);
+  }
   float x[8];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -164,7 +175,7 @@ __device__ __forceinline__ void insert8(State& a, const uint4& q, std::uint32_t 
 }
 
 __device__ __forceinline__ void absorb1(State& a, float x, std::uint32_t id, float cl) {
-  const float l = x * cl;
+  const float l = fmaxf(x, kFloor) * cl;  // -inf → a finite floor (see absorb8)
   if (l > a.m) {
     if (a.z > 0.f) {
       const float f = exp2f(a.m - l);

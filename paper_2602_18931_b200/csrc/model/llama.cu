@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -20,6 +21,15 @@ std::int64_t LlamaShape::params_mm() const {
 }
 
 LlamaShape shape_by_name(const std::string& name) {
+  // "<shape>:L<n>" — the named shape truncated to its first n layers (real-shape parity tests)
+  if (const std::size_t c = name.find(":L"); c != std::string::npos) {
+    LlamaShape s = shape_by_name(name.substr(0, c));
+    const int n = std::atoi(name.c_str() + c + 2);
+    if (n < 1 || n > s.layers) throw ConfigError("bad layer truncation: " + name);
+    s.layers = n;
+    s.name = name;
+    return s;
+  }
   // Llama-3.1-8B / Llama-3.2-1B / Llama-3.1-70B hyper-parameters (BASELINE configs 3 and 5).
   if (name == "llama3-8b") return LlamaShape{name, 32, 4096, 32, 8, 128, 14336, 128256, 1e-5f, 500000.f, 8.f, false};
   if (name == "llama3.2-1b") return LlamaShape{name, 16, 2048, 32, 8, 64, 8192, 128256, 1e-5f, 500000.f, 32.f, true};
@@ -136,7 +146,9 @@ std::unique_ptr<ForwardWorkspace> LlamaModel::make_workspace(int max_rows) const
   WS_CUDA(cudaSetDevice(device_));
   std::unique_ptr<ForwardWorkspace> ws(new ForwardWorkspace(device_));
   ensure_rows(*ws, max_rows, max_rows);
-  ws->gemm_ws_bytes = gemm_workspace_bytes(4096);  // split-K partials (row-sliced beyond 4096 rows)
+  // split-K partials (row-sliced beyond 4096 rows; WS_GEMM_WS_ROWS shrinks it for the slicing tests)
+  const char* wr = std::getenv("WS_GEMM_WS_ROWS");
+  ws->gemm_ws_bytes = gemm_workspace_bytes(wr ? std::max(1, std::atoi(wr)) : 4096);
   WS_CUDA(cudaMalloc(&ws->gemm_ws, ws->gemm_ws_bytes));
   WS_CUDA(cudaMemset(ws->gemm_ws, 0, ws->gemm_ws_bytes));
   return ws;

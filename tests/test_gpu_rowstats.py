@@ -182,3 +182,27 @@ def test_verify_greedy_epilogue(L, k):
             assert int(o["a"][j]) == a
             assert int(o["b"][j]) == int(argmax[j, a])
             assert float(o["h"][j]) == preds[j * (k + 1) + a][3]
+
+
+@pytest.mark.parametrize("V", [1000, 128256, 128257])
+def test_masked_minus_inf_columns(L, V):
+    """-inf logits (masked vocabulary) carry probability 0 and add 0 to the entropy
+    (entropy_of's 0 ln 0 = 0, oracle.hpp:21-33) instead of turning it into NaN; ids, probs and
+    entropy match the fp64 oracle on the same masked rows, in vector chunks and the scalar tail."""
+    rows = 9
+    x = make_logits(rows, V, 2.0, 11 + V, planted=5.0)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    mask = torch.rand(rows, V, device="cuda", generator=g) < 0.5
+    mask[1] = True
+    mask[1, [3, V - 1]] = False  # two survivors, one in the scalar tail when V % 8
+    mask[2, :] = False
+    mask[2, V - 3:] = True       # only the tail masked
+    x = x.masked_fill(mask, float("-inf"))
+    got, st = run_stats(L, x)
+    xf = x.float().cpu().numpy()
+    for r in range(rows):
+        n, ids, probs, h = po.row_stats(xf[r])
+        assert np.isfinite(got[r][3]), r
+        assert got[r][1] == ids, r
+        assert got[r][2] == pytest.approx(probs, rel=1e-3, abs=1e-9)
+        assert got[r][3] == pytest.approx(h, rel=1e-3, abs=1e-6)
