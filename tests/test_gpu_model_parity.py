@@ -25,7 +25,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-from tests import llama_ref as lr  # noqa: E402
+import llama_ref as lr  # noqa: E402  (tests/ is on sys.path under pytest)
 from paper_2602_18931_b200 import abi  # noqa: E402
 
 N_REQ = 104
