@@ -289,6 +289,18 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
 int ws_model_stats(ws_ctx* ctx, double* target_ms, double* draft_ms, uint64_t* target_rows,
                    uint64_t* draft_rows, uint64_t* target_forwards, uint64_t* draft_forwards);
 
+/* Per-unit device time of the last ws_run_model_sim (CUDA events on each unit's stream): the
+ * prompt-prefill phase (prefill_rows prompt tokens; target and draft forwards, no LM head), the
+ * verify forwards (verify_rows fed, verify_out_rows through the LM head + K3/K4 — k+1 per
+ * verify job) and the draft forwards (draft_rows fed, draft_out_rows = leaves + local drafts). */
+typedef struct ws_run_stats {
+  double verify_ms, draft_ms, prefill_target_ms, prefill_draft_ms;
+  uint64_t verify_rows, verify_out_rows, verify_forwards;
+  uint64_t draft_rows, draft_out_rows, draft_forwards;
+  uint64_t prefill_rows, prefill_forwards;
+} ws_run_stats;
+int ws_model_run_stats(ws_ctx* ctx, ws_run_stats* out);
+
 /* single-model forward surface (tests): rows (token, position, KV slot), attention groups
  * {row0, n_rows, prefix_slot, prefix_len, extra_off, extra_len, masked} (7 int32 each) over
  * the slot pool — causal within a group, or (masked) row j sees the extras whose bits are set

@@ -79,6 +79,12 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
       throw wsb::ConfigError("prompt + sequence_length + k exceeds max_ctx");
     WS_CUDA(cudaSetDevice(ctx->device));
     mp.reset_requests();
+    // prompt prefill: its own phase before the protocol starts (every verify then feeds k+1 rows)
+    const std::uint32_t first = c->first_request;
+    const std::uint32_t n_local = c->local_requests ? c->local_requests : c->num_requests - c->first_request;
+    std::vector<std::uint32_t> reqs(n_local);
+    for (std::uint32_t i = 0; i < n_local; ++i) reqs[i] = first + i;
+    const wsb::ModelPair::PrefillStats pre = mp.prefill_prompts(reqs.data(), reqs.size());
     const bool prof = std::getenv("WS_PROFILE") != nullptr;
     // host_threads protocol threads, each with its own backend (streams, workspaces) over a
     // contiguous range of the shard's requests: small per-thread batches still keep the GPU
@@ -127,12 +133,23 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
       st.draft_rows += bk->draft_rows_fed;
       st.target_forwards += bk->target_forwards;
       st.draft_forwards += bk->draft_forwards;
+      st.target_out_rows += bk->target_out_rows;
+      st.draft_out_rows += bk->draft_out_rows;
       for (int k = 0; k < 3; ++k) {
         rows_kind[k] += bk->rows_by_kind[k];
         jobs_kind[k] += bk->jobs_by_kind[k];
       }
     }
+    st.prefill_target_ms = pre.target_ms;
+    st.prefill_draft_ms = pre.draft_ms;
+    st.prefill_rows = pre.rows;
+    st.prefill_forwards = pre.target_forwards + pre.draft_forwards;
     ctx->last_stats = st;
+    if (out) {
+      out->gpu_launches += pre.launches;
+      out->h2d_bytes += pre.h2d;
+      out->kernel_ms += pre.target_ms + pre.draft_ms;
+    }
     if (std::getenv("WS_DEBUG_ROWS")) {
       std::fprintf(stderr,
                    "[ws] target rows %llu in %llu fwd (%.1f ms) | draft rows ctrl %llu / %llu jobs, worker %llu / "
@@ -168,6 +185,25 @@ int ws_model_stats(ws_ctx* ctx, double* target_ms, double* draft_ms, uint64_t* t
   if (target_forwards) *target_forwards = g_last.target_forwards;
   if (draft_forwards) *draft_forwards = g_last.draft_forwards;
   return WS_OK;
+}
+
+int ws_model_run_stats(ws_ctx* ctx, ws_run_stats* o) {
+  return guard("ws_model_run_stats", [&] {
+    if (!ctx || !o) throw std::invalid_argument("null argument");
+    const ws_ctx::ModelStats& s = ctx->last_stats;
+    o->verify_ms = s.target_ms;
+    o->draft_ms = s.draft_ms;
+    o->prefill_target_ms = s.prefill_target_ms;
+    o->prefill_draft_ms = s.prefill_draft_ms;
+    o->verify_rows = s.target_rows;
+    o->verify_out_rows = s.target_out_rows;
+    o->verify_forwards = s.target_forwards;
+    o->draft_rows = s.draft_rows;
+    o->draft_out_rows = s.draft_out_rows;
+    o->draft_forwards = s.draft_forwards;
+    o->prefill_rows = s.prefill_rows;
+    o->prefill_forwards = s.prefill_forwards;
+  });
 }
 
 int ws_model_create(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device, ws_model** out) {

@@ -22,6 +22,9 @@ struct ws_ctx {
   struct ModelStats {
     double target_ms = 0, draft_ms = 0;
     std::uint64_t target_rows = 0, draft_rows = 0, target_forwards = 0, draft_forwards = 0;
+    std::uint64_t target_out_rows = 0, draft_out_rows = 0;
+    double prefill_target_ms = 0, prefill_draft_ms = 0;
+    std::uint64_t prefill_rows = 0, prefill_forwards = 0;
   } last_stats;
 
   wsb::OracleLane& lane(std::size_t i) {

@@ -200,6 +200,16 @@ void* LlamaModel::weight(const std::string& w, int l, std::int64_t* numel) {
   if (w == "embed") return ret(embed_, d * s_.vocab);
   if (w == "lm_head") return ret(lm_head_, d * s_.vocab);
   if (w == "final_norm") return ret(final_norm_, d);
+  // the last forward's activations in the model's own workspace (stage-wise parity tests):
+  // ws_x = fp32 residual [cap_rows][d] (numel counted in bf16 units); ws_q / ws_attn / ws_h =
+  // the last layer's rotated q, attention output and SwiGLU output (bf16)
+  if (w == "ws_x") return ret(ws0_->x, 2ll * ws0_->cap_rows * d);
+  if (w == "ws_attn") return ret(ws0_->attn, static_cast<std::int64_t>(ws0_->cap_rows) * s_.n_q * s_.hd);
+  if (w == "ws_h") return ret(ws0_->h, static_cast<std::int64_t>(ws0_->cap_rows) * s_.ffn);
+  if (w == "ws_q") return ret(ws0_->q, static_cast<std::int64_t>(ws0_->cap_rows) * s_.n_q * s_.hd);
+  // the KV pools [layer][slot][n_kv][hd] (tests read back what the QKV epilogue stored)
+  if (w == "k_pool" || w == "v_pool")
+    return ret(w == "k_pool" ? k_pool_ : v_pool_, static_cast<std::int64_t>(s_.layers) * n_slots_ * s_.n_kv * s_.hd);
   if (l < 0 || l >= s_.layers) throw std::invalid_argument("layer out of range");
   if (w == "attn_norm") return ret(attn_norm_[l], d);
   if (w == "mlp_norm") return ret(mlp_norm_[l], d);

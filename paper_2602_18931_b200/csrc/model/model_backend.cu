@@ -111,6 +111,23 @@ struct TreeCache {
 struct ModelPair::Impl {
   std::vector<LinearCache> tgt, ctrl;
   std::vector<TreeCache> wrk;
+  // prefill phase: one stream + workspace per model, created on first use
+  struct Side {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    std::unique_ptr<ForwardWorkspace> ws;
+  } pre[2];
+  ~Impl() {
+    for (Side& sd : pre) {
+      if (!sd.st) continue;
+      cudaSetDevice(sd.dev);
+      sd.ws.reset();
+      cudaEventDestroy(sd.e0);
+      cudaEventDestroy(sd.e1);
+      cudaStreamDestroy(sd.st);
+    }
+  }
 };
 
 // One draft lane: its stream, forward workspace, K3/K4 buffers and pinned results. Several
@@ -206,6 +223,85 @@ void ModelPair::reset_requests() {
   impl->tgt.assign(cfg_.max_requests, LinearCache{});
   impl->ctrl.assign(cfg_.max_requests, LinearCache{});
   impl->wrk.assign(cfg_.max_requests, TreeCache{});
+}
+
+ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, std::size_t n) {
+  PrefillStats out;
+  const std::int32_t P = static_cast<std::int32_t>(cfg_.prompt_len);
+  if (n == 0 || P < 2) return out;
+  const std::int32_t MC = static_cast<std::int32_t>(cfg_.max_ctx);
+  const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg_.trie_slots);
+  constexpr std::int32_t kMaxRows = 8192;  // rows per prefill forward (the GEMMs' efficient regime)
+  const std::size_t per = static_cast<std::size_t>(std::max(1, kMaxRows / (P - 1)));
+  for (int side = 0; side < 2; ++side) {
+    Impl::Side& sd = impl->pre[side];
+    LlamaModel& m = side == 0 ? *target_ : *draft_;
+    const int dev = side == 0 ? device_ : draft_device_;
+    DeviceGuard dg(dev);
+    if (!sd.st) {
+      sd.dev = dev;
+      WS_CUDA(cudaStreamCreateWithFlags(&sd.st, cudaStreamNonBlocking));
+      WS_CUDA(cudaEventCreate(&sd.e0));
+      WS_CUDA(cudaEventCreate(&sd.e1));
+      sd.ws = m.make_workspace(64);
+    }
+    WS_CUDA(cudaEventRecord(sd.e0, sd.st));
+    const std::size_t h2d0 = sd.ws->h2d;
+    ForwardBatch b;
+    std::vector<std::int32_t> src, dst;
+    for (std::size_t i0 = 0; i0 < n; i0 += per) {
+      b.clear();
+      for (std::size_t i = i0; i < std::min(n, i0 + per); ++i) {
+        const std::uint32_t r = reqs[i];
+        const std::vector<TokenId>& pr = prompt(r);
+        // target: the linear verify cache; draft: the worker's committed prefix region
+        const std::int32_t base = side == 0 ? static_cast<std::int32_t>(r) * MC : static_cast<std::int32_t>(r) * S + MC;
+        const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
+        const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
+        for (std::int32_t p = 0; p < P - 1; ++p) {
+          b.tok.push_back(static_cast<std::int32_t>(pr[p]));
+          b.pos.push_back(p);
+          b.slot.push_back(base + p);
+          b.extra.push_back(base + p);
+          if (side == 1) {
+            src.push_back(base + p);
+            dst.push_back(static_cast<std::int32_t>(r) * S + p);  // the controller's draft cache
+          }
+        }
+        b.groups.push_back(AttnGroup{row0, P - 1, base, 0, eoff, P - 1});
+      }
+      b.row_mask.assign(b.tok.size(), 0ull);
+      m.forward(b, 0.f, sd.st, *sd.ws);  // no output rows: KV only, no LM head
+      out.rows += side == 0 ? b.tok.size() : 0;
+      (side == 0 ? out.target_forwards : out.draft_forwards) += 1;
+      out.launches += 1 + 4ull * m.shape().layers;
+    }
+    if (side == 1) {
+      m.copy_slots(src, dst, sd.st, *sd.ws);
+      out.launches += 1;
+    }
+    WS_CUDA(cudaEventRecord(sd.e1, sd.st));
+    out.h2d += sd.ws->h2d - h2d0;
+  }
+  for (int side = 0; side < 2; ++side) {
+    Impl::Side& sd = impl->pre[side];
+    DeviceGuard dg(sd.dev);
+    WS_CUDA(cudaEventSynchronize(sd.e1));
+    float ms = 0.f;
+    WS_CUDA(cudaEventElapsedTime(&ms, sd.e0, sd.e1));
+    (side == 0 ? out.target_ms : out.draft_ms) += ms;
+  }
+  for (std::size_t i = 0; i < n; ++i) {
+    const std::uint32_t r = reqs[i];
+    const std::vector<TokenId>& pr = prompt(r);
+    const std::vector<TokenId> head(pr.begin(), pr.begin() + (P - 1));
+    impl->tgt[r].valid = head;
+    impl->ctrl[r].valid = head;
+    TreeCache& t = impl->wrk[r];
+    t.reset(static_cast<std::int32_t>(r) * S + 2 * MC, static_cast<std::int32_t>(cfg_.trie_slots));
+    t.prefix = head;
+  }
+  return out;
 }
 
 void ModelPair::export_trace(std::uint32_t first, std::uint32_t n, std::uint32_t length, ws_token_record* out) {
@@ -368,6 +464,7 @@ void ModelBackend_Llama::reset_run(std::uint32_t seq_len, TokenId eos, std::uint
   stats = BackendStats{};
   target_ms = draft_ms = 0;
   target_rows = draft_rows_fed = target_forwards = draft_forwards = 0;
+  target_out_rows = draft_out_rows = 0;
   for (int i = 0; i < 3; ++i) rows_by_kind[i] = jobs_by_kind[i] = 0;
   host_submit_ms[0] = host_submit_ms[1] = host_wait_ms = 0;
 }
@@ -516,6 +613,7 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
   WS_CUDA(cudaMemcpyAsync(L.h_vout, L.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaEventRecord(L.done, st));
   target_rows += b.tok.size();
+  target_out_rows += b.out_rows.size();
   target_forwards += 1;
   stats.launches += 1 + 8ull * p_->target().shape().layers + 4;
   stats.h2d += nv * k_ * 4 + L.forced.size() * 4;
@@ -737,6 +835,7 @@ void ModelBackend_Llama::submit_draft(int lane, const RoundJobs& jobs) {
     WS_CUDA(cudaMemcpyAsync(D.h_pred, D.d_pred, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, sd));
     D.ran = true;
     draft_rows_fed += b.tok.size();
+    draft_out_rows += n_out;
     draft_forwards += 1;
     stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (D.copy_src.empty() ? 0 : 1);
     stats.d2h += n_out * sizeof(ws_pred);

@@ -57,6 +57,7 @@ class ModelBackend_Llama : public ModelBackend {
   void reset_run(std::uint32_t seq_len, TokenId eos, std::uint32_t k);
   double target_ms = 0, draft_ms = 0;
   std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
+  std::uint64_t target_out_rows = 0, draft_out_rows = 0;  // rows through the LM head + K3
   std::uint64_t rows_by_kind[3] = {0, 0, 0}, jobs_by_kind[3] = {0, 0, 0};  // JobKind
   double host_submit_ms[2] = {0, 0}, host_wait_ms = 0;  // host time in submit (per lane) / wait_any
 
@@ -81,6 +82,16 @@ class ModelPair {
   ModelPair(const ModelPairCfg& cfg, int device);
   ~ModelPair();
   void reset_requests();  // forget all cached KV state (new run)
+  // Prompt prefill (its own phase, before the first verify / draft): the KV of prompt positions
+  // [0, P-1) of each listed request is written for the target (verify cache), and once for the
+  // draft model into the worker's committed prefix, then copied into the controller's draft
+  // cache. Every later verify forward then feeds exactly k+1 rows (the last prompt token + the
+  // k candidates), so verify forwards and prefill forwards are timed as separate units.
+  struct PrefillStats {
+    double target_ms = 0, draft_ms = 0;
+    std::uint64_t rows = 0, target_forwards = 0, draft_forwards = 0, launches = 0, h2d = 0;
+  };
+  PrefillStats prefill_prompts(const std::uint32_t* reqs, std::size_t n);
   // Teacher-forced trace export: for requests [first, first + n), the target's
   // greedy continuation of the prompt for `length` positions; at every position the target's
   // and the draft's top-2 / entropy on the same (committed) context. out: n * length records,

@@ -11,7 +11,10 @@ fp32 at every point where the sm_100a kernels store a narrower value:
                                  are folded into Wqkv / Wgu at load (fold_norm_weight)
   q, k = bf16(rope(fp32(acc) * rs)), v = bf16(fp32(acc) * rs)   QKV epilogue (cos/sin fp32
                                  table from fp64 angles of fp32 inverse frequencies)
-  attn = bf16(softmax(q k^T / sqrt(hd)) v)   K2 (the kernel's bf16 P is not mirrored)
+  attn = bf16(o / l)   K2's online softmax, mirrored tile by tile: keys in 32-position tiles
+                       (the group's prefix, then its extras), s = fp32(q.k) * fp32(scale log2 e),
+                       running max per tile, p = exp2(s - max) in fp32, l += sum p (fp32),
+                       o = o * corr + bf16(p) . v  (P is the bf16 A operand of the PV mma)
   h = bf16(silu(g) * u), g, u = fp32(acc) * rs   SwiGLU epilogue
   xo = bf16(x * rsqrt(mean x^2 + eps) * w_final)  rmsnorm_rows
   logits = bf16(xo W_lm^T)
@@ -108,8 +111,49 @@ class RefModel:
         return torch.cat([a * c - b * s_, b * c + a * s_], dim=-1)
 
     @staticmethod
+    def _attention(q, k, v, allowed, tile=32):
+        """attn_mma_kernel (csrc/kernels/attention.cu) restated: one key slice, 32-key tiles."""
+        hd = q.shape[-1]
+        sl2 = torch.tensor(1.0 / math.sqrt(hd), dtype=torch.float32) * torch.tensor(1.4426950408889634,
+                                                                                     dtype=torch.float32)
+        s = f32(torch.einsum("thd,shd->hts", q, k)) * sl2.double()
+        s = f32(s).masked_fill(~allowed[None], float("-inf"))  # [H, Tq, Tk]
+        H, Tq, Tk = s.shape
+        m = torch.full((H, Tq), float("-inf"), dtype=torch.float64, device=s.device)
+        lsum = torch.zeros(H, Tq, dtype=torch.float64, device=s.device)
+        o = torch.zeros(H, Tq, hd, dtype=torch.float64, device=s.device)
+        vh = v.permute(1, 0, 2)  # [H, Tk, hd]
+        for t0 in range(0, Tk, tile):
+            st = s[:, :, t0:t0 + tile]
+            nmax = torch.maximum(m, st.max(-1).values)
+            base = torch.where(nmax == float("-inf"), torch.zeros_like(nmax), nmax)
+            corr = torch.exp2(m - base)
+            p = f32(torch.exp2(st - base[..., None]))
+            lsum = f32(lsum * corr + p.sum(-1))
+            o = o * corr[..., None] + torch.einsum("hts,hsd->htd", bf(p), vh[:, t0:t0 + tile])
+            m = nmax
+        inv = torch.where(lsum > 0, 1.0 / lsum, torch.zeros_like(lsum))
+        return bf(o * inv[..., None]).permute(1, 0, 2)
+
+    @staticmethod
     def _rs(x):
         return 1.0 / torch.sqrt((x * x).sum(-1, keepdim=True) / x.shape[-1] + EPS)
+
+    def head(self, x):
+        """Final RMSNorm + LM head from fp32 residual rows x [n, d] (rmsnorm_rows + the bf16 GEMM)."""
+        xo = bf(x * torch.rsqrt((x * x).mean(-1, keepdim=True) + EPS) * self.fn)
+        return bf(xo @ self.lm.T)
+
+    def kv0(self, tokens, pos):
+        """Layer-0 K (rotated) and V rows [T, n_kv * hd] of the given tokens (QKV epilogue)."""
+        s = self.s
+        nq, nkv, hd = s["nq"], s["nkv"], s["hd"]
+        T = len(tokens)
+        x = self.emb[torch.tensor(tokens, device="cuda")].double()
+        c, s_ = self._cs(torch.tensor(pos, device="cuda"))
+        a = f32(f32(bf(x) @ self.layers[0]["wqkv"].T) * self._rs(x))
+        k = bf(self._rope(a[:, nq * hd:(nq + nkv) * hd].view(T, nkv, hd), c, s_)).reshape(T, -1)
+        return k, bf(a[:, (nq + nkv) * hd:])
 
     def logits(self, tokens, pos, allowed, out_idx):
         """tokens/pos: length-T lists; allowed: [T, T] bool (row attends column); out_idx: the rows
@@ -132,18 +176,14 @@ class RefModel:
             q, k = bf(self._rope(q, c, s_)), bf(self._rope(k, c, s_))
             k = k.repeat_interleave(G, dim=1)
             v = v.repeat_interleave(G, dim=1)
-            att = torch.einsum("thd,shd->hts", q, k) / math.sqrt(hd)
-            att = att.masked_fill(~allowed[None], float("-inf"))
-            o = bf(torch.einsum("hts,shd->thd", att.softmax(-1), v).reshape(T, nq * hd))
+            o = self._attention(q, k, v, allowed).reshape(T, nq * hd)
             x = f32(x + f32(o @ Lw["wo"].T))
             xb, rs = bf(x), self._rs(x)
             g = f32(f32(xb @ Lw["wg"].T) * rs)
             u = f32(f32(xb @ Lw["wu"].T) * rs)
             hh = bf(g / (1.0 + torch.exp(-g)) * u)
             x = f32(x + f32(hh @ Lw["wd"].T))
-        xo = x[torch.tensor(out_idx, device="cuda")]
-        xo = bf(xo * torch.rsqrt((xo * xo).mean(-1, keepdim=True) + EPS) * self.fn)
-        return bf(xo @ self.lm.T)
+        return self.head(x[torch.tensor(out_idx, device="cuda")])
 
 
 def causal(T):
