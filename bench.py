@@ -151,47 +151,76 @@ def config_block(args, world, host_threads):
             "l2": "tables are L2-resident by design; L2 flushed (256 MB write) before every timed step"}
 
 
-def llama_roofline(stats, k, peak_bw, peak_tf, avg_ctx, target="llama3-8b"):
-    """Verify-step roofline (SURVEY §8d units): FLOPs = 2 P_mm rows + 4 L rows ctx n_q hd;
-    bytes = 2 P_mm + R ctx KVB + rows KVB + rows V 2 (+ K3 read of the logits)."""
-    if target == "llama3-70b":
-        P_mm, L, nq = 69.50e9, 80, 64  # Llama-3.1-70B matmul params incl. LM head (SURVEY §8d)
-    else:
-        P_mm, L, nq = 7.505e9, 32, 32  # Llama-3.1-8B
-    hd, V = 128, 128256
-    kvb = L * 2 * 8 * 128 * 2
-    fw = max(1, stats["target_forwards"])
-    rows = stats["target_rows"] / fw
-    reqs = rows / (k + 1)
-    flops = 2 * P_mm * rows + 4 * L * rows * avg_ctx * nq * hd
-    byts = 2 * P_mm + reqs * avg_ctx * kvb + rows * kvb + 2 * reqs * (k + 1) * V * 2
-    t_meas = stats["target_ms"] / 1e3 / fw
+MODEL_SHAPES = {  # shape_by_name (csrc/model/llama.cu)
+    "llama3-8b": dict(L=32, d=4096, nq=32, nkv=8, hd=128, ffn=14336, V=128256),
+    "llama3-70b": dict(L=80, d=8192, nq=64, nkv=8, hd=128, ffn=28672, V=128256),
+    "llama3.2-1b": dict(L=16, d=2048, nq=32, nkv=8, hd=64, ffn=8192, V=128256),
+}
+
+
+def unit_roofline(shape, fw, ms, rows, out_rows, kv_pos, attn_pairs, peak_bw, peak_tf, causal_half=False):
+    """Roofline of one forward unit (SURVEY §8d units, per forward = run totals / forwards):
+    FLOPs = 2 P_layers rows + 2 P_lm out_rows + 4 L pairs n_q hd   (pairs = rows x visible keys)
+    bytes = 2 P_layers + 2 P_lm [out_rows > 0] + KVB (keys read + rows written) + 4 V out_rows
+    (the bf16 logits written by the LM head and read once by K3/K4). time = measured device time
+    of the unit on its own stream (CUDA events), divided by its forwards."""
+    m = MODEL_SHAPES[shape]
+    per_layer = (m["nq"] + 2 * m["nkv"]) * m["hd"] * m["d"] + m["d"] * m["nq"] * m["hd"] + 3 * m["ffn"] * m["d"]
+    P_layers, P_lm = per_layer * m["L"], m["V"] * m["d"]
+    kvb = m["L"] * 2 * m["nkv"] * m["hd"] * 2
+    fw = max(1, fw)
+    r, o, kv, pairs = rows / fw, out_rows / fw, kv_pos / fw, attn_pairs / fw
+    if causal_half:  # prefill groups: causal over their own rows, about half the pairs are visible
+        pairs /= 2
+    flops = 2 * P_layers * r + 2 * P_lm * o + 4 * m["L"] * pairs * m["nq"] * m["hd"]
+    byts = 2 * P_layers + (2 * P_lm if o > 0 else 0) + kvb * (kv + r) + 4 * m["V"] * o
+    t = ms / 1e3 / fw
     t_tensor, t_hbm = flops / (peak_tf * 1e12), byts / (peak_bw * 1e9)
+    out = {"rows_per_forward": r, "out_rows_per_forward": o, "forwards": fw, "ms_per_forward": t * 1e3,
+           "alg_flops": flops, "alg_bytes": byts}
     if t_tensor >= t_hbm:
-        return {"bound": "tensor", "achieved": flops / t_meas / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": t_tensor / t_meas}, rows, flops, byts, t_meas
-    return {"bound": "hbm", "achieved": byts / t_meas / 1e9, "peak": peak_bw, "unit": "GB/s",
-            "frac": t_hbm / t_meas}, rows, flops, byts, t_meas
+        out.update({"bound": "tensor", "achieved": flops / t / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": t_tensor / t})
+    else:
+        out.update({"bound": "hbm", "achieved": byts / t / 1e9, "peak": peak_bw, "unit": "GB/s", "frac": t_hbm / t})
+    return out
 
 
-def k3_sample(rows, peak_bw, iters=20):
-    """K3 (fused softmax + entropy + top-2; the K4 accept walk is fused behind it) timed alone
-    on a verify-shaped bf16 logits block: CUDA events on the launching stream, L2 flushed
+def llama_rooflines(rs, target, peak_bw, peak_tf):
+    """verify (the headline), prefill and draft units from ws_model_run_stats of the timed runs."""
+    verify = unit_roofline(target, rs["verify_forwards"], rs["verify_ms"], rs["verify_rows"], rs["verify_out_rows"],
+                           rs["verify_kv_pos"], rs["verify_attn_pairs"], peak_bw, peak_tf)
+    prefill = unit_roofline(target, rs["prefill_forwards"], rs["prefill_target_ms"], rs["prefill_rows"], 0,
+                            rs["prefill_kv_pos"], rs["prefill_attn_pairs"], peak_bw, peak_tf, causal_half=True)
+    draft = unit_roofline("llama3.2-1b", rs["draft_forwards"], rs["draft_ms"], rs["draft_rows"], rs["draft_out_rows"],
+                          rs["draft_kv_pos"], rs["draft_attn_pairs"], peak_bw, peak_tf)
+    return verify, prefill, draft
+
+
+def k3_sample(rows, k, peak_bw, iters=20):
+    """K3 (fused softmax + entropy + top-2) with the K4 greedy accept walk fused behind it, timed
+    alone on a verify-shaped bf16 logits block of `rows` = verify jobs x (k+1) rows (the mean
+    verify forward of the run) with candidates: CUDA events on the launching stream, L2 flushed
     (256 MB write) before every launch. Algorithmic bytes = rows x V x 2 (logits read once)."""
     import ctypes as C
 
     import torch
 
     import paper_2602_18931_b200 as ws
+    from paper_2602_18931_b200 import abi
     L, V = ws.lib(), 128256
+    n_req = max(1, rows // (k + 1))
+    rows = n_req * (k + 1)
     L.ws_op_row_stats_workspace_bytes.restype = C.c_size_t
     L.ws_op_row_stats_workspace_bytes.argtypes = [C.c_uint32] * 3
-    L.ws_op_row_stats_bf16.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
-                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ws_op_verify_greedy_bf16.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     g = torch.Generator(device="cuda").manual_seed(7)
     x = (torch.randn(rows, V, device="cuda", generator=g) * 2).to(torch.bfloat16)
-    wsb = torch.zeros(L.ws_op_row_stats_workspace_bytes(rows, V, 0), dtype=torch.uint8, device="cuda")
-    out = torch.zeros(rows * 40, dtype=torch.uint8, device="cuda")
+    cand = torch.randint(0, V, (n_req * k,), device="cuda", generator=g, dtype=torch.int32)
+    wsb = torch.zeros(L.ws_op_row_stats_workspace_bytes(rows, V, n_req), dtype=torch.uint8, device="cuda")
+    vout = torch.zeros(n_req * C.sizeof(abi.VerifyOut), dtype=torch.uint8, device="cuda")
+    pred = torch.zeros(rows * C.sizeof(abi.Pred), dtype=torch.uint8, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     st = torch.cuda.current_stream()
     tot = 0.0
@@ -199,16 +228,18 @@ def k3_sample(rows, peak_bw, iters=20):
         flush.fill_(0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        L.ws_op_row_stats_bf16(x.data_ptr(), rows, V, V, 1.0, out.data_ptr(), None, wsb.data_ptr(), st.cuda_stream)
+        rc = L.ws_op_verify_greedy_bf16(x.data_ptr(), n_req, k, V, V, cand.data_ptr(), vout.data_ptr(),
+                                        pred.data_ptr(), wsb.data_ptr(), st.cuda_stream)
         e1.record(st)
         torch.cuda.synchronize()
+        assert rc == 0
         if it >= 3:
             tot += e0.elapsed_time(e1) / 1e3
     t = tot / iters
     gbs = rows * V * 2 / t / 1e9
-    return {"kernel": "K3 row_stats (softmax + entropy + top-2, K4 accept fused)", "rows": rows, "vocab": V,
+    return {"kernel": "K3 row_stats + K4 greedy accept (fused)", "rows": rows, "verify_jobs": n_req, "vocab": V,
             "us": t * 1e6, "bound": "hbm", "achieved": gbs, "peak": peak_bw, "unit": "GB/s", "frac": gbs / peak_bw,
-            "timing": "CUDA events, L2 flushed before each launch, verify-shaped rows (mean verify batch)"}
+            "timing": "CUDA events, L2 flushed before each launch, the mean verify forward's output rows"}
 
 
 def cpu_reference_llama(k, requests, samples=1):
@@ -346,8 +377,7 @@ def main():
     for _ in range(args.warmup if active else 0):
         run_once()
     tokens, total_ms, launches, kernel_ms, h2d, d2h = 0, 0.0, 0, 0.0, 0, 0
-    mstats = {"target_ms": 0.0, "draft_ms": 0.0, "target_rows": 0, "draft_rows": 0, "target_forwards": 0,
-              "draft_forwards": 0}
+    mstats = {}
     barrier()
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps if active else 0):
@@ -366,8 +396,8 @@ def main():
             h2d += b.out.h2d_bytes
             d2h += b.out.d2h_bytes + sum(b.ctrl_len[i] for i in range(b.n)) * 4
             if args.workload == "llama":
-                for kk, v in ctx.model_stats().items():
-                    mstats[kk] += v
+                for kk, v in ctx.run_stats().items():
+                    mstats[kk] = mstats.get(kk, 0) + v
     barrier()
 
     torch.cuda.set_device(local_rank)
@@ -397,23 +427,25 @@ def main():
                                 "region, so value and e2e are one measurement"},
                 "gpu_launches": int(launches_all), "clocks": clk.summary()}
         if args.workload == "llama":
-            local = cfg.local_requests
-            avg_ctx = 128 + 50 + args.k / 2
-            roof, rows, fl, by, t_meas = llama_roofline(mstats, args.k, peak_bw, peak_tf, avg_ctx, args.target)
+            verify, prefill, draft = llama_rooflines(mstats, args.target, peak_bw, peak_tf)
+            roof = dict(verify)
             traffic = None
-            tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_verify_traffic.json")
+            tpath = os.path.join(ROOT, "profiles", "r02_verify_traffic.json")
             if os.path.exists(tpath) and args.target == "llama3-8b":  # ncu dram bytes of one verify forward
                 with open(tpath) as f:
                     tj = json.load(f)
                 traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
                 roof["traffic_rows"] = tj["rows"]
-                roof["traffic_source"] = "profiles/r01_verify_traffic.json (ncu, verify forward at %d rows)" % tj["rows"]
-            roof.update({"traffic": traffic, "kernel": "verify step (target forward + K3/K4)",
-                         "peak_kind": peak_kind, "rows_per_verify": rows, "ms_per_verify": t_meas * 1e3,
-                         "alg_flops_per_verify": fl, "alg_bytes_per_verify": by})
+                roof["traffic_source"] = ("profiles/r02_verify_traffic.json (ncu, one verify forward + K3/K4 at "
+                                          "%d rows)" % tj["rows"])
+            roof.update({"traffic": traffic, "kernel": "verify forward (target model + K3/K4), prompt prefill "
+                                                       "excluded", "peak_kind": peak_kind,
+                         "prefill": prefill, "draft": draft,
+                         "note": "in-run device time of each unit on its own stream while the other lanes run "
+                                 "concurrently on the same GPU; per-forward averages"})
             line["roofline"] = roof
             try:
-                line["k3"] = k3_sample(max(1, int(round(rows))), peak_bw)
+                line["k3"] = k3_sample(max(args.k + 1, int(round(verify["out_rows_per_forward"]))), args.k, peak_bw)
             except Exception as e:  # a secondary figure: never fail the bench line over it
                 line["k3"] = {"unavailable": str(e)}
             line["model_time"] = {k: (v / args.steps if isinstance(v, float) else v // args.steps)

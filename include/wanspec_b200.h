@@ -297,7 +297,10 @@ typedef struct ws_run_stats {
   double verify_ms, draft_ms, prefill_target_ms, prefill_draft_ms;
   uint64_t verify_rows, verify_out_rows, verify_forwards;
   uint64_t draft_rows, draft_out_rows, draft_forwards;
-  uint64_t prefill_rows, prefill_forwards;
+  uint64_t prefill_rows, prefill_forwards;  /* target-side prefill forwards */
+  /* attention work per unit: keys read (sum over groups of prefix + extras) and rows x keys */
+  uint64_t verify_kv_pos, verify_attn_pairs, draft_kv_pos, draft_attn_pairs;
+  uint64_t prefill_kv_pos, prefill_attn_pairs;
 } ws_run_stats;
 int ws_model_run_stats(ws_ctx* ctx, ws_run_stats* out);
 

@@ -184,6 +184,12 @@ class Context:
         keys = ("target_ms", "draft_ms", "target_rows", "draft_rows", "target_forwards", "draft_forwards")
         return {k: x.value for k, x in zip(keys, v)}
 
+    def run_stats(self):
+        """ws_model_run_stats: verify / draft / prefill device time and rows of the last run."""
+        st = abi.RunStats()
+        _check(lib().ws_model_run_stats(self._h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in abi.RunStats._fields_}
+
     # -- whole runs --
     def run_sim_full(self, cfg, with_tokens=True, with_steps=True, resident=False):
         """run_sim_full (sim.hpp:429-442) through the batched GPU driver; returns RunBuffers."""

@@ -37,6 +37,11 @@ class Pred(C.Structure):
                 ("prob", C.c_double * 2), ("entropy", C.c_double)]
 
 
+class VerifyOut(C.Structure):
+    """ws_verify_out: one run_target_step result (oracle.hpp:127-139)."""
+    _fields_ = [("accepted", C.c_uint32), ("bonus", C.c_uint32), ("final_entropy", C.c_double)]
+
+
 class OracleCfg(C.Structure):
     _fields_ = [
         ("seed", C.c_uint64), ("vocab_size", C.c_uint32), ("eos_id", C.c_uint32),
@@ -232,3 +237,14 @@ class RunBuffers:
         n = min(self.out.n_steps, self.max_steps)
         return [(s.request, s.step, s.base, s.accepted, s.bonus, s.final_entropy, s.flags)
                 for s in self.steps[:n]]
+
+
+class RunStats(C.Structure):
+    """ws_run_stats (include/wanspec_b200.h): per-unit device time of the last model run."""
+    _fields_ = [("verify_ms", C.c_double), ("draft_ms", C.c_double), ("prefill_target_ms", C.c_double),
+                ("prefill_draft_ms", C.c_double), ("verify_rows", C.c_uint64), ("verify_out_rows", C.c_uint64),
+                ("verify_forwards", C.c_uint64), ("draft_rows", C.c_uint64), ("draft_out_rows", C.c_uint64),
+                ("draft_forwards", C.c_uint64), ("prefill_rows", C.c_uint64), ("prefill_forwards", C.c_uint64),
+                ("verify_kv_pos", C.c_uint64), ("verify_attn_pairs", C.c_uint64), ("draft_kv_pos", C.c_uint64),
+                ("draft_attn_pairs", C.c_uint64), ("prefill_kv_pos", C.c_uint64), ("prefill_attn_pairs", C.c_uint64)]
+

@@ -135,6 +135,10 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
       st.draft_forwards += bk->draft_forwards;
       st.target_out_rows += bk->target_out_rows;
       st.draft_out_rows += bk->draft_out_rows;
+      st.verify_kv_pos += bk->target_kv_pos();
+      st.verify_attn_pairs += bk->target_attn_pairs();
+      st.draft_kv_pos += bk->draft_kv_pos();
+      st.draft_attn_pairs += bk->draft_attn_pairs();
       for (int k = 0; k < 3; ++k) {
         rows_kind[k] += bk->rows_by_kind[k];
         jobs_kind[k] += bk->jobs_by_kind[k];
@@ -143,7 +147,9 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
     st.prefill_target_ms = pre.target_ms;
     st.prefill_draft_ms = pre.draft_ms;
     st.prefill_rows = pre.rows;
-    st.prefill_forwards = pre.target_forwards + pre.draft_forwards;
+    st.prefill_forwards = pre.target_forwards;
+    st.prefill_kv_pos = pre.kv_pos;
+    st.prefill_attn_pairs = pre.attn_pairs;
     ctx->last_stats = st;
     if (out) {
       out->gpu_launches += pre.launches;
@@ -203,6 +209,12 @@ int ws_model_run_stats(ws_ctx* ctx, ws_run_stats* o) {
     o->draft_forwards = s.draft_forwards;
     o->prefill_rows = s.prefill_rows;
     o->prefill_forwards = s.prefill_forwards;
+    o->verify_kv_pos = s.verify_kv_pos;
+    o->verify_attn_pairs = s.verify_attn_pairs;
+    o->draft_kv_pos = s.draft_kv_pos;
+    o->draft_attn_pairs = s.draft_attn_pairs;
+    o->prefill_kv_pos = s.prefill_kv_pos;
+    o->prefill_attn_pairs = s.prefill_attn_pairs;
   });
 }
 

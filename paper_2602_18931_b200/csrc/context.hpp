@@ -25,6 +25,8 @@ struct ws_ctx {
     std::uint64_t target_out_rows = 0, draft_out_rows = 0;
     double prefill_target_ms = 0, prefill_draft_ms = 0;
     std::uint64_t prefill_rows = 0, prefill_forwards = 0;
+    std::uint64_t verify_kv_pos = 0, verify_attn_pairs = 0, draft_kv_pos = 0, draft_attn_pairs = 0;
+    std::uint64_t prefill_kv_pos = 0, prefill_attn_pairs = 0;
   } last_stats;
 
   wsb::OracleLane& lane(std::size_t i) {

@@ -278,6 +278,10 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
   const int G = s_.n_q / s_.n_kv;
   const int vpc = attention_vectors_per_cta(s_.hd);
   grp_sorted_.clear();
+  for (const AttnGroup& g : b.groups) {
+    ws.kv_pos += static_cast<std::uint64_t>(g.prefix_len + g.extra_len);
+    ws.attn_pairs += static_cast<std::uint64_t>(g.n_rows) * (g.prefix_len + g.extra_len);
+  }
   for (const AttnGroup& g : b.groups)
     for (int v0 = 0; v0 < g.n_rows * G; v0 += vpc) {
       AttnGroup e = g;

@@ -97,6 +97,10 @@ struct ForwardWorkspace {
   std::size_t gemm_ws_bytes = 0;
   std::vector<AttnGroup> grp_sorted;
   std::size_t h2d = 0;
+  // algorithmic attention work of the forwards run on this workspace (roofline units):
+  // kv_pos = sum over groups of the keys read (prefix + extras), attn_pairs = sum over groups of
+  // rows x keys (an upper bound of the visible pairs; causal groups see about half their extras)
+  std::uint64_t kv_pos = 0, attn_pairs = 0;
   KernelProfiler prof;
 };
 

@@ -247,6 +247,7 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
     }
     WS_CUDA(cudaEventRecord(sd.e0, sd.st));
     const std::size_t h2d0 = sd.ws->h2d;
+    const std::uint64_t kv0 = sd.ws->kv_pos, ap0 = sd.ws->attn_pairs;
     ForwardBatch b;
     std::vector<std::int32_t> src, dst;
     for (std::size_t i0 = 0; i0 < n; i0 += per) {
@@ -282,6 +283,10 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
     }
     WS_CUDA(cudaEventRecord(sd.e1, sd.st));
     out.h2d += sd.ws->h2d - h2d0;
+    if (side == 0) {
+      out.kv_pos += sd.ws->kv_pos - kv0;
+      out.attn_pairs += sd.ws->attn_pairs - ap0;
+    }
   }
   for (int side = 0; side < 2; ++side) {
     Impl::Side& sd = impl->pre[side];
@@ -465,8 +470,23 @@ void ModelBackend_Llama::reset_run(std::uint32_t seq_len, TokenId eos, std::uint
   target_ms = draft_ms = 0;
   target_rows = draft_rows_fed = target_forwards = draft_forwards = 0;
   target_out_rows = draft_out_rows = 0;
+  ln_->ws_t->kv_pos = ln_->ws_t->attn_pairs = 0;
+  for (auto& d : ln_->dl) d->ws->kv_pos = d->ws->attn_pairs = 0;
   for (int i = 0; i < 3; ++i) rows_by_kind[i] = jobs_by_kind[i] = 0;
   host_submit_ms[0] = host_submit_ms[1] = host_wait_ms = 0;
+}
+
+std::uint64_t ModelBackend_Llama::target_kv_pos() const { return ln_->ws_t->kv_pos; }
+std::uint64_t ModelBackend_Llama::target_attn_pairs() const { return ln_->ws_t->attn_pairs; }
+std::uint64_t ModelBackend_Llama::draft_kv_pos() const {
+  std::uint64_t n = 0;
+  for (const auto& d : ln_->dl) n += d->ws->kv_pos;
+  return n;
+}
+std::uint64_t ModelBackend_Llama::draft_attn_pairs() const {
+  std::uint64_t n = 0;
+  for (const auto& d : ln_->dl) n += d->ws->attn_pairs;
+  return n;
 }
 
 int ModelBackend_Llama::n_lanes() const { return 1 + static_cast<int>(ln_->dl.size()); }

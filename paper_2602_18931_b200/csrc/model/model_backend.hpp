@@ -58,6 +58,10 @@ class ModelBackend_Llama : public ModelBackend {
   double target_ms = 0, draft_ms = 0;
   std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
   std::uint64_t target_out_rows = 0, draft_out_rows = 0;  // rows through the LM head + K3
+  std::uint64_t target_kv_pos() const;  // attention work of this backend's forwards (since reset_run)
+  std::uint64_t target_attn_pairs() const;
+  std::uint64_t draft_kv_pos() const;
+  std::uint64_t draft_attn_pairs() const;
   std::uint64_t rows_by_kind[3] = {0, 0, 0}, jobs_by_kind[3] = {0, 0, 0};  // JobKind
   double host_submit_ms[2] = {0, 0}, host_wait_ms = 0;  // host time in submit (per lane) / wait_any
 
@@ -90,6 +94,7 @@ class ModelPair {
   struct PrefillStats {
     double target_ms = 0, draft_ms = 0;
     std::uint64_t rows = 0, target_forwards = 0, draft_forwards = 0, launches = 0, h2d = 0;
+    std::uint64_t kv_pos = 0, attn_pairs = 0;  // target side
   };
   PrefillStats prefill_prompts(const std::uint32_t* reqs, std::size_t n);
   // Teacher-forced trace export: for requests [first, first + n), the target's
