@@ -289,6 +289,49 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
 int ws_model_stats(ws_ctx* ctx, double* target_ms, double* draft_ms, uint64_t* target_rows,
                    uint64_t* draft_rows, uint64_t* target_forwards, uint64_t* draft_forwards);
 
+/* ---- per-call model boundary (the reference's three model calls) ----
+ * For callers that keep their own controller / worker state machines (the reference's
+ * RequestSim or runtime) and call the loaded models once per step:
+ *   run_target_step  (oracle.hpp:127-139; callers sim.hpp:297, runtime.hpp:308)  -> ws_model_verify
+ *   draft_prediction (oracle.hpp:96-98;  callers sim.hpp:307/:314, runtime.hpp:197/:319)
+ *                                                                                 -> ws_model_draft
+ * A job names a request (its seeded prompt and KV region in the loaded pair) and the tokens
+ * after the prompt: the committed output, then (drafts) the speculative path. Real models are
+ * context-dependent, so the draft calls take the leaf's path where the reference passes only
+ * its anchor position. KV caches are content-addressed: every job's context is matched
+ * against the request's cached tokens (longest common prefix for the verify and controller
+ * draft caches, a token trie of speculative nodes over the committed prefix for the worker),
+ * only the missing rows are fed, and accepted speculative KV migrates into the prefix on the
+ * next job — commit and fork need no call (a fork is two children in the trie; attention
+ * masks let them share every ancestor's KV in place). Results equal ws_run_model_sim's for the
+ * same contexts bit for bit (batch-invariant kernels). Rows predicting committed index >=
+ * sequence_length - 1 emit eos_id with probability 1, the tiny pair's past-end rule
+ * (oracle.hpp:88-102). */
+#define WS_JOB_VERIFY 0u
+#define WS_JOB_CTRL_DRAFT 1u   /* controller local draft / catch-up (controller.hpp:194-208) */
+#define WS_JOB_WORKER_DRAFT 2u /* worker frontier leaf (worker.hpp:93-96) */
+typedef struct ws_model_job {
+  uint32_t request;
+  uint32_t kind;        /* WS_JOB_* */
+  uint32_t n_committed; /* committed tokens at the head of the context */
+  uint32_t len;         /* context tokens after the prompt (verify: == n_committed) */
+  uint64_t off;         /* offset of this job's context in the tokens array */
+} ws_model_job;
+/* Starts a per-call session on the loaded pair: forgets every cached KV, sets k and the
+ * generation cap. */
+int ws_model_open(ws_ctx* ctx, uint32_t k, uint32_t sequence_length, uint32_t eos_id);
+/* Prompt prefill of the listed requests (optional: a first job would feed its prompt too). */
+int ws_model_prefill(ws_ctx* ctx, uint32_t n, const uint32_t* requests);
+/* run_target_step x n in one target forward + K3/K4: job j verifies cand[j*k .. j*k+k) after
+ * its committed context. out[j] = (accepted, bonus, final_entropy); rows_opt (may be NULL):
+ * the n*(k+1) per-row predictions (top-2 + entropy) the walk read. */
+int ws_model_verify(ws_ctx* ctx, uint32_t n, const ws_model_job* jobs, const uint32_t* tokens,
+                    const uint32_t* cand, ws_verify_out* out, ws_pred* rows_opt);
+/* draft_prediction x n in one draft forward + K3: the prediction after each job's context. */
+int ws_model_draft(ws_ctx* ctx, uint32_t n, const ws_model_job* jobs, const uint32_t* tokens, ws_pred* out);
+/* Forget one request's cached KV (its slots are reused by the next job naming it). */
+int ws_model_evict(ws_ctx* ctx, uint32_t request);
+
 /* Per-unit device time of the last ws_run_model_sim (CUDA events on each unit's stream): the
  * prompt-prefill phase (prefill_rows prompt tokens; target and draft forwards, no LM head), the
  * verify forwards (verify_rows fed, verify_out_rows through the LM head + K3/K4 — k+1 per

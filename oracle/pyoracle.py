@@ -193,6 +193,48 @@ def ref_run_sim(cfg, threads=1, with_tokens=True, with_steps=True):
     return bufs
 
 
+REF_VERIFY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32), C.c_uint32,
+                            C.POINTER(C.c_uint32), C.c_uint32, C.POINTER(abi.VerifyOut))
+REF_DRAFT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32), C.c_uint32,
+                           C.c_uint32, C.POINTER(abi.Pred))
+
+
+def ref_run_sim_models(cfg, verify_fn, draft_fn, with_tokens=True, with_steps=True):
+    """The reference's own RequestSim (sim.hpp:166-416) with its model calls answered by
+    verify_fn(request, committed, cands) -> (accepted, bonus, final_entropy) and
+    draft_fn(request, kind, context, n_committed) -> abi.Pred (ref_shim.cpp model mode)."""
+    bufs = abi.RunBuffers(cfg, with_tokens, with_steps)
+    err = C.create_string_buffer(512)
+
+    def vtramp(user, req, committed, n, cand, k, out):
+        try:
+            a, b, h = verify_fn(req, [committed[i] for i in range(n)], [cand[i] for i in range(k)])
+            out[0].accepted, out[0].bonus, out[0].final_entropy = a, b, h
+            return 0
+        except Exception:
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def dtramp(user, req, kind, context, n, n_committed, out):
+        try:
+            out[0] = draft_fn(req, kind, [context[i] for i in range(n)], n_committed)
+            return 0
+        except Exception:
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    vcb, dcb = REF_VERIFY_FN(vtramp), REF_DRAFT_FN(dtramp)
+    lib = ref_lib()
+    lib.ref_run_sim_models.argtypes = [C.POINTER(abi.SimCfg), REF_VERIFY_FN, REF_DRAFT_FN, C.c_void_p,
+                                       C.POINTER(abi.RunOut), C.c_char_p, C.c_size_t]
+    rc = lib.ref_run_sim_models(C.byref(cfg), vcb, dcb, None, C.byref(bufs.out), err, 512)
+    if rc != 0:
+        raise RuntimeError(f"ref_run_sim_models rc={rc}: {err.value.decode()}")
+    return bufs
+
+
 def ref_run_sim_trace(cfg, path, threads=1, with_tokens=True, with_steps=True):
     """run_sim_full with the reference's trace oracle (OracleKind::trace) replaying `path`."""
     lib = ref_lib()

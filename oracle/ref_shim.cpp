@@ -9,17 +9,35 @@
 // (a) logs each verify step for per-step parity and (b) in WS_VERIFY_REJECTION mode replaces
 // the greedy rule by the restated rejection rule (oracle/restate.c) — the reference state
 // machines, scheduler and tree stay byte-for-byte the reference's.
+#include "wanspec/controller.hpp"
 #include "wanspec/oracle.hpp"
+#include "wanspec/worker.hpp"
 
 #include <span>
 
 namespace wanspec {
 ValidationResult hooked_target_step(const SequenceTrace& trace, std::uint64_t base,
                                     std::span<const TokenId> candidates);
-}
+// Model mode (ref_run_sim_models): the fold-back calls at the same seam (sim.hpp:299, :306,
+// :315) receive the state the real-model calls need — the controller's committed tokens, the
+// local-draft plan's context, the worker tree's leaf paths — and replace the oracle's
+// predictions by the caller's model before delegating to the reference's own functions.
+std::vector<Message> hooked_apply_target_result(ControllerState& st, const ControllerConfig& cfg,
+                                                const ValidationResult& result, SimTime now);
+void hooked_apply_local_draft(ControllerState& st, const ControllerConfig& cfg, const StepDraftLocal& plan,
+                              const Prediction& prediction);
+std::vector<Message> hooked_apply_draft_output(WorkerState& st, const WorkerConfig& cfg,
+                                               std::span<const LeafOutput> outputs);
+}  // namespace wanspec
 #define run_target_step hooked_target_step
+#define apply_target_result hooked_apply_target_result
+#define apply_local_draft hooked_apply_local_draft
+#define apply_draft_output hooked_apply_draft_output
 #include "wanspec/sim.hpp"
 #undef run_target_step
+#undef apply_target_result
+#undef apply_local_draft
+#undef apply_draft_output
 
 extern "C" {
 #include "restate.h"
@@ -34,13 +52,33 @@ extern "C" {
 
 namespace {
 
+// Model callbacks of ref_run_sim_models (the caller's GPU models behind the C ABI's per-call
+// boundary): the context is the tokens after the prompt — committed, then the speculative path.
+typedef int (*ref_verify_fn)(void* user, std::uint32_t request, const std::uint32_t* committed, std::uint32_t n,
+                             const std::uint32_t* cand, std::uint32_t k, ws_verify_out* out);
+typedef int (*ref_draft_fn)(void* user, std::uint32_t request, std::uint32_t kind, const std::uint32_t* context,
+                            std::uint32_t len, std::uint32_t n_committed, ws_pred* out);
+
 struct HookCtx {
   const ws_sim_cfg* cfg = nullptr;
   std::uint64_t request = 0;
   std::uint32_t step = 0;
   std::vector<ws_step_log>* log = nullptr;
+  // model mode
+  ref_verify_fn verify = nullptr;
+  ref_draft_fn draft = nullptr;
+  void* user = nullptr;
+  std::vector<wanspec::TokenId> cands;  // the pending target step's candidates (sim.hpp:297)
+  std::uint64_t base = 0;
 };
 thread_local HookCtx g_hook;
+
+wanspec::Prediction from_pred(const ws_pred& p) {
+  wanspec::Prediction out;
+  for (std::uint32_t j = 0; j < p.n && j < 2; ++j) out.top_candidates.push_back({p.id[j], p.prob[j]});
+  out.entropy = p.entropy;
+  return out;
+}
 
 void to_pred(const wanspec::Prediction& p, ws_pred* out) {
   std::memset(out, 0, sizeof(*out));
@@ -128,6 +166,11 @@ ValidationResult hooked_target_step(const SequenceTrace& trace, std::uint64_t ba
   } else {
     v = run_target_step(trace, base, candidates);  // the reference's own (oracle.hpp:127)
   }
+  if (g_hook.verify) {  // model mode: the result is computed in hooked_apply_target_result
+    g_hook.cands.assign(candidates.begin(), candidates.end());
+    g_hook.base = base;
+    return v;
+  }
   if (g_hook.log && cfg) {
     ws_step_log s{};
     s.request = static_cast<std::uint32_t>(g_hook.request);
@@ -147,9 +190,109 @@ ValidationResult hooked_target_step(const SequenceTrace& trace, std::uint64_t ba
   ++g_hook.step;
   return v;
 }
+
+namespace {
+void log_step(const ValidationResult& v, std::uint64_t base) {
+  const ws_sim_cfg* cfg = g_hook.cfg;
+  if (!g_hook.log || !cfg) return;
+  ws_step_log s{};
+  s.request = static_cast<std::uint32_t>(g_hook.request);
+  s.step = g_hook.step;
+  s.base = base;
+  s.accepted = static_cast<std::uint32_t>(v.accepted.size());
+  s.bonus = v.bonus_token;
+  s.final_entropy = v.final_entropy;
+  s.time = -1;
+  if (v.length() < cfg->k + 1)
+    s.flags = WS_STEP_SYNC_STALL;
+  else if (v.final_entropy > cfg->phi)
+    s.flags = WS_STEP_ENTROPY_RESET;
+  g_hook.log->push_back(s);
+}
+}  // namespace
+
+std::vector<Message> hooked_apply_target_result(ControllerState& st, const ControllerConfig& cfg,
+                                                const ValidationResult& result, SimTime now) {
+  if (!g_hook.verify) return apply_target_result(st, cfg, result, now);
+  // the model's run_target_step over committed[0, base) + the candidates captured at sim.hpp:297
+  if (st.committed.size() != g_hook.base) throw std::logic_error("model seam: committed length != base");
+  ws_verify_out o{};
+  const auto k = static_cast<std::uint32_t>(g_hook.cands.size());
+  if (g_hook.verify(g_hook.user, static_cast<std::uint32_t>(g_hook.request), st.committed.data(),
+                    static_cast<std::uint32_t>(st.committed.size()), g_hook.cands.data(), k, &o) != 0)
+    throw std::runtime_error("model seam: verify callback failed");
+  ValidationResult v;
+  v.accepted.assign(g_hook.cands.begin(), g_hook.cands.begin() + o.accepted);
+  v.bonus_token = o.bonus;
+  v.final_entropy = o.final_entropy;
+  log_step(v, g_hook.base);
+  ++g_hook.step;
+  return apply_target_result(st, cfg, v, now);
+}
+
+void hooked_apply_local_draft(ControllerState& st, const ControllerConfig& cfg, const StepDraftLocal& plan,
+                              const Prediction& prediction) {
+  if (!g_hook.draft) return apply_local_draft(st, cfg, plan, prediction);
+  ws_pred p{};
+  if (g_hook.draft(g_hook.user, static_cast<std::uint32_t>(g_hook.request), WS_JOB_CTRL_DRAFT, plan.context.data(),
+                   static_cast<std::uint32_t>(plan.context.size()), static_cast<std::uint32_t>(st.committed.size()),
+                   &p) != 0)
+    throw std::runtime_error("model seam: draft callback failed");
+  apply_local_draft(st, cfg, plan, from_pred(p));
+}
+
+std::vector<Message> hooked_apply_draft_output(WorkerState& st, const WorkerConfig& cfg,
+                                               std::span<const LeafOutput> outputs) {
+  if (!g_hook.draft) return apply_draft_output(st, cfg, outputs);
+  std::vector<LeafOutput> mine(outputs.begin(), outputs.end());
+  std::vector<TokenId> ctx;
+  for (LeafOutput& o : mine) {
+    if (o.leaf != kRootId && !st.tree.contains(o.leaf)) continue;  // dropped by the fold anyway
+    ctx = st.committed;
+    const std::vector<TokenId> path = st.tree.path_tokens(o.leaf);
+    ctx.insert(ctx.end(), path.begin(), path.end());
+    ws_pred p{};
+    if (g_hook.draft(g_hook.user, static_cast<std::uint32_t>(g_hook.request), WS_JOB_WORKER_DRAFT, ctx.data(),
+                     static_cast<std::uint32_t>(ctx.size()), static_cast<std::uint32_t>(st.committed.size()), &p) != 0)
+      throw std::runtime_error("model seam: draft callback failed");
+    o.prediction = from_pred(p);
+  }
+  return apply_draft_output(st, cfg, std::span<const LeafOutput>(mine));
+}
+
 }  // namespace wanspec
 
 extern "C" {
+
+// The reference's own RequestSim (sim.hpp:166-416) for requests [first, first + local) of cfg,
+// one at a time (sim.hpp:433), with its three model calls answered by the caller's models
+// through the callbacks (the drop-in at the reference's seam). Outputs as
+// ref_run_sim. Traces are still dealt from the tiny oracle (they fix sequence lengths only;
+// every prediction the state machines see comes from the callbacks).
+int ref_run_sim_models(const ws_sim_cfg* c, ref_verify_fn verify, ref_draft_fn draft, void* user, ws_run_out* out,
+                       char* err, std::size_t errlen);
+
+static ref_verify_fn g_verify_cb = nullptr;
+static ref_draft_fn g_draft_cb = nullptr;
+static void* g_cb_user = nullptr;
+
+int ref_run_sim(const ws_sim_cfg* c, int threads, ws_run_out* out, char* err, std::size_t errlen);
+
+int ref_run_sim_models(const ws_sim_cfg* c, ref_verify_fn verify, ref_draft_fn draft, void* user, ws_run_out* out,
+                       char* err, std::size_t errlen) {
+  if (!verify || !draft) {
+    set_err(err, errlen, "ref_run_sim_models: null callback");
+    return WS_EARG;
+  }
+  g_verify_cb = verify;
+  g_draft_cb = draft;
+  g_cb_user = user;
+  const int rc = ref_run_sim(c, 1, out, err, errlen);  // callbacks are not thread-safe: one thread
+  g_verify_cb = nullptr;
+  g_draft_cb = nullptr;
+  g_cb_user = nullptr;
+  return rc;
+}
 
 // run_sim_full (sim.hpp:429-442): traces dealt in request order from one Oracle, then each
 // request runs the reference RequestSim. threads > 1 partitions the shard's requests over a
@@ -182,6 +325,9 @@ int ref_run_sim(const ws_sim_cfg* c, int threads, ws_run_out* out, char* err, st
         g_hook.request = r;
         g_hook.step = 0;
         g_hook.log = out && out->steps ? &logs[i] : nullptr;
+        g_hook.verify = g_verify_cb;
+        g_hook.draft = g_draft_cb;
+        g_hook.user = g_cb_user;
         try {
           wanspec::detail::RequestSim sim(cfg, traces[r], r,
                                           cfg.oracle.seed ^ (0x9e3779b97f4a7c15ULL * (r + 1)));

@@ -184,6 +184,52 @@ class Context:
         keys = ("target_ms", "draft_ms", "target_rows", "draft_rows", "target_forwards", "draft_forwards")
         return {k: x.value for k, x in zip(keys, v)}
 
+    # -- per-call model boundary (include/wanspec_b200.h "per-call model boundary") --
+    def model_open(self, k, sequence_length, eos_id):
+        _check(lib().ws_model_open(self._h, k, sequence_length, eos_id))
+        self._call_k = k
+
+    def model_prefill(self, requests):
+        r = (C.c_uint32 * max(1, len(requests)))(*requests)
+        _check(lib().ws_model_prefill(self._h, len(requests), r))
+
+    def model_verify(self, jobs, with_rows=False):
+        """jobs: [(request, committed tokens, candidates)] -> [(accepted, bonus, entropy)] (and
+        the per-row predictions when with_rows)."""
+        n, k = len(jobs), self._call_k
+        js = (abi.ModelJob * max(1, n))()
+        toks, cand = [], []
+        for j, (req, committed, cands) in enumerate(jobs):
+            js[j].request, js[j].kind, js[j].n_committed, js[j].len, js[j].off = (
+                req, abi.WS_JOB_VERIFY, len(committed), len(committed), len(toks))
+            toks += committed
+            assert len(cands) == k
+            cand += cands
+        t = (C.c_uint32 * max(1, len(toks)))(*toks)
+        c = (C.c_uint32 * max(1, len(cand)))(*cand)
+        out = (abi.VerifyOut * max(1, n))()
+        rows = (abi.Pred * (n * (k + 1))) () if with_rows else None
+        _check(lib().ws_model_verify(self._h, n, js, t, c, out, rows))
+        res = [(o.accepted, o.bonus, o.final_entropy) for o in out[:n]]
+        return (res, list(rows)) if with_rows else res
+
+    def model_draft(self, jobs):
+        """jobs: [(request, kind, context tokens, n_committed)] -> [abi.Pred]."""
+        n = len(jobs)
+        js = (abi.ModelJob * max(1, n))()
+        toks = []
+        for j, (req, kind, context, n_committed) in enumerate(jobs):
+            js[j].request, js[j].kind, js[j].n_committed, js[j].len, js[j].off = (
+                req, kind, n_committed, len(context), len(toks))
+            toks += context
+        t = (C.c_uint32 * max(1, len(toks)))(*toks)
+        out = (abi.Pred * max(1, n))()
+        _check(lib().ws_model_draft(self._h, n, js, t, out))
+        return list(out[:n])
+
+    def model_evict(self, request):
+        _check(lib().ws_model_evict(self._h, request))
+
     def run_stats(self):
         """ws_model_run_stats: verify / draft / prefill device time and rows of the last run."""
         st = abi.RunStats()

@@ -248,3 +248,12 @@ class RunStats(C.Structure):
                 ("verify_kv_pos", C.c_uint64), ("verify_attn_pairs", C.c_uint64), ("draft_kv_pos", C.c_uint64),
                 ("draft_attn_pairs", C.c_uint64), ("prefill_kv_pos", C.c_uint64), ("prefill_attn_pairs", C.c_uint64)]
 
+
+WS_JOB_VERIFY, WS_JOB_CTRL_DRAFT, WS_JOB_WORKER_DRAFT = 0, 1, 2
+
+
+class ModelJob(C.Structure):
+    """ws_model_job: one per-call model job (request, kind, committed / context lengths)."""
+    _fields_ = [("request", C.c_uint32), ("kind", C.c_uint32), ("n_committed", C.c_uint32), ("len", C.c_uint32),
+                ("off", C.c_uint64)]
+

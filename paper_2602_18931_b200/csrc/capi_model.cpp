@@ -60,6 +60,7 @@ int ws_model_load_split(ws_ctx* ctx, const ws_model_cfg* c, int draft_device) {
     }
     WS_CUDA(cudaSetDevice(ctx->device));
     ctx->model_lanes.clear();
+    ctx->call_backend.reset();
     ctx->models.reset();
     ctx->models.reset(new wsb::ModelPair(m, ctx->device));
   });
@@ -191,6 +192,116 @@ int ws_model_stats(ws_ctx* ctx, double* target_ms, double* draft_ms, uint64_t* t
   if (target_forwards) *target_forwards = g_last.target_forwards;
   if (draft_forwards) *draft_forwards = g_last.draft_forwards;
   return WS_OK;
+}
+
+int ws_model_open(ws_ctx* ctx, uint32_t k, uint32_t sequence_length, uint32_t eos_id) {
+  return guard("ws_model_open", [&] {
+    if (!ctx) throw std::invalid_argument("null argument");
+    if (!ctx->models) throw wsb::ConfigError("no model loaded (ws_model_load)");
+    if (k < 1 || sequence_length < 1) throw wsb::ConfigError("k and sequence_length must be >= 1");
+    wsb::DeviceGuard dg(ctx->device);
+    wsb::ModelPair& mp = *ctx->models;
+    if (mp.cfg().prompt_len + sequence_length + k + 2 > mp.cfg().max_ctx)
+      throw wsb::ConfigError("prompt + sequence_length + k exceeds max_ctx");
+    mp.reset_requests();
+    if (!ctx->call_backend) ctx->call_backend.reset(new wsb::ModelBackend_Llama(&mp, sequence_length, eos_id, k));
+    ctx->call_backend->reset_run(sequence_length, eos_id, k);
+    ctx->call_k = k;
+  });
+}
+
+int ws_model_prefill(ws_ctx* ctx, uint32_t n, const uint32_t* requests) {
+  return guard("ws_model_prefill", [&] {
+    if (!ctx || (n && !requests)) throw std::invalid_argument("null argument");
+    if (!ctx->call_backend) throw wsb::ConfigError("no per-call session (ws_model_open)");
+    for (uint32_t i = 0; i < n; ++i)
+      if (requests[i] >= ctx->models->cfg().max_requests) throw std::invalid_argument("request out of range");
+    wsb::DeviceGuard dg(ctx->device);
+    ctx->models->prefill_prompts(requests, n);
+  });
+}
+
+namespace {
+// One lane's batch through the per-call backend: submit (until every job is taken), wait, fold.
+void call_lane(ws_ctx* ctx, int lane, wsb::RoundJobs& jobs, wsb::RoundResults& res) {
+  wsb::ModelBackend_Llama& bk = *ctx->call_backend;
+  const std::size_t took = bk.submit(lane, jobs, WS_VERIFY_GREEDY, 0);
+  const std::size_t n = lane == 0 ? jobs.verify.size() : jobs.draft.size();
+  if (took != n) throw std::logic_error("per-call batch was trimmed (unset WS_VERIFY_TRIM)");
+  while (bk.wait_any(1u << lane) != lane) {
+  }
+  bk.complete(lane, res);
+}
+
+void check_jobs(ws_ctx* ctx, uint32_t n, const ws_model_job* jobs, const uint32_t* tokens, bool verify) {
+  if (!ctx || (n && (!jobs || !tokens))) throw std::invalid_argument("null argument");
+  if (!ctx->call_backend) throw wsb::ConfigError("no per-call session (ws_model_open)");
+  for (uint32_t j = 0; j < n; ++j) {
+    const ws_model_job& q = jobs[j];
+    if (q.request >= ctx->models->cfg().max_requests) throw std::invalid_argument("request out of range");
+    if (verify ? (q.kind != WS_JOB_VERIFY || q.len != q.n_committed)
+               : (q.kind != WS_JOB_CTRL_DRAFT && q.kind != WS_JOB_WORKER_DRAFT) || q.n_committed > q.len)
+      throw std::invalid_argument("bad job kind / lengths");
+  }
+}
+
+void fill_tokens(wsb::RoundJobs& r, uint32_t n, const ws_model_job* jobs, const uint32_t* tokens) {
+  std::uint64_t end = 0;
+  for (uint32_t j = 0; j < n; ++j) end = std::max<std::uint64_t>(end, jobs[j].off + jobs[j].len);
+  r.ctx_tokens.assign(tokens, tokens + end);
+}
+}  // namespace
+
+int ws_model_verify(ws_ctx* ctx, uint32_t n, const ws_model_job* jobs, const uint32_t* tokens, const uint32_t* cand,
+                    ws_verify_out* out, ws_pred* rows_opt) {
+  return guard("ws_model_verify", [&] {
+    check_jobs(ctx, n, jobs, tokens, true);
+    if (n && (!cand || !out)) throw std::invalid_argument("null argument");
+    if (!n) return;
+    wsb::DeviceGuard dg(ctx->device);
+    const uint32_t k = ctx->call_k;
+    wsb::RoundJobs r;
+    r.want_ctx = true;
+    fill_tokens(r, n, jobs, tokens);
+    for (uint32_t j = 0; j < n; ++j) {
+      const ws_model_job& q = jobs[j];
+      r.verify.push_back(ws_verify_job{q.request, k, q.n_committed, q.request, 0, j * k});
+      r.verify_ctx.push_back(wsb::JobCtx{static_cast<std::uint32_t>(q.off), q.len, q.n_committed, wsb::kJobVerify});
+    }
+    r.cands.assign(cand, cand + static_cast<std::size_t>(n) * k);
+    wsb::RoundResults res;
+    call_lane(ctx, 0, r, res);
+    std::memcpy(out, res.verify.data(), n * sizeof(ws_verify_out));
+    if (rows_opt) ctx->call_backend->verify_rows(rows_opt, static_cast<std::size_t>(n) * (k + 1));
+  });
+}
+
+int ws_model_draft(ws_ctx* ctx, uint32_t n, const ws_model_job* jobs, const uint32_t* tokens, ws_pred* out) {
+  return guard("ws_model_draft", [&] {
+    check_jobs(ctx, n, jobs, tokens, false);
+    if (n && !out) throw std::invalid_argument("null argument");
+    if (!n) return;
+    wsb::DeviceGuard dg(ctx->device);
+    wsb::RoundJobs r;
+    r.want_ctx = true;
+    fill_tokens(r, n, jobs, tokens);
+    for (uint32_t j = 0; j < n; ++j) {
+      const ws_model_job& q = jobs[j];
+      r.draft.push_back(ws_draft_job{q.request, 0, q.len});
+      r.draft_ctx.push_back(wsb::JobCtx{static_cast<std::uint32_t>(q.off), q.len, q.n_committed, q.kind});
+    }
+    wsb::RoundResults res;
+    call_lane(ctx, 1, r, res);
+    std::memcpy(out, res.draft.data(), n * sizeof(ws_pred));
+  });
+}
+
+int ws_model_evict(ws_ctx* ctx, uint32_t request) {
+  return guard("ws_model_evict", [&] {
+    if (!ctx) throw std::invalid_argument("null argument");
+    if (!ctx->models) throw wsb::ConfigError("no model loaded (ws_model_load)");
+    ctx->models->evict(request);
+  });
 }
 
 int ws_model_run_stats(ws_ctx* ctx, ws_run_stats* o) {

@@ -18,6 +18,9 @@ struct ws_ctx {
   std::unique_ptr<wsb::ModelPair> models;
   // real-model protocol threads' backends (streams, workspaces), kept across runs
   std::vector<std::unique_ptr<wsb::ModelBackend_Llama>> model_lanes;
+  // per-call model boundary (ws_model_open / _verify / _draft): its own streams and workspaces
+  std::unique_ptr<wsb::ModelBackend_Llama> call_backend;
+  std::uint32_t call_k = 0;
   // model-step statistics of this context's last ws_run_model_sim (ws_model_stats)
   struct ModelStats {
     double target_ms = 0, draft_ms = 0;

@@ -309,6 +309,13 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
   return out;
 }
 
+void ModelPair::evict(std::uint32_t r) {
+  if (r >= cfg_.max_requests) throw ConfigError("evict: request index exceeds max_requests");
+  impl->tgt[r] = LinearCache{};
+  impl->ctrl[r] = LinearCache{};
+  impl->wrk[r] = TreeCache{};
+}
+
 void ModelPair::export_trace(std::uint32_t first, std::uint32_t n, std::uint32_t length, ws_token_record* out) {
   if (first + n > cfg_.max_requests) throw ConfigError("export_trace: requests exceed max_requests");
   if (cfg_.prompt_len + length > cfg_.max_ctx) throw ConfigError("export_trace: prompt + length exceeds max_ctx");
@@ -908,6 +915,14 @@ int ModelBackend_Llama::wait_any(std::uint32_t busy) {
     }
     std::this_thread::yield();
   }
+}
+
+void ModelBackend_Llama::verify_rows(ws_pred* host, std::size_t n_rows) {
+  Lanes& L = *ln_;
+  if (n_rows > static_cast<std::size_t>(L.nv) * (k_ + 1)) throw std::invalid_argument("verify_rows: too many rows");
+  if (!n_rows) return;
+  DeviceGuard dg(L.device);
+  WS_CUDA(cudaMemcpy(host, L.d_pred, n_rows * sizeof(ws_pred), cudaMemcpyDeviceToHost));
 }
 
 void ModelBackend_Llama::complete(int lane, RoundResults& res) {

@@ -52,6 +52,9 @@ class ModelBackend_Llama : public ModelBackend {
   int wait_any(std::uint32_t busy) override;
   void complete(int lane, RoundResults& res) override;
   KernelProfiler& profiler(int lane);  // lane 0: target forwards; lanes 1..n: draft forwards
+  // After complete(0): the per-row predictions (top-2 + entropy, K3) of the last verify batch,
+  // n_rows = verify jobs x (k + 1), request-major (the per-call boundary's rows export).
+  void verify_rows(ws_pred* host, std::size_t n_rows);
   // New run on the same pair (the caller reset the per-request caches): run parameters, zeroed
   // counters; streams, workspaces and device buffers are kept.
   void reset_run(std::uint32_t seq_len, TokenId eos, std::uint32_t k);
@@ -86,6 +89,7 @@ class ModelPair {
   ModelPair(const ModelPairCfg& cfg, int device);
   ~ModelPair();
   void reset_requests();  // forget all cached KV state (new run)
+  void evict(std::uint32_t r);  // forget request r's cached KV (target, controller draft, worker)
   // Prompt prefill (its own phase, before the first verify / draft): the KV of prompt positions
   // [0, P-1) of each listed request is written for the target (verify cache), and once for the
   // draft model into the worker's committed prefix, then copied into the controller's draft
