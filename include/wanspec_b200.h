@@ -107,6 +107,10 @@ typedef struct ws_sim_cfg {
   uint32_t host_threads;  /* protocol threads for ws_run_sim (0 = 1); one CUDA stream each */
   uint64_t sample_seed;   /* Philox key for WS_VERIFY_REJECTION */
   ws_oracle_cfg oracle;
+  /* model path, WS_VERIFY_REJECTION only (K4R, kernels/sample.cuh): nucleus mass (0 or >= 1 =
+   * no truncation) and softmax temperature (0 = 1) of the target distribution */
+  float top_p;
+  float temperature;
 } ws_sim_cfg;
 
 /* RequestMetrics (sim.hpp:121-134). */
@@ -249,6 +253,16 @@ int ws_op_row_stats_bf16(const void* logits, uint32_t rows, uint32_t vocab, uint
 int ws_op_verify_greedy_bf16(const void* logits, uint32_t n_req, uint32_t k, uint32_t vocab,
                              uint32_t ld, const uint32_t* cand, ws_verify_out* out,
                              ws_pred* rows_out, void* workspace, void* stream);
+
+/* K4R: speculative rejection sampling over n_req groups of k+1 bf16 logits rows (extension,
+ * kernels/sample.cuh): accept c_i iff u * q_i < p'(c_i) with u from Philox4x32-10 keyed seed,
+ * counter (request[j], step[j], i); residual / bonus draws over the full vocabulary; optional
+ * top-p nucleus and temperature. All pointers device memory; forced (may be NULL): per row,
+ * >= 0 = a point mass on that token. */
+int ws_op_verify_rejection_bf16(const void* logits, uint32_t n_req, uint32_t k, uint32_t vocab, uint32_t ld,
+                                float inv_temp, float top_p, const uint32_t* cand, const double* cand_prob,
+                                uint64_t seed, const uint64_t* request, const uint32_t* step,
+                                const int32_t* forced, ws_verify_out* out, void* stream);
 
 /* ---- real-model pair (BASELINE config 3): Llama-shape target + draft on one GPU ----
  * Random-init bf16 weights of the named shapes ("llama3-8b", "llama3.2-1b", "tiny", ...),

@@ -183,6 +183,26 @@ def row_stats(row, inv_temp=1.0):
     return (p.n, tuple(p.id[:p.n]), tuple(p.prob[:p.n]), p.entropy)
 
 
+def model_rejection_verify(rows, k, cands, cand_probs, seed, request, step, inv_temp=1.0, top_p=1.0, forced=None):
+    """K4R restatement (oracle/restate.c or_model_rejection_verify) over one request's k+1
+    float32 rows (numpy [k+1, V]): returns (accepted, bonus, final_entropy)."""
+    import numpy as np
+    x = np.ascontiguousarray(np.asarray(rows, dtype=np.float32))
+    V = x.shape[1]
+    c = (C.c_uint32 * max(1, k))(*cands)
+    q = (C.c_double * max(1, k))(*cand_probs)
+    f = (C.c_int32 * (k + 1))(*forced) if forced is not None else None
+    a, b, h = C.c_uint32(), C.c_uint32(), C.c_double()
+    lib = oracle_lib()
+    lib.or_model_rejection_verify.argtypes = [_P(C.c_float), C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
+                                              C.c_float, _P(C.c_uint32), _P(C.c_double), C.c_uint64, C.c_uint64,
+                                              C.c_uint32, _P(C.c_int32), _P(C.c_uint32), _P(C.c_uint32),
+                                              _P(C.c_double)]
+    lib.or_model_rejection_verify(x.ctypes.data_as(_P(C.c_float)), k, V, V, inv_temp, top_p, c, q, seed, request,
+                                  step, f, C.byref(a), C.byref(b), C.byref(h))
+    return a.value, b.value, h.value
+
+
 def ref_run_sim(cfg, threads=1, with_tokens=True, with_steps=True):
     """The reference's run_sim_full over cfg's shard. Returns abi.RunBuffers."""
     bufs = abi.RunBuffers(cfg, with_tokens, with_steps)

@@ -466,3 +466,199 @@ void or_row_stats(const float* x, uint32_t vocab, double it, ws_pred* out) {
   double h = log(z) - s / z;
   out->entropy = h < 0.0 ? 0.0 : h;
 }
+
+/* ---------------- extension: K4R rejection sampling over real-model rows ---------------- */
+/* Restates paper_2602_18931_b200/csrc/kernels/sample.cuh (the rule) step for step: the same
+ * fp64 operations in the same order — per-chunk sequential sums over ceil(V/512)-id chunks, a
+ * fixed pairwise tree over the 512 partials, a sequential prefix over the chunks for the
+ * inverse CDF. Parity is unpinned by the reference (greedy only); this is the
+ * checker. Only exp() may differ by an ulp between glibc and libdevice. */
+#define OR_T 512
+
+typedef struct {
+  const float* x;
+  uint32_t V;
+  double tau, zmax, Z, S, M;
+  int32_t forced;
+  uint32_t t_star;
+} or_row;
+
+static uint32_t or_key16(float x) {
+  uint32_t b;
+  memcpy(&b, &x, 4);
+  b >>= 16;
+  return (b & 0x8000u) ? (~b & 0xFFFFu) : (b | 0x8000u);
+}
+
+static double or_tree(double* s) {
+  for (int st = OR_T / 2; st > 0; st >>= 1)
+    for (int i = 0; i < st; ++i) s[i] = s[i] + s[i + st];
+  return s[0];
+}
+
+static void or_chunk(uint32_t V, int t, uint32_t* lo, uint32_t* hi) {
+  uint32_t C = (V + OR_T - 1) / OR_T;
+  uint64_t l = (uint64_t)t * C;
+  *lo = l > V ? V : (uint32_t)l;
+  *hi = *lo + C > V ? V : *lo + C;
+}
+
+static double or_z(const or_row* r, uint32_t i) { return (double)r->x[i] * r->tau; }
+
+static double or_pprime(const or_row* r, uint32_t i) {
+  if (r->forced >= 0) return (uint32_t)r->forced == i ? 1.0 : 0.0;
+  if (or_key16(r->x[i]) < r->t_star) return 0.0;
+  double p = exp(or_z(r, i) - r->zmax) / r->Z;
+  return r->M == 1.0 ? p : p / r->M;
+}
+
+static void or_row_dist(or_row* r, float top_p) {
+  r->t_star = 0;
+  r->M = 1.0;
+  if (r->forced >= 0) {
+    r->Z = 1.0;
+    r->S = 0.0;
+    r->zmax = 0.0;
+    return;
+  }
+  float mx = -INFINITY;
+  for (uint32_t i = 0; i < r->V; ++i) mx = r->x[i] > mx ? r->x[i] : mx;
+  r->zmax = (double)mx * r->tau;
+  double pz[OR_T], ps[OR_T];
+  for (int t = 0; t < OR_T; ++t) {
+    uint32_t lo, hi;
+    or_chunk(r->V, t, &lo, &hi);
+    double z = 0.0, sv = 0.0;
+    for (uint32_t i = lo; i < hi; ++i) {
+      double d = or_z(r, i) - r->zmax;
+      double e = exp(d);
+      z = z + e;
+      if (e > 0.0) sv = sv + e * d;
+    }
+    pz[t] = z;
+    ps[t] = sv;
+  }
+  r->Z = or_tree(pz);
+  r->S = or_tree(ps);
+  if (top_p < 1.f) {
+    double tp = (double)top_p;
+    uint32_t lo = 0, hi = 65536;
+    double m_lo = 1.0;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) / 2;
+      double part[OR_T];
+      for (int t = 0; t < OR_T; ++t) {
+        uint32_t a, b;
+        or_chunk(r->V, t, &a, &b);
+        double s = 0.0;
+        for (uint32_t i = a; i < b; ++i)
+          if (or_key16(r->x[i]) >= mid) s = s + exp(or_z(r, i) - r->zmax);
+        part[t] = s;
+      }
+      double mass = or_tree(part) / r->Z;
+      if (mass >= tp) {
+        lo = mid;
+        m_lo = mass;
+      } else {
+        hi = mid;
+      }
+    }
+    r->t_star = lo;
+    r->M = m_lo;
+  }
+}
+
+static double or_w(const or_row* r, int resid, uint32_t c, double q, double tail, uint32_t i) {
+  double p = or_pprime(r, i);
+  if (!resid) return p;
+  double d = p - (i == c ? q : tail);
+  return d > 0.0 ? d : 0.0;
+}
+
+static uint32_t or_sample_row(const or_row* r, int has_d, uint32_t c, double q, double u) {
+  uint32_t V = r->V;
+  double tail = V > 1 ? (1.0 - q) / (double)(V - 1) : 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    int resid = has_d && pass == 0;
+    double part[OR_T], start[OR_T];
+    for (int t = 0; t < OR_T; ++t) {
+      uint32_t a, b;
+      or_chunk(V, t, &a, &b);
+      double s = 0.0;
+      for (uint32_t i = a; i < b; ++i) s = s + or_w(r, resid, c, q, tail, i);
+      part[t] = s;
+    }
+    double acc = 0.0;
+    for (int t = 0; t < OR_T; ++t) {
+      start[t] = acc;
+      acc = acc + part[t];
+    }
+    double R = acc;
+    if (resid && !(R > 0.0)) continue;
+    double target = u * R;
+    uint32_t pick = 0xFFFFFFFFu, lastpos = 0;
+    for (int t = 0; t < OR_T; ++t) {
+      if (!(part[t] > 0.0)) continue;
+      uint32_t a, b;
+      or_chunk(V, t, &a, &b);
+      if (pick == 0xFFFFFFFFu && target >= start[t] && target < start[t] + part[t]) {
+        double w_acc = start[t];
+        for (uint32_t i = a; i < b; ++i) {
+          double v = or_w(r, resid, c, q, tail, i);
+          if (v > 0.0) {
+            double nx = w_acc + v;
+            if (nx > target) {
+              pick = i;
+              break;
+            }
+            w_acc = nx;
+          }
+        }
+      }
+      for (uint32_t i = a; i < b; ++i)
+        if (or_w(r, resid, c, q, tail, i) > 0.0 && i > lastpos) lastpos = i;
+    }
+    return pick != 0xFFFFFFFFu ? pick : lastpos;
+  }
+  return 0;
+}
+
+void or_model_rejection_verify(const float* rows, uint32_t k, uint32_t vocab, uint32_t ld, float inv_temp,
+                               float top_p, const uint32_t* cand, const double* cand_prob, uint64_t seed,
+                               uint64_t request, uint32_t step, const int32_t* forced, uint32_t* acc_len,
+                               uint32_t* bonus, double* final_entropy) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  or_row r;
+  r.V = vocab;
+  r.tau = (double)inv_temp;
+  for (uint32_t i = 0; i <= k; ++i) {
+    r.x = rows + (size_t)i * ld;
+    r.forced = forced ? forced[i] : -1;
+    or_row_dist(&r, top_p);
+    const uint32_t ctr[4] = {(uint32_t)request, (uint32_t)(request >> 32), step, i};
+    uint32_t w[4];
+    or_philox4x32_10(ctr, key, w);
+    double u2 = or_unit_from_words(w[2], w[3]);
+    int reject = 0;
+    uint32_t c = 0;
+    double q = 0.0;
+    if (i < k) {
+      c = cand[i];
+      q = cand_prob[i];
+      q = q < 0.0 ? 0.0 : (q > 1.0 ? 1.0 : q);
+      double u = or_unit_from_words(w[0], w[1]);
+      reject = !(u * q < or_pprime(&r, c));
+    }
+    if (i == k || reject) {
+      *acc_len = i;
+      *bonus = or_sample_row(&r, reject, c, q, u2);
+      if (r.forced >= 0) {
+        *final_entropy = 0.0;
+      } else {
+        double h = log(r.Z) - r.S / r.Z;
+        *final_entropy = h < 0.0 ? 0.0 : h;
+      }
+      return;
+    }
+  }
+}

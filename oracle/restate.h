@@ -98,6 +98,12 @@ uint64_t or_fnv1a_tokens(uint64_t h, const uint32_t* toks, size_t n);
 /* ---- K3 restatement: fp64 softmax statistics of one logits row ----
  * top-2 of softmax(x * inv_temp) (ties to the lower id) and entropy in nats. */
 void or_row_stats(const float* logits, uint32_t vocab, double inv_temp, ws_pred* out);
+/* K4R restated (kernels/sample.cuh): rejection sampling over k+1 float rows (the bf16 logits of
+ * one request's verify rows, row stride ld) — extension, parity unpinned by the reference. */
+void or_model_rejection_verify(const float* rows, uint32_t k, uint32_t vocab, uint32_t ld, float inv_temp,
+                               float top_p, const uint32_t* cand, const double* cand_prob, uint64_t seed,
+                               uint64_t request, uint32_t step, const int32_t* forced, uint32_t* acc_len,
+                               uint32_t* bonus, double* final_entropy);
 
 #ifdef __cplusplus
 }

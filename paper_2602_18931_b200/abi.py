@@ -63,6 +63,7 @@ class SimCfg(C.Structure):
         ("local_requests", C.c_uint32), ("host_threads", C.c_uint32),
         ("sample_seed", C.c_uint64),
         ("oracle", OracleCfg),
+        ("top_p", C.c_float), ("temperature", C.c_float),
     ]
 
 

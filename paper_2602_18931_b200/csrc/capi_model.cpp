@@ -99,6 +99,7 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
     std::vector<wsb::ModelBackend_Llama*> used;
     for (std::uint32_t t = 0; t < threads; ++t) {
       owned[t]->reset_run(c->oracle.sequence_length, c->oracle.eos_id, c->k);
+      owned[t]->set_sampling(c->temperature, c->top_p);
       for (int lane = 0; lane < owned[t]->n_lanes(); ++lane) owned[t]->profiler(lane).enable(prof);
       backends.push_back(owned[t].get());
       used.push_back(owned[t].get());

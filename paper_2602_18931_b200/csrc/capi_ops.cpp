@@ -9,6 +9,7 @@
 #include "kernels/cuda_check.hpp"
 #include "kernels/gemm_tc.cuh"
 #include "kernels/rowstats.cuh"
+#include "kernels/sample.cuh"
 #include "wanspec_b200.h"
 
 namespace wsb {
@@ -77,6 +78,16 @@ int ws_op_verify_greedy_bf16(const void* logits, uint32_t n_req, uint32_t k, uin
     if (!rows_out || !cand || !out) throw std::invalid_argument("verify_greedy: null argument");
     wsb::row_stats_bf16(logits, n_req * (k + 1), vocab, ld, 1.0f, rows_out, nullptr, workspace, n_req, k, cand, out,
                         static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ws_op_verify_rejection_bf16(const void* logits, uint32_t n_req, uint32_t k, uint32_t vocab, uint32_t ld,
+                                float inv_temp, float top_p, const uint32_t* cand, const double* cand_prob,
+                                uint64_t seed, const uint64_t* request, const uint32_t* step, const int32_t* forced,
+                                ws_verify_out* out, void* stream) {
+  return op_guarded("ws_op_verify_rejection_bf16", [&] {
+    wsb::verify_rejection_bf16(logits, n_req, k, vocab, ld, inv_temp, top_p, cand, cand_prob, seed, request, step,
+                               forced, out, static_cast<cudaStream_t>(stream));
   });
 }
 

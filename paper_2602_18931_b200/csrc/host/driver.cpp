@@ -302,6 +302,7 @@ class RequestRun {
         jv.cands.insert(jv.cands.end(), target_.tokens.begin(), target_.tokens.end());
         jv.verify.push_back(j);
         if (jv.want_ctx) {  // committed output (stable until this verify folds)
+          for (NodeId id : target_.ids) jv.cand_probs.push_back(ctrl_.tree.node(id).prob);
           jv.verify_ctx.push_back(JobCtx{static_cast<std::uint32_t>(jv.ctx_tokens.size()),
                                          static_cast<std::uint32_t>(ctrl_.committed.size()),
                                          static_cast<std::uint32_t>(ctrl_.committed.size()), kJobVerify});
@@ -430,6 +431,7 @@ void requeue_verify(RoundJobs& fly, std::vector<RequestRun*>& fly_slots, std::si
     pend.cands.insert(pend.cands.end(), fly.cands.begin() + off, fly.cands.begin() + off + v.k);
     pend.verify.push_back(v);
     if (fly.want_ctx) {
+      pend.cand_probs.insert(pend.cand_probs.end(), fly.cand_probs.begin() + off, fly.cand_probs.begin() + off + v.k);
       JobCtx c = fly.verify_ctx[j];
       const std::uint32_t o = c.off;
       c.off = static_cast<std::uint32_t>(pend.ctx_tokens.size());

@@ -53,6 +53,7 @@ struct JobCtx {
 struct RoundJobs {
   std::vector<VerifyJob> verify;
   std::vector<TokenId> cands;
+  std::vector<double> cand_probs;  // (want_ctx) the draft probability of each candidate (tree node)
   std::vector<DraftJob> draft;
   bool want_ctx = false;  // set by backends that need contexts (real models)
   std::vector<JobCtx> verify_ctx, draft_ctx;
@@ -60,6 +61,7 @@ struct RoundJobs {
   void clear() {
     verify.clear();
     cands.clear();
+    cand_probs.clear();
     draft.clear();
     verify_ctx.clear();
     draft_ctx.clear();

@@ -11,6 +11,7 @@
 
 #include "../kernels/cuda_check.hpp"
 #include "../kernels/rowstats.cuh"
+#include "../kernels/sample.cuh"
 
 namespace wsb {
 
@@ -173,6 +174,9 @@ struct ModelBackend_Llama::Lanes {
   ws_verify_out* d_vout = nullptr;
   std::uint32_t* d_cands = nullptr;
   std::int32_t* d_forced = nullptr;
+  double* d_cprob = nullptr;           // K4R inputs: candidate draft probabilities,
+  std::uint64_t* d_req = nullptr;      // per-job request ids (Philox counter words)
+  std::uint32_t* d_step = nullptr;     // and per-request verify step indices
   void* d_ws = nullptr;
   unsigned char* h_stage = nullptr;
   ws_verify_out* h_vout = nullptr;
@@ -186,7 +190,8 @@ struct ModelBackend_Llama::Lanes {
     dl.clear();
     cudaSetDevice(device);
     for (void* q : {static_cast<void*>(d_pred), static_cast<void*>(d_vout), static_cast<void*>(d_cands),
-                    static_cast<void*>(d_forced), d_ws})
+                    static_cast<void*>(d_forced), static_cast<void*>(d_cprob), static_cast<void*>(d_req),
+                    static_cast<void*>(d_step), d_ws})
       if (q) cudaFree(q);
     for (void* q : {static_cast<void*>(h_stage), static_cast<void*>(h_vout)})
       if (q) cudaFreeHost(q);
@@ -578,7 +583,8 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
   const std::size_t need = static_cast<std::size_t>(nv) * (k_ + 1) + 16;
   if (need > L.cap_v) {  // the lane is idle here (the driver submits only to idle lanes)
     for (void* q : {static_cast<void*>(L.d_pred), static_cast<void*>(L.d_vout), static_cast<void*>(L.d_cands),
-                    static_cast<void*>(L.d_forced), L.d_ws})
+                    static_cast<void*>(L.d_forced), static_cast<void*>(L.d_cprob), static_cast<void*>(L.d_req),
+                    static_cast<void*>(L.d_step), L.d_ws})
       if (q) cudaFree(q);
     for (void* q : {static_cast<void*>(L.h_stage), static_cast<void*>(L.h_vout)})
       if (q) cudaFreeHost(q);
@@ -587,13 +593,17 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
     WS_CUDA(cudaMalloc(&L.d_vout, L.cap_v * sizeof(ws_verify_out)));
     WS_CUDA(cudaMalloc(&L.d_cands, L.cap_v * k_ * 4 + 64));
     WS_CUDA(cudaMalloc(&L.d_forced, L.cap_v * 4));
+    WS_CUDA(cudaMalloc(&L.d_cprob, L.cap_v * k_ * sizeof(double) + 64));
+    WS_CUDA(cudaMalloc(&L.d_req, L.cap_v * sizeof(std::uint64_t)));
+    WS_CUDA(cudaMalloc(&L.d_step, L.cap_v * sizeof(std::uint32_t)));
     const std::size_t wsb_ = rowstats_workspace_bytes(static_cast<std::uint32_t>(L.cap_v), V,
                                                       static_cast<std::uint32_t>(L.cap_v));
     WS_CUDA(cudaMalloc(&L.d_ws, wsb_));
     WS_CUDA(cudaMemset(L.d_ws, 0, wsb_));
     WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&L.h_vout), L.cap_v * sizeof(ws_verify_out),
                           cudaHostAllocDefault));
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&L.h_stage), L.cap_v * (k_ * 4 + 8) + 256, cudaHostAllocDefault));
+    // staging: cands (k u32) + forced ((k+1) i32) + cand probs (k f64) + request (u64) + step (u32) per job
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&L.h_stage), L.cap_v * (k_ * 16 + 24) + 256, cudaHostAllocDefault));
   }
   ForwardBatch& b = L.tb;
   b.clear();
@@ -632,10 +642,33 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
   std::memcpy(hc + nv * k_, L.forced.data(), L.forced.size() * 4);
   WS_CUDA(cudaMemcpyAsync(L.d_cands, hc, nv * k_ * 4, cudaMemcpyHostToDevice, st));
   WS_CUDA(cudaMemcpyAsync(L.d_forced, hc + nv * k_, L.forced.size() * 4, cudaMemcpyHostToDevice, st));
+  const bool rejection = verify_mode_ == WS_VERIFY_REJECTION;
+  if (rejection) {  // K4R inputs, staged after the candidates and forced rows
+    if (jobs.cand_probs.size() < jobs.cands.size()) throw std::logic_error("model path: candidate probabilities missing");
+    unsigned char* h = reinterpret_cast<unsigned char*>(hc + nv * k_ + L.forced.size());
+    h = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(h) + 7) & ~std::uintptr_t(7));
+    double* hp = reinterpret_cast<double*>(h);
+    std::uint64_t* hr = reinterpret_cast<std::uint64_t*>(hp + static_cast<std::size_t>(nv) * k_);
+    std::uint32_t* hs = reinterpret_cast<std::uint32_t*>(hr + nv);
+    for (std::uint32_t j = 0; j < nv; ++j) {
+      const VerifyJob& vj = jobs.verify[j];
+      std::memcpy(hp + static_cast<std::size_t>(j) * k_, jobs.cand_probs.data() + vj.cand_off, k_ * sizeof(double));
+      hr[j] = vj.request;
+      hs[j] = vj.step;
+    }
+    WS_CUDA(cudaMemcpyAsync(L.d_cprob, hp, static_cast<std::size_t>(nv) * k_ * sizeof(double), cudaMemcpyHostToDevice, st));
+    WS_CUDA(cudaMemcpyAsync(L.d_req, hr, nv * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
+    WS_CUDA(cudaMemcpyAsync(L.d_step, hs, nv * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    stats.h2d += static_cast<std::size_t>(nv) * (k_ * 8 + 12);
+  }
   WS_CUDA(cudaEventRecord(L.e0, st));
   p_->target().forward(b, cfg.plant_target, st, *L.ws_t);
-  row_stats_bf16(L.ws_t->logits, nv * (k_ + 1), V, V, 1.0f, L.d_pred, nullptr, L.d_ws, nv, k_, L.d_cands,
-                 L.d_vout, st, L.d_forced);
+  if (rejection)
+    verify_rejection_bf16(L.ws_t->logits, nv, k_, V, V, inv_temp_, top_p_, L.d_cands, L.d_cprob, sample_seed_,
+                          L.d_req, L.d_step, L.d_forced, L.d_vout, st);
+  else
+    row_stats_bf16(L.ws_t->logits, nv * (k_ + 1), V, V, 1.0f, L.d_pred, nullptr, L.d_ws, nv, k_, L.d_cands,
+                   L.d_vout, st, L.d_forced);
   WS_CUDA(cudaEventRecord(L.e1, st));
   WS_CUDA(cudaMemcpyAsync(L.h_vout, L.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaEventRecord(L.done, st));
@@ -878,9 +911,11 @@ cudaStream_t ModelBackend_Llama::draft_stream(int lane) const {
   return serial && ln_->device_d == ln_->device ? ln_->st_t : ln_->dl.at(lane - 1)->st;
 }
 
-std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t) {
-  if (verify_mode != WS_VERIFY_GREEDY)
-    throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
+std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed) {
+  if (verify_mode != WS_VERIFY_GREEDY && verify_mode != WS_VERIFY_REJECTION)
+    throw ConfigError("model path: unknown verify mode");
+  verify_mode_ = verify_mode;
+  sample_seed_ = sample_seed;
   stats.rounds += 1;
   const auto t0 = std::chrono::steady_clock::now();
   std::size_t took;
@@ -961,9 +996,10 @@ void ModelBackend_Llama::complete(int lane, RoundResults& res) {
 }
 
 // Lockstep round (WS_LOCKSTEP=1): both lanes, then both results.
-void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode, std::uint64_t) {
-  if (verify_mode != WS_VERIFY_GREEDY)
-    throw ConfigError("model path: only greedy verify is built (rejection sampling runs on the oracle tables)");
+void ModelBackend_Llama::run_round(const RoundJobs& jobs, RoundResults& res, int verify_mode,
+                                   std::uint64_t sample_seed) {
+  verify_mode_ = verify_mode;
+  sample_seed_ = sample_seed;
   stats.rounds += 1;
   submit_verify(jobs, jobs.verify.size());  // lockstep rounds take every job
   submit_draft(1, jobs);

@@ -58,6 +58,11 @@ class ModelBackend_Llama : public ModelBackend {
   // New run on the same pair (the caller reset the per-request caches): run parameters, zeroed
   // counters; streams, workspaces and device buffers are kept.
   void reset_run(std::uint32_t seq_len, TokenId eos, std::uint32_t k);
+  // WS_VERIFY_REJECTION on the model path (K4R): the target's softmax temperature and nucleus
+  void set_sampling(float temperature, float top_p) {
+    inv_temp_ = temperature > 0.f ? 1.f / temperature : 1.f;
+    top_p_ = top_p > 0.f && top_p < 1.f ? top_p : 1.f;
+  }
   double target_ms = 0, draft_ms = 0;
   std::uint64_t target_rows = 0, draft_rows_fed = 0, target_forwards = 0, draft_forwards = 0;
   std::uint64_t target_out_rows = 0, draft_out_rows = 0;  // rows through the LM head + K3
@@ -79,6 +84,9 @@ class ModelBackend_Llama : public ModelBackend {
   TokenId eos_;
   std::uint32_t k_;
   std::uint64_t draft_batch_ = 0;
+  int verify_mode_ = WS_VERIFY_GREEDY;
+  std::uint64_t sample_seed_ = 0;
+  float inv_temp_ = 1.f, top_p_ = 1.f;
   struct Lanes;
   std::unique_ptr<Lanes> ln_;
 };

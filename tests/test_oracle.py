@@ -185,3 +185,34 @@ def test_unit_from_words_range():
     lib.or_unit_from_words.argtypes = [C.c_uint32, C.c_uint32]
     assert lib.or_unit_from_words(0, 0) == 0.0
     assert lib.or_unit_from_words(0xffffffff, 0xffffffff) < 1.0
+
+
+def test_model_rejection_restatement_samples_the_target():
+    """or_model_rejection_verify (the K4R checker): with no candidates (k = 0) the bonus is a
+    draw from the target row p' — empirical frequencies over 20000 Philox counters match the
+    softmax; with top_p, tokens outside the nucleus never appear; a candidate whose target
+    probability is 1 is always accepted."""
+    import math
+
+    import numpy as np
+    row = np.array([[2.0, 1.0, 0.5, 0.0, -1.0, 3.0, 0.25, 1.5]], dtype=np.float32)
+    p = np.exp(row[0] - row[0].max())
+    p /= p.sum()
+    counts = np.zeros(8)
+    for r in range(20000):
+        a, b, h = po.model_rejection_verify(row, 0, [], [], 42, r, 0)
+        assert a == 0
+        counts[b] += 1
+    assert np.abs(counts / 20000 - p).max() < 0.012
+    assert h == pytest.approx(-(p * np.log(p)).sum(), rel=1e-12)
+    order = np.argsort(-p)
+    nucleus = set(order[:np.searchsorted(np.cumsum(p[order]), 0.6) + 1].tolist())
+    for r in range(3000):
+        _, b, _ = po.model_rejection_verify(row, 0, [], [], 7, r, 0, top_p=0.6)
+        assert b in nucleus
+    sharp = np.full((3, 8), -1e4, dtype=np.float32)
+    sharp[:, 5] = 0.0
+    for r in range(200):
+        a, b, _ = po.model_rejection_verify(sharp, 2, [5, 5], [0.3, 1.0], 1, r, 3)
+        assert (a, b) == (2, 5)
+    assert math.isfinite(h)
