@@ -281,7 +281,7 @@ typedef struct ws_model_cfg {
   float plant_target;
   float plant_draft;
   float draft_plant_rate;
-  uint32_t pad;
+  uint32_t tp;  /* target tensor-parallel ranks on GPUs device .. device+tp-1 (0/1 = one GPU) */
 } ws_model_cfg;
 int ws_model_load(ws_ctx* ctx, const ws_model_cfg* cfg);
 /* Split placement: the target (verify) model on the context's GPU and the draft
@@ -368,6 +368,12 @@ int ws_model_run_stats(ws_ctx* ctx, ws_run_stats* out);
 typedef struct ws_model ws_model;
 int ws_model_create(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device,
                     ws_model** out);
+/* The same model split tensor-parallel over GPUs device .. device + tp - 1 (config 5's layout:
+ * column-parallel QKV / gate-up, row-parallel O / down with the peer-memory all-reduce fused into
+ * the residual update, vocabulary-parallel LM head); weights identical to the one-GPU model of
+ * the same seed. Logits land on `device`. */
+int ws_model_create_tp(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device, int tp,
+                       ws_model** out);
 int ws_model_destroy(ws_model* m);
 int ws_model_copy_weight(ws_model* m, const char* which, int layer, void* dst_dev, int64_t numel);
 int ws_model_forward(ws_model* m, int n_rows, const int32_t* tok, const int32_t* pos,

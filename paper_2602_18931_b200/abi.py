@@ -100,14 +100,15 @@ class ModelCfg(C.Structure):
     _fields_ = [("target", C.c_char_p), ("draft", C.c_char_p), ("seed", C.c_uint64),
                 ("prompt_len", C.c_uint32), ("max_requests", C.c_uint32), ("max_ctx", C.c_uint32),
                 ("trie_slots", C.c_uint32), ("plant_target", C.c_float), ("plant_draft", C.c_float),
-                ("draft_plant_rate", C.c_float), ("pad", C.c_uint32)]
+                ("draft_plant_rate", C.c_float), ("tp", C.c_uint32)]
 
 
 def model_cfg(target="llama3-8b", draft="llama3.2-1b", seed=1, prompt_len=128, max_requests=256,
-              max_ctx=256, trie_slots=512, plant_target=16.0, plant_draft=16.0, draft_plant_rate=0.8):
-    """The config-3 model pair (random-init Llama shapes + planted shared bigram bias)."""
+              max_ctx=256, trie_slots=512, plant_target=16.0, plant_draft=16.0, draft_plant_rate=0.8, tp=1):
+    """The config-3 model pair (random-init Llama shapes + planted shared bigram bias); tp > 1
+    splits the target over GPUs device .. device + tp - 1 (BASELINE config 5)."""
     return ModelCfg(target.encode(), draft.encode(), seed, prompt_len, max_requests, max_ctx, trie_slots,
-                    plant_target, plant_draft, draft_plant_rate, 0)
+                    plant_target, plant_draft, draft_plant_rate, tp)
 
 
 LLAMA_VOCAB = 128256

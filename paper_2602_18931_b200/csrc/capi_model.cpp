@@ -52,6 +52,7 @@ int ws_model_load_split(ws_ctx* ctx, const ws_model_cfg* c, int draft_device) {
     m.plant_draft = c->plant_draft;
     m.draft_plant_rate = c->draft_plant_rate;
     m.draft_device = draft_device;
+    m.tp = c->tp > 1 ? static_cast<int>(c->tp) : 1;
     if (m.prompt_len < 1) throw wsb::ConfigError("prompt_len must be >= 1");
     if (draft_device >= 0) {
       int n = 0;
@@ -330,14 +331,20 @@ int ws_model_run_stats(ws_ctx* ctx, ws_run_stats* o) {
   });
 }
 
-int ws_model_create(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device, ws_model** out) {
+int ws_model_create_tp(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device, int tp,
+                       ws_model** out) {
   return guard("ws_model_create", [&] {
     if (!shape || !out || n_slots <= 0) throw std::invalid_argument("bad argument");
     auto h = std::make_unique<ws_model>();
     h->device = device;
-    h->m.reset(new wsb::LlamaModel(wsb::shape_by_name(shape), seed, n_slots, max_rows > 0 ? max_rows : 64, device));
+    h->m.reset(new wsb::LlamaModel(wsb::shape_by_name(shape), seed, n_slots, max_rows > 0 ? max_rows : 64, device,
+                                   tp > 1 ? tp : 1));
     *out = h.release();
   });
+}
+
+int ws_model_create(const char* shape, uint64_t seed, int64_t n_slots, int max_rows, int device, ws_model** out) {
+  return ws_model_create_tp(shape, seed, n_slots, max_rows, device, 1, out);
 }
 
 int ws_model_destroy(ws_model* m) {

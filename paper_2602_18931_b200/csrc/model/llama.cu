@@ -11,6 +11,7 @@
 
 #include "../kernels/cuda_check.hpp"
 #include "../kernels/gemm_tc.cuh"
+#include "llama_tp.hpp"
 
 namespace wsb {
 
@@ -68,11 +69,15 @@ std::size_t al(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255
 
 }  // namespace
 
-LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device)
-    : s_(s), device_(device), n_slots_(n_slots) {
+LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device, int tp)
+    : s_(s), device_(device), n_slots_(n_slots), tp_(tp < 1 ? 1 : tp) {
   WS_CUDA(cudaSetDevice(device));
   if (s.d % 64 || s.ffn % 64 || (s.n_q * s.hd) % 64) throw ConfigError("model dims must be multiples of 64");
   if (s.n_q % s.n_kv) throw ConfigError("n_q must be a multiple of n_kv");
+  if (tp_ > 1) {  // weights, KV pools and activations live in the per-rank shards
+    init_tp(seed, max_rows);
+    return;
+  }
   // ---- weights in one block ----
   const std::size_t d = s.d, V = s.vocab;
   std::vector<std::pair<void**, std::size_t>> tensors;
@@ -171,6 +176,7 @@ LlamaModel::~LlamaModel() {
 }
 
 void LlamaModel::ensure_rows(ForwardWorkspace& ws, int rows, int out_rows) const {
+  if (tp_ > 1) return ensure_tp(ws, rows, out_rows);
   if (rows <= ws.cap_rows && out_rows <= ws.cap_out) return;
   rows = std::max(rows, ws.cap_rows);
   out_rows = std::max(out_rows, ws.cap_out);
@@ -247,6 +253,68 @@ void LlamaModel::copy_slots(const std::vector<std::int32_t>& src, const std::vec
   WS_CUDA(cudaStreamSynchronize(st));
 }
 
+MetaLayout LlamaModel::pack_meta(const ForwardBatch& b, ForwardWorkspace& ws, cudaStream_t st) const {
+  const int n = static_cast<int>(b.tok.size());
+  const int n_out = static_cast<int>(b.out_rows.size());
+  // ---- one packed H2D for all metadata ----
+  // attention entries: one per CTA pass of attention_vectors_per_cta query vectors (a catch-up
+  // group larger than that becomes several entries; pad = its first vector)
+  const int G = s_.n_q / s_.n_kv;
+  const int vpc = attention_vectors_per_cta(s_.hd);
+  ws.grp_sorted.clear();
+  for (const AttnGroup& g : b.groups) {
+    ws.kv_pos += static_cast<std::uint64_t>(g.prefix_len + g.extra_len);
+    ws.attn_pairs += static_cast<std::uint64_t>(g.n_rows) * (g.prefix_len + g.extra_len);
+  }
+  for (const AttnGroup& g : b.groups)
+    for (int v0 = 0; v0 < g.n_rows * G; v0 += vpc) {
+      AttnGroup e = g;
+      e.pad = v0;
+      ws.grp_sorted.push_back(e);
+    }
+  const std::size_t s_tok = al(n * 4), s_grp = al(ws.grp_sorted.size() * sizeof(AttnGroup)), s_ext = al(b.extra.size() * 4 + 4),
+                    s_out = al(n_out * 4 + 4);
+  const std::size_t s_msk = al(b.row_mask.size() * 8 + 8);
+  const std::size_t need = 3 * s_tok + s_grp + s_ext + 2 * s_out + s_msk;
+  if (need > ws.cap_meta) {
+    if (ws.d_meta) cudaFree(ws.d_meta);
+    if (ws.h_meta) cudaFreeHost(ws.h_meta);
+    ws.cap_meta = std::max(need, 2 * ws.cap_meta);
+    WS_CUDA(cudaMalloc(&ws.d_meta, ws.cap_meta));
+    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ws.h_meta), ws.cap_meta, cudaHostAllocDefault));
+  }
+  WS_CUDA(cudaStreamSynchronize(st));  // previous use of the staging buffer retired
+  std::size_t o = 0;
+  auto put = [&](const void* src, std::size_t bytes, std::size_t slot_bytes) {
+    if (bytes) std::memcpy(ws.h_meta + o, src, bytes);
+    const std::size_t at = o;
+    o += slot_bytes;
+    return at;
+  };
+  const std::size_t o_tok = put(b.tok.data(), n * 4, s_tok);
+  const std::size_t o_pos = put(b.pos.data(), n * 4, s_tok);
+  const std::size_t o_slot = put(b.slot.data(), n * 4, s_tok);
+  const std::size_t o_grp = put(ws.grp_sorted.data(), ws.grp_sorted.size() * sizeof(AttnGroup), s_grp);
+  const std::size_t o_ext = put(b.extra.data(), b.extra.size() * 4, s_ext);
+  const std::size_t o_out = put(b.out_rows.data(), n_out * 4, s_out);
+  const std::size_t o_pl = put(b.plant.data(), b.plant.size() * 4, s_out);
+  const std::size_t o_msk = put(b.row_mask.data(), b.row_mask.size() * 8, s_msk);
+  WS_CUDA(cudaMemcpyAsync(ws.d_meta, ws.h_meta, o, cudaMemcpyHostToDevice, st));
+  ws.h2d += o;
+  MetaLayout ml;
+  ml.tok = o_tok;
+  ml.pos = o_pos;
+  ml.slot = o_slot;
+  ml.grp = o_grp;
+  ml.ext = o_ext;
+  ml.out = o_out;
+  ml.pl = o_pl;
+  ml.msk = o_msk;
+  ml.bytes = o;
+  ml.n_entries = static_cast<int>(ws.grp_sorted.size());
+  return ml;
+}
+
 void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, ForwardWorkspace& ws) {
   const int n = static_cast<int>(b.tok.size());
   const int n_out = static_cast<int>(b.out_rows.size());
@@ -254,6 +322,7 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
   if (b.pos.size() != b.tok.size() || b.slot.size() != b.tok.size()) throw std::invalid_argument("forward: ragged rows");
   for (std::int32_t p : b.pos)
     if (p < 0 || p >= kMaxPos) throw std::invalid_argument("forward: position out of the RoPE table range");
+  if (tp_ > 1) return forward_tp(b, plant, st, ws);
   ensure_rows(ws, n, n_out);
   float* const x_ = ws.x;
   void* const xb_ = ws.xb;
@@ -272,51 +341,9 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
   const int cap_rows_ = ws.cap_rows;
   void* const gemm_ws_ = ws.gemm_ws;
   const std::size_t gemm_ws_bytes_ = ws.gemm_ws_bytes;
-  // ---- one packed H2D for all metadata ----
-  // attention entries: one per CTA pass of attention_vectors_per_cta query vectors (a catch-up
-  // group larger than that becomes several entries; pad = its first vector)
-  const int G = s_.n_q / s_.n_kv;
-  const int vpc = attention_vectors_per_cta(s_.hd);
-  grp_sorted_.clear();
-  for (const AttnGroup& g : b.groups) {
-    ws.kv_pos += static_cast<std::uint64_t>(g.prefix_len + g.extra_len);
-    ws.attn_pairs += static_cast<std::uint64_t>(g.n_rows) * (g.prefix_len + g.extra_len);
-  }
-  for (const AttnGroup& g : b.groups)
-    for (int v0 = 0; v0 < g.n_rows * G; v0 += vpc) {
-      AttnGroup e = g;
-      e.pad = v0;
-      grp_sorted_.push_back(e);
-    }
-  const std::size_t s_tok = al(n * 4), s_grp = al(grp_sorted_.size() * sizeof(AttnGroup)), s_ext = al(b.extra.size() * 4 + 4),
-                    s_out = al(n_out * 4 + 4);
-  const std::size_t s_msk = al(b.row_mask.size() * 8 + 8);
-  const std::size_t need = 3 * s_tok + s_grp + s_ext + 2 * s_out + s_msk;
-  if (need > cap_meta_) {
-    if (d_meta_) cudaFree(d_meta_);
-    if (h_meta_) cudaFreeHost(h_meta_);
-    cap_meta_ = std::max(need, 2 * cap_meta_);
-    WS_CUDA(cudaMalloc(&d_meta_, cap_meta_));
-    WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_meta_), cap_meta_, cudaHostAllocDefault));
-  }
-  WS_CUDA(cudaStreamSynchronize(st));  // previous use of the staging buffer retired
-  std::size_t o = 0;
-  auto put = [&](const void* src, std::size_t bytes, std::size_t slot_bytes) {
-    if (bytes) std::memcpy(h_meta_ + o, src, bytes);
-    const std::size_t at = o;
-    o += slot_bytes;
-    return at;
-  };
-  const std::size_t o_tok = put(b.tok.data(), n * 4, s_tok);
-  const std::size_t o_pos = put(b.pos.data(), n * 4, s_tok);
-  const std::size_t o_slot = put(b.slot.data(), n * 4, s_tok);
-  const std::size_t o_grp = put(grp_sorted_.data(), grp_sorted_.size() * sizeof(AttnGroup), s_grp);
-  const std::size_t o_ext = put(b.extra.data(), b.extra.size() * 4, s_ext);
-  const std::size_t o_out = put(b.out_rows.data(), n_out * 4, s_out);
-  const std::size_t o_pl = put(b.plant.data(), b.plant.size() * 4, s_out);
-  const std::size_t o_msk = put(b.row_mask.data(), b.row_mask.size() * 8, s_msk);
-  WS_CUDA(cudaMemcpyAsync(d_meta_, h_meta_, o, cudaMemcpyHostToDevice, st));
-  h2d_ += o;
+  const MetaLayout ml = pack_meta(b, ws, st);
+  const std::size_t o_tok = ml.tok, o_pos = ml.pos, o_slot = ml.slot, o_grp = ml.grp, o_ext = ml.ext, o_out = ml.out,
+                    o_pl = ml.pl, o_msk = ml.msk;
   auto I = [&](std::size_t off) { return reinterpret_cast<const std::int32_t*>(d_meta_ + off); };
 
   const int d = s_.d, qd = s_.n_q * s_.hd;

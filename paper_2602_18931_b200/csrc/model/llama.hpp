@@ -74,6 +74,35 @@ class KernelProfiler {
 // Activation state of one caller's forwards: several callers (protocol threads, each with its
 // own streams) run forwards of the same model concurrently — weights and KV pools are shared,
 // these buffers are not.
+// Per-rank activation buffers of a tensor-parallel forward (llama_tp.cu): rank 0's live on the
+// workspace's device, the others on theirs; all are peer-accessible.
+struct TPActs {
+  struct Rank {
+    int device = 0;
+    cudaStream_t st = nullptr;  // rank 0: the caller's stream (not owned)
+    cudaEvent_t ev = nullptr;
+    float* x = nullptr;         // fp32 residual replica [cap][d]
+    void* xb = nullptr;         // bf16 replica [cap][d]
+    float* ss = nullptr;        // chunk statistics replica [d/32][cap]
+    float* part = nullptr;      // fp32 partial of the row-parallel projections [cap][d]
+    void* q = nullptr;          // local heads
+    void* attn = nullptr;
+    void* h = nullptr;          // local ffn slice
+    void* xo = nullptr;         // final-norm rows [cap_out][d]
+    unsigned char* d_meta = nullptr;
+    std::size_t cap_meta = 0;
+    unsigned long long* flags = nullptr;  // [2][kMaxTP] epochs (a: partial ready, b: broadcast done)
+    unsigned int* counter = nullptr;
+    void* gemm_ws = nullptr;
+    std::size_t gemm_ws_bytes = 0;
+  };
+  std::vector<Rank> r;
+  int cap = 0, cap_out = 0;
+  unsigned long long epoch = 0;
+  cudaEvent_t ev_in = nullptr;  // on the caller's stream: the ranks start after it
+  ~TPActs();
+};
+
 struct ForwardWorkspace {
   explicit ForwardWorkspace(int dev) : device(dev) {}
   ~ForwardWorkspace();
@@ -102,6 +131,13 @@ struct ForwardWorkspace {
   // rows x keys (an upper bound of the visible pairs; causal groups see about half their extras)
   std::uint64_t kv_pos = 0, attn_pairs = 0;
   KernelProfiler prof;
+  std::unique_ptr<TPActs> tp;  // tensor-parallel models only
+};
+
+// Offsets of one forward's packed metadata block (one H2D per forward and device).
+struct MetaLayout {
+  std::size_t tok = 0, pos = 0, slot = 0, grp = 0, ext = 0, out = 0, pl = 0, msk = 0, bytes = 0;
+  int n_entries = 0;
 };
 
 class LlamaModel {
@@ -109,7 +145,9 @@ class LlamaModel {
   KernelProfiler& profiler() { return ws0_->prof; }
   // Cap on the persistent GEMM grids (0 = every SM): leaves SMs to a concurrent forward.
   void set_max_ctas(int n) { max_ctas_ = n; }
-  LlamaModel(const LlamaShape& shape, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device);
+  // tp > 1: the target split over GPUs device .. device + tp - 1 (tensor parallel, llama_tp.cu)
+  LlamaModel(const LlamaShape& shape, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device, int tp = 1);
+  int tp() const { return tp_; }
   ~LlamaModel();
   LlamaModel(const LlamaModel&) = delete;
   LlamaModel& operator=(const LlamaModel&) = delete;
@@ -137,6 +175,14 @@ class LlamaModel {
 
  private:
   void ensure_rows(ForwardWorkspace& ws, int rows, int out_rows) const;
+  MetaLayout pack_meta(const ForwardBatch& b, ForwardWorkspace& ws, cudaStream_t st) const;
+  // tensor parallelism (llama_tp.cu)
+  struct TPShard;
+  void init_tp(std::uint64_t seed, int max_rows);
+  void ensure_tp(ForwardWorkspace& ws, int rows, int out_rows) const;
+  void forward_tp(const ForwardBatch& b, float plant, cudaStream_t st, ForwardWorkspace& ws);
+  int tp_ = 1;
+  std::vector<std::unique_ptr<TPShard>> shards_;
   std::unique_ptr<ForwardWorkspace> ws0_;  // the model's own workspace (test / single-caller API)
   int max_ctas_ = 0;
   LlamaShape s_;

@@ -209,7 +209,7 @@ ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(d
   const std::int64_t R = cfg.max_requests, C = cfg.max_ctx;
   max_rows_ = static_cast<int>(std::min<std::int64_t>(R * 20, 8192));
   draft_device_ = cfg.draft_device >= 0 ? cfg.draft_device : device;
-  target_.reset(new LlamaModel(ts, cfg.seed * 2 + 1, R * C, max_rows_, device));
+  target_.reset(new LlamaModel(ts, cfg.seed * 2 + 1, R * C, max_rows_, device, cfg.tp));
   draft_.reset(new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows_, draft_device_));
   WS_CUDA(cudaSetDevice(device));
   prompts_.resize(cfg.max_requests);

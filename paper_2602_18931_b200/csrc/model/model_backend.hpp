@@ -35,6 +35,7 @@ struct ModelPairCfg {
   float plant_draft = 16.f;
   float draft_plant_rate = 0.8f;   // fraction of input tokens whose plant the draft also sees
   int draft_device = -1;           // split placement: the draft model on another GPU (-1: same)
+  int tp = 1;                      // target tensor-parallel ranks (GPUs device .. device + tp - 1)
 };
 
 class ModelPair;
