@@ -46,8 +46,11 @@ def parse():
                         "target GPU r + draft GPU r + N/2; SURVEY §8e), 'shared' shards requests over all GPUs")
     p.add_argument("--cpu-sample-s", type=float, default=6.0)
     p.add_argument("--target", choices=["llama3-8b", "llama3-70b"], default="llama3-8b",
-                   help="llama: the target model shape; llama3-70b (BASELINE config 5's model) runs whole on "
-                        "one GPU per rank (141 GB of bf16 weights; use --requests 128), no tensor parallelism")
+                   help="llama: the target model shape; llama3-70b is BASELINE config 5's model (141 GB of "
+                        "bf16 weights; use --requests 128)")
+    p.add_argument("--tp", type=int, default=1,
+                   help="llama: tensor-parallel ranks of the target per process (BASELINE config 5): the "
+                        "process drives GPUs local_rank*tp .. +tp-1, the draft model sits on the last of them")
     return p.parse_args()
 
 
@@ -131,7 +134,10 @@ def tiny_cfg(args, world, rank):
 def config_block(args, world, host_threads):
     if args.workload == "llama":
         tname = {"llama3-8b": "Llama-3.1-8B", "llama3-70b": "Llama-3.1-70B"}[args.target]
-        return {"workload": ("BASELINE configs[2]: " if args.target == "llama3-8b" else
+        return {"workload": ("BASELINE configs[2]: " if args.target == "llama3-8b" and args.tp == 1 else
+                             f"BASELINE configs[4]: target tensor-parallel over {args.tp} GPUs per process "
+                             f"(peer-memory all-reduce fused into the residual update), draft on the last of them: "
+                             if args.tp > 1 else
                              "BASELINE configs[4]'s model, whole on one GPU per rank (no TP): ") +
                             f"{tname}-shape target / Llama-3.2-1B-shape draft "
                             "(random-init bf16), 128-token seeded prompts, 100 generated tokens, "
@@ -186,12 +192,15 @@ def unit_roofline(shape, fw, ms, rows, out_rows, kv_pos, attn_pairs, peak_bw, pe
     return out
 
 
-def llama_rooflines(rs, target, peak_bw, peak_tf):
+def llama_rooflines(rs, target, peak_bw, peak_tf, tp=1):
     """verify (the headline), prefill and draft units from ws_model_run_stats of the timed runs."""
     verify = unit_roofline(target, rs["verify_forwards"], rs["verify_ms"], rs["verify_rows"], rs["verify_out_rows"],
-                           rs["verify_kv_pos"], rs["verify_attn_pairs"], peak_bw, peak_tf)
+                           rs["verify_kv_pos"], rs["verify_attn_pairs"], peak_bw * tp, peak_tf * tp)
     prefill = unit_roofline(target, rs["prefill_forwards"], rs["prefill_target_ms"], rs["prefill_rows"], 0,
-                            rs["prefill_kv_pos"], rs["prefill_attn_pairs"], peak_bw, peak_tf, causal_half=True)
+                            rs["prefill_kv_pos"], rs["prefill_attn_pairs"], peak_bw * tp, peak_tf * tp,
+                            causal_half=True)
+    if tp > 1:
+        verify["gpus"] = prefill["gpus"] = tp
     draft = unit_roofline("llama3.2-1b", rs["draft_forwards"], rs["draft_ms"], rs["draft_rows"], rs["draft_out_rows"],
                           rs["draft_kv_pos"], rs["draft_attn_pairs"], peak_bw, peak_tf)
     return verify, prefill, draft
@@ -327,13 +336,14 @@ def main():
     import paper_2602_18931_b200 as ws
     from paper_2602_18931_b200 import abi
 
-    torch.cuda.set_device(local_rank)
+    dev0 = local_rank * max(1, args.tp)  # first GPU of this process (tensor-parallel ranks follow)
+    torch.cuda.set_device(dev0)
     dist = None
     host_group = None
     split = args.workload == "llama" and args.placement == "split" and world >= 2 and world % 2 == 0
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev0))
         if split:
             # Under split placement rank r's draft lane runs on rank r + N/2's GPU: the idle ranks
             # must not park an NCCL barrier kernel there (a second context on that GPU is
@@ -348,7 +358,7 @@ def main():
 
     ncpu = os.cpu_count() or 1
     host_threads = args.host_threads or max(1, min(16, ncpu // max(1, world)))
-    ctx = ws.Context(local_rank)
+    ctx = ws.Context(dev0)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     peak_bw, peak_tf, peak_kind = peaks()
 
@@ -360,8 +370,10 @@ def main():
             cfg = llama_cfg(args, world, rank)
         cfg.host_threads = max(1, args.shards)
         if active:
-            ctx.load_models(abi.model_cfg(target=args.target, max_requests=args.requests),
-                            draft_device=local_rank + world // 2 if split else -1)
+            ctx.load_models(abi.model_cfg(target=args.target, max_requests=args.requests, tp=args.tp),
+                            draft_device=(local_rank + world // 2 if split else
+                                          dev0 + int(os.environ.get("WS_TP_DRAFT_RANK", args.tp - 1))
+                                          if args.tp > 1 else -1))
 
         def run_once(tokens_out=False):
             return ctx.run_model_sim(cfg, with_tokens=tokens_out, with_steps=False)
@@ -379,7 +391,7 @@ def main():
     tokens, total_ms, launches, kernel_ms, h2d, d2h = 0, 0.0, 0, 0.0, 0, 0
     mstats = {}
     barrier()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev0) as clk:
         for _ in range(args.steps if active else 0):
             if args.workload == "tiny":
                 flush.fill_(1.0)
@@ -400,9 +412,9 @@ def main():
                     mstats[kk] = mstats.get(kk, 0) + v
     barrier()
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(dev0)
     stats = torch.tensor([total_ms, float(tokens), float(launches)], dtype=torch.float64,
-                         device="cpu" if host_group is not None else torch.device("cuda", local_rank))
+                         device="cpu" if host_group is not None else torch.device("cuda", dev0))
     if dist:
         mx, sm = stats.clone(), stats.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=host_group)
@@ -413,7 +425,7 @@ def main():
 
     if rank == 0:
         value = tokens_all / (total_ms_max / 1000.0)
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world * max(1, args.tp), "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong" if args.workload == "llama" else "weak", "vs_baseline": None,
                 "dtype": "bf16" if args.workload == "llama" else "f64", "data": "synthetic",
@@ -427,7 +439,8 @@ def main():
                                 "region, so value and e2e are one measurement"},
                 "gpu_launches": int(launches_all), "clocks": clk.summary()}
         if args.workload == "llama":
-            verify, prefill, draft = llama_rooflines(mstats, args.target, peak_bw, peak_tf)
+            # a tensor-parallel verify / prefill forward runs on tp GPUs: its roofline is tp x one GPU's
+            verify, prefill, draft = llama_rooflines(mstats, args.target, peak_bw, peak_tf, tp=args.tp)
             roof = dict(verify)
             traffic = None
             tpath = os.path.join(ROOT, "profiles", "r02_verify_traffic.json")

@@ -187,6 +187,11 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, Wait&& wait, int BN
     float* orow = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0;
     float4 cur[8], nxt[8];
     auto load = [&](int c, float4 (&v)[8]) {
+      if (nm.store_only) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+      }
       if (live && c + 32 <= ncols) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) v[q] = reinterpret_cast<const float4*>(orow + c)[q];
@@ -221,7 +226,7 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, Wait&& wait, int BN
           for (int j = 0; j < 32; ++j) {
             x[j] = 0.f;
             if (c + j < ncols) {
-              o[j] += __uint_as_float(r[j]);
+              o[j] = (nm.store_only ? 0.f : o[j]) + __uint_as_float(r[j]);
               x[j] = o[j];
             }
           }

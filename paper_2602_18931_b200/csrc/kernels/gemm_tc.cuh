@@ -38,6 +38,7 @@ struct NormEpi {
   const float* ss_in = nullptr;  // consumer: fp32 chunk-major [K / 32][ld_ss]
   int ld_ss = 0;
   float eps = 0.f;
+  int store_only = 0;            // kEpiAddF32: out = acc (no residual read) — TP partials
 };
 
 struct GemmArgs {

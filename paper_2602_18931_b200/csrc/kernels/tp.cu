@@ -38,29 +38,52 @@ __global__ void __launch_bounds__(kThreads) tp_allreduce_kernel(TPPeers p, int r
   const int r0 = static_cast<int>(static_cast<long long>(rows) * rank / p.tp);
   const int r1 = static_cast<int>(static_cast<long long>(rows) * (rank + 1) / p.tp);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int chunks = d / 32;
+  const int quads = d / 128;  // a warp covers 128 columns: lane = one float4, 8 lanes = one 32-column chunk
   float* xo = p.x[rank];
-  // one warp per (row, 32-column chunk): coalesced 128-byte reads of every rank's partial
+  const int gbase = lane & ~7;
   for (long long u = static_cast<long long>(blockIdx.x) * (kThreads / 32) + warp;
-       u < static_cast<long long>(r1 - r0) * chunks; u += static_cast<long long>(gridDim.x) * (kThreads / 32)) {
-    const int row = r0 + static_cast<int>(u / chunks);
-    const int c = static_cast<int>(u % chunks);
-    const std::size_t off = static_cast<std::size_t>(row) * d + c * 32 + lane;
-    float s = p.part[0][off];
-    for (int t = 1; t < p.tp; ++t) s += p.part[t][off];
-    const float v = xo[off] + s;
-    xo[off] = v;
-    // chunk statistic: a sequential fmaf chain in lane order (as embed_kernel)
+       u < static_cast<long long>(r1 - r0) * quads; u += static_cast<long long>(gridDim.x) * (kThreads / 32)) {
+    const int row = r0 + static_cast<int>(u / quads);
+    const int cq = static_cast<int>(u % quads);
+    const std::size_t off = static_cast<std::size_t>(row) * d + cq * 128 + lane * 4;
+    // every rank's partial in flight at once (NVLink reads for the peers), then the rank-ordered sum
+    float4 a[kMaxTP];
+#pragma unroll
+    for (int t = 0; t < kMaxTP; ++t)
+      if (t < p.tp) a[t] = *reinterpret_cast<const float4*>(p.part[t] + off);
+    const float4 xv = *reinterpret_cast<const float4*>(xo + off);
+    float4 s = a[0];
+#pragma unroll
+    for (int t = 1; t < kMaxTP; ++t)
+      if (t < p.tp) {
+        s.x += a[t].x;
+        s.y += a[t].y;
+        s.z += a[t].z;
+        s.w += a[t].w;
+      }
+    const float4 v = make_float4(xv.x + s.x, xv.y + s.y, xv.z + s.z, xv.w + s.w);
+    *reinterpret_cast<float4*>(xo + off) = v;
+    // the 32-column chunk statistic: a sequential fmaf chain in column order (as the GEMM's
+    // producer epilogue) over the 8 lanes of the chunk
     float q = 0.f;
-    for (int j = 0; j < 32; ++j) {
-      const float w = __shfl_sync(0xffffffffu, v, j);
-      q = fmaf(w, w, q);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float wx = __shfl_sync(0xffffffffu, v.x, gbase + j), wy = __shfl_sync(0xffffffffu, v.y, gbase + j);
+      const float wz = __shfl_sync(0xffffffffu, v.z, gbase + j), ww = __shfl_sync(0xffffffffu, v.w, gbase + j);
+      q = fmaf(wx, wx, q);
+      q = fmaf(wy, wy, q);
+      q = fmaf(wz, wz, q);
+      q = fmaf(ww, ww, q);
     }
-    const __nv_bfloat16 b = __float2bfloat16_rn(v);
+    const __nv_bfloat162 b01 = __floats2bfloat162_rn(v.x, v.y), b23 = __floats2bfloat162_rn(v.z, v.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<const unsigned int*>(&b01);
+    pk.y = *reinterpret_cast<const unsigned int*>(&b23);
+    const int chunk = cq * 4 + (lane >> 3);
     for (int t = 0; t < p.tp; ++t) {
-      static_cast<__nv_bfloat16*>(p.xb[t])[off] = b;
-      if (write_x_all && t != rank) p.x[t][off] = v;
-      if (lane == 0) p.ss[t][static_cast<std::size_t>(c) * ld_ss + row] = q;
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.xb[t]) + off) = pk;
+      if (write_x_all && t != rank) *reinterpret_cast<float4*>(p.x[t] + off) = v;
+      if ((lane & 7) == 0) p.ss[t][static_cast<std::size_t>(chunk) * ld_ss + row] = q;
     }
   }
   __threadfence_system();
@@ -121,10 +144,10 @@ __global__ void fill_2d_kernel(__nv_bfloat16* out, std::int64_t rows, std::int64
 void tp_allreduce_residual(const TPPeers& p, int rank, int rows, int d, int ld_ss, unsigned long long epoch,
                            bool write_x_all, cudaStream_t st) {
   if (p.tp < 2 || p.tp > kMaxTP || rank < 0 || rank >= p.tp) throw std::invalid_argument("tp_allreduce: bad rank");
-  if (d % 32) throw std::invalid_argument("tp_allreduce: d % 32");
+  if (d % 128) throw std::invalid_argument("tp_allreduce: d % 128");
   // every CTA must become resident while others spin: at most one wave (148 SMs)
   const int owned = (rows + p.tp - 1) / p.tp;
-  const long long units = static_cast<long long>(owned) * (d / 32);
+  const long long units = static_cast<long long>(owned) * (d / 128);
   int grid = static_cast<int>(std::min<long long>(148, (units + kThreads / 32 - 1) / (kThreads / 32)));
   if (grid < 1) grid = 1;
   launch_pdl(tp_allreduce_kernel, dim3(grid), dim3(kThreads), 0, st, 1, p, rank, rows, d, ld_ss, epoch,

@@ -441,7 +441,7 @@ void KernelProfiler::collect() {
 }
 const char* KernelProfiler::name(int cls) {
   static const char* n[] = {"embed", "rmsnorm", "gemm_qkv", "rope_kv_append", "attention", "gemm_o_add",
-                            "gemm_gate_up_swiglu", "gemm_down_add", "gemm_lm_head", "plant_bias"};
+                            "gemm_gate_up_swiglu", "gemm_down_add", "gemm_lm_head", "plant_bias", "tp_allreduce"};
   return cls >= 0 && cls < kClasses ? n[cls] : "?";
 }
 

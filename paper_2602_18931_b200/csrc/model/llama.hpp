@@ -53,7 +53,7 @@ struct ForwardBatch {
 // the model's stream (enabled by WS_PROFILE=1; used for the time-share tables in profiles/).
 class KernelProfiler {
  public:
-  enum Cls { kEmbed, kNorm, kQKV, kRope, kAttn, kO, kGateUp, kDown, kLMHead, kPlant, kClasses };
+  enum Cls { kEmbed, kNorm, kQKV, kRope, kAttn, kO, kGateUp, kDown, kLMHead, kPlant, kAllReduce, kClasses };
   void enable(bool on);
   bool on() const { return on_; }
   void begin(cudaStream_t st);

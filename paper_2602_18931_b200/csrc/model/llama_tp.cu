@@ -1,5 +1,5 @@
 // Tensor-parallel Llama target (BASELINE config 5: the Llama-3.1-70B shape over the GPUs of one
-// box). One host thread drives every rank's stream; rank 0 is the caller's GPU and
+// box). One host thread per rank submits that rank's stream; rank 0 is the caller's GPU and
 // stream, ranks 1.. the next GPUs. Per layer and rank:
 //   QKV GEMM (local heads; fused norm, RoPE, KV append into the rank's KV pool)
 //   -> attention over the local heads (K2)
@@ -18,7 +18,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <stdexcept>
+#include <thread>
 
 #include "../kernels/cuda_check.hpp"
 #include "../kernels/gemm_tc.cuh"
@@ -295,83 +297,91 @@ void LlamaModel::forward_tp(const ForwardBatch& b, float plant, cudaStream_t st,
     peers.flag_b[g] = A.r[g].flags + kMaxTP;
   }
   const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
-  for (int g = 0; g < P; ++g) {
-    DeviceGuard dg(A.r[g].device);
-    embed_rows(shards_[g]->embed, I(g, ml.tok), n, d, A.r[g].x, A.r[g].xb, A.r[g].ss, cap, A.r[g].st);
-  }
-  auto all_reduce = [&](bool last) {
-    const unsigned long long e = ++A.epoch;
-    for (int g = 0; g < P; ++g) {
-      DeviceGuard dg(A.r[g].device);
-      TPPeers p = peers;
-      p.counter = A.r[g].counter;
-      tp_allreduce_residual(p, g, n, d, cap, e, last, A.r[g].st);
-    }
-  };
-  for (int l = 0; l < s_.layers; ++l) {
-    for (int g = 0; g < P; ++g) {
-      const TPShard& sh = *shards_[g];
-      TPActs::Rank& q = A.r[g];
-      DeviceGuard dg(q.device);
-      const std::int64_t layer_stride = n_slots_ * sh.nkv * hd;
+  const unsigned long long epoch0 = A.epoch;
+  A.epoch += 2ull * s_.layers;  // two all-reduces per layer, the same epochs on every rank
+  // One host thread per rank submits that rank's whole layer stack (no device switching, a
+  // quarter of the launch latency each); the ranks meet only in the device-side all-reduces.
+  auto run_rank = [&](int g) {
+    const TPShard& sh = *shards_[g];
+    TPActs::Rank& q = A.r[g];
+    DeviceGuard dg(q.device);
+    TPPeers pg = peers;
+    pg.counter = q.counter;
+    const std::int64_t layer_stride = n_slots_ * sh.nkv * hd;
+    const int qkv_n = (sh.nq + 2 * sh.nkv) * hd, qd = sh.nq * hd;
+    NormEpi consume;
+    consume.ss_in = q.ss;
+    consume.ld_ss = cap;
+    consume.eps = s_.eps;
+    NormEpi store;
+    store.store_only = 1;  // the row-parallel partial overwrites its buffer
+    KernelProfiler* prof = g == 0 && ws.prof.on() ? &ws.prof : nullptr;  // rank 0's stream only
+    if (prof) prof->begin(q.st);
+    embed_rows(sh.embed, I(g, ml.tok), n, d, q.x, q.xb, q.ss, cap, q.st);
+    if (prof) prof->mark(KernelProfiler::kEmbed, q.st);
+    for (int l = 0; l < s_.layers; ++l) {
       __nv_bfloat16* kp = static_cast<__nv_bfloat16*>(sh.k_pool) + l * layer_stride;
       __nv_bfloat16* vp = static_cast<__nv_bfloat16*>(sh.v_pool) + l * layer_stride;
-      const int qkv_n = (sh.nq + 2 * sh.nkv) * hd, qd = sh.nq * hd;
-      NormEpi consume;
-      consume.ss_in = q.ss;
-      consume.ld_ss = cap;
-      consume.eps = s_.eps;
       GemmArgs qa{q.xb, sh.wqkv[l], nullptr, n, qkv_n, d, d, d, qkv_n, kEpiQKVRope, 0};
       qa.rope = RopeEpi{I(g, ml.pos), I(g, ml.slot), sh.rope_cs, q.q, kp, vp, sh.nq, sh.nkv, hd};
       qa.norm = consume;
       qa.max_ctas = max_ctas_;
       gemm_tn(qa, q.st);
+      if (prof) prof->mark(KernelProfiler::kQKV, q.st);
       attention(q.q, kp, vp, reinterpret_cast<const AttnGroup*>(meta(g) + ml.grp), ml.n_entries, I(g, ml.ext),
                 reinterpret_cast<const unsigned long long*>(meta(g) + ml.msk),
                 AttnShape{sh.nq, sh.nkv, hd, sh.nkv * hd, scale}, q.attn, q.st);
-      WS_CUDA(cudaMemsetAsync(q.part, 0, static_cast<std::size_t>(n) * d * 4, q.st));
+      if (prof) prof->mark(KernelProfiler::kAttn, q.st);
       GemmArgs oa{q.attn, sh.wo[l], q.part, n, d, qd, qd, qd, d, kEpiAddF32, 0};
+      oa.norm = store;
       oa.max_ctas = max_ctas_;
       gemm_tn(oa, q.st);
-    }
-    all_reduce(false);
-    for (int g = 0; g < P; ++g) {
-      const TPShard& sh = *shards_[g];
-      TPActs::Rank& q = A.r[g];
-      DeviceGuard dg(q.device);
-      NormEpi consume;
-      consume.ss_in = q.ss;
-      consume.ld_ss = cap;
-      consume.eps = s_.eps;
+      if (prof) prof->mark(KernelProfiler::kO, q.st);
+      tp_allreduce_residual(pg, g, n, d, cap, epoch0 + 2ull * l + 1, false, q.st);
+      if (prof) prof->mark(KernelProfiler::kAllReduce, q.st);
       GemmArgs ga{q.xb, sh.wgu[l], q.h, n, 2 * sh.ffn, d, d, d, sh.ffn, kEpiSwiGLU, 0};
       ga.norm = consume;
       ga.max_ctas = max_ctas_;
       gemm_tn(ga, q.st);
-      WS_CUDA(cudaMemsetAsync(q.part, 0, static_cast<std::size_t>(n) * d * 4, q.st));
+      if (prof) prof->mark(KernelProfiler::kGateUp, q.st);
       GemmArgs da{q.h, sh.wdown[l], q.part, n, d, sh.ffn, sh.ffn, sh.ffn, d, kEpiAddF32, 0};
+      da.norm = store;
       da.max_ctas = max_ctas_;
       gemm_tn(da, q.st);
+      if (prof) prof->mark(KernelProfiler::kDown, q.st);
+      tp_allreduce_residual(pg, g, n, d, cap, epoch0 + 2ull * l + 2, l + 1 == s_.layers, q.st);
+      if (prof) prof->mark(KernelProfiler::kAllReduce, q.st);
     }
-    all_reduce(l + 1 == s_.layers);
-  }
-  if (n_out > 0) {
-    for (int g = 0; g < P; ++g) {
-      const TPShard& sh = *shards_[g];
-      TPActs::Rank& q = A.r[g];
-      DeviceGuard dg(q.device);
+    if (n_out > 0) {
       rmsnorm_rows(q.x, d, I(g, ml.out), sh.final_norm, s_.eps, n_out, d, q.xo, d, q.st);
       // the rank's vocabulary slice, written into rank 0's logits (peer stores for g > 0)
       void* out = static_cast<__nv_bfloat16*>(ws.logits) + sh.v0;
       GemmArgs ha{q.xo, sh.lm_head, out, n_out, sh.vs, d, d, d, s_.vocab, kEpiBF16, 0};
       ha.max_ctas = max_ctas_;
       gemm_tn(ha, q.st);
+      if (prof) prof->mark(KernelProfiler::kLMHead, q.st);
     }
+    if (g > 0) WS_CUDA(cudaEventRecord(q.ev, q.st));
+  };
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(P);
+  for (int g = 1; g < P; ++g)
+    th.emplace_back([&, g] {
+      try {
+        run_rank(g);
+      } catch (...) {
+        err[g] = std::current_exception();
+      }
+    });
+  try {
+    run_rank(0);
+  } catch (...) {
+    err[0] = std::current_exception();
   }
-  for (int g = 1; g < P; ++g) {  // rank 0's stream (the caller's) covers every rank's work
-    DeviceGuard dg(A.r[g].device);
-    WS_CUDA(cudaEventRecord(A.r[g].ev, A.r[g].st));
-  }
-  DeviceGuard dg(device_);
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+  DeviceGuard dg(device_);  // rank 0's stream (the caller's) covers every rank's work
   for (int g = 1; g < P; ++g) WS_CUDA(cudaStreamWaitEvent(st, A.r[g].ev, 0));
   if (n_out > 0 && plant > 0.f && !b.plant.empty()) plant_bias(ws.logits, s_.vocab, I(0, ml.pl), plant, n_out, st);
 }
