@@ -299,6 +299,14 @@ int ws_model_export_trace(ws_ctx* ctx, uint32_t first_request, uint32_t n, uint3
 /* run_sim_full (sim.hpp:429-442) with the verify / draft model calls on the loaded models;
  * cfg->oracle supplies vocab_size (must equal the models'), eos_id and sequence_length. */
 int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out);
+/* Wall-clock mode (the reference's networked runtime, runtime.hpp:153-386, in-box): every
+ * request's controller and worker state machines run on the host against real time; model steps
+ * complete when their GPU work completes (not after t_target / t_draft); proposals and
+ * validations cross per-request host queues whose frames become visible rtt/2 (+/- jitter) after
+ * sending, FIFO-clamped (LatencyEmulator, net.hpp:149-163). metrics.latency is real µs.
+ * decision_log (may be NULL): an NDJSON controller decision log (DecisionLog, runtime.hpp:227-237,
+ * plus the model results) that a fresh state machine replays to the same decisions. */
+int ws_run_model_wallclock(ws_ctx* ctx, const ws_sim_cfg* cfg, ws_run_out* out, const char* decision_log);
 /* model-step timing of the last ws_run_model_sim: device ms and rows fed per model */
 int ws_model_stats(ws_ctx* ctx, double* target_ms, double* draft_ms, uint64_t* target_rows,
                    uint64_t* draft_rows, uint64_t* target_forwards, uint64_t* draft_forwards);

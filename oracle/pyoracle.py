@@ -255,6 +255,21 @@ def ref_run_sim_models(cfg, verify_fn, draft_fn, with_tokens=True, with_steps=Tr
     return bufs
 
 
+def ref_replay_model_log(cfg, path):
+    """The reference's controller state machine replaying a wall-clock decision log
+    (ref_shim.cpp ref_replay_model_log): (RunBuffers with the replayed streams / counters, turns)."""
+    bufs = abi.RunBuffers(cfg, True, False)
+    err = C.create_string_buffer(1024)
+    turns = C.c_uint64()
+    lib = ref_lib()
+    lib.ref_replay_model_log.argtypes = [C.POINTER(abi.SimCfg), C.c_char_p, C.POINTER(abi.RunOut),
+                                         C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]
+    rc = lib.ref_replay_model_log(C.byref(cfg), path.encode(), C.byref(bufs.out), C.byref(turns), err, 1024)
+    if rc != 0:
+        raise RuntimeError(f"ref_replay_model_log rc={rc}: {err.value.decode()}")
+    return bufs, turns.value
+
+
 def ref_run_sim_trace(cfg, path, threads=1, with_tokens=True, with_steps=True):
     """run_sim_full with the reference's trace oracle (OracleKind::trace) replaying `path`."""
     lib = ref_lib()

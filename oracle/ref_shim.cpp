@@ -44,6 +44,8 @@ extern "C" {
 }
 
 #include <atomic>
+#include <fstream>
+#include <optional>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -383,6 +385,152 @@ int ref_run_sim(const ws_sim_cfg* c, int threads, ws_run_out* out, char* err, st
   } catch (const wanspec::ConfigError& e) {
     set_err(err, errlen, e.what());
     return WS_ECONFIG;
+  } catch (const wanspec::ProtocolError& e) {
+    set_err(err, errlen, e.what());
+    return WS_EPROTO;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return WS_ELOGIC;
+  }
+}
+
+// Replays a wall-clock decision log (ws_run_model_wallclock, host/wallclock.hpp: one NDJSON
+// line per controller turn) through the REFERENCE's controller state machine, the way
+// replay_decision_log (runtime.hpp:404-454) replays a runtime recording: the same fold-in order
+// and clock readings, with the logged model results standing in for the oracle (real models
+// cannot be recomputed). Every step the reference launches must equal the logged launch (base +
+// candidate tokens, local-draft anchor + context), and t_update after every turn must match;
+// out receives the replayed committed streams and metrics of requests [first, first + local).
+// Returns WS_OK, or WS_EPROTO with the first divergence in err.
+int ref_replay_model_log(const ws_sim_cfg* c, const char* path, ws_run_out* out, std::uint64_t* turns, char* err,
+                         std::size_t errlen) {
+  try {
+    wanspec::SimConfig cfg = to_sim(c);
+    wanspec::ControllerConfig ccfg = cfg.controller_config();
+    const std::uint32_t local = c->local_requests ? c->local_requests : c->num_requests - c->first_request;
+    struct St {
+      wanspec::ControllerState st;
+      wanspec::ControllerDevices dev;
+      std::vector<wanspec::Message> inbox;
+      std::optional<wanspec::StepTarget> target;
+      std::optional<wanspec::StepDraftLocal> plan;
+      bool started = false;
+      explicit St(std::size_t mn) : st(mn) {}
+    };
+    std::vector<St> rs;
+    rs.reserve(local);
+    for (std::uint32_t i = 0; i < local; ++i) rs.emplace_back(cfg.max_nodes);
+    std::ifstream f(path);
+    if (!f) throw std::runtime_error(std::string("cannot open ") + path);
+    std::string line;
+    std::uint64_t n = 0;
+    auto fail = [&](const std::string& what) {
+      throw wanspec::ProtocolError("turn " + std::to_string(n) + ": " + what);
+    };
+    while (std::getline(f, line)) {
+      if (line.empty()) continue;
+      const nlohmann::json j = nlohmann::json::parse(line);
+      const std::uint32_t r = j.at("r").get<std::uint32_t>();
+      if (r < c->first_request || r >= c->first_request + local) fail("request outside the shard");
+      St& q = rs[r - c->first_request];
+      const wanspec::SimTime now = j.at("now").get<wanspec::SimTime>();
+      if (j.contains("start")) {
+        q.st.reset(r, j.at("start").get<wanspec::SimTime>(), cfg.max_nodes);
+        q.dev = {};
+        q.inbox.clear();
+        q.started = true;
+      }
+      if (!q.started) fail("turn before the request start");
+      for (const auto& fr : j.at("frames")) {
+        wanspec::Message m;
+        m.request_id = r;
+        m.seq_no = fr.at("seq").get<std::uint64_t>();
+        if (fr.at("kind").get<int>() != 2) fail("controller frame is not a speculation");
+        wanspec::SpeculationMsg sm;
+        sm.base = fr.at("base").get<std::uint64_t>();
+        sm.path = fr.at("path").get<std::vector<wanspec::TokenId>>();
+        for (const auto& cd : fr.at("cands"))
+          sm.candidates.push_back({cd.at(0).get<wanspec::TokenId>(), cd.at(1).get<double>(), cd.at(2).get<double>()});
+        m.body = std::move(sm);
+        q.inbox.push_back(std::move(m));
+      }
+      if (j.contains("target")) {
+        const auto& t = j.at("target");
+        q.dev.target_busy = false;
+        if (!q.target || q.target->base != t.at("base").get<std::uint64_t>() ||
+            q.target->tokens() != t.at("tokens").get<std::vector<wanspec::TokenId>>())
+          fail("target completion does not match the step the reference launched");
+        const auto tokens = q.target->tokens();
+        wanspec::ValidationResult v;
+        const std::size_t a = t.at("accepted").get<std::size_t>();
+        v.accepted.assign(tokens.begin(), tokens.begin() + a);
+        v.bonus_token = t.at("bonus").get<wanspec::TokenId>();
+        v.final_entropy = t.at("h").get<double>();
+        wanspec::apply_target_result(q.st, ccfg, v, now);
+        q.target.reset();
+      }
+      if (j.contains("local")) {
+        const auto& l = j.at("local");
+        q.dev.draft_busy = false;
+        if (!q.plan || q.plan->anchor != l.at("anchor").get<std::uint64_t>() ||
+            q.plan->context != l.at("context").get<std::vector<wanspec::TokenId>>())
+          fail("local-draft completion does not match the plan the reference launched");
+        const auto& pj = l.at("pred");
+        wanspec::Prediction p;
+        const std::uint32_t np = pj.at("n").get<std::uint32_t>();
+        for (std::uint32_t i = 0; i < np && i < 2; ++i)
+          p.top_candidates.push_back({pj.at("id").at(i).get<wanspec::TokenId>(), pj.at("prob").at(i).get<double>()});
+        p.entropy = pj.at("h").get<double>();
+        wanspec::apply_local_draft(q.st, ccfg, *q.plan, p);
+        q.plan.reset();
+      }
+      if (q.st.t_update != j.at("t_update").get<wanspec::SimTime>()) fail("t_update differs");
+      std::vector<nlohmann::json> launched;
+      if (!q.st.finished) {
+        for (;;) {
+          wanspec::ControllerAction act = wanspec::controller_poll(q.st, ccfg, now, q.inbox, q.dev);
+          q.inbox.clear();
+          if (auto* t = std::get_if<wanspec::StepTarget>(&act)) {
+            q.dev.target_busy = true;
+            launched.push_back({{"target", {{"base", t->base}, {"tokens", t->tokens()}}}});
+            q.target = std::move(*t);
+          } else if (auto* d = std::get_if<wanspec::StepDraftLocal>(&act)) {
+            q.dev.draft_busy = true;
+            launched.push_back({{"local", {{"anchor", d->anchor}, {"context", d->context}}}});
+            q.plan = std::move(*d);
+          } else {
+            break;
+          }
+        }
+      }
+      if (nlohmann::json(launched) != j.at("launch")) fail("launch decisions differ: " + nlohmann::json(launched).dump());
+      ++n;
+    }
+    if (turns) *turns = n;
+    if (out) {
+      for (std::uint32_t i = 0; i < local; ++i) {
+        const auto& st = rs[i].st;
+        if (out->metrics) {
+          ws_request_metrics m{};
+          m.tokens_committed = st.committed.size();
+          m.target_steps = st.counters.target_steps;
+          m.ctrl_draft_passes = st.counters.draft_passes;
+          m.ctrl_local_draft_steps = st.counters.local_draft_steps;
+          m.ctrl_catchup_batches = st.counters.catchup_batches;
+          m.sync_stalls = st.counters.sync_stalls;
+          m.entropy_resets = st.counters.entropy_resets;
+          m.stale_specs = st.counters.stale_specs_dropped;
+          out->metrics[i] = m;
+        }
+        if (out->ctrl_len) {
+          out->ctrl_len[i] = static_cast<std::uint32_t>(st.committed.size());
+          if (out->ctrl_tokens)
+            for (std::size_t t = 0; t < st.committed.size() && t < out->max_len; ++t)
+              out->ctrl_tokens[static_cast<std::size_t>(i) * out->max_len + t] = st.committed[t];
+        }
+      }
+    }
+    return WS_OK;
   } catch (const wanspec::ProtocolError& e) {
     set_err(err, errlen, e.what());
     return WS_EPROTO;

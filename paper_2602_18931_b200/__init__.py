@@ -178,6 +178,14 @@ class Context:
         _check(lib().ws_run_model_sim(self._h, C.byref(cfg), C.byref(bufs.out)))
         return bufs
 
+    def run_model_wallclock(self, cfg, decision_log=None, with_tokens=True, with_steps=True):
+        """Wall-clock mode (ws_run_model_wallclock): real time, GPU completions, injected RTT/2
+        queues; optional NDJSON decision log for the reference replay."""
+        bufs = abi.RunBuffers(cfg, with_tokens, with_steps)
+        _check(lib().ws_run_model_wallclock(self._h, C.byref(cfg), C.byref(bufs.out),
+                                            decision_log.encode() if decision_log else None))
+        return bufs
+
     def model_stats(self):
         v = [C.c_double(), C.c_double(), C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()]
         _check(lib().ws_model_stats(self._h, *[C.byref(x) for x in v]))

@@ -67,11 +67,30 @@ int ws_model_load_split(ws_ctx* ctx, const ws_model_cfg* c, int draft_device) {
   });
 }
 
+namespace {
+void run_model(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out, bool wallclock, const char* log_path);
+}
+
 int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
-  return guard("ws_run_model_sim", [&] {
+  return guard("ws_run_model_sim", [&] { run_model(ctx, c, out, false, nullptr); });
+}
+
+int ws_run_model_wallclock(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out, const char* decision_log) {
+  return guard("ws_run_model_wallclock", [&] { run_model(ctx, c, out, true, decision_log); });
+}
+
+}  // extern "C"
+
+namespace {
+void run_model(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out, bool wallclock, const char* log_path) {
+  {
     if (!ctx || !c) throw std::invalid_argument("null argument");
     if (!ctx->models) throw wsb::ConfigError("no model loaded (ws_model_load)");
-    const wsb::SimCfg cfg = wsb::sim_cfg_from_abi(*c);
+    wsb::SimCfg cfg = wsb::sim_cfg_from_abi(*c);
+    cfg.wallclock = wallclock;
+    if (log_path) cfg.decision_log = log_path;
+    if (wallclock && c->host_threads > 1 && log_path && *log_path)
+      throw wsb::ConfigError("wall-clock decision log: one protocol thread only");
     wsb::ModelPair& mp = *ctx->models;
     const auto& mc = mp.cfg();
     if (c->oracle.vocab_size != static_cast<std::uint32_t>(mp.target().shape().vocab))
@@ -171,8 +190,11 @@ int ws_run_model_sim(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out) {
         std::fprintf(stderr, "[ws] host ms: submit verify %.1f, submit draft %.1f, wait %.1f\n", bk->host_submit_ms[0],
                      bk->host_submit_ms[1], bk->host_wait_ms);
     }
-  });
+  }
 }
+}  // namespace
+
+extern "C" {
 
 int ws_model_export_trace(ws_ctx* ctx, uint32_t first_request, uint32_t n, uint32_t length, ws_token_record* out) {
   return guard("ws_model_export_trace", [&] {

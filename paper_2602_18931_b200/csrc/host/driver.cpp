@@ -1,6 +1,7 @@
 // Batched event driver; RequestRun restates RequestSim (sim.hpp:166-416) with the model-call
 // seam turned into launch-time jobs (see driver.hpp).
 #include "driver.hpp"
+#include "wallclock.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -569,6 +570,10 @@ void ModelBackend::complete(int, RoundResults&) { throw std::logic_error("backen
 
 void run_requests(const SimCfg& cfg, const std::uint32_t* requests, std::size_t n,
                   ModelBackend& backend, RequestOutput* outs, bool log_steps) {
+  if (cfg.wallclock) {
+    run_requests_wallclock(cfg, requests, n, backend, outs, cfg.decision_log, nullptr);
+    return;
+  }
   static const bool lockstep = std::getenv("WS_LOCKSTEP") != nullptr;  // A/B switch for the bench
   if (backend.has_lanes() && !lockstep) {
     run_requests_lanes(cfg, requests, n, backend, outs, log_steps);

@@ -14,6 +14,7 @@
 
 #include <cstdint>
 #include <random>
+#include <string>
 #include <vector>
 
 namespace wsb {
@@ -30,6 +31,9 @@ struct SimCfg {
   std::uint64_t sample_seed = 0;
   std::uint64_t oracle_seed = 1;
   TokenId eos = 32767;
+  // wall-clock mode (host/wallclock.hpp): real time, GPU completions, injected RTT queues
+  bool wallclock = false;
+  std::string decision_log;  // NDJSON decision log path ("" = none; one file per protocol thread)
 
   ControllerCfg controller_cfg() const;  // sim.hpp:54-68
   WorkerCfg worker_cfg() const;          // sim.hpp:70-79
@@ -101,6 +105,7 @@ class ModelBackend {
   // backend may trim a batch to a tile-friendly size).
   virtual std::size_t submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed);
   virtual int wait_any(std::uint32_t busy_lanes);      // blocks until a busy lane (bit) is done
+  virtual int poll_any(std::uint32_t busy_lanes) { return wait_any(busy_lanes); }  // -1: none done yet
   virtual void complete(int lane, RoundResults& res);  // fills res.verify (lane 0) / res.draft
   BackendStats stats;
 };

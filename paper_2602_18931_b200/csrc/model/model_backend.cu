@@ -960,6 +960,18 @@ void ModelBackend_Llama::verify_rows(ws_pred* host, std::size_t n_rows) {
   WS_CUDA(cudaMemcpy(host, L.d_pred, n_rows * sizeof(ws_pred), cudaMemcpyDeviceToHost));
 }
 
+int ModelBackend_Llama::poll_any(std::uint32_t busy) {
+  Lanes& L = *ln_;
+  for (int lane = 0; lane < n_lanes(); ++lane) {
+    if (!(busy & (1u << lane))) continue;
+    DeviceGuard dg(lane == 0 ? L.device : L.device_d);
+    const cudaError_t e = cudaEventQuery(lane == 0 ? L.done : L.dl[lane - 1]->done);
+    if (e == cudaSuccess) return lane;
+    if (e != cudaErrorNotReady) WS_CUDA(e);
+  }
+  return -1;
+}
+
 void ModelBackend_Llama::complete(int lane, RoundResults& res) {
   Lanes& L = *ln_;
   DeviceGuard dg(lane == 0 ? L.device : L.device_d);

@@ -51,6 +51,7 @@ class ModelBackend_Llama : public ModelBackend {
   int n_lanes() const override;
   std::size_t submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed) override;
   int wait_any(std::uint32_t busy) override;
+  int poll_any(std::uint32_t busy) override;
   void complete(int lane, RoundResults& res) override;
   KernelProfiler& profiler(int lane);  // lane 0: target forwards; lanes 1..n: draft forwards
   // After complete(0): the per-row predictions (top-2 + entropy, K3) of the last verify batch,
