@@ -39,6 +39,8 @@ std::vector<Message> hooked_apply_draft_output(WorkerState& st, const WorkerConf
 #undef apply_local_draft
 #undef apply_draft_output
 
+#include "wanspec/experiment.hpp"  // after sim.hpp: its model seams stay the hooked ones (inert here)
+
 extern "C" {
 #include "restate.h"
 }
@@ -537,6 +539,29 @@ int ref_replay_model_log(const ws_sim_cfg* c, const char* path, ws_run_out* out,
   } catch (const std::exception& e) {
     set_err(err, errlen, e.what());
     return WS_ELOGIC;
+  }
+}
+
+// The reference's experiment front-end end to end (experiment.hpp): parse_experiment on `text`,
+// run_experiment with `seed` as the effective seed, and its three renderings.
+int ref_experiment(const char* text, std::uint64_t seed, char* csv, std::size_t csv_len, char* per_seed,
+                   std::size_t ps_len, char* manifest, std::size_t m_len, char* err, std::size_t errlen) {
+  try {
+    wanspec::ExperimentConfig cfg = wanspec::parse_experiment(text);
+    wanspec::ExperimentResult r = wanspec::run_experiment(cfg, seed, 1);
+    const std::string a = wanspec::render_csv(r), b = wanspec::render_per_seed_csv(r),
+                      c = wanspec::render_manifest(r);
+    if (a.size() >= csv_len || b.size() >= ps_len || c.size() >= m_len) throw std::runtime_error("buffer too small");
+    std::memcpy(csv, a.c_str(), a.size() + 1);
+    std::memcpy(per_seed, b.c_str(), b.size() + 1);
+    std::memcpy(manifest, c.c_str(), c.size() + 1);
+    return WS_OK;
+  } catch (const wanspec::ParseError& e) {
+    set_err(err, errlen, e.what());
+    return WS_EPARSE;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return WS_ECONFIG;
   }
 }
 
