@@ -389,6 +389,41 @@ int ws_model_forward(ws_model* m, int n_rows, const int32_t* tok, const int32_t*
                      const int32_t* extra, const uint64_t* row_mask, int n_out,
                      const int32_t* out_rows, void* logits_out, void* stream);
 
+/* ---- wire framing (wire.hpp:149-323, docs/protocol.md) ----
+ * The reference's frame format for the protocol messages (big-endian u32 length, kind tag, then
+ * the kind's fields), for a cross-host deployment; in-box, the wall-clock driver carries these
+ * exact frames on its RTT queues. Speculations carry at most two candidates (the worker's top-2,
+ * worker.hpp:121-125) and validations at most WS_WIRE_MAX_ACCEPTED accepted tokens. */
+#define WS_MSG_HELLO 1
+#define WS_MSG_SPECULATION 2
+#define WS_MSG_VALIDATION 3
+#define WS_MSG_EOS 4
+#define WS_MSG_BYE 5
+#define WS_WIRE_MAX_PATH 1024
+#define WS_WIRE_MAX_ACCEPTED 255
+#define WS_WIRE_NEED_MORE 1  /* ws_wire_decode: the frame is truncated */
+typedef struct ws_wire_msg {
+  uint32_t kind;                            /* WS_MSG_* */
+  uint32_t n_path;                          /* speculation */
+  uint64_t request_id, seq_no, base;
+  uint64_t config_digest;                   /* hello */
+  uint64_t final_length;                    /* eos */
+  uint32_t n_cands;                         /* speculation: 1 or 2 */
+  uint32_t cand_token[2];
+  double cand_prob[2], cand_entropy[2];
+  uint32_t n_accepted, bonus;               /* validation */
+  double final_entropy;
+  uint32_t path[WS_WIRE_MAX_PATH];
+  uint32_t accepted[WS_WIRE_MAX_ACCEPTED];
+  uint32_t pad;
+} ws_wire_msg;
+/* Encodes one frame into out[0, cap); *len = its size (WS_EARG when cap is too small). */
+int ws_wire_encode(const ws_wire_msg* m, uint8_t* out, size_t cap, size_t* len);
+/* Decodes the frame at the head of bytes[0, n) (decode_frame, wire.hpp:198-280): WS_OK with
+ * *consumed = its size, WS_WIRE_NEED_MORE on truncation, WS_EPROTO on a malformed frame (bad tag,
+ * length outside (0, 1 MiB], short or overlong payload; ws_last_error has the reason). */
+int ws_wire_decode(const uint8_t* bytes, size_t n, ws_wire_msg* out, size_t* consumed);
+
 /* ---- host-logic seam (tests / alternative model providers) ----
  * The batched driver with the model round supplied by the caller instead of the GPU: one
  * callback per round receives every pending verify job and draft row, exactly what the K9

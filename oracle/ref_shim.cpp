@@ -565,6 +565,79 @@ int ref_experiment(const char* text, std::uint64_t seed, char* csv, std::size_t 
   }
 }
 
+// The reference's wire codec (wire.hpp:149-280) over the flat ws_wire_msg.
+int ref_wire_encode(const ws_wire_msg* m, std::uint8_t* out, std::size_t cap, std::size_t* len) {
+  wanspec::Message msg;
+  msg.request_id = m->request_id;
+  msg.seq_no = m->seq_no;
+  switch (m->kind) {
+    case WS_MSG_HELLO: msg.body = wanspec::HelloMsg{m->config_digest}; break;
+    case WS_MSG_SPECULATION: {
+      wanspec::SpeculationMsg sm;
+      sm.base = m->base;
+      sm.path.assign(m->path, m->path + m->n_path);
+      for (std::uint32_t i = 0; i < m->n_cands; ++i)
+        sm.candidates.push_back({m->cand_token[i], m->cand_prob[i], m->cand_entropy[i]});
+      msg.body = std::move(sm);
+      break;
+    }
+    case WS_MSG_VALIDATION: {
+      wanspec::ValidationMsg v;
+      v.base = m->base;
+      v.result.accepted.assign(m->accepted, m->accepted + m->n_accepted);
+      v.result.bonus_token = m->bonus;
+      v.result.final_entropy = m->final_entropy;
+      msg.body = std::move(v);
+      break;
+    }
+    case WS_MSG_EOS: msg.body = wanspec::EosMsg{m->final_length}; break;
+    default: msg.body = wanspec::ByeMsg{}; break;
+  }
+  const std::vector<std::uint8_t> f = wanspec::encode(msg);
+  if (f.size() > cap) return WS_EARG;
+  std::memcpy(out, f.data(), f.size());
+  *len = f.size();
+  return WS_OK;
+}
+
+// decode_frame (wire.hpp:198-280): WS_OK / WS_WIRE_NEED_MORE / WS_EPROTO (+ message in err).
+int ref_wire_decode(const std::uint8_t* bytes, std::size_t n, ws_wire_msg* out, std::size_t* consumed, char* err,
+                    std::size_t errlen) {
+  const wanspec::Decoded d = wanspec::decode_frame(std::span<const std::uint8_t>(bytes, n));
+  if (d.status == wanspec::DecodeStatus::need_more) return WS_WIRE_NEED_MORE;
+  if (d.status == wanspec::DecodeStatus::error) {
+    set_err(err, errlen, ("wire: " + d.error).c_str());
+    return WS_EPROTO;
+  }
+  std::memset(out, 0, sizeof(*out));
+  const wanspec::Message& m = d.message;
+  out->kind = static_cast<std::uint32_t>(m.kind());
+  out->request_id = m.request_id;
+  out->seq_no = m.seq_no;
+  if (const auto* h = std::get_if<wanspec::HelloMsg>(&m.body)) out->config_digest = h->config_digest;
+  if (const auto* sm = std::get_if<wanspec::SpeculationMsg>(&m.body)) {
+    out->base = sm->base;
+    out->n_path = static_cast<std::uint32_t>(sm->path.size());
+    std::copy(sm->path.begin(), sm->path.end(), out->path);
+    out->n_cands = static_cast<std::uint32_t>(sm->candidates.size());
+    for (std::size_t i = 0; i < sm->candidates.size() && i < 2; ++i) {
+      out->cand_token[i] = sm->candidates[i].token;
+      out->cand_prob[i] = sm->candidates[i].prob;
+      out->cand_entropy[i] = sm->candidates[i].entropy;
+    }
+  }
+  if (const auto* v = std::get_if<wanspec::ValidationMsg>(&m.body)) {
+    out->base = v->base;
+    out->n_accepted = static_cast<std::uint32_t>(v->result.accepted.size());
+    std::copy(v->result.accepted.begin(), v->result.accepted.end(), out->accepted);
+    out->bonus = v->result.bonus_token;
+    out->final_entropy = v->result.final_entropy;
+  }
+  if (const auto* e = std::get_if<wanspec::EosMsg>(&m.body)) out->final_length = e->final_length;
+  *consumed = d.consumed;
+  return WS_OK;
+}
+
 // Trace oracle selection for ref_run_sim / ref_trace_deal (nullptr or "" = stochastic).
 void ref_set_trace_path(const char* path) { g_trace_path = path ? path : ""; }
 

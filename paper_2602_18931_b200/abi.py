@@ -259,3 +259,13 @@ class ModelJob(C.Structure):
     _fields_ = [("request", C.c_uint32), ("kind", C.c_uint32), ("n_committed", C.c_uint32), ("len", C.c_uint32),
                 ("off", C.c_uint64)]
 
+
+class WireMsg(C.Structure):
+    """ws_wire_msg (include/wanspec_b200.h): one protocol message, flat."""
+    _fields_ = [("kind", C.c_uint32), ("n_path", C.c_uint32), ("request_id", C.c_uint64), ("seq_no", C.c_uint64),
+                ("base", C.c_uint64), ("config_digest", C.c_uint64), ("final_length", C.c_uint64),
+                ("n_cands", C.c_uint32), ("cand_token", C.c_uint32 * 2), ("cand_prob", C.c_double * 2),
+                ("cand_entropy", C.c_double * 2), ("n_accepted", C.c_uint32), ("bonus", C.c_uint32),
+                ("final_entropy", C.c_double), ("path", C.c_uint32 * 1024), ("accepted", C.c_uint32 * 255),
+                ("pad", C.c_uint32)]
+

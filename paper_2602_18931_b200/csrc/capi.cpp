@@ -19,6 +19,7 @@
 #include "kernels/k9_oracle.cuh"
 
 #include "context.hpp"
+#include "host/wire.hpp"
 
 namespace {
 
@@ -267,6 +268,70 @@ void run_shard_threads(const ws_sim_cfg* c, const SimCfg& cfg, const std::vector
 extern "C" {
 
 int ws_abi_version(void) { return WS_ABI_VERSION; }
+
+int ws_wire_encode(const ws_wire_msg* m, uint8_t* out, size_t cap, size_t* len) {
+  return guarded([&] {
+    need(m && out && len, "ws_wire_encode: null argument");
+    if (m->kind < WS_MSG_HELLO || m->kind > WS_MSG_BYE) throw std::invalid_argument("ws_wire_encode: bad kind");
+    if (m->n_path > WS_WIRE_MAX_PATH || m->n_cands > 2 || m->n_accepted > WS_WIRE_MAX_ACCEPTED)
+      throw std::invalid_argument("ws_wire_encode: field count out of range");
+    wsb::Message msg;
+    msg.kind = static_cast<wsb::MsgKind>(m->kind);
+    msg.request_id = m->request_id;
+    msg.seq_no = m->seq_no;
+    msg.base = m->base;
+    msg.config_digest = m->config_digest;
+    msg.final_length = m->final_length;
+    msg.path.assign(m->path, m->path + m->n_path);
+    msg.n_cands = m->n_cands;
+    for (uint32_t i = 0; i < m->n_cands; ++i) msg.cands[i] = wsb::CandIn{m->cand_token[i], m->cand_prob[i], m->cand_entropy[i]};
+    msg.result.accepted.assign(m->accepted, m->accepted + m->n_accepted);
+    msg.result.bonus = m->bonus;
+    msg.result.final_entropy = m->final_entropy;
+    std::vector<std::uint8_t> buf;
+    wsb::wire_encode(msg, buf);
+    if (buf.size() > cap) throw std::invalid_argument("ws_wire_encode: output buffer too small");
+    std::memcpy(out, buf.data(), buf.size());
+    *len = buf.size();
+  });
+}
+
+int ws_wire_decode(const uint8_t* bytes, size_t n, ws_wire_msg* out, size_t* consumed) {
+  bool more = false;
+  const int rc = guarded([&] {
+    need((bytes || n == 0) && out && consumed, "ws_wire_decode: null argument");
+    const wsb::Decoded d = wsb::wire_decode_frame(bytes, n);
+    if (d.status == wsb::DecodeStatus::need_more) {
+      more = true;
+      *consumed = 0;
+      return;
+    }
+    if (d.status == wsb::DecodeStatus::error) throw wsb::ProtocolError("wire: " + d.error);
+    const wsb::Message& m = d.message;
+    if (m.path.size() > WS_WIRE_MAX_PATH) throw wsb::ProtocolError("wire: path longer than WS_WIRE_MAX_PATH");
+    std::memset(out, 0, sizeof(*out));
+    out->kind = static_cast<uint32_t>(m.kind);
+    out->request_id = m.request_id;
+    out->seq_no = m.seq_no;
+    out->base = m.base;
+    out->config_digest = m.config_digest;
+    out->final_length = m.final_length;
+    out->n_path = static_cast<uint32_t>(m.path.size());
+    std::copy(m.path.begin(), m.path.end(), out->path);
+    out->n_cands = m.n_cands;
+    for (uint32_t i = 0; i < m.n_cands; ++i) {
+      out->cand_token[i] = m.cands[i].token;
+      out->cand_prob[i] = m.cands[i].prob;
+      out->cand_entropy[i] = m.cands[i].entropy;
+    }
+    out->n_accepted = static_cast<uint32_t>(m.result.accepted.size());
+    std::copy(m.result.accepted.begin(), m.result.accepted.end(), out->accepted);
+    out->bonus = m.result.bonus;
+    out->final_entropy = m.result.final_entropy;
+    *consumed = d.consumed;
+  });
+  return rc == WS_OK && more ? WS_WIRE_NEED_MORE : rc;
+}
 
 const char* ws_last_error(void) { return g_err.c_str(); }
 

@@ -74,6 +74,7 @@ struct Message {
   std::uint32_t n_cands = 0;
   Validation result;               // validation
   std::uint64_t final_length = 0;  // eos
+  std::uint64_t config_digest = 0; // hello (wire.hpp:32-34)
 };
 
 }  // namespace wsb

@@ -1,6 +1,8 @@
 // Wall-clock driver (see wallclock.hpp).
 #include "wallclock.hpp"
 
+#include "wire.hpp"
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -35,9 +37,11 @@ struct LatencyEmulator {
   }
 };
 
+// A message in flight: its wire frame (host/wire.hpp, the reference's encoding) and the
+// instant it becomes visible at the receiver.
 struct Frame {
   SimTime visible = 0;
-  Message msg;
+  std::vector<std::uint8_t> bytes;
 };
 
 // ---- decision-log NDJSON (read back by oracle/ref_shim.cpp ref_replay_model_log) ----
@@ -121,12 +125,18 @@ class WallRequest {
     // frames that became visible
     std::vector<Message> new_ctrl;
     while (!to_ctrl_.empty() && to_ctrl_.front().visible <= now) {
-      new_ctrl.push_back(std::move(to_ctrl_.front().msg));
+      const std::vector<std::uint8_t>& b = to_ctrl_.front().bytes;
+      rd_ctrl_.feed(b.data(), b.size());  // the receiver's frame reader (FIFO seq check)
       to_ctrl_.pop_front();
+      Message m;
+      while (rd_ctrl_.next(m)) new_ctrl.push_back(std::move(m));
     }
     while (!to_wrk_.empty() && to_wrk_.front().visible <= now) {
-      Message m = std::move(to_wrk_.front().msg);
+      const std::vector<std::uint8_t>& b = to_wrk_.front().bytes;
+      rd_wrk_.feed(b.data(), b.size());
       to_wrk_.pop_front();
+      Message m;
+      if (!rd_wrk_.next(m)) continue;
       if (m.kind == MsgKind::hello)
         worker_started_ = true;
       else
@@ -188,11 +198,15 @@ class WallRequest {
   void send_to_worker(Message&& m, SimTime now) {
     if (cfg_.baseline) return;
     m.seq_no = ++seq_to_worker_;
-    to_wrk_.push_back(Frame{to_wrk_emu_.visible_at(now), std::move(m)});
+    Frame f{to_wrk_emu_.visible_at(now), {}};
+    wire_encode(m, f.bytes);
+    to_wrk_.push_back(std::move(f));
   }
   void send_to_ctrl(Message&& m, SimTime now) {
     m.seq_no = ++seq_to_ctrl_;
-    to_ctrl_.push_back(Frame{to_ctrl_emu_.visible_at(now), std::move(m)});
+    Frame f{to_ctrl_emu_.visible_at(now), {}};
+    wire_encode(m, f.bytes);
+    to_ctrl_.push_back(std::move(f));
   }
 
   // serve_controller's loop body (runtime.hpp:262-335) for one wake-up
@@ -376,6 +390,7 @@ class WallRequest {
   WorkerState wrk_;
   ControllerDevices devices_;
   std::deque<Frame> to_ctrl_, to_wrk_;
+  FrameReader rd_ctrl_, rd_wrk_;
   LatencyEmulator to_ctrl_emu_, to_wrk_emu_;
   std::uint64_t seq_to_ctrl_ = 0, seq_to_worker_ = 0;
   std::vector<Message> inbox_ctrl_, inbox_wrk_;

@@ -4,7 +4,9 @@
 // when its CUDA work completes (not after a virtual t_target / t_draft); proposals and
 // validations cross per-request host queues whose frames become visible one_way = rtt/2 (+/-
 // uniform jitter) after they are sent, never out of order — the LatencyEmulator's
-// visible_at = max(sent + delay, last_visible) (net.hpp:149-163). Requests run concurrently and
+// visible_at = max(sent + delay, last_visible) (net.hpp:149-163); every message travels as its
+// wire frame (host/wire.hpp, the reference's encoding) through a FrameReader that enforces the
+// per-request FIFO seq contract (wire.hpp:296-323). Requests run concurrently and
 // share the GPU lanes (continuous batching); each one's protocol is the reference's.
 //
 // Optional decision log (the reference's DecisionLog, runtime.hpp:227-237, extended with the
