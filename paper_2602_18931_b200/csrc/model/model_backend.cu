@@ -13,6 +13,8 @@
 #include "../kernels/rowstats.cuh"
 #include "../kernels/sample.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace wsb {
 
 namespace {
@@ -277,7 +279,9 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
         b.groups.push_back(AttnGroup{row0, P - 1, base, 0, eoff, P - 1});
       }
       b.row_mask.assign(b.tok.size(), 0ull);
+      nvtxRangePushA(side == 0 ? "ws.prefill.target" : "ws.prefill.draft");
       m.forward(b, 0.f, sd.st, *sd.ws);  // no output rows: KV only, no LM head
+      nvtxRangePop();
       out.rows += side == 0 ? b.tok.size() : 0;
       (side == 0 ? out.target_forwards : out.draft_forwards) += 1;
       out.launches += 1 + 4ull * m.shape().layers;
@@ -662,6 +666,9 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
     stats.h2d += static_cast<std::size_t>(nv) * (k_ * 8 + 12);
   }
   WS_CUDA(cudaEventRecord(L.e0, st));
+  // NVTX: one range per verify / draft forward submission (SURVEY §5 tracing; host ranges that
+  // nsys / ncu correlate with the launches they enclose)
+  nvtxRangePushA("ws.verify");
   p_->target().forward(b, cfg.plant_target, st, *L.ws_t);
   if (rejection)
     verify_rejection_bf16(L.ws_t->logits, nv, k_, V, V, inv_temp_, top_p_, L.d_cands, L.d_cprob, sample_seed_,
@@ -669,6 +676,7 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
   else
     row_stats_bf16(L.ws_t->logits, nv * (k_ + 1), V, V, 1.0f, L.d_pred, nullptr, L.d_ws, nv, k_, L.d_cands,
                    L.d_vout, st, L.d_forced);
+  nvtxRangePop();
   WS_CUDA(cudaEventRecord(L.e1, st));
   WS_CUDA(cudaMemcpyAsync(L.h_vout, L.d_vout, nv * sizeof(ws_verify_out), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaEventRecord(L.done, st));
@@ -888,9 +896,11 @@ void ModelBackend_Llama::submit_draft(int lane, const RoundJobs& jobs) {
   if (n_out) {
     p_->draft().copy_slots(D.copy_src, D.copy_dst, sd, *D.ws);
     WS_CUDA(cudaEventRecord(D.e_start, sd));
+    nvtxRangePushA("ws.draft");
     p_->draft().forward(b, cfg.plant_draft, sd, *D.ws);
     row_stats_bf16(D.ws->logits, n_out, V, V, 1.0f, D.d_pred, nullptr, D.d_ws, 0, 0, nullptr, nullptr, sd,
                    nullptr);
+    nvtxRangePop();
     WS_CUDA(cudaEventRecord(D.e_end, sd));
     WS_CUDA(cudaMemcpyAsync(D.h_pred, D.d_pred, n_out * sizeof(ws_pred), cudaMemcpyDeviceToHost, sd));
     D.ran = true;
