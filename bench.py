@@ -45,6 +45,8 @@ def parse():
                    help="llama, N >= 2: 'split' puts the draft model on its own GPU (ranks < N/2 drive "
                         "target GPU r + draft GPU r + N/2; SURVEY §8e), 'shared' shards requests over all GPUs")
     p.add_argument("--cpu-sample-s", type=float, default=6.0)
+    p.add_argument("--cpu-seq", type=int, default=8,
+                   help="llama CPU baseline: committed tokens per measured CPU sample (one request)")
     p.add_argument("--target", choices=["llama3-8b", "llama3-70b"], default="llama3-8b",
                    help="llama: the target model shape; llama3-70b is BASELINE config 5's model (141 GB of "
                         "bf16 weights; use --requests 128)")
@@ -136,7 +138,8 @@ def config_block(args, world, host_threads):
         tname = {"llama3-8b": "Llama-3.1-8B", "llama3-70b": "Llama-3.1-70B"}[args.target]
         return {"workload": ("BASELINE configs[2]: " if args.target == "llama3-8b" and args.tp == 1 else
                              f"BASELINE configs[4]: target tensor-parallel over {args.tp} GPUs per process "
-                             f"(peer-memory all-reduce fused into the residual update), draft on the last of them: "
+                             f"(peer-memory all-reduce fused into the residual update), the draft model replicated on "
+                             f"every rank (request r's drafts on rank r % {args.tp}): "
                              if args.tp > 1 else
                              "BASELINE configs[4]'s model, whole on one GPU per rank (no TP): ") +
                             f"{tname}-shape target / Llama-3.2-1B-shape draft "
@@ -199,8 +202,13 @@ def llama_rooflines(rs, target, peak_bw, peak_tf, tp=1):
     prefill = unit_roofline(target, rs["prefill_forwards"], rs["prefill_target_ms"], rs["prefill_rows"], 0,
                             rs["prefill_kv_pos"], rs["prefill_attn_pairs"], peak_bw * tp, peak_tf * tp,
                             causal_half=True)
-    if tp > 1:
+    if tp > 1:  # the draft model is replicated on every rank (one replica per rank's share)
         verify["gpus"] = prefill["gpus"] = tp
+        if not os.environ.get("WS_TP_DRAFT_RANK"):
+            draft = unit_roofline("llama3.2-1b", rs["draft_forwards"], rs["draft_ms"], rs["draft_rows"],
+                                  rs["draft_out_rows"], rs["draft_kv_pos"], rs["draft_attn_pairs"], peak_bw * tp,
+                                  peak_tf * tp)
+            draft["gpus"] = tp
     draft = unit_roofline("llama3.2-1b", rs["draft_forwards"], rs["draft_ms"], rs["draft_rows"], rs["draft_out_rows"],
                           rs["draft_kv_pos"], rs["draft_attn_pairs"], peak_bw, peak_tf)
     return verify, prefill, draft
@@ -251,40 +259,41 @@ def k3_sample(rows, k, peak_bw, iters=20):
             "timing": "CUDA events, L2 flushed before each launch, the mean verify forward's output rows"}
 
 
-def cpu_reference_llama(k, requests, samples=1):
-    """The reference's CPU implementation of the config-3 path: the reference protocol itself
-    (run_sim_full via oracle/_ref — or the restatement when the reference is absent — on its
-    default tiny pair, match 0.8, the same k/b/s/theta/phi/RTT and 100 tokens) supplies the
-    per-request model-call counts; the numpy fp32 port (oracle/llama_cpu.py, all host cores)
-    supplies the cost of each call on a bounded sample: one 8B verify forward of k+1 rows, one
-    1B draft forward of s=4 leaves and one of 1 row, after a 160-token context. One request at
-    a time (the reference runs requests sequentially, sim.hpp:433)."""
-    from oracle import llama_cpu
-    from oracle import pyoracle as po
-    from paper_2602_18931_b200 import abi
-    c = abi.apply_stage(abi.sim_cfg(k=k, rtt=20000, num_requests=min(requests, 64), max_nodes=256), "full")
-    if po.ref_available():
-        m = po.ref_run_sim(c, threads=os.cpu_count() or 1, with_tokens=False, with_steps=False).metrics_list()
-    else:
-        import paper_2602_18931_b200 as ws
-        m = ws.run_sim_with_model(c, po.model_round_fn(c), with_tokens=False, with_steps=False).metrics_list()
-    n = len(m)
-    tv = td4 = td1 = 0.0
-    for _ in range(samples):
-        tv += llama_cpu.time_forward("llama3-8b", k + 1, 160, lm_rows=k + 1)
-        td4 += llama_cpu.time_forward("llama3.2-1b", 4, 160, lm_rows=4)
-        td1 += llama_cpu.time_forward("llama3.2-1b", 1, 160, lm_rows=1)
-    tv, td4, td1 = tv / samples, td4 / samples, td1 / samples
-    tokens = sum(x["tokens_committed"] for x in m)
-    secs = sum(x["target_steps"] * tv + x["worker_draft_steps"] * td4 + x["ctrl_draft_passes"] * td1 for x in m)
-    return tokens / secs, (f"reference protocol counts over {n} requests x numpy fp32 port costs on all host cores: "
-                           f"8B verify ({k + 1} rows) {tv:.2f} s, 1B draft step (4 leaves) {td4:.3f} s, "
-                           f"1B local draft pass {td1:.3f} s; {samples} sample(s)")
+_CPU_PAIR = None
+
+
+def cpu_measured(target, k, seq, steps, warmup):
+    """The CPU baseline of the Llama workload, measured end to end: the reference's own
+    RequestSim (oracle/_ref, unmodified) with its model calls answered by a torch-CPU bf16 port
+    of the same Llama pair on all host cores (oracle/cpu_pair.py: same planted bias and
+    generation cap), one request at a time as the reference runs them (sim.hpp:433), its prompt
+    prefilled before the clock starts. A sample = request 0 decoded to `seq` committed tokens
+    (the same deterministic protocol trajectory every sample, so samples differ only by CPU
+    timing noise). Returns the line's cpu_baseline object."""
+    global _CPU_PAIR
+    from oracle import cpu_pair
+    if _CPU_PAIR is None or _CPU_PAIR.L != seq or _CPU_PAIR.k != k:
+        _CPU_PAIR = cpu_pair.CpuPair(target=target, seq_len=seq, k=k)
+    for _ in range(warmup):
+        cpu_pair.measure(requests=1, first=0, pair=_CPU_PAIR)
+    rates, toks, secs, threads = [], 0, 0.0, 1
+    for _ in range(max(1, steps)):
+        r, t, el, threads = cpu_pair.measure(requests=1, first=0, pair=_CPU_PAIR)
+        rates.append(r)
+        toks += t
+        secs += el
+    value = toks / secs
+    spread = (max(rates) - min(rates)) / value if len(rates) > 1 else 0.0
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "protocol": "reference RequestSim (oracle/_ref) — its model calls answered by the CPU port",
+            "sample": f"{len(rates)} timed sample(s) after {warmup} warm-up: request 0 of config 3 decoded to "
+                      f"{seq} committed tokens (prompt prefilled untimed), {target} + llama3.2-1b in torch bf16 on "
+                      f"{threads} host threads; per-sample tokens/s min {min(rates):.3f} / median "
+                      f"{statistics.median(rates):.3f} / max {max(rates):.3f} (spread {100 * spread:.1f}%)"}
 
 
 def cpu_port_sample(args, k):
-    value, sample = cpu_reference_llama(k, args.requests)
-    return {"value": value, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port", "sample": sample}
+    return cpu_measured("llama3-8b", k, args.cpu_seq, steps=3, warmup=1)
 
 
 # ------------------------------------------------------------------ reference arm
@@ -310,10 +319,10 @@ def run_reference(args, rank, world):
         value, sample, kind = toks / el, f"{args.steps} full runs of {cfg.num_requests} requests " \
                                          "(run_sim_full via oracle/_ref, requests over threads)", "reference"
     else:
-        # The reference has no model: its CPU implementation of the config-3 path is
-        # the reference protocol's own call counts x the numpy fp32 port's per-call cost.
-        value, sample = cpu_reference_llama(args.k, args.requests, samples=max(1, args.steps))
-        kind = "port"
+        # The reference has no model: its CPU path for the config-3 workload is its
+        # own RequestSim with the model calls answered by the CPU port, measured end to end.
+        cb = cpu_measured(args.target, args.k, args.cpu_seq, steps=args.steps, warmup=min(args.warmup, 1))
+        value, sample, kind = cb["value"], cb["sample"], cb["kind"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "strong" if args.workload == "llama" else "weak", "vs_baseline": None,
@@ -372,8 +381,8 @@ def main():
         if active:
             ctx.load_models(abi.model_cfg(target=args.target, max_requests=args.requests, tp=args.tp),
                             draft_device=(local_rank + world // 2 if split else
-                                          dev0 + int(os.environ.get("WS_TP_DRAFT_RANK", args.tp - 1))
-                                          if args.tp > 1 else -1))
+                                          dev0 + int(os.environ["WS_TP_DRAFT_RANK"])
+                                          if args.tp > 1 and "WS_TP_DRAFT_RANK" in os.environ else -1))
 
         def run_once(tokens_out=False):
             return ctx.run_model_sim(cfg, with_tokens=tokens_out, with_steps=False)

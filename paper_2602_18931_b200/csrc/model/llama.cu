@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -144,6 +145,7 @@ LlamaModel::LlamaModel(const LlamaShape& s, std::uint64_t seed, std::int64_t n_s
   WS_CUDA(cudaMemset(k_pool_, 0, pool));
   WS_CUDA(cudaMemset(v_pool_, 0, pool));
   ws0_ = make_workspace(max_rows);
+  if (std::getenv("WS_PROFILE_MODEL")) ws0_->prof.enable(true);  // per-class times (probes)
   WS_CUDA(cudaDeviceSynchronize());
 }
 
@@ -169,6 +171,15 @@ ForwardWorkspace::~ForwardWorkspace() {
 
 LlamaModel::~LlamaModel() {
   cudaSetDevice(device_);
+  if (ws0_ && ws0_->prof.on()) {  // WS_PROFILE_MODEL: the own workspace's per-class device time
+    KernelProfiler& p = ws0_->prof;
+    p.collect();
+    std::fprintf(stderr, "[ws-profile] {\"model\": \"%s\"", s_.name.c_str());
+    for (int k = 0; k < KernelProfiler::kClasses; ++k)
+      std::fprintf(stderr, ", \"%s\": [%.3f, %llu]", KernelProfiler::name(k), p.ms[k],
+                   static_cast<unsigned long long>(p.count[k]));
+    std::fprintf(stderr, "}\n");
+  }
   if (rope_cs_) cudaFree(rope_cs_);
   ws0_.reset();
   for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_})

@@ -120,7 +120,8 @@ struct ModelPair::Impl {
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     std::unique_ptr<ForwardWorkspace> ws;
-  } pre[2];
+  };
+  std::vector<Side> pre;  // [0] target, [1 + rep] draft replica rep
   ~Impl() {
     for (Side& sd : pre) {
       if (!sd.st) continue;
@@ -136,7 +137,9 @@ struct ModelPair::Impl {
 // One draft lane: its stream, forward workspace, K3/K4 buffers and pinned results. Several
 // draft lanes let the host plan and launch the next draft batch while the previous one runs
 // (every actor has at most one draft job set in flight, so lanes never touch the same KV).
-struct DraftLane {
+struct DraftSub {  // one draft replica's share of a draft batch
+  int rep = 0;
+  std::vector<std::uint32_t> idx;  // the batch's job indices this replica runs
   int device = 0;
   cudaStream_t st = nullptr;
   std::unique_ptr<ForwardWorkspace> ws;
@@ -149,7 +152,7 @@ struct DraftLane {
   std::uint32_t nd = 0;
   bool ran = false;
   cudaEvent_t e_start = nullptr, e_end = nullptr, done = nullptr;
-  ~DraftLane() {
+  ~DraftSub() {
     cudaSetDevice(device);
     if (d_pred) cudaFree(d_pred);
     if (d_ws) cudaFree(d_ws);
@@ -158,6 +161,20 @@ struct DraftLane {
       if (e) cudaEventDestroy(e);
     ws.reset();
     if (st) cudaStreamDestroy(st);
+  }
+};
+
+// One draft lane: a sub-lane per draft replica; the lane completes when every sub-lane has.
+struct DraftLane {
+  std::vector<std::unique_ptr<DraftSub>> sub;
+  std::uint32_t nd = 0;
+  cudaEvent_t done = nullptr;  // on sub[0]'s device, after every sub-lane's work
+  ~DraftLane() {
+    if (done) {
+      cudaSetDevice(sub[0]->device);
+      cudaEventDestroy(done);
+    }
+    sub.clear();
   }
 };
 
@@ -213,6 +230,17 @@ ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(d
   draft_device_ = cfg.draft_device >= 0 ? cfg.draft_device : device;
   target_.reset(new LlamaModel(ts, cfg.seed * 2 + 1, R * C, max_rows_, device, cfg.tp));
   draft_.reset(new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows_, draft_device_));
+  draft_reps_.emplace_back();
+  rep_devices_.push_back(draft_device_);
+  // a tensor-parallel target with no explicit draft GPU: one draft replica per rank (the same
+  // weights), each serving the requests r with r % tp == its index — the draft work is spread
+  // over the ranks instead of skewing one of them
+  if (cfg.tp > 1 && cfg.draft_device < 0)
+    for (int g = 1; g < cfg.tp; ++g) {
+      draft_reps_.emplace_back(
+          new LlamaModel(ds, cfg.seed * 2 + 2, R * (2 * C + cfg.trie_slots), max_rows_, device + g));
+      rep_devices_.push_back(device + g);
+    }
   WS_CUDA(cudaSetDevice(device));
   prompts_.resize(cfg.max_requests);
   if (const char* e = std::getenv("WS_TARGET_CTAS")) target_->set_max_ctas(std::atoi(e));
@@ -240,10 +268,13 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
   const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg_.trie_slots);
   constexpr std::int32_t kMaxRows = 8192;  // rows per prefill forward (the GEMMs' efficient regime)
   const std::size_t per = static_cast<std::size_t>(std::max(1, kMaxRows / (P - 1)));
-  for (int side = 0; side < 2; ++side) {
+  const int n_sides = 1 + draft_replicas();
+  if (impl->pre.size() < static_cast<std::size_t>(n_sides)) impl->pre.resize(n_sides);
+  for (int side = 0; side < n_sides; ++side) {
     Impl::Side& sd = impl->pre[side];
-    LlamaModel& m = side == 0 ? *target_ : *draft_;
-    const int dev = side == 0 ? device_ : draft_device_;
+    const int rep = side - 1;
+    LlamaModel& m = side == 0 ? *target_ : draft(rep);
+    const int dev = side == 0 ? device_ : draft_device(rep);
     DeviceGuard dg(dev);
     if (!sd.st) {
       sd.dev = dev;
@@ -252,15 +283,19 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
       WS_CUDA(cudaEventCreate(&sd.e1));
       sd.ws = m.make_workspace(64);
     }
+    // this side's requests: all (target), or those served by the draft replica
+    std::vector<std::uint32_t> mine;
+    for (std::size_t i = 0; i < n; ++i)
+      if (side == 0 || replica_of(reqs[i]) == rep) mine.push_back(reqs[i]);
     WS_CUDA(cudaEventRecord(sd.e0, sd.st));
     const std::size_t h2d0 = sd.ws->h2d;
     const std::uint64_t kv0 = sd.ws->kv_pos, ap0 = sd.ws->attn_pairs;
     ForwardBatch b;
     std::vector<std::int32_t> src, dst;
-    for (std::size_t i0 = 0; i0 < n; i0 += per) {
+    for (std::size_t i0 = 0; i0 < mine.size(); i0 += per) {
       b.clear();
-      for (std::size_t i = i0; i < std::min(n, i0 + per); ++i) {
-        const std::uint32_t r = reqs[i];
+      for (std::size_t i = i0; i < std::min(mine.size(), i0 + per); ++i) {
+        const std::uint32_t r = mine[i];
         const std::vector<TokenId>& pr = prompt(r);
         // target: the linear verify cache; draft: the worker's committed prefix region
         const std::int32_t base = side == 0 ? static_cast<std::int32_t>(r) * MC : static_cast<std::int32_t>(r) * S + MC;
@@ -271,7 +306,7 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
           b.pos.push_back(p);
           b.slot.push_back(base + p);
           b.extra.push_back(base + p);
-          if (side == 1) {
+          if (side > 0) {
             src.push_back(base + p);
             dst.push_back(static_cast<std::int32_t>(r) * S + p);  // the controller's draft cache
           }
@@ -286,7 +321,7 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
       (side == 0 ? out.target_forwards : out.draft_forwards) += 1;
       out.launches += 1 + 4ull * m.shape().layers;
     }
-    if (side == 1) {
+    if (side > 0 && !src.empty()) {
       m.copy_slots(src, dst, sd.st, *sd.ws);
       out.launches += 1;
     }
@@ -297,14 +332,19 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
       out.attn_pairs += sd.ws->attn_pairs - ap0;
     }
   }
-  for (int side = 0; side < 2; ++side) {
+  float draft_max = 0.f;
+  for (int side = 0; side < n_sides; ++side) {
     Impl::Side& sd = impl->pre[side];
     DeviceGuard dg(sd.dev);
     WS_CUDA(cudaEventSynchronize(sd.e1));
     float ms = 0.f;
     WS_CUDA(cudaEventElapsedTime(&ms, sd.e0, sd.e1));
-    (side == 0 ? out.target_ms : out.draft_ms) += ms;
+    if (side == 0)
+      out.target_ms += ms;
+    else
+      draft_max = std::max(draft_max, ms);  // the replicas prefill concurrently
   }
+  out.draft_ms += draft_max;
   for (std::size_t i = 0; i < n; ++i) {
     const std::uint32_t r = reqs[i];
     const std::vector<TokenId>& pr = prompt(r);
@@ -462,16 +502,23 @@ ModelBackend_Llama::ModelBackend_Llama(ModelPair* pair, std::uint32_t seq_len, T
   // WS_DRAFT_LANES: draft lanes per protocol thread (default 1)
   int n_draft = 1;
   if (const char* e = std::getenv("WS_DRAFT_LANES")) n_draft = std::max(1, std::min(8, std::atoi(e)));
-  WS_CUDA(cudaSetDevice(L.device_d));
   for (int i = 0; i < n_draft; ++i) {
-    std::unique_ptr<DraftLane> d(new DraftLane);
-    d->device = L.device_d;
-    WS_CUDA(cudaStreamCreateWithPriority(&d->st, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
-    WS_CUDA(cudaEventCreate(&d->e_start));
-    WS_CUDA(cudaEventCreate(&d->e_end));
-    WS_CUDA(cudaEventCreateWithFlags(&d->done, cudaEventDisableTiming));
-    d->ws = pair->draft().make_workspace(64);
-    L.dl.push_back(std::move(d));
+    std::unique_ptr<DraftLane> g(new DraftLane);
+    for (int rep = 0; rep < pair->draft_replicas(); ++rep) {
+      std::unique_ptr<DraftSub> d(new DraftSub);
+      d->rep = rep;
+      d->device = pair->draft_device(rep);
+      WS_CUDA(cudaSetDevice(d->device));
+      WS_CUDA(cudaStreamCreateWithPriority(&d->st, cudaStreamNonBlocking, draft_first ? prio_hi : prio_lo));
+      WS_CUDA(cudaEventCreate(&d->e_start));
+      WS_CUDA(cudaEventCreate(&d->e_end));
+      WS_CUDA(cudaEventCreateWithFlags(&d->done, cudaEventDisableTiming));
+      d->ws = pair->draft(rep).make_workspace(64);
+      g->sub.push_back(std::move(d));
+    }
+    WS_CUDA(cudaSetDevice(g->sub[0]->device));
+    WS_CUDA(cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming));
+    L.dl.push_back(std::move(g));
   }
   WS_CUDA(cudaSetDevice(L.device));
 }
@@ -487,7 +534,8 @@ void ModelBackend_Llama::reset_run(std::uint32_t seq_len, TokenId eos, std::uint
   target_rows = draft_rows_fed = target_forwards = draft_forwards = 0;
   target_out_rows = draft_out_rows = 0;
   ln_->ws_t->kv_pos = ln_->ws_t->attn_pairs = 0;
-  for (auto& d : ln_->dl) d->ws->kv_pos = d->ws->attn_pairs = 0;
+  for (auto& g : ln_->dl)
+    for (auto& d : g->sub) d->ws->kv_pos = d->ws->attn_pairs = 0;
   for (int i = 0; i < 3; ++i) rows_by_kind[i] = jobs_by_kind[i] = 0;
   host_submit_ms[0] = host_submit_ms[1] = host_wait_ms = 0;
 }
@@ -496,19 +544,21 @@ std::uint64_t ModelBackend_Llama::target_kv_pos() const { return ln_->ws_t->kv_p
 std::uint64_t ModelBackend_Llama::target_attn_pairs() const { return ln_->ws_t->attn_pairs; }
 std::uint64_t ModelBackend_Llama::draft_kv_pos() const {
   std::uint64_t n = 0;
-  for (const auto& d : ln_->dl) n += d->ws->kv_pos;
+  for (const auto& g : ln_->dl)
+    for (const auto& d : g->sub) n += d->ws->kv_pos;
   return n;
 }
 std::uint64_t ModelBackend_Llama::draft_attn_pairs() const {
   std::uint64_t n = 0;
-  for (const auto& d : ln_->dl) n += d->ws->attn_pairs;
+  for (const auto& g : ln_->dl)
+    for (const auto& d : g->sub) n += d->ws->attn_pairs;
   return n;
 }
 
 int ModelBackend_Llama::n_lanes() const { return 1 + static_cast<int>(ln_->dl.size()); }
 
 KernelProfiler& ModelBackend_Llama::profiler(int lane) {
-  return lane == 0 ? ln_->ws_t->prof : ln_->dl.at(lane - 1)->ws->prof;
+  return lane == 0 ? ln_->ws_t->prof : ln_->dl.at(lane - 1)->sub[0]->ws->prof;
 }
 
 namespace {
@@ -692,19 +742,42 @@ void ModelBackend_Llama::submit_verify(const RoundJobs& jobs, std::size_t nv_tak
 // Lanes 1..n: one draft forward over every pending draft job (worker leaves as shared-prefix
 // tree groups, controller local drafts / catch-up as causal groups), then K3/K4 row statistics.
 void ModelBackend_Llama::submit_draft(int lane, const RoundJobs& jobs) {
+  DraftLane& G = *ln_->dl.at(lane - 1);
+  G.nd = static_cast<std::uint32_t>(jobs.draft.size());
+  for (auto& d : G.sub) {
+    d->idx.clear();
+    d->nd = 0;
+    d->ran = false;
+  }
+  if (!G.nd) return;
+  ++draft_batch_;
+  for (std::uint32_t j = 0; j < G.nd; ++j) G.sub[p_->replica_of(jobs.draft[j].seq)]->idx.push_back(j);
+  for (auto& d : G.sub)
+    if (!d->idx.empty()) submit_draft_sub(lane, *d, jobs);
+  for (auto& d : G.sub)
+    if (d->ran) {  // one logical draft forward (its replicas' shares run concurrently)
+      draft_forwards += 1;
+      break;
+    }
+  // the lane's completion: sub-lane 0's stream after every other sub-lane's work
+  DraftSub& s0 = *G.sub[0];
+  DeviceGuard dg(s0.device);
+  for (std::size_t i = 1; i < G.sub.size(); ++i)
+    if (!G.sub[i]->idx.empty()) WS_CUDA(cudaStreamWaitEvent(s0.st, G.sub[i]->done, 0));
+  WS_CUDA(cudaEventRecord(G.done, draft_stream(lane)));
+}
+
+void ModelBackend_Llama::submit_draft_sub(int lane, DraftSub& D, const RoundJobs& jobs) {
   ModelPair::Impl& I = *p_->impl;
   Lanes& L = *ln_;
-  DraftLane& D = *L.dl.at(lane - 1);
-  DeviceGuard dg(L.device_d);
+  DeviceGuard dg(D.device);
+  LlamaModel& dm = p_->draft(D.rep);
   const ModelPairCfg& cfg = p_->cfg();
   const std::int32_t P = static_cast<std::int32_t>(cfg.prompt_len);
   const std::int32_t MC = static_cast<std::int32_t>(cfg.max_ctx);
-  const std::int32_t V = p_->draft().shape().vocab;
-  const std::uint32_t nd = static_cast<std::uint32_t>(jobs.draft.size());
+  const std::int32_t V = dm.shape().vocab;
+  const std::uint32_t nd = static_cast<std::uint32_t>(D.idx.size());
   D.nd = nd;
-  D.ran = false;
-  if (!nd) return;
-  ++draft_batch_;
   const std::size_t need = static_cast<std::size_t>(nd) + 16;
   if (need > D.cap) {  // the lane is idle here (the driver submits only to idle lanes)
     if (D.d_pred) cudaFree(D.d_pred);
@@ -746,8 +819,8 @@ void ModelBackend_Llama::submit_draft(int lane, const RoundJobs& jobs) {
   };
   const std::int32_t S = 2 * MC + static_cast<std::int32_t>(cfg.trie_slots);
   for (std::uint32_t j = 0; j < nd; ++j) {
-    const DraftJob& dj = jobs.draft[j];
-    const JobCtx& jc = jobs.draft_ctx[j];
+    const DraftJob& dj = jobs.draft[D.idx[j]];
+    const JobCtx& jc = jobs.draft_ctx[D.idx[j]];
     const std::uint32_t r = dj.seq;
     fill_ctx(jobs, r, jc);
     const std::int32_t n_ctx = static_cast<std::int32_t>(L.ctx.size());
@@ -892,12 +965,12 @@ void ModelBackend_Llama::submit_draft(int lane, const RoundJobs& jobs) {
   flush_wg();
   if (b.row_mask.size() != b.tok.size()) throw std::logic_error("model path: row mask bookkeeping");
   const std::uint32_t n_out = static_cast<std::uint32_t>(b.out_rows.size());
-  cudaStream_t sd = draft_stream(lane);
+  cudaStream_t sd = D.rep == 0 ? draft_stream(lane) : D.st;
   if (n_out) {
-    p_->draft().copy_slots(D.copy_src, D.copy_dst, sd, *D.ws);
+    dm.copy_slots(D.copy_src, D.copy_dst, sd, *D.ws);
     WS_CUDA(cudaEventRecord(D.e_start, sd));
     nvtxRangePushA("ws.draft");
-    p_->draft().forward(b, cfg.plant_draft, sd, *D.ws);
+    dm.forward(b, cfg.plant_draft, sd, *D.ws);
     row_stats_bf16(D.ws->logits, n_out, V, V, 1.0f, D.d_pred, nullptr, D.d_ws, 0, 0, nullptr, nullptr, sd,
                    nullptr);
     nvtxRangePop();
@@ -906,8 +979,7 @@ void ModelBackend_Llama::submit_draft(int lane, const RoundJobs& jobs) {
     D.ran = true;
     draft_rows_fed += b.tok.size();
     draft_out_rows += n_out;
-    draft_forwards += 1;
-    stats.launches += 1 + 8ull * p_->draft().shape().layers + 4 + (D.copy_src.empty() ? 0 : 1);
+    stats.launches += 1 + 8ull * dm.shape().layers + 4 + (D.copy_src.empty() ? 0 : 1);
     stats.d2h += n_out * sizeof(ws_pred);
   }
   WS_CUDA(cudaEventRecord(D.done, sd));
@@ -918,7 +990,8 @@ cudaStream_t ModelBackend_Llama::draft_stream(int lane) const {
   // WS_SERIAL=1 serialises every forward on one stream (clean per-kernel profiles); default
   // overlaps the lanes
   static const bool serial = std::getenv("WS_SERIAL") != nullptr;
-  return serial && ln_->device_d == ln_->device ? ln_->st_t : ln_->dl.at(lane - 1)->st;
+  const DraftSub& s0 = *ln_->dl.at(lane - 1)->sub[0];
+  return serial && s0.device == ln_->device ? ln_->st_t : s0.st;
 }
 
 std::size_t ModelBackend_Llama::submit(int lane, const RoundJobs& jobs, int verify_mode, std::uint64_t sample_seed) {
@@ -953,7 +1026,7 @@ int ModelBackend_Llama::wait_any(std::uint32_t busy) {
     for (int lane = 0; lane < n; ++lane) {
       if (!(busy & (1u << lane))) continue;
       // each event is queried with its own GPU current (split placement: two devices)
-      DeviceGuard dg(lane == 0 ? L.device : L.device_d);
+      DeviceGuard dg(lane == 0 ? L.device : L.dl[lane - 1]->sub[0]->device);
       const cudaError_t e = cudaEventQuery(lane == 0 ? L.done : L.dl[lane - 1]->done);
       if (e == cudaSuccess) return lane;
       if (e != cudaErrorNotReady) WS_CUDA(e);
@@ -974,7 +1047,7 @@ int ModelBackend_Llama::poll_any(std::uint32_t busy) {
   Lanes& L = *ln_;
   for (int lane = 0; lane < n_lanes(); ++lane) {
     if (!(busy & (1u << lane))) continue;
-    DeviceGuard dg(lane == 0 ? L.device : L.device_d);
+    DeviceGuard dg(lane == 0 ? L.device : L.dl[lane - 1]->sub[0]->device);
     const cudaError_t e = cudaEventQuery(lane == 0 ? L.done : L.dl[lane - 1]->done);
     if (e == cudaSuccess) return lane;
     if (e != cudaErrorNotReady) WS_CUDA(e);
@@ -984,7 +1057,7 @@ int ModelBackend_Llama::poll_any(std::uint32_t busy) {
 
 void ModelBackend_Llama::complete(int lane, RoundResults& res) {
   Lanes& L = *ln_;
-  DeviceGuard dg(lane == 0 ? L.device : L.device_d);
+  DeviceGuard dg(lane == 0 ? L.device : L.dl.at(lane - 1)->sub[0]->device);
   float ms = 0.f;
   if (lane == 0) {
     res.verify.resize(L.nv);
@@ -994,25 +1067,32 @@ void ModelBackend_Llama::complete(int lane, RoundResults& res) {
     WS_CUDA(cudaEventElapsedTime(&ms, L.e0, L.e1));
     target_ms += ms;
   } else {
-    DraftLane& D = *L.dl.at(lane - 1);
-    res.draft.resize(D.nd);
-    if (!D.nd) return;
-    WS_CUDA(cudaEventSynchronize(D.done));
-    for (std::uint32_t j = 0; j < D.nd; ++j) {
-      if (D.job_out[j] >= 0) {
-        res.draft[j] = D.h_pred[D.job_out[j]];
-      } else {
-        ws_pred e{};
-        e.n = 1;
-        e.id[0] = eos_;
-        e.prob[0] = 1.0;
-        res.draft[j] = e;
+    DraftLane& G = *L.dl.at(lane - 1);
+    res.draft.resize(G.nd);
+    if (!G.nd) return;
+    WS_CUDA(cudaEventSynchronize(G.done));
+    float lane_ms = 0.f;  // the sub-lanes run concurrently: the unit's time is the longest
+    for (auto& dp : G.sub) {
+      DraftSub& D = *dp;
+      for (std::uint32_t t = 0; t < D.nd; ++t) {
+        const std::uint32_t j = D.idx[t];
+        if (D.job_out[t] >= 0) {
+          res.draft[j] = D.h_pred[D.job_out[t]];
+        } else {
+          ws_pred e{};
+          e.n = 1;
+          e.id[0] = eos_;
+          e.prob[0] = 1.0;
+          res.draft[j] = e;
+        }
+      }
+      if (D.ran) {
+        DeviceGuard dd(D.device);
+        WS_CUDA(cudaEventElapsedTime(&ms, D.e_start, D.e_end));
+        lane_ms = std::max(lane_ms, ms);
       }
     }
-    if (D.ran) {
-      WS_CUDA(cudaEventElapsedTime(&ms, D.e_start, D.e_end));
-      draft_ms += ms;
-    }
+    draft_ms += lane_ms;
   }
   stats.kernel_ms = target_ms + draft_ms;
 }

@@ -80,6 +80,7 @@ class ModelBackend_Llama : public ModelBackend {
   std::size_t verify_take(const RoundJobs& jobs);  // padding-aware batch trim (lanes driver)
   void submit_verify(const RoundJobs& jobs, std::size_t nv);
   void submit_draft(int lane, const RoundJobs& jobs);
+  void submit_draft_sub(int lane, struct DraftSub& sub, const RoundJobs& jobs);
   cudaStream_t draft_stream(int lane) const;
   ModelPair* p_;
   std::uint32_t L_;
@@ -119,6 +120,12 @@ class ModelPair {
   const ModelPairCfg& cfg() const { return cfg_; }
   LlamaModel& target() { return *target_; }
   LlamaModel& draft() { return *draft_; }
+  // Draft replicas (a tensor-parallel target spreads the draft model over its ranks: request r's
+  // draft jobs always run on replica r % n, whose KV holds its caches)
+  int draft_replicas() const { return static_cast<int>(draft_reps_.size()); }
+  LlamaModel& draft(int rep) { return rep == 0 ? *draft_ : *draft_reps_[static_cast<std::size_t>(rep)]; }
+  int draft_device(int rep) const { return rep_devices_[static_cast<std::size_t>(rep)]; }
+  int replica_of(std::uint32_t request) const { return static_cast<int>(request % draft_reps_.size()); }
   const std::vector<TokenId>& prompt(std::uint32_t r);
   std::int32_t plant(TokenId t, bool draft) const;
   int device() const { return device_; }  // the target model's GPU
@@ -132,6 +139,8 @@ class ModelPair {
   ModelPairCfg cfg_;
   int device_;
   std::unique_ptr<LlamaModel> target_, draft_;
+  std::vector<std::unique_ptr<LlamaModel>> draft_reps_;  // [0] empty (draft_ is replica 0)
+  std::vector<int> rep_devices_;
   std::vector<std::vector<TokenId>> prompts_;
   int max_rows_ = 0;
   int draft_device_ = 0;
