@@ -30,5 +30,45 @@ def main():
         print(json.dumps({"tag": os.environ.get("TAG", ""), **res}), flush=True)
 
 
+
+
+def timeline_small():
+    """WS_GEMM_ABLATE=8: per-phase timeline (ns from CTA 0's entry) of small-M GEMMs at the 1B
+    shapes, each measured after a warm-up: where a ~13 µs small GEMM spends its time."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2602_18931_b200 as ws
+    from paper_2602_18931_b200 import ops
+    L = ws.lib()
+    L.ws_debug_gemm_trace.argtypes = [C.c_void_p]
+    names = ["entry", "prologue", "dep_wait", "first_full", "last_mma", "acc_ready", "epi_done", "exit"]
+    for M in (48, 160, 512):
+        for (N, K, epi, name) in [(3072, 2048, 0, "1B qkv(bf16 epi)"), (2048, 2048, 1, "1B o"),
+                                  (2048, 8192, 1, "1B down"), (16384, 2048, 2, "1B gate_up")]:
+            A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+            W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+            out = torch.zeros(M, N, device="cuda", dtype=torch.float32) if epi == 1 else None
+            for _ in range(3):
+                ops.gemm(A, W, out=out, epi=epi)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ops.gemm(A, W, out=out, epi=epi)
+            e1.record()
+            torch.cuda.synchronize()
+            buf = (C.c_ulonglong * 8)()
+            assert L.ws_debug_gemm_trace(buf) == 0
+            t0 = buf[0]
+            print(json.dumps({"gemm": f"{name} M={M}", "event_us": round(e0.elapsed_time(e1) * 1e3, 1),
+                              **{n: round((buf[i] - t0) / 1e3, 2) for i, n in enumerate(names)}}), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "timeline":
+    timeline_small()
+    sys.exit(0)
+
+
 if __name__ == "__main__":
     main()
