@@ -391,12 +391,14 @@ void attention(const void* q, const void* k_pool, const void* v_pool, const Attn
                cudaStream_t st) {
   if (n_entries <= 0) return;
   const float sl2 = s.scale * 1.4426950408889634f;
-  // One key slice and a 2-deep K/V ring for both head dims (ncu launch lists of
-  // scripts/forward_probe.py, profiles/r01_driver_policy.md): with Q riding in the first
-  // cp.async group, hd 64 runs 32.2 µs per layer with one slice against 37.2 with two and 47.7
-  // with a 3-deep ring; deeper rings cost occupancy.
+  // A 2-deep K/V ring for both head dims. hd 64 (the 1B draft): one key slice (ncu launch lists
+  // of scripts/forward_probe.py, profiles/r01_driver_policy.md): with Q riding in the first
+  // cp.async group, 32.2 µs per layer against 37.2 with two slices and 47.7 with a 3-deep ring.
+  // hd 128 (the 8B verify): two key slices — 32.6 µs per layer against 35.0 with one (105 x 5-row
+  // groups over 176-position prefixes, WS_PROFILE_MODEL of scripts/forward_probe.py); 3-deep
+  // rings and four slices were slower (profiles/r02_attention_hd128.md).
   if (s.hd == 128)
-    launch_attn<128, 2, 1, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
+    launch_attn<128, 2, 2, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
   else if (s.hd == 64)
     launch_attn<64, 1, 1, 2>(q, k_pool, v_pool, entries, n_entries, extra, row_mask, s, sl2, out, st);
   else

@@ -17,9 +17,9 @@ struct RowStats {
   float h;   // entropy (nats)
 };
 
-// Vocab chunk per CTA: fixed (not derived from the row count) so a row's statistics are
-// bit-identical at any batch size (batch invariance) — splits = ceil(V / kRowChunk).
-constexpr std::uint32_t kRowChunk = 65536;
+// Vocab tile per warp: fixed (not derived from the row count) so a row's statistics are
+// bit-identical at any batch size (batch invariance) — tiles = ceil(V / kRowTile).
+constexpr std::uint32_t kRowTile = 8192;
 
 std::size_t rowstats_workspace_bytes(std::uint32_t rows, std::uint32_t vocab, std::uint32_t n_req);
 

@@ -1,0 +1,5 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_rowstats.py tests/test_gpu_sample.py -x -q -m gpu > gpurun_out/k3v3_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/k3v3_tests.log
+for n in 107 10 256; do timeout 300 python scripts/k3_probe.py $n 4 >> gpurun_out/k3v3_probe.log 2>&1; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:row_stats -c 1 -o gpurun_out/r02_ncu_k3v3_535 python scripts/k3_probe.py 107 4 > gpurun_out/k3v3_ncu.log 2>&1
+ls -la gpurun_out | tail -5

@@ -11,7 +11,8 @@ fp32 at every point where the sm_100a kernels store a narrower value:
                                  are folded into Wqkv / Wgu at load (fold_norm_weight)
   q, k = bf16(rope(fp32(acc) * rs)), v = bf16(fp32(acc) * rs)   QKV epilogue (cos/sin fp32
                                  table from fp64 angles of fp32 inverse frequencies)
-  attn = bf16(o / l)   K2's online softmax, mirrored tile by tile: keys in 32-position tiles
+  attn = bf16(o / l)   K2's online softmax, mirrored tile by tile (hd 128: two key slices, merged
+                       at the end): keys in 32-position tiles
                        (the group's prefix, then its extras), s = fp32(q.k) * fp32(scale log2 e),
                        running max per tile, p = exp2(s - max) in fp32, l += sum p (fp32),
                        o = o * corr + bf16(p) . v  (P is the bf16 A operand of the PV mma)
@@ -112,26 +113,40 @@ class RefModel:
 
     @staticmethod
     def _attention(q, k, v, allowed, tile=32):
-        """attn_mma_kernel (csrc/kernels/attention.cu) restated: one key slice, 32-key tiles."""
+        """attn_mma_kernel (csrc/kernels/attention.cu) restated: 32-key tiles; hd 128 runs two key
+        slices (slice ks takes tiles ks, ks+2, ...; the slices' states merge in slice order at the
+        end), hd 64 one."""
         hd = q.shape[-1]
+        slices = 2 if hd == 128 else 1
         sl2 = torch.tensor(1.0 / math.sqrt(hd), dtype=torch.float32) * torch.tensor(1.4426950408889634,
                                                                                      dtype=torch.float32)
         s = f32(torch.einsum("thd,shd->hts", q, k)) * sl2.double()
         s = f32(s).masked_fill(~allowed[None], float("-inf"))  # [H, Tq, Tk]
         H, Tq, Tk = s.shape
-        m = torch.full((H, Tq), float("-inf"), dtype=torch.float64, device=s.device)
-        lsum = torch.zeros(H, Tq, dtype=torch.float64, device=s.device)
-        o = torch.zeros(H, Tq, hd, dtype=torch.float64, device=s.device)
         vh = v.permute(1, 0, 2)  # [H, Tk, hd]
-        for t0 in range(0, Tk, tile):
-            st = s[:, :, t0:t0 + tile]
-            nmax = torch.maximum(m, st.max(-1).values)
-            base = torch.where(nmax == float("-inf"), torch.zeros_like(nmax), nmax)
-            corr = torch.exp2(m - base)
-            p = f32(torch.exp2(st - base[..., None]))
-            lsum = f32(lsum * corr + p.sum(-1))
-            o = o * corr[..., None] + torch.einsum("hts,hsd->htd", bf(p), vh[:, t0:t0 + tile])
-            m = nmax
+        states = []
+        for ks in range(slices):
+            m = torch.full((H, Tq), float("-inf"), dtype=torch.float64, device=s.device)
+            lsum = torch.zeros(H, Tq, dtype=torch.float64, device=s.device)
+            o = torch.zeros(H, Tq, hd, dtype=torch.float64, device=s.device)
+            for t0 in range(ks * tile, Tk, slices * tile):
+                st = s[:, :, t0:t0 + tile]
+                nmax = torch.maximum(m, st.max(-1).values)
+                base = torch.where(nmax == float("-inf"), torch.zeros_like(nmax), nmax)
+                corr = torch.exp2(m - base)
+                p = f32(torch.exp2(st - base[..., None]))
+                lsum = f32(lsum * corr + p.sum(-1))
+                o = o * corr[..., None] + torch.einsum("hts,hsd->htd", bf(p), vh[:, t0:t0 + tile])
+                m = nmax
+            states.append((m, lsum, o))
+        m, lsum, o = states[0]
+        for om, ol, oo in states[1:]:
+            nm = torch.maximum(m, om)
+            b = torch.where(nm == float("-inf"), torch.zeros_like(nm), nm)
+            ca, cb = f32(torch.exp2(m - b)), f32(torch.exp2(om - b))
+            lsum = f32(lsum * ca + ol * cb)
+            o = o * ca[..., None] + oo * cb[..., None]
+            m = nm
         inv = torch.where(lsum > 0, 1.0 / lsum, torch.zeros_like(lsum))
         return bf(o * inv[..., None]).permute(1, 0, 2)
 

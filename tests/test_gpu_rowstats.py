@@ -83,12 +83,13 @@ def test_ties_resolve_to_lower_id(L):
 
 
 def test_top2_vector_and_thread_placements(L):
-    """K3 finds each thread's top-2 from its two best 8-element vectors (by vector maximum),
-    then rescans those two. Plant the top-2 where that could go wrong: both in one vector, in two
-    vectors of one thread (ids 2048 apart inside a 65536-wide chunk), ties inside one thread,
-    ties between a same-vector element and another thread's, and across chunks."""
+    """K3 keeps each lane's two best 8-element vectors (by vector maximum), merges them over the
+    warp and rescans the tile's best two. Plant the top-2 where that could go wrong: both in one
+    vector, in two vectors of one lane (ids 256 apart inside an 8192-wide tile), ties inside one
+    lane, ties between a same-vector element and another lane's, across tiles, in the short last
+    tile (and the round-1 64K-chunk geometry: ids 2048 / 65536 apart)."""
     V = 128256
-    x = (torch.randn(8, V, device="cuda", generator=torch.Generator(device="cuda").manual_seed(11)) * 0.1)
+    x = (torch.randn(16, V, device="cuda", generator=torch.Generator(device="cuda").manual_seed(11)) * 0.1)
     plants = [
         {100: 5.0, 103: 4.0},                      # same vector
         {5: 5.0, 5 + 2048 * 3: 4.0},               # same thread, different vectors
@@ -98,9 +99,15 @@ def test_top2_vector_and_thread_placements(L):
         {40: 5.0, 47: 4.0, 8: 4.0},                # tie for second: lower id in another thread wins
         {65536 + 10: 5.0, 10: 5.0},                # tie across chunks
         {128255: 5.0, 128254: 5.0},                # last vector of the row
+        {5: 5.0, 5 + 256 * 3: 4.0},                # same lane, different vectors
+        {9: 5.0, 9 + 256: 5.0, 12: 4.5},           # tie for first in one lane; 3rd in 1st's vector
+        {8192 + 3: 5.0, 3: 5.0},                   # tie across tiles
+        {8192 * 15 + 5000: 5.0, 8192 * 15 + 4999: 4.9},  # short last tile
+        {300: 5.0, 301: 4.0, 300 + 8: 4.0},        # tie for second: same vector vs the next lane's
     ]
     want = [(100, 103), (5, 5 + 2048 * 3), (7, 7 + 2048), (1, 1 + 2048 * 2), (16, 17), (40, 8),
-            (10, 65546), (128254, 128255)]
+            (10, 65546), (128254, 128255), (5, 5 + 256 * 3), (9, 9 + 256), (3, 8195),
+            (8192 * 15 + 5000, 8192 * 15 + 4999), (300, 301)]
     for r, pl in enumerate(plants):
         for i, v in pl.items():
             x[r, i] = v
