@@ -150,6 +150,10 @@ def config_block(args, world, host_threads):
                 "parallelism": (f"split placement: requests sharded over {world // 2} target GPU(s), each "
                                 f"paired with its own draft GPU (SURVEY §8e), no collective"
                                 if args.placement == "split" and world >= 2 and world % 2 == 0 else
+                                f"dp{world} x tp{args.tp}: requests sharded over {world} process(es) (strong "
+                                f"scaling, no collective between them), each target tensor-parallel over "
+                                f"{args.tp} GPUs (peer-memory all-reduce)"
+                                if args.tp > 1 else
                                 f"requests sharded over {world} GPU(s) (strong scaling), no collective"),
                 "l2": "weights (>=18.5 GB) and KV (>126 MB) exceed L2; no explicit flush needed"}
     return {"workload": "BASELINE configs[1]: tiny draft/target pair (oracle tables, V=32768), "
