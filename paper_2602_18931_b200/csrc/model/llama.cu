@@ -1,6 +1,8 @@
 // Batched Llama forward (see llama.hpp).
 #include "llama.hpp"
 
+#include <chrono>
+
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -180,6 +182,9 @@ LlamaModel::~LlamaModel() {
                    static_cast<unsigned long long>(p.count[k]));
     std::fprintf(stderr, "}\n");
   }
+  if (ws0_ && ws0_->host_fwd && std::getenv("WS_PROFILE_HOST"))
+    std::fprintf(stderr, "[ws-host] {\"model\": \"%s\", \"forwards\": %llu, \"host_ms_per_forward\": %.4f}\n",
+                 s_.name.c_str(), static_cast<unsigned long long>(ws0_->host_fwd), ws0_->host_ms / ws0_->host_fwd);
   if (rope_cs_) cudaFree(rope_cs_);
   ws0_.reset();
   for (void* p : {weight_block_, static_cast<void*>(inv_freq_), k_pool_, v_pool_})
@@ -334,6 +339,14 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
   for (std::int32_t p : b.pos)
     if (p < 0 || p >= kMaxPos) throw std::invalid_argument("forward: position out of the RoPE table range");
   if (tp_ > 1) return forward_tp(b, plant, st, ws);
+  struct HostClock {  // the forward's host enqueue time (returns when the last kernel is queued)
+    ForwardWorkspace& w;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~HostClock() {
+      w.host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      ++w.host_fwd;
+    }
+  } host_clock{ws};
   ensure_rows(ws, n, n_out);
   float* const x_ = ws.x;
   void* const xb_ = ws.xb;

@@ -130,6 +130,9 @@ struct ForwardWorkspace {
   // kv_pos = sum over groups of the keys read (prefix + extras), attn_pairs = sum over groups of
   // rows x keys (an upper bound of the visible pairs; causal groups see about half their extras)
   std::uint64_t kv_pos = 0, attn_pairs = 0;
+  // host time spent enqueueing forwards (metadata staging + kernel launches; WS_PROFILE_HOST)
+  double host_ms = 0.0;
+  std::uint64_t host_fwd = 0;
   KernelProfiler prof;
   std::unique_ptr<TPActs> tp;  // tensor-parallel models only
 };
