@@ -30,6 +30,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "cuda_check.hpp"
 #include "pdl.cuh"
@@ -850,8 +851,26 @@ int pick_splits(int N, int K) {
   // serialised last-split epilogue cost more than the extra parallelism buys (8B O-proj 187 →
   // 380 ms/run, 1B down 318 → 766 ms/run), so the model path does not split; the machinery
   // stays available (explicit splits) and tested.
-  (void)N;
-  (void)K;
+  // WS_GEMM_SPLITS="N:K:S[,N:K:S...]" (experiments): a fixed split count for those shapes
+  struct Rule {
+    int n, k, s;
+  };
+  static const std::vector<Rule> rules = [] {
+    std::vector<Rule> r;
+    if (const char* e = std::getenv("WS_GEMM_SPLITS")) {
+      std::string v(e);
+      std::size_t at = 0;
+      while (at < v.size()) {
+        const std::size_t end = std::min(v.find(',', at), v.size());
+        int n = 0, k = 0, sp = 0;
+        if (std::sscanf(v.substr(at, end - at).c_str(), "%d:%d:%d", &n, &k, &sp) == 3 && sp >= 1) r.push_back({n, k, sp});
+        at = end + 1;
+      }
+    }
+    return r;
+  }();
+  for (const Rule& r : rules)
+    if (r.n == N && r.k == K) return r.s;
   return 1;
 }
 
