@@ -702,7 +702,22 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D K-major bf16 tensor [rows, cols] (row stride ld elements), box = box_rows x 64, SW128.
+// Encoded maps are cached per host thread (direct-mapped on the parameters): a forward's weight
+// maps and its activation buffers' maps repeat every forward, and a map holds only the address,
+// shape and box, so a hit is exact.
 CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, std::uint64_t ld, std::uint32_t box_rows) {
+  struct Entry {
+    const void* p = nullptr;
+    std::uint64_t rows = 0, cols = 0, ld = 0;
+    std::uint32_t box = 0;
+    CUtensorMap m;
+  };
+  thread_local Entry cache[512];
+  std::uint64_t h = reinterpret_cast<std::uintptr_t>(ptr) * 0x9E3779B97F4A7C15ull;
+  h ^= (rows * 0xBF58476D1CE4E5B9ull) ^ (cols << 20) ^ (ld << 7) ^ box_rows;
+  h ^= h >> 29;
+  Entry& e = cache[h % 512];
+  if (e.p == ptr && e.rows == rows && e.cols == cols && e.ld == ld && e.box == box_rows) return e.m;
   CUtensorMap m;
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {ld * 2};
@@ -712,6 +727,12 @@ CUtensorMap make_map(const void* ptr, std::uint64_t rows, std::uint64_t cols, st
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  e.p = ptr;
+  e.rows = rows;
+  e.cols = cols;
+  e.ld = ld;
+  e.box = box_rows;
+  e.m = m;
   return m;
 }
 

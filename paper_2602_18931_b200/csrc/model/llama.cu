@@ -169,6 +169,7 @@ ForwardWorkspace::~ForwardWorkspace() {
                   static_cast<void*>(d_meta), gemm_ws})
     if (p) cudaFree(p);
   if (h_meta) cudaFreeHost(h_meta);
+  if (meta_ev) cudaEventDestroy(meta_ev);
 }
 
 LlamaModel::~LlamaModel() {
@@ -292,14 +293,19 @@ MetaLayout LlamaModel::pack_meta(const ForwardBatch& b, ForwardWorkspace& ws, cu
                     s_out = al(n_out * 4 + 4);
   const std::size_t s_msk = al(b.row_mask.size() * 8 + 8);
   const std::size_t need = 3 * s_tok + s_grp + s_ext + 2 * s_out + s_msk;
+  // the previous forward's metadata copy out of the pinned staging has retired (only that copy —
+  // not the whole previous forward, so the host can queue this forward while that one runs;
+  // the device block d_meta is overwritten in stream order after the previous forward's kernels)
+  if (ws.meta_pending) WS_CUDA(cudaEventSynchronize(ws.meta_ev));
+  ws.meta_pending = false;
   if (need > ws.cap_meta) {
+    WS_CUDA(cudaStreamSynchronize(st));  // d_meta may still be read by the previous forward
     if (ws.d_meta) cudaFree(ws.d_meta);
     if (ws.h_meta) cudaFreeHost(ws.h_meta);
     ws.cap_meta = std::max(need, 2 * ws.cap_meta);
     WS_CUDA(cudaMalloc(&ws.d_meta, ws.cap_meta));
     WS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ws.h_meta), ws.cap_meta, cudaHostAllocDefault));
   }
-  WS_CUDA(cudaStreamSynchronize(st));  // previous use of the staging buffer retired
   std::size_t o = 0;
   auto put = [&](const void* src, std::size_t bytes, std::size_t slot_bytes) {
     if (bytes) std::memcpy(ws.h_meta + o, src, bytes);
@@ -316,6 +322,9 @@ MetaLayout LlamaModel::pack_meta(const ForwardBatch& b, ForwardWorkspace& ws, cu
   const std::size_t o_pl = put(b.plant.data(), b.plant.size() * 4, s_out);
   const std::size_t o_msk = put(b.row_mask.data(), b.row_mask.size() * 8, s_msk);
   WS_CUDA(cudaMemcpyAsync(ws.d_meta, ws.h_meta, o, cudaMemcpyHostToDevice, st));
+  if (!ws.meta_ev) WS_CUDA(cudaEventCreateWithFlags(&ws.meta_ev, cudaEventDisableTiming));
+  WS_CUDA(cudaEventRecord(ws.meta_ev, st));
+  ws.meta_pending = true;
   ws.h2d += o;
   MetaLayout ml;
   ml.tok = o_tok;

@@ -122,6 +122,8 @@ struct ForwardWorkspace {
   unsigned char* d_meta = nullptr;  // batch metadata (device) + pinned staging
   unsigned char* h_meta = nullptr;
   std::size_t cap_meta = 0;
+  cudaEvent_t meta_ev = nullptr;  // recorded after a forward's metadata H2D (staging reuse)
+  bool meta_pending = false;
   void* gemm_ws = nullptr;  // split-K workspace (K1)
   std::size_t gemm_ws_bytes = 0;
   std::vector<AttnGroup> grp_sorted;

@@ -259,7 +259,7 @@ void LlamaModel::forward_tp(const ForwardBatch& b, float plant, cudaStream_t st,
   ensure_tp(ws, n, n_out);
   TPActs& A = *ws.tp;
   A.r[0].st = st;
-  for (int g = 1; g < P; ++g) {  // the ranks' previous metadata copies retired (staging reuse)
+  for (int g = 0; g < P; ++g) {  // every rank's previous forward retired (staging and peer buffers)
     DeviceGuard dg(A.r[g].device);
     WS_CUDA(cudaStreamSynchronize(A.r[g].st));
   }
