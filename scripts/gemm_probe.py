@@ -44,9 +44,13 @@ def timeline_small():
     L = ws.lib()
     L.ws_debug_gemm_trace.argtypes = [C.c_void_p]
     names = ["entry", "prologue", "dep_wait", "first_full", "last_mma", "acc_ready", "epi_done", "exit"]
-    for M in (48, 160, 512):
-        for (N, K, epi, name) in [(3072, 2048, 0, "1B qkv(bf16 epi)"), (2048, 2048, 1, "1B o"),
-                                  (2048, 8192, 1, "1B down"), (16384, 2048, 2, "1B gate_up")]:
+    shapes = [(3072, 2048, 0, "1B qkv(bf16 epi)"), (2048, 2048, 1, "1B o"), (2048, 8192, 1, "1B down"),
+              (16384, 2048, 2, "1B gate_up")]
+    if os.environ.get("WS_TIMELINE_8B"):
+        shapes = [(6144, 4096, 0, "8B qkv(bf16 epi)"), (4096, 4096, 1, "8B o"), (4096, 14336, 1, "8B down"),
+                  (28672, 4096, 2, "8B gate_up")]
+    for M in [int(x) for x in os.environ.get("WS_TIMELINE_M", "48,160,512").split(",")]:
+        for (N, K, epi, name) in shapes:
             A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
             out = torch.zeros(M, N, device="cuda", dtype=torch.float32) if epi == 1 else None
