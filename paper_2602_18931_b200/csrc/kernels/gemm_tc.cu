@@ -287,6 +287,11 @@ __device__ __forceinline__ void trace_point(int ablate, int i) {
 
 struct SplitArgs {
   int splits = 1;
+  // canonical K chunks of the whole K range (pick_chunks: from (N, K) only): every chunk
+  // accumulates from zero in its own TMEM columns and the chunks are summed in order, so a
+  // unit computing all of them in one CTA and `chunks` split units reducing their partials in
+  // split order give identical bits — the split can then follow the batch size
+  int chunks = 1;
   bool cluster = false;              // splits == 2 on CTA pairs: reduce through DSMEM (CS = 2)
   float* ws = nullptr;               // fp32 partials [splits][m_blocks*BM][N]
   unsigned int* tickets = nullptr;   // [m_blocks * n_tiles], zero-initialised, self-resetting
@@ -450,7 +455,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         tc_fence_after();
         const std::uint32_t d = tmem_base + acc * kAccStride;
+        const int chunk_len = num_k / sk.chunks;
         for (int kb = kb0; kb < kb1; ++kb) {
+          const int lk = kb - kb0;
+          const std::uint32_t dc = d + static_cast<std::uint32_t>((lk / chunk_len) * BN);  // this chunk's columns
+          const int in_chunk = lk % chunk_len;
           mbar_wait(&full[stage], phase);  // TMA → MMA: both async proxy, ordered by the mbarrier
           if (local == 0 && kb == kb0 && lane == 0) trace_point(ablate, 3);
           // descriptor start-address field is addr >> 4 (stage offsets are 16-byte multiples)
@@ -461,9 +470,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < BK / 16; ++k) {  // advance 16 elements = 32 B = 2 descriptor units
               if (ablate & 1) continue;
               if constexpr (CG == 2)
-                mma_bf16_pair(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+                mma_bf16_pair(dc, da + 2 * k, db + 2 * k, idesc, (in_chunk | k) != 0);
               else
-                mma_bf16(d, da + 2 * k, db + 2 * k, idesc, ((kb - kb0) | k) != 0);
+                mma_bf16(dc, da + 2 * k, db + 2 * k, idesc, (in_chunk | k) != 0);
             }
             // frees the smem slot (in both CTAs of a pair) when these MMAs retire
             if constexpr (CG == 2)
@@ -523,9 +532,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
       };
       const std::uint32_t t_row = tmem_base + acc * kAccStride + (static_cast<std::uint32_t>(grp * 32) << 16);
+      const int local_chunks = sk.chunks / KSPLITS;  // S == 1: all chunks; a split unit: one
       auto tmem_fetch = [&](int col, std::uint32_t (&r)[32]) {
         tmem_ld32(t_row + col, r);
         tmem_ld_wait();
+        if (local_chunks > 1) {  // 0 + c0 + c1 + ...: the split path's ordered sum of partials
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f + __uint_as_float(r[j]);
+          for (int c = 1; c < local_chunks; ++c) {
+            tmem_ld32(t_row + static_cast<std::uint32_t>(c * BN + col), r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
+        }
         if (norm.ss_in != nullptr) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rs);
@@ -838,13 +861,13 @@ void launch_cg(const GemmArgs& g, const SplitArgs& sk, int bn, int cg, cudaStrea
 struct TileChoice {
   int cg, bn;
 };
-TileChoice pick_tile(int M, int N, int granule, bool allow_pair) {
+TileChoice pick_tile(int M, int N, int granule, bool allow_pair, int bn_max = 256) {
   const int step = std::max(32, granule);
   const int mb = (M + BM - 1) / BM;
   TileChoice best{1, step};
   long best_cost = -1;
   for (int cg = 1; cg <= (allow_pair && mb > 1 ? 2 : 1); ++cg) {
-    for (int bn = 256 / step * step; bn >= std::max(64, step); bn -= step) {
+    for (int bn = bn_max / step * step; bn >= std::max(std::min(64, bn_max), step); bn -= step) {
       const long units = static_cast<long>((mb + cg - 1) / cg) * ((N + bn - 1) / bn);
       const long slots = cg == 2 ? kNumSMs / 2 : kNumSMs;
       const long per = cg == 2 ? std::max(2L * bn, 256L + bn) : 256L + 2L * bn;
@@ -895,6 +918,36 @@ int pick_splits(int N, int K) {
   return 1;
 }
 
+int pick_chunks(int N, int K) {
+  // Canonical K chunks, from (N, K) only (batch invariance). WS_GEMM_CHUNKS="N:K:C[,...]"
+  // overrides / extends the defaults (experiments).
+  struct Rule {
+    int n, k, c;
+  };
+  static const std::vector<Rule> rules = [] {
+    std::vector<Rule> r;
+    if (const char* e = std::getenv("WS_GEMM_CHUNKS")) {
+      std::string v(e);
+      std::size_t at = 0;
+      while (at < v.size()) {
+        const std::size_t end = std::min(v.find(',', at), v.size());
+        int n = 0, k = 0, c = 0;
+        if (std::sscanf(v.substr(at, end - at).c_str(), "%d:%d:%d", &n, &k, &c) == 3 && c >= 1) r.push_back({n, k, c});
+        at = end + 1;
+      }
+    }
+    return r;
+  }();
+  for (const Rule& r : rules)
+    if (r.n == N && r.k == K) return (K / BK) % r.c == 0 && r.c <= 4 ? r.c : 1;
+  // Default: the 1B down projection (N 2048, K 8192: 128 k-blocks on 16-32 CTAs at draft
+  // batches) in two chunks — split over two CTA sets below ~256 rows, -8 to -11 % per 1B
+  // forward at 48-192 rows, neutral at 496 (profiles/r02_gemm_chunks.md). The 8B shapes lose
+  // their BN = 256 pair tiles to the chunk accumulators (+11 % at 535 rows) and stay at one.
+  if (N == 2048 && K == 8192) return 2;
+  return 1;
+}
+
 // Workspace layout (fixed, whatever the GEMM shape): [tickets: kMaxTiles u32 | fp32 partials].
 // The self-resetting tickets must never move between launches of different shapes.
 constexpr std::size_t kMaxTiles = 65536;
@@ -924,9 +977,21 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   const char* pe = std::getenv("WS_GEMM_PAIR");
   const int pair_env = pe ? std::atoi(pe) : -1;
   const bool pair_ok = pair_env != 0 && g.cta_group != 1;
-  TileChoice tc = pick_tile(g.M, g.N, granule, pair_ok);
+  // canonical K chunks (only on the automatic path): all chunks in one CTA's TMEM (BN <= 256 /
+  // chunks), or — when even the split units fit in one wave of slots — one split unit per chunk
+  const int chunks = g.chunks_ > 0 ? g.chunks_
+                     : (g.splits == 0 && g.ws && !g.bn && g.epi != kEpiQKVRope) ? pick_chunks(g.N, g.K)
+                                                                                  : 1;
+  TileChoice tc = pick_tile(g.M, g.N, granule, pair_ok, 256 / chunks);
   if (g.cta_group == 2 || (pair_env == 2 && pair_ok)) tc.cg = 2;
   if (g.bn) tc.bn = g.bn;
+  bool chunk_split = false;
+  if (chunks > 1) {
+    const long m_units = tc.cg == 2 ? ((g.M + BM - 1) / BM + 1) / 2 : (g.M + BM - 1) / BM;
+    const long units = m_units * ((g.N + tc.bn - 1) / tc.bn);
+    const long slots = tc.cg == 2 ? pair_clusters() : kNumSMs;
+    chunk_split = units * chunks <= slots;
+  }
   bool csplit_now = false;
   // WS_GEMM_CSPLIT=1 (experiment): residual-epilogue projections (O, down) run as cluster
   // split-K on CTA pairs — a fixed split count whatever M, so results stay batch-invariant —
@@ -955,7 +1020,12 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   if (bn % 32 && g.cta_group != 2) tc.cg = 1;  // an explicit odd-16 width runs on single CTAs
   if (tc.cg == 2 && bn % 32) throw std::invalid_argument("gemm: CTA pairs need BN % 32");
   SplitArgs sk;
-  sk.splits = csplit_now ? 2 : g.splits > 0 ? g.splits : (g.ws ? pick_splits(g.N, g.K) : 1);
+  sk.splits = csplit_now ? 2 : g.splits > 0 ? g.splits : chunk_split ? chunks : (g.ws ? pick_splits(g.N, g.K) : 1);
+  sk.chunks = csplit_now ? 1 : chunks;
+  if (sk.chunks > 1 && sk.splits != 1 && sk.splits != sk.chunks)
+    throw std::logic_error("gemm: canonical chunks need splits of 1 or chunks");
+  if (sk.chunks > 1 && (g.K / BK) % sk.chunks) throw std::invalid_argument("gemm: K not a multiple of the chunks");
+  if (sk.chunks / sk.splits * bn > kAccStride) throw std::invalid_argument("gemm: chunk accumulators exceed TMEM");
 
   // two K halves on CTA pairs reduce through distributed shared memory (no workspace);
   // WS_GEMM_DSMEM=0 keeps them on the global-partials path (tests compare the two bit for bit)
@@ -993,6 +1063,7 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
         s.bn = bn;
         s.splits = sk.splits;
         s.cta_group = tc.cg;
+        s.chunks_ = sk.chunks;
         gemm_tn(s, st);
       }
       return;

@@ -58,6 +58,7 @@ struct GemmArgs {
   void* ws = nullptr;
   std::size_t ws_bytes = 0;
   int splits = 0;
+  int chunks_ = 0;  // canonical K chunks (0 = from (N, K); internal: row slices inherit the parent's)
 };
 
 // C = A · W^T on tcgen05 (sm_100a). Throws on bad shapes / CUDA errors.

@@ -230,6 +230,7 @@ void* LlamaModel::weight(const std::string& w, int l, std::int64_t* numel) {
   if (w == "ws_attn") return ret(ws0_->attn, static_cast<std::int64_t>(ws0_->cap_rows) * s_.n_q * s_.hd);
   if (w == "ws_h") return ret(ws0_->h, static_cast<std::int64_t>(ws0_->cap_rows) * s_.ffn);
   if (w == "ws_q") return ret(ws0_->q, static_cast<std::int64_t>(ws0_->cap_rows) * s_.n_q * s_.hd);
+  if (w == "ws_xo") return ret(ws0_->xo, static_cast<std::int64_t>(ws0_->cap_out) * d);
   // the KV pools [layer][slot][n_kv][hd] (tests read back what the QKV epilogue stored)
   if (w == "k_pool" || w == "v_pool")
     return ret(w == "k_pool" ? k_pool_ : v_pool_, static_cast<std::int64_t>(s_.layers) * n_slots_ * s_.n_kv * s_.hd);
