@@ -945,6 +945,7 @@ int pick_chunks(int N, int K) {
   // forward at 48-192 rows, neutral at 496 (profiles/r02_gemm_chunks.md). The 8B shapes lose
   // their BN = 256 pair tiles to the chunk accumulators (+11 % at 535 rows) and stay at one.
   if (N == 2048 && K == 8192) return 2;
+  if (N == 4096 && K == 14336) return 2;  // the 8B down projection (224 k-blocks)
   return 1;
 }
 
@@ -982,15 +983,52 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   const int chunks = g.chunks_ > 0 ? g.chunks_
                      : (g.splits == 0 && g.ws && !g.bn && g.epi != kEpiQKVRope) ? pick_chunks(g.N, g.K)
                                                                                   : 1;
-  TileChoice tc = pick_tile(g.M, g.N, granule, pair_ok, 256 / chunks);
+  // The C chunk accumulators of an unsplit unit take C x BN TMEM columns: within one of the two
+  // 256-column buffers, or — when every CTA (pair) holds a single unit, so the second buffer is
+  // never used — within all 512.
+  auto units_of = [&](const TileChoice& t) {
+    const long m_units = t.cg == 2 ? ((g.M + BM - 1) / BM + 1) / 2 : (g.M + BM - 1) / BM;
+    return m_units * ((g.N + t.bn - 1) / t.bn);
+  };
+  auto slots_of = [&](const TileChoice& t) { return t.cg == 2 ? static_cast<long>(pair_clusters()) : kNumSMs; };
+  // whether some CTA (pair) may run more than one unit (the launch's grid, see launch())
+  auto multi_unit = [&](const TileChoice& t) {
+    if (g.max_ctas < 0) return false;
+    const long cap = g.max_ctas > 0 ? (t.cg == 2 ? std::max(1, g.max_ctas / 2) : g.max_ctas) : slots_of(t);
+    return units_of(t) > std::min(cap, slots_of(t));
+  };
+  TileChoice tc = pick_tile(g.M, g.N, granule, pair_ok);
   if (g.cta_group == 2 || (pair_env == 2 && pair_ok)) tc.cg = 2;
   if (g.bn) tc.bn = g.bn;
   bool chunk_split = false;
   if (chunks > 1) {
-    const long m_units = tc.cg == 2 ? ((g.M + BM - 1) / BM + 1) / 2 : (g.M + BM - 1) / BM;
-    const long units = m_units * ((g.N + tc.bn - 1) / tc.bn);
-    const long slots = tc.cg == 2 ? pair_clusters() : kNumSMs;
-    chunk_split = units * chunks <= slots;
+    // Tile and split chosen together from the shared-memory cost model of pick_tile: unsplit
+    // (all chunks in one CTA) or one unit per chunk (two chunks on CTA pairs reduce through
+    // distributed shared memory, otherwise through global partials — the latter charged extra).
+    const int step = std::max(32, granule);
+    const int num_k = g.K / BK;
+    const int mb = (g.M + BM - 1) / BM;
+    long best = -1;
+    for (int cg = 1; cg <= (pair_ok && mb > 1 ? 2 : 1); ++cg) {
+      if (g.cta_group && cg != g.cta_group) continue;
+      for (int bn = 256 / step * step; bn >= std::max(64, step); bn -= step) {
+        const TileChoice t{cg, bn};
+        const long per = cg == 2 ? std::max(2L * bn, 256L + bn) : 256L + 2L * bn;
+        for (int sp : {1, chunks}) {
+          if (sp == 1 && chunks * bn > kAccStride && (multi_unit(t) || chunks * bn > kTmemCols)) continue;
+          const long units = units_of(t) * sp;
+          const long rounds = (units + slots_of(t) - 1) / slots_of(t);
+          const long overhead = sp == 1 ? 0 : (cg == 2 && chunks == 2 ? 2048 : 8192);
+          const long cost = rounds * per * (num_k / sp) + overhead;
+          if (best < 0 || cost < best) {
+            best = cost;
+            tc = t;
+            chunk_split = sp > 1;
+          }
+        }
+      }
+    }
+    if (g.bn) tc.bn = g.bn;
   }
   bool csplit_now = false;
   // WS_GEMM_CSPLIT=1 (experiment): residual-epilogue projections (O, down) run as cluster
@@ -1025,7 +1063,17 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   if (sk.chunks > 1 && sk.splits != 1 && sk.splits != sk.chunks)
     throw std::logic_error("gemm: canonical chunks need splits of 1 or chunks");
   if (sk.chunks > 1 && (g.K / BK) % sk.chunks) throw std::invalid_argument("gemm: K not a multiple of the chunks");
-  if (sk.chunks / sk.splits * bn > kAccStride) throw std::invalid_argument("gemm: chunk accumulators exceed TMEM");
+  if (sk.chunks / sk.splits * bn > kAccStride) {
+    // only with one unit per CTA (pair): the unit's chunks may span both accumulator buffers
+    TileChoice t = tc;
+    t.bn = bn;
+    if (sk.chunks / sk.splits * bn > kTmemCols || multi_unit(t))
+      throw std::invalid_argument("gemm: chunk accumulators exceed TMEM (M " + std::to_string(g.M) + " N " +
+                                  std::to_string(g.N) + " K " + std::to_string(g.K) + " bn " + std::to_string(bn) +
+                                  " cg " + std::to_string(tc.cg) + " chunks " + std::to_string(sk.chunks) +
+                                  " splits " + std::to_string(sk.splits) + " units " + std::to_string(units_of(t)) +
+                                  " slots " + std::to_string(slots_of(t)) + ")");
+  }
 
   // two K halves on CTA pairs reduce through distributed shared memory (no workspace);
   // WS_GEMM_DSMEM=0 keeps them on the global-partials path (tests compare the two bit for bit)

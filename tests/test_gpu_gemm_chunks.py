@@ -21,7 +21,7 @@ sys.path.insert(0, sys.argv[1])
 from paper_2602_18931_b200 import ops
 torch.manual_seed(0)
 out = []
-for (N, K) in [(2048, 8192), (2048, 2048), (4096, 4096)]:
+for (N, K) in [(2048, 8192), (2048, 2048), (4096, 4096), (4096, 14336)]:
     W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
     A = torch.randn(1200, K, device="cuda").to(torch.bfloat16)
     R = torch.randn(1200, N, device="cuda")
@@ -51,7 +51,7 @@ print(out)
 
 @pytest.mark.gpu
 def test_chunked_split_equals_in_cta_chunks():
-    env = dict(os.environ, WS_GEMM_CHUNKS="2048:8192:2,2048:2048:4,4096:4096:2")
+    env = dict(os.environ, WS_GEMM_CHUNKS="2048:8192:2,2048:2048:4,4096:4096:2,4096:14336:2")
     r = subprocess.run([sys.executable, "-c", CHILD, ROOT], capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     res = eval(r.stdout.strip().splitlines()[-1])
