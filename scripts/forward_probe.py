@@ -114,8 +114,11 @@ def main():
     devs = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0"])]
     for dev in devs:
         nv = int(os.environ.get("WS_PROBE_VERIFY_REQ", "105"))  # 198 = the mean batch under verify batching
-        print(json.dumps(run(L, "llama3-8b", verify_batch(n_req=nv), nv * 256, iters, dev)))
-        print(json.dumps(run(L, "llama3.2-1b", draft_batch(), 256 * 1024, iters, dev)))
+        only = os.environ.get("WS_PROBE_ONLY", "")  # "verify" / "draft": one of the two forwards
+        if only != "draft":
+            print(json.dumps(run(L, "llama3-8b", verify_batch(n_req=nv), nv * 256, iters, dev)))
+        if only != "verify":
+            print(json.dumps(run(L, "llama3.2-1b", draft_batch(), 256 * 1024, iters, dev)))
 
 
 if __name__ == "__main__":
