@@ -103,6 +103,7 @@ void run_model(ws_ctx* ctx, const ws_sim_cfg* c, ws_run_out* out, bool wallclock
     // prompt prefill: its own phase before the protocol starts (every verify then feeds k+1 rows)
     const std::uint32_t first = c->first_request;
     const std::uint32_t n_local = c->local_requests ? c->local_requests : c->num_requests - c->first_request;
+    mp.set_pdl_late_for(n_local);
     std::vector<std::uint32_t> reqs(n_local);
     for (std::uint32_t i = 0; i < n_local; ++i) reqs[i] = first + i;
     const wsb::ModelPair::PrefillStats pre = mp.prefill_prompts(reqs.data(), reqs.size());

@@ -277,6 +277,7 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, Wait&& wait, int BN
 // slot full, last MMA of the unit issued, accumulator ready in the epilogue, epilogue done, exit.
 __device__ unsigned long long g_gemm_trace[8];
 constexpr int kEarlyTrigger = 1 << 16;  // (flag bit in `ablate`) trigger dependents at entry
+constexpr int kLateTrigger = 1 << 17;   // (flag bit) trigger dependents once the last accumulator is ready
 __device__ __forceinline__ void trace_point(int ablate, int i) {
   if ((ablate & 8) && blockIdx.x == 0) {
     unsigned long long t;
@@ -529,6 +530,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto acc_wait = [&] {
         mbar_wait(&tfull[acc], (local >> 1) & 1);
         if (local == 0 && warp == 2 && lane == 0) trace_point(ablate, 5);
+        // the CTA's last accumulator is complete: only its epilogue remains, so the next kernel
+        // of the chain may start its prologue and weight prefetch on the SMs that free up
+        if ((ablate & kLateTrigger) && u + step >= total && warp == 2 && lane == 0) pdl_trigger_now();
         tc_fence_after();
       };
       const std::uint32_t t_row = tmem_base + acc * kAccStride + (static_cast<std::uint32_t>(grp * 32) << 16);
@@ -800,6 +804,7 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
     const char* e = std::getenv("WS_PDL_EARLY_GRID");
     return e ? std::atoi(e) : 0;
   }();
+  const int late = g.pdl_late > 0 ? kLateTrigger : 0;
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, BM);
   const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, static_cast<std::uint32_t>(bn / CG));
   const int m_blocks = (g.M + BM - 1) / BM;
@@ -810,7 +815,7 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
     // max_ctas < 0: one CTA per unit (not persistent: SMs free up between units, so a
     // concurrent higher-priority stream's kernels get scheduled sooner)
     const int grid = g.max_ctas < 0 ? total : std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
-    const int flags = ablate | (grid <= early_grid ? kEarlyTrigger : 0);
+    const int flags = ablate | late | (grid <= early_grid ? kEarlyTrigger : 0);
     launch_pdl(gemm_tn_kernel<EPI, 1>, dim3(grid), dim3(kThreads), smem, st, 1, ta, tb, g.M, g.N, g.K, m_blocks,
                n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
   } else if constexpr (CS == 2) {
@@ -820,14 +825,14 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
                           total, max_clusters<4>(), bn, stages);
     int clusters = g.max_ctas < 0 ? total : std::min(total, max_clusters<4>());
     if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 4));
-    const int flags = ablate | (4 * clusters <= early_grid ? kEarlyTrigger : 0);
+    const int flags = ablate | late | (4 * clusters <= early_grid ? kEarlyTrigger : 0);
     launch_pdl(gemm_tn_kernel<EPI, 2, 2>, dim3(4 * clusters), dim3(kThreads), smem, st, 4, ta, tb, g.M, g.N, g.K,
                m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
   } else {
     const int total = (m_blocks + 1) / 2 * n_tiles * sk.splits;
     int clusters = g.max_ctas < 0 ? total : std::min(total, pair_clusters());
     if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 2));
-    const int flags = ablate | (2 * clusters <= early_grid ? kEarlyTrigger : 0);
+    const int flags = ablate | late | (2 * clusters <= early_grid ? kEarlyTrigger : 0);
     launch_pdl(gemm_tn_kernel<EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2, ta, tb, g.M, g.N, g.K,
                m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
   }

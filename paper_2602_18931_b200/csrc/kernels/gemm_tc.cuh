@@ -59,6 +59,7 @@ struct GemmArgs {
   std::size_t ws_bytes = 0;
   int splits = 0;
   int chunks_ = 0;  // canonical K chunks (0 = from (N, K); internal: row slices inherit the parent's)
+  int pdl_late = 0;  // 1: dependents may launch once each CTA's last accumulator is ready
 };
 
 // C = A · W^T on tcgen05 (sm_100a). Throws on bad shapes / CUDA errors.

@@ -385,6 +385,7 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
     g.ws = gemm_ws_;
     g.ws_bytes = gemm_ws_bytes_;
     g.max_ctas = max_ctas_;
+    g.pdl_late = pdl_late_ ? 1 : 0;
     return g;
   };
   const std::int64_t layer_stride = n_slots_ * s_.n_kv * s_.hd;

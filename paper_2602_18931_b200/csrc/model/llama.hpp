@@ -150,6 +150,8 @@ class LlamaModel {
   KernelProfiler& profiler() { return ws0_->prof; }
   // Cap on the persistent GEMM grids (0 = every SM): leaves SMs to a concurrent forward.
   void set_max_ctas(int n) { max_ctas_ = n; }
+  // the GEMMs let the next kernel launch once their last accumulator is ready (see ModelPair)
+  void set_pdl_late(bool on) { pdl_late_ = on; }
   // tp > 1: the target split over GPUs device .. device + tp - 1 (tensor parallel, llama_tp.cu)
   LlamaModel(const LlamaShape& shape, std::uint64_t seed, std::int64_t n_slots, int max_rows, int device, int tp = 1);
   int tp() const { return tp_; }
@@ -190,6 +192,7 @@ class LlamaModel {
   std::vector<std::unique_ptr<TPShard>> shards_;
   std::unique_ptr<ForwardWorkspace> ws0_;  // the model's own workspace (test / single-caller API)
   int max_ctas_ = 0;
+  bool pdl_late_ = false;
   LlamaShape s_;
   int device_;
   std::int64_t n_slots_;

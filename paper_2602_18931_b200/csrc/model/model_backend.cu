@@ -248,6 +248,20 @@ ModelPair::ModelPair(const ModelPairCfg& cfg, int device) : cfg_(cfg), device_(d
   reset_requests();
 }
 
+// Late PDL trigger: a model's GEMMs let the next kernel of its chain launch once their last
+// accumulator is ready, so its prologue and weight prefetch overlap the epilogue on the SMs that
+// free up — at the price of dependents parked on those SMs, which the other lane's kernels then
+// cannot use. Measured on config 3 (profiles/r02_pdl_late.md): for the draft model, +3.9 % at
+// 64 requests per GPU (the draft chain is the critical path), -0.5 % at 128 and neutral at 256
+// (the verify lane loses what the draft lane gains); for both models, -1 % at 256. Default: the
+// draft model's GEMMs at <= 96 requests per GPU. WS_PDL_LATE = 0 | 1 | draft | target forces.
+void ModelPair::set_pdl_late_for(std::uint32_t n_local) {
+  const char* e = std::getenv("WS_PDL_LATE");
+  const std::string v = e ? e : (n_local <= 96 ? "draft" : "0");
+  target_->set_pdl_late(v == "1" || v == "target");
+  for (int r = 0; r < draft_replicas(); ++r) draft(r).set_pdl_late(v == "1" || v == "draft");
+}
+
 ModelPair::~ModelPair() {
   cudaSetDevice(device_);
   target_.reset();

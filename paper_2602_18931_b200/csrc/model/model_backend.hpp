@@ -100,6 +100,8 @@ class ModelPair {
   ModelPair(const ModelPairCfg& cfg, int device);
   ~ModelPair();
   void reset_requests();  // forget all cached KV state (new run)
+  // Late PDL trigger policy for a run over n_local requests (see model_backend.cu)
+  void set_pdl_late_for(std::uint32_t n_local);
   void evict(std::uint32_t r);  // forget request r's cached KV (target, controller draft, worker)
   // Prompt prefill (its own phase, before the first verify / draft): the KV of prompt positions
   // [0, P-1) of each listed request is written for the target (verify cache), and once for the
