@@ -871,7 +871,15 @@ TileChoice pick_tile(int M, int N, int granule, bool allow_pair, int bn_max = 25
   const int mb = (M + BM - 1) / BM;
   TileChoice best{1, step};
   long best_cost = -1;
-  for (int cg = 1; cg <= (allow_pair && mb > 1 ? 2 : 1); ++cg) {
+  // WS_GEMM_PAIR1=1: CTA pairs also for a single 128-row block (the second CTA's A rows are all
+  // padding; a pair tile moves half the weight rows per SM). Isolated small-batch forwards gain
+  // 2-4 %, but a pair takes two SMs per tile and the 4-GPU bench, where both lanes share the
+  // SMs, lost 1 % (profiles/r02_gemm_chunks.md): off by default.
+  static const bool pair1 = [] {
+    const char* e = std::getenv("WS_GEMM_PAIR1");
+    return e && e[0] == '1';
+  }();
+  for (int cg = 1; cg <= (allow_pair && (mb > 1 || pair1) ? 2 : 1); ++cg) {
     for (int bn = bn_max / step * step; bn >= std::max(std::min(64, bn_max), step); bn -= step) {
       const long units = static_cast<long>((mb + cg - 1) / cg) * ((N + bn - 1) / bn);
       const long slots = cg == 2 ? kNumSMs / 2 : kNumSMs;
@@ -1014,7 +1022,11 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
     const int num_k = g.K / BK;
     const int mb = (g.M + BM - 1) / BM;
     long best = -1;
-    for (int cg = 1; cg <= (pair_ok && mb > 1 ? 2 : 1); ++cg) {
+    static const bool pair1 = [] {
+      const char* e = std::getenv("WS_GEMM_PAIR1");
+      return e && e[0] == '1';
+    }();
+    for (int cg = 1; cg <= (pair_ok && (mb > 1 || pair1) ? 2 : 1); ++cg) {
       if (g.cta_group && cg != g.cta_group) continue;
       for (int bn = 256 / step * step; bn >= std::max(64, step); bn -= step) {
         const TileChoice t{cg, bn};
