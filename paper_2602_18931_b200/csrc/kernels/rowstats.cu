@@ -143,6 +143,10 @@ __device__ __forceinline__ Stats merge(const Stats& a, const Stats& b) {
 // contiguous and ids grow with the vector index, so a tie keeps the earlier vector, matching the
 // Prediction tie rule.
 constexpr float kSlack = 16.f;
+#ifndef WS_K3_SLOTS
+#define WS_K3_SLOTS 2
+#endif
+constexpr int kSlots = WS_K3_SLOTS;  // accumulator slots in use (alternate chunks)
 
 struct Lane {
   float m;        // log2-domain reference of (z, s)
@@ -306,7 +310,10 @@ template <int W>
 __device__ __forceinline__ void stream_chunks(Lane& a, const __nv_bfloat16* __restrict__ x, std::uint32_t lo,
                                               std::uint32_t nch, float cl, std::uint32_t lane) {
   constexpr std::uint32_t E = 2 * W;
-  constexpr int B = 4;
+#ifndef WS_K3_B
+#define WS_K3_B 4
+#endif
+  constexpr int B = WS_K3_B;
   const float slack_x = kSlack / cl;
   const std::uint32_t* base = reinterpret_cast<const std::uint32_t*>(x + lo) + lane * W;
   const int nj = lane < nch ? static_cast<int>((nch - lane + 31) / 32) : 0;
@@ -318,7 +325,7 @@ __device__ __forceinline__ void stream_chunks(Lane& a, const __nv_bfloat16* __re
     for (int u = 0; u < B; ++u) q[u] = ld_chunk<W>(base + (j + u) * 32 * W);
 #pragma unroll
     for (int u = 0; u < B; ++u) {
-      if (u & 1)
+      if ((u & 1) && kSlots > 1)
         absorb<W, 1>(a, q[u], id(j + u), cl, slack_x);
       else
         absorb<W, 0>(a, q[u], id(j + u), cl, slack_x);
@@ -482,8 +489,11 @@ __device__ __forceinline__ void finish_segment(const RowArgs& g, Stats r, std::u
 }
 
 // 4 CTAs of 8 warps per SM (<= 64 registers): measured best against 1-3 (profiles/r02_ncu_k3.md)
+#ifndef WS_K3_MINB
+#define WS_K3_MINB 4
+#endif
 template <int vw>
-__global__ void __launch_bounds__(kThreads, 4) row_stats_kernel(const __grid_constant__ RowArgs g) {
+__global__ void __launch_bounds__(kThreads, WS_K3_MINB) row_stats_kernel(const __grid_constant__ RowArgs g) {
   pdl_trigger();
   pdl_wait();  // inputs come from the previous kernel of the chain
   const std::uint32_t lane = threadIdx.x & 31;
