@@ -993,9 +993,11 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
   const bool pair_ok = pair_env != 0 && g.cta_group != 1;
   // canonical K chunks (only on the automatic path): all chunks in one CTA's TMEM (BN <= 256 /
   // chunks), or — when even the split units fit in one wave of slots — one split unit per chunk
+  // (without a split workspace only the distributed-shared-memory split — two chunks on CTA
+  // pairs — can be taken; the unsplit in-CTA chunks need none)
   const int chunks = g.chunks_ > 0 ? g.chunks_
-                     : (g.splits == 0 && g.ws && !g.bn && g.epi != kEpiQKVRope) ? pick_chunks(g.N, g.K)
-                                                                                  : 1;
+                     : (g.splits == 0 && !g.bn && g.epi != kEpiQKVRope) ? pick_chunks(g.N, g.K)
+                                                                       : 1;
   // The C chunk accumulators of an unsplit unit take C x BN TMEM columns: within one of the two
   // 256-column buffers, or — when every CTA (pair) holds a single unit, so the second buffer is
   // never used — within all 512.
@@ -1033,6 +1035,7 @@ void gemm_tn(const GemmArgs& g, cudaStream_t st) {
         const long per = cg == 2 ? std::max(2L * bn, 256L + bn) : 256L + 2L * bn;
         for (int sp : {1, chunks}) {
           if (sp == 1 && chunks * bn > kAccStride && (multi_unit(t) || chunks * bn > kTmemCols)) continue;
+          if (sp > 1 && !g.ws && !(cg == 2 && chunks == 2)) continue;  // global partials need a workspace
           const long units = units_of(t) * sp;
           const long rounds = (units + slots_of(t) - 1) / slots_of(t);
           const long overhead = sp == 1 ? 0 : (cg == 2 && chunks == 2 ? 2048 : 8192);
