@@ -341,6 +341,15 @@ MetaLayout LlamaModel::pack_meta(const ForwardBatch& b, ForwardWorkspace& ws, cu
   return ml;
 }
 
+// WS_PREFILL_CHUNKS=1 (A/B): prompt-prefill forwards use the shapes' canonical chunks too
+static bool prefill_one_chunk() {
+  static const bool one = [] {
+    const char* e = std::getenv("WS_PREFILL_CHUNKS");
+    return !(e && e[0] == '1');
+  }();
+  return one;
+}
+
 void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, ForwardWorkspace& ws) {
   const int n = static_cast<int>(b.tok.size());
   const int n_out = static_cast<int>(b.out_rows.size());
@@ -386,6 +395,7 @@ void LlamaModel::forward(const ForwardBatch& b, float plant, cudaStream_t st, Fo
     g.ws_bytes = gemm_ws_bytes_;
     g.max_ctas = max_ctas_;
     g.pdl_late = pdl_late_ ? 1 : 0;
+    if (b.prefill && prefill_one_chunk()) g.chunks_ = 1;
     return g;
   };
   const std::int64_t layer_stride = n_slots_ * s_.n_kv * s_.hd;

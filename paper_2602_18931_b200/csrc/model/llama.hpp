@@ -37,7 +37,14 @@ struct ForwardBatch {
   std::vector<std::int32_t> out_rows;
   std::vector<std::int32_t> plant;  // per output row: planted token (or -1)
   std::vector<unsigned long long> row_mask;  // per row (only read for masked groups)
+  // A prompt-prefill forward (ModelPair::prefill_prompts, and the prompt step of export_trace):
+  // its GEMMs keep one canonical K chunk. Every position's KV is computed by the same kind of
+  // forward in every run (the prompt [0, P-1) by prefill forwards, later positions by verify /
+  // draft forwards), so each kind only has to be batch-invariant on its own — and the 8 128-row
+  // prefill batches keep their widest tiles (profiles/r02_gemm_chunks.md).
+  bool prefill = false;
   void clear() {
+    prefill = false;
     row_mask.clear();
     tok.clear();
     pos.clear();

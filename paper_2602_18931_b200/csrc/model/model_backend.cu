@@ -328,6 +328,7 @@ ModelPair::PrefillStats ModelPair::prefill_prompts(const std::uint32_t* reqs, st
         b.groups.push_back(AttnGroup{row0, P - 1, base, 0, eoff, P - 1});
       }
       b.row_mask.assign(b.tok.size(), 0ull);
+      b.prefill = true;
       nvtxRangePushA(side == 0 ? "ws.prefill.target" : "ws.prefill.draft");
       m.forward(b, 0.f, sd.st, *sd.ws);  // no output rows: KV only, no LM head
       nvtxRangePop();
@@ -409,6 +410,32 @@ void ModelPair::export_trace(std::uint32_t first, std::uint32_t n, std::uint32_t
     WS_CUDA(cudaMemset(sd.d_rs, 0, wb));
     sd.h.resize(n);
   }
+  // The prompt head [0, P-1) as in a model run: one prompt-prefill forward (KV only, the
+  // prefill kind of ForwardBatch), so every position's KV comes from the same kind of forward
+  // as in ModelPair::prefill_prompts + the verify / draft forwards.
+  if (P > 1) {
+    for (Side& sd : sides) {
+      DeviceGuard dg(sd.dev);
+      ForwardBatch b;
+      for (std::uint32_t j = 0; j < n; ++j) {
+        const std::uint32_t r = first + j;
+        const std::vector<TokenId>& pr = prompt(r);
+        const std::int32_t base = static_cast<std::int32_t>(r) * sd.stride;
+        const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
+        const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
+        for (std::int32_t p = 0; p < P - 1; ++p) {
+          b.tok.push_back(static_cast<std::int32_t>(pr[p]));
+          b.pos.push_back(p);
+          b.slot.push_back(base + p);
+          b.extra.push_back(base + p);
+        }
+        b.groups.push_back(AttnGroup{row0, P - 1, base, 0, eoff, P - 1});
+      }
+      b.row_mask.assign(b.tok.size(), 0ull);
+      b.prefill = true;
+      sd.m->forward(b, 0.f, sd.st, *sd.ws);
+    }
+  }
   std::vector<TokenId> last(n);  // the token fed at each step (prompt tail, then greedy)
   for (std::uint32_t i = 0; i < length; ++i) {
     for (Side& sd : sides) {
@@ -420,17 +447,15 @@ void ModelPair::export_trace(std::uint32_t first, std::uint32_t n, std::uint32_t
         const std::int32_t base = static_cast<std::int32_t>(r) * sd.stride;
         const std::int32_t row0 = static_cast<std::int32_t>(b.tok.size());
         const std::int32_t eoff = static_cast<std::int32_t>(b.extra.size());
-        // step 0 prefills the prompt; step i feeds the greedy token of position i - 1
-        const std::int32_t p0 = i == 0 ? 0 : P + static_cast<std::int32_t>(i) - 1;
-        const std::int32_t p1 = i == 0 ? P : p0 + 1;
-        for (std::int32_t p = p0; p < p1; ++p) {
-          const TokenId t = i == 0 ? pr[p] : last[j];
-          b.tok.push_back(static_cast<std::int32_t>(t));
-          b.pos.push_back(p);
-          b.slot.push_back(base + p);
-          b.extra.push_back(base + p);
-        }
-        b.groups.push_back(AttnGroup{row0, p1 - p0, base, p0, eoff, p1 - p0});
+        // step 0 feeds the last prompt token (position P - 1) over the prefilled head; step i
+        // feeds the greedy token of position P + i - 1
+        const std::int32_t p0 = P - 1 + static_cast<std::int32_t>(i);
+        const TokenId t = i == 0 ? pr[P - 1] : last[j];
+        b.tok.push_back(static_cast<std::int32_t>(t));
+        b.pos.push_back(p0);
+        b.slot.push_back(base + p0);
+        b.extra.push_back(base + p0);
+        b.groups.push_back(AttnGroup{row0, 1, base, p0, eoff, 1});
         b.out_rows.push_back(static_cast<std::int32_t>(b.tok.size()) - 1);
         b.plant.push_back(plant(static_cast<TokenId>(b.tok.back()), sd.draft));
       }
