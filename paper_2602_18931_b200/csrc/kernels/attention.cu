@@ -112,7 +112,19 @@ __global__ void __launch_bounds__(32 * VW * KS) attn_mma_kernel(const __nv_bfloa
   const int nvec = g.n_rows * G;
   const int ctx = g.prefix_len + g.extra_len;
   const std::size_t slot_stride = static_cast<std::size_t>(nkv) * HD;
-  const int n_tiles = (ctx + kTile - 1) / kTile;
+  // Causal groups: this entry's rows see keys up to the last row's own position, so the tiles past
+  // it are masked for every row of the entry and are skipped (a fully masked tile leaves the
+  // online-softmax state unchanged). Prompt-prefill groups of 127 rows come as many entries, the
+  // early ones seeing only a fraction of the keys.
+  int ctx_eff = ctx;
+#ifndef WS_ATTN_SKIP
+#define WS_ATTN_SKIP 1
+#endif
+  if (WS_ATTN_SKIP && !g.masked) {
+    const int v_last = min(nvec, g.pad + 16 * VW) - 1;
+    if (v_last >= 0) ctx_eff = min(ctx, g.prefix_len + g.extra_len - g.n_rows + v_last / G + 1);
+  }
+  const int n_tiles = (ctx_eff + kTile - 1) / kTile;
   const int n_iter = (n_tiles + KS - 1) / KS;
 
   auto slot_of = [&](int p) -> int {
