@@ -61,11 +61,17 @@ __host__ __device__ constexpr int stage_bytes(int bn, int cg) { return a_bytes()
 // cluster split-K (CS = 2): the receiving CTA's two 128 x 33 fp32 chunk buffers, after the ring
 constexpr int kCsStride = 36;  // floats per row of a chunk buffer (16-byte rows, spread banks)
 constexpr int kCsBufBytes = 2 * 128 * kCsStride * 4;
-inline int ring_stages(int bn, int cg, int cs = 1) {
-  return std::min(8, (kSmemBudget - 2048 - (cs == 2 ? kCsBufBytes : 0)) / stage_bytes(bn, cg));
+// fp32-residual epilogue staging (launches whose CTAs run several units): per epilogue warp a
+// [32][33] fp32 tile + a [32][17] bf16-pair tile
+constexpr int kEpiStageFloats = 32 * 33 + 32 * 17;
+constexpr int kEpiStageBytes = 4 * kEpiStageFloats * 4;
+inline int ring_stages(int bn, int cg, int cs = 1, bool epi_stage = false) {
+  return std::min(8, (kSmemBudget - 2048 - (cs == 2 ? kCsBufBytes : 0) - (epi_stage ? kEpiStageBytes : 0)) /
+                         stage_bytes(bn, cg));
 }
-inline int smem_bytes(int bn, int cg, int cs = 1) {
-  return 1024 + ring_stages(bn, cg, cs) * stage_bytes(bn, cg) + 256 + (cs == 2 ? kCsBufBytes : 0);
+inline int smem_bytes(int bn, int cg, int cs = 1, bool epi_stage = false) {
+  return 1024 + ring_stages(bn, cg, cs, epi_stage) * stage_bytes(bn, cg) + 256 + (cs == 2 ? kCsBufBytes : 0) +
+         (epi_stage ? kEpiStageBytes : 0);
 }
 
 __device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
@@ -96,9 +102,10 @@ __device__ __forceinline__ void store_bf16_tail(__nv_bfloat16* dst, const std::u
 // by every lane (TMEM loads are warp-collective). wait() blocks until the accumulator is ready:
 // inputs that do not depend on it (the residual row) are loaded before the call, so their L2
 // latency overlaps the main loop instead of following it.
-template <int EPI, class Fetch, class Wait>
+template <int EPI, bool STG, class Fetch, class Wait>
 __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, Wait&& wait, int BN, int row, int M, int N, int n_blk,
-                                              void* out, int ldo, const RopeEpi& rp, const NormEpi& nm) {
+                                              void* out, int ldo, const RopeEpi& rp, const NormEpi& nm,
+                                              float* estage = nullptr) {
   const bool live = row < M;
   if constexpr (EPI != kEpiAddF32 && EPI != kEpiQKVRope) wait();
   if constexpr (EPI == kEpiSwiGLU) {
@@ -181,6 +188,115 @@ __device__ __forceinline__ void epilogue_tile(Fetch&& fetch, Wait&& wait, int BN
       }
     }
   } else if constexpr (EPI == kEpiAddF32) {
+    if constexpr (STG) {
+    // Staged variant (launches whose CTAs run several units, where the epilogue overlaps the next
+    // unit's main loop and its load/store traffic competes with it): the residual / output / bf16
+    // tiles move through this warp's shared-memory staging (32 rows x 32 columns, padded rows),
+    // so every global access is a coalesced row segment — lane l moves float4 column l % 8 of
+    // rows l / 8 + 4 i (profiles/r02_prefill_probe.md). Same arithmetic as the direct path.
+    const int n0 = n_blk * BN;
+    const int ncols = min(BN, N - n0);
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    const int row0 = row - lane;  // the warp's first row
+    const int cq = lane & 7, rq = lane >> 3;
+    float* ft = estage;                                                    // [32][33] fp32
+    std::uint32_t* bt = reinterpret_cast<std::uint32_t*>(estage + 32 * 33);  // [32][17] bf16 pairs
+    float* orow = static_cast<float*>(out) + static_cast<std::size_t>(row) * ldo + n0;
+    const bool res = !nm.store_only;
+    float4 cur[8], nxt[8];
+    auto load = [&](int c, float4 (&v)[8]) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = row0 + rq + 4 * i;
+        v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (res && rr < M && c + 32 <= ncols)
+          v[i] = reinterpret_cast<const float4*>(static_cast<const float*>(out) + static_cast<std::size_t>(rr) * ldo +
+                                                 n0 + c)[cq];
+      }
+    };
+    load(0, cur);
+    wait();
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      std::uint32_t r[32];
+      fetch(c, r);
+      if (c + 32 < BN) load(c + 32, nxt);
+      if (c + 32 <= ncols) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float* d = ft + (rq + 4 * i) * 33 + 4 * cq;
+          d[0] = cur[i].x;
+          d[1] = cur[i].y;
+          d[2] = cur[i].z;
+          d[3] = cur[i].w;
+        }
+        __syncwarp();
+        float x[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = ft[lane * 33 + j] + __uint_as_float(r[j]);
+        if (nm.ss != nullptr && live) {
+          float t = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) t = fmaf(x[j], x[j], t);
+          nm.ss[static_cast<std::size_t>((n0 + c) / 32) * nm.ld_ss + row] = t;  // chunk-major: coalesced
+#pragma unroll
+          for (int j = 0; j < 16; ++j) bt[lane * 17 + j] = pack_bf16(x[2 * j], x[2 * j + 1]);
+        }
+        __syncwarp();  // every lane has read its residual row
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ft[lane * 33 + j] = x[j];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = row0 + rq + 4 * i;
+          if (rr < M) {
+            const float* sp = ft + (rq + 4 * i) * 33 + 4 * cq;
+            reinterpret_cast<float4*>(static_cast<float*>(out) + static_cast<std::size_t>(rr) * ldo + n0 + c)[cq] =
+                make_float4(sp[0], sp[1], sp[2], sp[3]);
+          }
+        }
+        if (nm.ss != nullptr) {
+          const int bq = lane & 3, br = lane >> 2;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = row0 + br + 8 * i;
+            if (rr < M) {
+              const std::uint32_t* sp = bt + (br + 8 * i) * 17 + 4 * bq;
+              *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(nm.xb) + static_cast<std::size_t>(rr) * nm.ld_xb +
+                                        n0 + c + 8 * bq) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
+            }
+          }
+        }
+        __syncwarp();  // the staging is reused by the next chunk
+      } else if (live && c < ncols) {  // the ragged last chunk, element-wise
+        float* o = orow + c;
+        float x[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          x[j] = 0.f;
+          if (c + j < ncols) {
+            o[j] = (nm.store_only ? 0.f : o[j]) + __uint_as_float(r[j]);
+            x[j] = o[j];
+          }
+        }
+        if (nm.ss != nullptr) {
+          float t = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) t = fmaf(x[j], x[j], t);
+          nm.ss[static_cast<std::size_t>((n0 + c) / 32) * nm.ld_ss + row] = t;
+          std::uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(x[2 * j], x[2 * j + 1]);
+          store_bf16_tail(static_cast<__nv_bfloat16*>(nm.xb) + static_cast<std::size_t>(row) * nm.ld_xb + n0 + c, pk,
+                          ncols - c);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+    }
+    return;
+    }
+
     // out[row, n] += acc (+ the fused-RMSNorm outputs of the new row). The residual chunk c + 32
     // is loaded while chunk c is processed, chunk 0 before the accumulator wait.
     const int n0 = n_blk * BN;
@@ -307,7 +423,7 @@ struct SplitArgs {
 // through distributed shared memory into the first pair's CTAs, which add it to their own
 // (split 0 + split 1, the order of the ordered global split-K sum) and run the epilogue. Half
 // the K loop per SM, twice the tiles in flight, no partial traffic through L2.
-template <int EPI, int CG, int CS = 1>
+template <int EPI, int CG, int CS = 1, bool STG = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, int m_blocks, int n_tiles, void* __restrict__ out, int ldo, const RopeEpi rope,
@@ -327,6 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* rfull = reinterpret_cast<std::uint64_t*>(tmem_slot + 2);  // [2] CS == 2: peer chunk landed
   std::uint64_t* sfree = rfull + 2;                                         // [2] CS == 2: chunk buffer consumed
   float* rbuf = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);  // CS == 2: [2][128][36]
+  // the staged epilogue's per-warp blocks, after the CS buffers (kStagedEpi launches only)
+  float* estage_base = STG ? reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256 + (CS == 2 ? kCsBufBytes : 0))
+                            : nullptr;
 
   const int num_k = K / BK;
   const int S = sk.splits;  // 1 for pairs
@@ -500,6 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {  // epilogue warps 2..5 → TMEM lane groups (warp % 4)
     pdl_wait();  // the epilogues read the residual / norm statistics / rope tables
     const int grp = static_cast<int>(warp & 3);
+    float* estage = estage_base ? estage_base + grp * kEpiStageFloats : nullptr;
     const int m_slots = m_units * CG;  // 128-row blocks incl. a pair's padding block
     const int rows_pad = m_slots * BM;
     int local = 0;
@@ -608,7 +728,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive_cluster_relaxed(&sfree[b], static_cast<std::uint32_t>(crank + 2));
             ++cs_q;
           };
-          epilogue_tile<EPI>(cs_fetch, acc_wait, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
+          epilogue_tile<EPI, STG>(cs_fetch, acc_wait, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm,
+                            estage);
         }
         tc_fence_before();
         __syncwarp();
@@ -616,7 +737,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       if (S == 1) {
-        epilogue_tile<EPI>(tmem_fetch, acc_wait, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm);
+        epilogue_tile<EPI, STG>(tmem_fetch, acc_wait, BN, row, (ablate & 4) ? 0 : M, N, n_blk, out, ldo, rope, norm,
+                          estage);
         if (local == 0 && warp == 2 && lane == 0) trace_point(ablate, 6);
         tc_fence_before();
         __syncwarp();
@@ -698,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(norm.ss_in != nullptr ? v[j] * rs : v[j]);
         };
-        epilogue_tile<EPI>(ws_fetch, [] {}, BN, row, M, N, n_blk, out, ldo, rope, norm);
+        epilogue_tile<EPI, STG>(ws_fetch, [] {}, BN, row, M, N, n_blk, out, ldo, rope, norm, estage);
       }
       epi_bar();  // last_flag is reused by the next unit
     }
@@ -787,12 +909,24 @@ int max_clusters() {  // co-resident clusters of CSZ CTAs at one CTA per SM (sam
 }
 int pair_clusters() { return max_clusters<2>(); }
 
+// the staged-epilogue instantiation exists for the fp32-residual epilogue only
+template <int EPI, int CG, int CS>
+auto pick_kernel(bool staged) {
+  if constexpr (EPI == kEpiAddF32) {
+    if (staged) return gemm_tn_kernel<EPI, CG, CS, true>;
+  }
+  return gemm_tn_kernel<EPI, CG, CS, false>;
+}
+
 template <int EPI, int CG, int CS = 1>
 void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   static std::atomic<std::uint32_t> attr_done{0};
   once_per_device(attr_done, [] {
     WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI, CG, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemBudget));
+    if constexpr (EPI == kEpiAddF32)
+      WS_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<EPI, CG, CS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemBudget));
   });
   static const int ablate = [] {  // WS_GEMM_ABLATE (measurement only): 1 no MMA,
     const char* e = std::getenv("WS_GEMM_ABLATE");  // 4 no epilogue stores
@@ -809,32 +943,51 @@ void launch(const GemmArgs& g, const SplitArgs& sk, int bn, cudaStream_t st) {
   const CUtensorMap tb = make_map(g.W, g.N, g.K, g.ldw, static_cast<std::uint32_t>(bn / CG));
   const int m_blocks = (g.M + BM - 1) / BM;
   const int n_tiles = (g.N + bn - 1) / bn;  // SwiGLU: N counts gate+up rows
-  const int smem = smem_bytes(bn, CG, CS), stages = ring_stages(bn, CG, CS);
+  // The fp32-residual epilogue goes through shared-memory staging when CTAs run several units
+  // (its traffic then overlaps the next unit's main loop); a single unit keeps the direct path,
+  // which is shorter on the critical path (profiles/r02_prefill_probe.md). WS_EPI_STAGE=0: never.
+  static const bool stage_ok = [] {
+    const char* e = std::getenv("WS_EPI_STAGE");
+    return !(e && e[0] == '0');
+  }();
+  bool staged = false;
+  auto plan = [&](int units, int ctas_or_clusters, int& smem, int& stages, int& flags) {
+    staged = EPI == kEpiAddF32 && stage_ok && units > ctas_or_clusters;
+    smem = smem_bytes(bn, CG, CS, staged);
+    stages = ring_stages(bn, CG, CS, staged);
+    flags = ablate | late;
+  };
+  int smem = 0, stages = 0, flags = 0;
   if constexpr (CG == 1) {
     const int total = m_blocks * n_tiles * sk.splits;
     // max_ctas < 0: one CTA per unit (not persistent: SMs free up between units, so a
     // concurrent higher-priority stream's kernels get scheduled sooner)
     const int grid = g.max_ctas < 0 ? total : std::min(total, g.max_ctas > 0 ? g.max_ctas : kNumSMs);
-    const int flags = ablate | late | (grid <= early_grid ? kEarlyTrigger : 0);
-    launch_pdl(gemm_tn_kernel<EPI, 1>, dim3(grid), dim3(kThreads), smem, st, 1, ta, tb, g.M, g.N, g.K, m_blocks,
-               n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
+    plan(total, grid, smem, stages, flags);
+    flags |= (grid <= early_grid ? kEarlyTrigger : 0);
+    launch_pdl(pick_kernel<EPI, 1, 1>(staged), dim3(grid), dim3(kThreads), smem, st,
+               1, ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
   } else if constexpr (CS == 2) {
     const int total = (m_blocks + 1) / 2 * n_tiles;  // tiles; each cluster of 4 holds both K halves
+    int clusters = g.max_ctas < 0 ? total : std::min(total, max_clusters<4>());
+    if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 4));
+    plan(total, clusters, smem, stages, flags);
     static const bool dbg = std::getenv("WS_GEMM_DEBUG") != nullptr;
     if (dbg) std::fprintf(stderr, "[gemm] cluster split: %d tiles, %d co-resident clusters of 4, bn %d, %d stages\n",
                           total, max_clusters<4>(), bn, stages);
-    int clusters = g.max_ctas < 0 ? total : std::min(total, max_clusters<4>());
-    if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 4));
-    const int flags = ablate | late | (4 * clusters <= early_grid ? kEarlyTrigger : 0);
-    launch_pdl(gemm_tn_kernel<EPI, 2, 2>, dim3(4 * clusters), dim3(kThreads), smem, st, 4, ta, tb, g.M, g.N, g.K,
-               m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
+    flags |= (4 * clusters <= early_grid ? kEarlyTrigger : 0);
+    launch_pdl(pick_kernel<EPI, 2, 2>(staged), dim3(4 * clusters),
+               dim3(kThreads), smem, st, 4, ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo, g.rope, sk,
+               g.norm, bn, stages, flags);
   } else {
     const int total = (m_blocks + 1) / 2 * n_tiles * sk.splits;
     int clusters = g.max_ctas < 0 ? total : std::min(total, pair_clusters());
     if (g.max_ctas > 0) clusters = std::max(1, std::min(clusters, g.max_ctas / 2));
-    const int flags = ablate | late | (2 * clusters <= early_grid ? kEarlyTrigger : 0);
-    launch_pdl(gemm_tn_kernel<EPI, 2>, dim3(2 * clusters), dim3(kThreads), smem, st, 2, ta, tb, g.M, g.N, g.K,
-               m_blocks, n_tiles, g.out, g.ldo, g.rope, sk, g.norm, bn, stages, flags);
+    plan(total, clusters, smem, stages, flags);
+    flags |= (2 * clusters <= early_grid ? kEarlyTrigger : 0);
+    launch_pdl(pick_kernel<EPI, 2, 1>(staged), dim3(2 * clusters),
+               dim3(kThreads), smem, st, 2, ta, tb, g.M, g.N, g.K, m_blocks, n_tiles, g.out, g.ldo, g.rope, sk,
+               g.norm, bn, stages, flags);
   }
 }
 
