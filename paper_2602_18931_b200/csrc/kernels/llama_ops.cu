@@ -3,6 +3,8 @@
 // accesses where the layout allows.
 #include "llama_ops.cuh"
 
+#include <algorithm>
+
 #include <cuda_bf16.h>
 
 #include <stdexcept>
@@ -32,24 +34,35 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const std::i
                              int ld_ss) {
   pdl_trigger();
   pdl_wait();  // inputs come from the previous kernel of the chain
+  // One row per CTA; each thread moves 8 consecutive elements (one 16-byte load, two 16-byte fp32
+  // stores, one 16-byte bf16 store). A 32-element norm-statistics chunk is 4 threads: each sums
+  // its 8 squares in order, then the chunk combines ((t0 + t1) + (t2 + t3)) — a fixed order per
+  // row, so the statistics are the same at any batch size.
   const int row = blockIdx.x;
-  const int lane = threadIdx.x & 31;
   const __nv_bfloat16* e = emb + static_cast<std::size_t>(tok[row]) * d;
-  for (int c = threadIdx.x / 32; c < d / 32; c += blockDim.x / 32) {
-    const int i = c * 32 + lane;
-    const __nv_bfloat16 b = e[i];
-    const float f = __bfloat162float(b);
-    x[static_cast<std::size_t>(row) * d + i] = f;
-    if (xb) xb[static_cast<std::size_t>(row) * d + i] = b;
+  for (int i8 = threadIdx.x; i8 < d / 8; i8 += blockDim.x) {
+    const uint4 q = reinterpret_cast<const uint4*>(e)[i8];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+    float f[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 v = __bfloat1622float2(h[j]);
+      f[2 * j] = v.x;
+      f[2 * j + 1] = v.y;
+    }
+    float4* xo = reinterpret_cast<float4*>(x + static_cast<std::size_t>(row) * d) + 2 * i8;
+    xo[0] = make_float4(f[0], f[1], f[2], f[3]);
+    xo[1] = make_float4(f[4], f[5], f[6], f[7]);
+    if (xb) reinterpret_cast<uint4*>(xb + static_cast<std::size_t>(row) * d)[i8] = q;
     if (ss) {
-      // the producer GEMM epilogue sums a chunk sequentially (fmaf chain); any fixed order is
-      // valid — this one is the lane order of a sequential chain too, done by lane 0
       float t = 0.f;
-      for (int j = 0; j < 32; ++j) {
-        const float v = __shfl_sync(0xffffffffu, f, j);
-        t = fmaf(v, v, t);
-      }
-      if (lane == 0) ss[static_cast<std::size_t>(c) * ld_ss + row] = t;  // chunk-major
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t = fmaf(f[j], f[j], t);
+      const float t1 = __shfl_xor_sync(0xffffffffu, t, 1);
+      const float a = (threadIdx.x & 1) ? t1 + t : t + t1;  // (t0 + t1) in the lower thread's order
+      const float a2 = __shfl_xor_sync(0xffffffffu, a, 2);
+      const float c = (threadIdx.x & 2) ? a2 + a : a + a2;
+      if ((threadIdx.x & 3) == 0) ss[static_cast<std::size_t>(i8 / 4) * ld_ss + row] = c;  // chunk-major
     }
   }
 }
@@ -201,8 +214,9 @@ void embed_rows(const void* emb, const std::int32_t* tok, int rows, int d, float
                 cudaStream_t st) {
   if (rows <= 0) return;
   if (d % 32) throw std::invalid_argument("embed: d % 32");
-  launch_pdl(embed_kernel, dim3(rows), dim3(256), 0, st, 1, static_cast<const __nv_bfloat16*>(emb), tok, d, x,
-             static_cast<__nv_bfloat16*>(xb), ss, ld_ss);
+  if (d % 256) throw std::invalid_argument("embed: d % 256");  // whole warps of 8-element threads
+  launch_pdl(embed_kernel, dim3(rows), dim3(std::min(256, d / 8)), 0, st, 1, static_cast<const __nv_bfloat16*>(emb),
+             tok, d, x, static_cast<__nv_bfloat16*>(xb), ss, ld_ss);
 }
 
 void fold_norm_weight(void* W, std::int64_t rows, int cols, const void* w, cudaStream_t st) {
